@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark of the pathwise CVA hot path (BASELINE.json metric 1):
+
+  Y x X x step scenarios/s = M * N * n / time of [Y diffusion + MtM cube +
+  X over-simulation + labels for every pricing step]
+
+on the paper case C2 (configs/paper_shape.json, 8 clients, 500 swaps,
+M = 2^14 Y-paths x N = 2^7 X-replicas, n = 100 quarterly steps, 25 substeps)
+per GPU.  A "step" is one in-place re-run of that whole pipeline with fresh
+stream keys (hcva_sim_rerun); it writes ~2.5 GB (market block, cube, default
+steps, labels of all 101 steps), far beyond the 126 MB L2, so no flush is
+needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Multi-GPU (torchrun): weak scaling -- rank r simulates its own 2^14 paths
+(global path offset r * 2^14); no collective on the data path.  Device time
+is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "Y×X×step scenarios/s"
+UNIT = "scenarios/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--paths", type=int, default=0, help="override M per GPU")
+    ap.add_argument("--replicas", type=int, default=0, help="override N")
+    ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def workload(args):
+    import cases
+    import paper_2211_17005_b200 as hcva
+
+    j = cases.case(args.config)
+    if args.paths:
+        j["simulation"]["paths"] = args.paths
+    if args.replicas:
+        j["simulation"]["replicas"] = args.replicas
+    cfg = hcva.parse_config(json.dumps(j))
+    return cfg, j
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- CPU arm
+def run_reference_sample(cfg, seconds_target, probe_paths=64):
+    """Time the reference's own CPU pipeline (oracle/_ref, built from
+    /root/reference's sources) on a bounded sample of the workload: the same
+    config with fewer Y-paths.  Returns (scenarios/s, dict)."""
+    import ctypes as C
+
+    import cases
+    import oracle_api
+
+    ref = oracle_api.reference()
+    kind = "reference"
+    if ref is None:
+        ref, kind = oracle_api.restatement(), "port"
+    threads = cpu_threads()
+    os.environ["HIERCVA_THREADS"] = str(threads)
+    m = cases.oracle_model(cfg)
+    root = ref.key(cfg.seed)
+    book = ref.generate_book(m, cfg.book_count, cfg.notional_min, cfg.notional_max, ref.split(root, 0))
+    key_sim = ref.split(root, 1)
+    mm = ref.model(m)
+    bookc = np.ascontiguousarray(book, dtype=oracle_api.SWAP_DTYPE)
+
+    def run(paths):
+        sec, chk = C.c_double(), C.c_double()
+        rc = ref.lib.or_pipeline_bench(C.byref(mm), bookc.ctypes.data_as(C.c_void_p), len(bookc), paths,
+                                       cfg.replicas, C.c_uint64(key_sim), 0, C.byref(sec), C.byref(chk))
+        if rc:
+            raise RuntimeError(ref.lib.or_last_error().decode())
+        return sec.value
+
+    t_probe = run(probe_paths)
+    paths = int(max(probe_paths, min(cfg.paths, probe_paths * seconds_target / max(t_probe, 1e-3))))
+    paths = max(threads, (paths // threads) * threads)
+    t = run(paths)
+    value = paths * cfg.replicas * cfg.n_steps / t
+    return value, dict(kind=kind, cores=threads if kind == "reference" else 1, paths=paths, seconds=t)
+
+
+def reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    cfg, j = workload(args)
+    vals = []
+    info = None
+    per_step = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    for s in range(args.warmup + args.steps):
+        v, info = run_reference_sample(cfg, per_step)
+        if s >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    sample = (f"{info['paths']} of {cfg.paths} Y-paths x {cfg.replicas} X-replicas x {cfg.n_steps} steps "
+              f"per step ({info['seconds']:.1f} s; simulate_set + features_at/defaults_label for i=n..1)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * info["seconds"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (configs/paper_shape.json model, generated book)",
+        "config": config_obj(cfg, args, world=1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_obj(cfg, args, world):
+    return {"workload": f"{args.config}: paper CVA case, {cfg.n_clients} clients, {cfg.book_count} swaps, "
+                        f"{cfg.n_economies} economies",
+            "paths_per_gpu": cfg.paths, "replicas": cfg.replicas, "pricing_steps": cfg.n_steps,
+            "substeps": cfg.substeps, "dt_years": cfg.dt, "n_factors": cfg.n_factors,
+            "global_paths": cfg.paths * world, "parallelism": f"y-path shards x{world}",
+            "l2": "per-step working set ~2.5 GB/GPU >> 126 MB L2 (no flush needed)"}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- GPU arm
+# Algorithmic FP64 work of K1 per path: n*sub*[D*F_N + D(D+1) + 20*D],
+# F_N = 120 flop per normal (Acklam + Halley step with erfc/exp, 3 divides).
+F_N = 120
+
+
+def k1_flops_per_path(cfg):
+    D = cfg.n_factors
+    return cfg.n_steps * cfg.substeps * (D * F_N + D * (D + 1) + 20 * D)
+
+
+def ours_arm(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2211_17005_b200 as hcva
+
+    cfg, _ = workload(args)
+    ctx = hcva.context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    book = hcva.generate_book(cfg)
+    M, N, n = cfg.paths, cfg.replicas, cfg.n_steps
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    sim = hcva.simulate_set(cfg, book, M, N, root, path_offset=rank * M, ctx=ctx)
+    sim.labels_all("defaults", to_host=False)
+    ctx.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for w in range(args.warmup):
+        sim.rerun(root.split(1000 + w), "defaults")
+    ctx.synchronize()
+    barrier()
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for s in range(args.steps):
+            sim.rerun(root.split(2000 + s), "defaults", event_slot=s)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    phases = np.array([sim.phase_times(s) for s in range(args.steps)])  # ms [K, 4]
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    scen = M * N * n * world
+    value = scen / (ms_step * 1e-3)
+
+    # Roofline of the dominant kernel (K1, FP64 pipe): algorithmic flop per
+    # launch / mean launch time measured with events on the launch stream.
+    fp64_peak = ctypes_peak(ctx)
+    k1_ms = float(phases[:, 0].mean())
+    k1_flop = k1_flops_per_path(cfg) * M
+    achieved = k1_flop / (k1_ms * 1e-3) / 1e12
+    phase_ms = {k: float(v) for k, v in zip(["market_K1", "defaults_K3", "cube_K2", "labels_K4"], phases.mean(0))}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+               "sample": f"{info['paths']} of {M} Y-paths x {N} replicas x {n} steps, "
+                         f"{info['seconds']:.1f} s (simulate_set + features_at/defaults_label for i=n..1)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (configs/paper_shape.json model, generated 500-swap book, quarterly grid)",
+            "config": config_obj(cfg, args, world),
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "phase_ms": phase_ms,
+            "roofline": {"bound": "fp64", "kernel": "k_market (K1 diffusion)", "achieved": achieved,
+                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                         "peak_source": "measured DFMA microbenchmark on this GPU (hcva_diag_fp64_peak)",
+                         "algorithmic_flop_per_launch": k1_flop, "traffic": None,
+                         "k1_share_of_step": k1_ms / ms_step},
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def ctypes_peak(ctx):
+    import ctypes as C
+
+    from paper_2211_17005_b200 import _lib
+
+    v = C.c_double()
+    _lib.check(_lib.lib().hcva_diag_fp64_peak(ctx.handle, C.byref(v)))
+    return v.value
+
+
+def e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args):
+    """The same metric through the public API with host inputs: per step the
+    model/book go host->device inside hcva_simulate_set, the engine simulates
+    and labels every step, and the CVA profile (n+1 doubles) comes back."""
+    import torch
+
+    M, N, n = cfg.paths, cfg.replicas, cfg.n_steps
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    steps = max(2, min(args.steps, 5))
+    for w in range(1):
+        sim = hcva.simulate_set(cfg, book, M, N, root.split(3000 + w), path_offset=rank * M, ctx=ctx)
+        sim.cva_profile("defaults")
+        del sim
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        sim = hcva.simulate_set(cfg, book, M, N, root.split(4000 + s), path_offset=rank * M, ctx=ctx)
+        prof = sim.cva_profile("defaults")
+        del sim
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        t = torch.tensor([dt], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    h2d = book.nbytes + cfg.rates.nbytes + cfg.fx.nbytes + cfg.credit.nbytes
+    return {"value": M * N * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(prof.nbytes), "ms_per_step": dt * 1e3,
+            "path": "hcva.simulate_set (hcva_simulate_set: stage + K1/K3/K2) + cva_profile (K4 + reduction)",
+            "cva0": float(prof[0])}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * hcva_gpu.h -- C ABI of the B200-native pathwise CVA engine (libhcva_gpu.so).
+ *
+ * Drop-in boundary for the hot path of the reference `hiercva` library
+ * (arXiv 2211.17005; /root/reference/proj).  The reference exposes its hot
+ * path as C++ free functions; each entry point below names the reference
+ * interface it replaces (file:line under proj/).  A C++ or pybind caller binds
+ * these symbols exactly as INTEGRATION.md shows.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "host or device" output pointers may be
+ *    pageable/pinned host memory or device memory of the context's GPU
+ *    (copied with cudaMemcpyDefault through UVA).
+ *  - Every function returns hcva_status; on failure hcva_last_error() holds
+ *    the message.  Status codes map one to one onto the reference's exception
+ *    types (proj/include/hiercva/errors.hpp:9-25):
+ *      HCVA_ERR_CONFIG   -> config_error   (bad parameters, non-PSD correlation)
+ *      HCVA_ERR_CONTRACT -> contract_error (precondition / shape violations)
+ *      HCVA_ERR_NUMERIC  -> numeric_error  (degenerate annuity, NaN loss)
+ *      HCVA_ERR_CUDA     -> (no reference counterpart: device failure)
+ *  - Stream keys are the 64-bit Philox keys of the reference's RandomStream
+ *    (rng.cpp:44-55): a caller holding a RandomStream passes the key of the
+ *    stream it would have handed to the reference function.
+ *  - Layouts: exports reproduce the reference's AoS blocks exactly
+ *    (market.hpp:80-123, defaults.hpp:38-40, portfolio.hpp:30-37,
+ *    labels.hpp:15-37); device-resident data is SoA, path index fastest.
+ */
+#ifndef HCVA_GPU_H
+#define HCVA_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HCVA_OK = 0,
+    HCVA_ERR_CONFIG = 1,
+    HCVA_ERR_CONTRACT = 2,
+    HCVA_ERR_NUMERIC = 3,
+    HCVA_ERR_CUDA = 4
+} hcva_status;
+
+typedef struct hcva_ctx hcva_ctx; /* one GPU + one CUDA stream + scratch */
+typedef struct hcva_sim hcva_sim; /* a simulated set resident on the GPU  */
+
+/* --- model description (market.hpp:13-75, portfolio.hpp:14-22) --------- */
+typedef struct { double a, b, sigma, r0; } hcva_vasicek;      /* VasicekParams */
+typedef struct { double sigma, rho, chi0; } hcva_fx;          /* FxParams      */
+typedef struct { double alpha, delta, nu, gamma0; } hcva_cir; /* CirParams     */
+
+typedef struct {
+    int n_economies;            /* E, economy 0 = reference currency             */
+    int n_clients;              /* Cc; credit names = Cc + 1 (bank first)         */
+    const hcva_vasicek* rates;  /* [E]                                            */
+    const hcva_fx* fx;          /* [E-1] (may be NULL when E == 1)                */
+    const hcva_cir* credit;     /* [Cc+1]                                         */
+    const double* correlation;  /* [D*D] row-major or NULL (block default)        */
+} hcva_model;
+
+typedef struct { int n_steps; int substeps; double dt; } hcva_grid; /* TimeGrid */
+
+typedef struct {                 /* SwapSpec, portfolio.hpp:14-22 */
+    int economy;
+    int client;
+    double notional;
+    double tenor;
+    double maturity;
+    double fixed_rate;
+} hcva_swap;
+
+/* --- runtime ------------------------------------------------------------ */
+const char* hcva_last_error(void);
+const char* hcva_version(void);
+hcva_status hcva_ctx_create(int device, hcva_ctx** out);
+hcva_status hcva_ctx_destroy(hcva_ctx* ctx);
+/* cudaStream_t the context launches on (for events / interop). */
+hcva_status hcva_ctx_stream(hcva_ctx* ctx, void** stream_out);
+hcva_status hcva_ctx_synchronize(hcva_ctx* ctx);
+/* Number of kernels this context launched since creation (evidence counter). */
+hcva_status hcva_ctx_launch_count(hcva_ctx* ctx, uint64_t* out);
+
+/* Diagnostic: measured FP64 FMA throughput of this GPU in TFLOP/s (the
+ * roofline denominator of the FP64-bound simulation kernels). */
+hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops);
+
+/* --- RNG (rng.hpp:16-52, rng.cpp:44-130) --------------------------------- */
+uint64_t hcva_rng_root_key(uint64_t seed);               /* RandomStream(seed) */
+uint64_t hcva_rng_split_key(uint64_t key, uint64_t k);   /* .split(k)          */
+/* Draws j = start .. start+count-1 of stream `key` on the GPU.
+ * kind: 0 = next_u64 (out is uint64_t*), 1 = next_uniform, 2 = next_normal,
+ * 3 = next_exponential (out is double*).  Replaces RandomStream::next_*. */
+hcva_status hcva_rng_draw(hcva_ctx* ctx, uint64_t key, uint64_t start, size_t count, int kind,
+                          void* out);
+
+/* --- host-side model utilities ------------------------------------------- */
+/* cholesky_lower of the effective correlation (market.cpp:49-65,136-159). */
+hcva_status hcva_cholesky(const hcva_model* model, double* chol_out /* [D*D] */);
+/* par_rate (portfolio.cpp:47-56) and zc_price (portfolio.cpp:34-45). */
+hcva_status hcva_par_rate(double maturity, double tenor, const hcva_vasicek* v, double* out);
+hcva_status hcva_zc_price(double r, double tau, const hcva_vasicek* v, double* out);
+/* generate_book (portfolio.cpp:149-174); key = root.split(kBook). */
+hcva_status hcva_generate_book(const hcva_model* model, const hcva_grid* grid, int count,
+                               double notional_min, double notional_max, uint64_t key,
+                               hcva_swap* out /* [count] */);
+
+/* --- simulation (the Y / X / MtM engine) ---------------------------------- */
+/* simulate_set (pipeline.cpp:63-70): market from key_market (= stream.split(0)),
+ * defaults from key_defaults (= stream.split(1)), MtM cube from the book.
+ * Paths path_offset .. path_offset+n_paths-1 of the global path index space
+ * (shard of a multi-GPU run; 0 for a single GPU).  n_replicas == 0 skips the
+ * default block; book == NULL skips the cube. */
+hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                              const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
+                              int n_replicas, uint64_t key_market, uint64_t key_defaults,
+                              hcva_sim** out);
+/* simulate_conditional_market (market.cpp:236-310) for ONE outer state:
+ * state = rates[E], log_fx[E-1], intensities[Cc+1], lagged_rates[E]. */
+hcva_status hcva_simulate_conditional(hcva_ctx* ctx, const hcva_model* model,
+                                      const hcva_grid* grid, const double* state_rates,
+                                      const double* state_log_fx, const double* state_intens,
+                                      const double* state_lagged, int start_step, int horizon,
+                                      int n_inner, uint64_t key, hcva_sim** out);
+/* sample_default_block (defaults.cpp:20-45) on an existing market block. */
+hcva_status hcva_sample_defaults(hcva_sim* sim, int n_replicas, uint64_t key);
+/* build_mtm_cube (portfolio.cpp:97-147) on an existing market block. */
+hcva_status hcva_build_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps);
+hcva_status hcva_sim_destroy(hcva_sim* sim);
+/* Re-run an outer set in place with new stream keys: market, defaults, cube
+ * and (labels_kind >= 0) the labels of every step, launched asynchronously on
+ * the context stream with no host synchronisation (the execution plan staged
+ * by hcva_simulate_set is reused).  event_slot >= 0 records CUDA events around
+ * the four phases; hcva_sim_phase_times() reads them after a synchronise. */
+hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defaults, int labels_kind,
+                           int event_slot);
+/* ms[0..3] = market, defaults, cube, labels durations of slot `event_slot`. */
+hcva_status hcva_sim_phase_times(hcva_sim* sim, int event_slot, float* ms /* [4] */);
+
+/* dims: [0]=paths [1]=steps [2]=economies [3]=credit names [4]=replicas
+ *       [5]=start_step [6]=factors D [7]=substeps */
+hcva_status hcva_sim_dims(const hcva_sim* sim, int* dims /* [8] */);
+/* Threshold ties of the last default sampling: (k,l,c) whose exponential
+ * threshold lies within tol_ulps ulps of a cumulative hazard it was compared
+ * against.  counts[0] = within 1 ulp, counts[1] = within 1e-12 relative. */
+hcva_status hcva_sim_tie_counts(const hcva_sim* sim, uint64_t* counts /* [2] */);
+
+/* Exports in the reference's AoS layouts (host or device destination). */
+hcva_status hcva_sim_export_market(const hcva_sim* sim, double* rates, double* fx,
+                                   double* intensities, double* lagged, double* discounts,
+                                   double* hazards);
+hcva_status hcva_sim_export_defaults(const hcva_sim* sim, uint16_t* steps);
+hcva_status hcva_sim_export_cube(const hcva_sim* sim, double* cube);
+
+/* --- labels / features (labels.cpp:21-88,142-167) ------------------------- */
+/* kind: 0 = defaults_label, 1 = intensity_label. out[k*N+l]. */
+hcva_status hcva_labels(hcva_sim* sim, int step, int kind, double* out);
+/* Labels for every step 0..n in one pass, out[i*M*N + k*N + l] (host or
+ * device); out == NULL keeps them on the device only (bench / regression). */
+hcva_status hcva_labels_all(hcva_sim* sim, int kind, double* out);
+/* CVA profile: out[i] = mean over (k,l) of the step-i labels, i = 0..n (the
+ * pathwise CVA estimator E[xi_i]; out[0] is the time-0 CVA).  Host or device. */
+hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out /* [n+1] */);
+/* features_at: row-major (M*N) x (p+q) FP64. */
+hcva_status hcva_features(hcva_sim* sim, int step, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HCVA_GPU_H */

@@ -1,0 +1,133 @@
+// common.cuh -- internal structures of libhcva_gpu.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hcva_gpu.h"
+
+namespace hcva {
+
+// Exception types mirroring proj/include/hiercva/errors.hpp:9-25; the C ABI
+// converts them to hcva_status codes.
+struct config_error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct contract_error : std::logic_error { using std::logic_error::logic_error; };
+struct numeric_error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct cuda_error : std::runtime_error { using std::runtime_error::runtime_error; };
+
+void set_last_error(const std::string& msg);
+
+#define HCVA_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t err__ = (call);                                                        \
+        if (err__ != cudaSuccess)                                                          \
+            throw ::hcva::cuda_error(std::string(#call) + ": " + cudaGetErrorString(err__)); \
+    } while (0)
+
+template <typename F>
+hcva_status guarded(F&& f) {
+    try {
+        f();
+        return HCVA_OK;
+    } catch (const config_error& e) {
+        set_last_error(e.what());
+        return HCVA_ERR_CONFIG;
+    } catch (const contract_error& e) {
+        set_last_error(e.what());
+        return HCVA_ERR_CONTRACT;
+    } catch (const numeric_error& e) {
+        set_last_error(e.what());
+        return HCVA_ERR_NUMERIC;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return HCVA_ERR_CUDA;
+    }
+}
+
+// Host copy of the model with derived quantities.
+struct Model {
+    int E = 0, Cc = 0, Cn = 0, D = 0;
+    std::vector<hcva_vasicek> rates;
+    std::vector<hcva_fx> fx;
+    std::vector<hcva_cir> credit;
+    std::vector<double> corr;  // effective D x D
+    std::vector<double> chol;  // lower Cholesky factor
+    int n_steps = 0, substeps = 1;
+    double dt = 1.0;
+};
+
+Model make_model(const hcva_model* m, const hcva_grid* g);  // validates (market.cpp:12-75)
+std::vector<double> cholesky_lower(const std::vector<double>& a, int n, const std::string& what);
+double zc_price(double r, double tau, const hcva_vasicek& p);
+double par_rate(double maturity, double tenor, const hcva_vasicek& p);
+bool is_multiple(double x, double step);
+
+// Device-side per-launch constants for the diffusion kernel: per-factor
+// coefficient quads staged into shared memory, CSR of the Cholesky factor.
+struct FactorCoef {
+    double c0, c1, c2, c3;
+};
+
+struct DeviceBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b) {
+        release();
+        if (b) HCVA_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    ~DeviceBuf() { release(); }
+    DeviceBuf() = default;
+    DeviceBuf(const DeviceBuf&) = delete;
+    DeviceBuf& operator=(const DeviceBuf&) = delete;
+};
+
+}  // namespace hcva
+
+struct hcva_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    int sm_count = 148;
+};
+
+// Simulated set, device resident, SoA with the path index fastest:
+//   rates [(i*E + e)*M + k], fx [(i*(E-1) + e-1)*M + k], intens/hazard
+//   [(i*Cn + c)*M + k], disc [i*M + k], cube [(i*Cc + c-1)*M + k],
+//   default steps [c*R + k*N + l] (uint16, 0xFFFF = survives), R = M*N.
+// Lagged rates are not stored: lag(i,e) = rates(i-1,e) for i > 0 and the
+// start state's lag (r0 for outer blocks) at i = 0 (market.cpp:186-195).
+struct hcva_sim {
+    hcva_ctx* ctx = nullptr;
+    hcva::Model model;
+    int M = 0, n = 0, N = 0, start_step = 0, path_offset = 0;
+    int n_groups = 1;  // conditional blocks: states, each with M / n_groups inner paths
+    hcva::DeviceBuf rates, fx, intens, hazard, disc, lag0, cube, steps, labels, ties, scratch, profile;
+    bool has_cube = false, has_defaults = false;
+    int labels_kind = -1;
+    // --- execution plan (staged once, reused by every re-run) ---
+    // market: per-factor coefficients, Cholesky CSR, initial states, group keys
+    hcva::DeviceBuf m_coef, m_row, m_col, m_val, m_init, m_keys;
+    int m_nnz = 0, m_T = 0, m_ppg = 1;
+    uint64_t m_local_offset = 0;
+    size_t m_smem = 0;
+    // MtM: coefficient tables (linear form) or the book (direct form)
+    hcva::DeviceBuf c_lnA, c_B, c_Nsuf, c_N, c_NSsuf, c_H, c_book, c_vas;
+    bool c_linear = true;
+    int c_nswaps = 0;
+    // per-phase CUDA events of re-runs: [slot][market, defaults, cube, labels, end]
+    std::vector<cudaEvent_t> events;
+    ~hcva_sim() {
+        for (auto e : events) cudaEventDestroy(e);
+    }
+};

@@ -1,0 +1,50 @@
+// diag.cu -- roofline denominators measured on the box (FP64 pipe peak).
+#include "common.cuh"
+
+namespace hcva {
+
+// 8 independent DFMA chains per thread; the chains' values stay bounded.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+    double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace hcva
+
+using namespace hcva;
+
+extern "C" hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops) {
+    return guarded([&] {
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        DeviceBuf out;
+        out.alloc(8);
+        const int blocks = ctx->sm_count * 8, iters = 2048;
+        cudaEvent_t e0, e1;
+        HCVA_CUDA(cudaEventCreate(&e0));
+        HCVA_CUDA(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            HCVA_CUDA(cudaEventRecord(e0, ctx->stream));
+            k_dfma_peak<<<blocks, 256, 0, ctx->stream>>>(out.as<double>(), iters, 0.999999, 1e-7);
+            HCVA_CUDA(cudaEventRecord(e1, ctx->stream));
+            HCVA_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            HCVA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0) best = std::min(best, ms);
+        }
+        ctx->launches += 5;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double flops = 2.0 * 64.0 * iters * 256.0 * blocks;
+        *tflops = flops / (best * 1e-3) / 1e12;
+    });
+}

@@ -1,0 +1,1138 @@
+// simulate.cu -- the Y / MtM / X engine on sm_100a and its C ABI.
+//
+// Kernels (see DESIGN.md for the roofline of each):
+//   k_draws        K0  raw stream draws (RandomStream::next_* on the device)
+//   k_market       K1  Euler diffusion of rates / log-FX / CIR (market.cpp:161-310)
+//   k_mtm_linear   K2  closed-form swap MtM cube, coefficient form (portfolio.cpp:58-147)
+//   k_mtm_direct   K2' per-swap MtM in the reference's exact summation order
+//   k_defaults     K3  hierarchical over-simulation of X (defaults.cpp:20-45)
+//   k_labels_all   K4  defaults labels for every step in one pass (labels.cpp:21-48)
+//   k_intensity_*  K4' intensity labels (labels.cpp:50-88)
+//   k_features     K4" feature rows of one step (labels.cpp:142-167)
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace hcva {
+
+// Non-contracting FP64 helpers: the reference is compiled without FMA
+// (x86-64, no -march), so the diffusion recursion uses explicitly rounded
+// adds and multiplies to stay bit-faithful to it.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// ------------------------------------------------------------------ K0
+__global__ void k_draws(uint64_t key, uint64_t start, size_t count, int kind, void* out) {
+    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (t >= count) return;
+    const uint64_t x = draw_u64(key, start + t);
+    if (kind == 0) {
+        static_cast<uint64_t*>(out)[t] = x;
+        return;
+    }
+    const double u = u64_to_uniform(x);
+    double v = u;
+    if (kind == 2) v = inverse_normal_cdf(u);
+    if (kind == 3) v = -log(u);
+    static_cast<double*>(out)[t] = v;
+}
+
+// ------------------------------------------------------------------ K1
+struct MarketArgs {
+    int E, Cn, D, substeps, n_store, M, T, nnz;
+    int paths_per_group;
+    uint64_t local_offset;
+    double h, sqh;
+    uint64_t key0;               // key of group 0 when group_keys == nullptr
+    const uint64_t* group_keys;  // [groups] or nullptr
+    const double* init_state;    // [groups][D]
+    const FactorCoef* coef;      // [D]
+    const int* chol_row;         // [D+1]
+    const int* chol_col;         // [nnz]
+    const double* chol_val;      // [nnz]
+    double *rates, *fx, *intens, *hazard, *disc;
+};
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// One CTA = P paths.  Warp 0 runs the per-path Euler recursion (one lane per
+// path); warps 1..G generate the chunk's normals cooperatively (the draws are
+// counter-addressable, so the P*T*D normals of a chunk are independent work)
+// into a double-buffered shared-memory ring.  Named barriers hand chunks over:
+// FULL[b] = 1+b, EMPTY[b] = 3+b.
+template <int P, int G>
+__global__ void __launch_bounds__(32 * (G + 1)) k_market(MarketArgs a) {
+    extern __shared__ double smem[];
+    constexpr int NT = 32 * (G + 1);
+    const int E = a.E, Cn = a.Cn, D = a.D, T = a.T;
+    FactorCoef* coef = reinterpret_cast<FactorCoef*>(smem);
+    double* chol_val = smem + 4 * D;
+    int* chol_col = reinterpret_cast<int*>(chol_val + a.nnz);
+    int* chol_row = chol_col + a.nnz;
+    double* state = smem + 4 * D + a.nnz + (a.nnz + D + 2) / 2;  // [(D+Cn+1)][P]
+    double* zbuf = state + (D + Cn + 1) * P;                              // [2][T*D][P]
+
+    for (int t = threadIdx.x; t < D; t += NT) coef[t] = a.coef[t];
+    for (int t = threadIdx.x; t < a.nnz; t += NT) {
+        chol_val[t] = a.chol_val[t];
+        chol_col[t] = a.chol_col[t];
+    }
+    for (int t = threadIdx.x; t <= D; t += NT) chol_row[t] = a.chol_row[t];
+    __syncthreads();
+
+    const int total_sub = a.n_store * a.substeps;
+    const int n_chunks = (total_sub + T - 1) / T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp > 0) {
+        // ---------------- normal generators
+        const int g = threadIdx.x - 32;
+        const int p = g % P;
+        const int kloc = min(static_cast<int>(blockIdx.x) * P + p, a.M - 1);
+        const int grp = kloc / a.paths_per_group;
+        const uint64_t within = static_cast<uint64_t>(kloc - grp * a.paths_per_group) + a.local_offset;
+        const uint64_t pkey = split_key(a.group_keys ? a.group_keys[grp] : a.key0, within);
+        for (int c = 0; c < n_chunks; ++c) {
+            const int buf = c & 1;
+            if (c >= 2) bar_sync(3 + buf, NT);
+            const int tc = min(T, total_sub - c * T);
+            const int nn = tc * D;
+            const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
+            double* zb = zbuf + buf * (T * D * P);
+            for (int b = g / P; 2 * b < nn; b += (32 * G) / P) {
+                uint64_t w0, w1;
+                philox2x64(blk0 + b, pkey, w0, w1);
+                zb[(2 * b) * P + p] = inverse_normal_cdf(u64_to_uniform(w0));
+                if (2 * b + 1 < nn) zb[(2 * b + 1) * P + p] = inverse_normal_cdf(u64_to_uniform(w1));
+            }
+            bar_arrive(1 + buf, NT);
+        }
+        return;
+    }
+
+    // ---------------- recursion warp
+    const int kloc = static_cast<int>(blockIdx.x) * P + lane;
+    const bool active = lane < P && kloc < a.M;
+    const int M = a.M;
+    double* st = state + lane;  // slot f at st[f * P]
+    if (lane < P) {
+        const int grp = min(kloc, M - 1) / a.paths_per_group;
+        for (int f = 0; f < D; ++f) st[f * P] = a.init_state[static_cast<size_t>(grp) * D + f];
+        for (int c = 0; c <= Cn; ++c) st[(D + c) * P] = 0.0;  // hazards, log beta
+    }
+    auto store = [&](int i) {
+        if (!active) return;
+        for (int e = 0; e < E; ++e) a.rates[(static_cast<size_t>(i) * E + e) * M + kloc] = st[e * P];
+        for (int e = 1; e < E; ++e)
+            a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + kloc] = exp(st[(E + e - 1) * P]);
+        for (int c = 0; c < Cn; ++c) {
+            a.intens[(static_cast<size_t>(i) * Cn + c) * M + kloc] = st[(2 * E - 1 + c) * P];
+            a.hazard[(static_cast<size_t>(i) * Cn + c) * M + kloc] = st[(D + c) * P];
+        }
+        a.disc[static_cast<size_t>(i) * M + kloc] = exp(-st[(D + Cn) * P]);
+    };
+    store(0);
+    const double h = a.h, sqh = a.sqh;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int buf = c & 1;
+        bar_sync(1 + buf, NT);
+        const int tc = min(T, total_sub - c * T);
+        const double* zb = zbuf + buf * (T * D * P) + lane;
+        if (lane < P) {
+            for (int t = 0; t < tc; ++t) {
+                const double* zt = zb + t * D * P;
+                auto zcorr = [&](int d) {
+                    double acc = 0.0;
+                    for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
+                        acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
+                    return acc;
+                };
+                // Left-endpoint quadrature of -ln beta and the hazards (market.cpp:208-209).
+                const double r0 = st[0];
+                st[(D + Cn) * P] = dadd(st[(D + Cn) * P], dmul(r0, h));
+                for (int cc = 0; cc < Cn; ++cc)
+                    st[(D + cc) * P] = dadd(st[(D + cc) * P], dmul(st[(2 * E - 1 + cc) * P], h));
+                // log-FX first: it reads the pre-step rates (market.cpp:211-223).
+                for (int e = 1; e < E; ++e) {
+                    const FactorCoef k = coef[E + e - 1];  // {half_s2, sig_sqh}
+                    const double lc = st[(E + e - 1) * P];
+                    const double drift = dmul(dsub(dsub(r0, st[e * P]), k.c0), h);
+                    st[(E + e - 1) * P] = dadd(dadd(lc, drift), dmul(k.c1, zcorr(E + e - 1)));
+                }
+                for (int e = 0; e < E; ++e) {
+                    const FactorCoef k = coef[e];  // {a, b, quanto, sig_sqh}
+                    const double r = st[e * P];
+                    const double drift = dmul(dsub(dmul(k.c0, dsub(k.c1, r)), k.c2), h);
+                    st[e * P] = dadd(dadd(r, drift), dmul(k.c3, zcorr(e)));
+                }
+                for (int cc = 0; cc < Cn; ++cc) {
+                    const int f = 2 * E - 1 + cc;
+                    const FactorCoef k = coef[f];  // {alpha, delta, nu}
+                    const double gm = st[f * P];
+                    const double gp = (gm < 0.0) ? 0.0 : gm;
+                    const double drift = dmul(dmul(k.c0, dsub(k.c1, gp)), h);
+                    const double diff = dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(f));
+                    const double nx = dadd(dadd(gm, drift), diff);
+                    st[f * P] = (nx < 0.0) ? 0.0 : nx;
+                }
+                const int s_done = c * T + t + 1;
+                if (s_done % a.substeps == 0) store(s_done / a.substeps);
+            }
+        }
+        if (c + 2 < n_chunks) bar_arrive(3 + buf, NT);
+    }
+}
+
+// ------------------------------------------------------------------ K2
+struct MtmArgs {
+    int E, Cc, M, n_local, start, n_total, paths_per_group;
+    const double* lnA;   // [E][n_total+1]
+    const double* B;     // [E][n_total+1]
+    const double* Nsuf;  // [E][n_total+1][Cc]  sum notional, maturity >= j
+    const double* N;     // [E][n_total+1][Cc]  sum notional, maturity == j
+    const double* NSsuf; // [E][n_total+1][Cc]  sum notional*delta*Sigma, maturity >= j
+    const double* H;     // [E][n_total+1][Cc]  N[j] + NSsuf[j]
+    const double* rates;
+    const double* fx;
+    const double* lag0;  // [groups][E]
+    double* cube;
+};
+
+// Thread per (path, local step).  With every swap resetting each pricing step
+// (tenor == dt, the reference's generated books, portfolio.cpp:166), the book
+// collapses per (economy, client) onto maturity-indexed coefficient vectors:
+//   MtM_c = sum_e chi_e [ lead*Nsuf_g - N_g - [g>0] NSsuf_g - sum_{m>=1} Z_m H_{g+m} ]
+// with Z_m = exp(lnA_m - B_m r) the Vasicek ZC to g+m (portfolio.cpp:34-45),
+// lead = 1/ZC(r_lag, dt) for g > 0 and 1 at g = 0 (portfolio.cpp:65-92).
+// Cost per path: E*n^2/2 exponentials instead of the reference's O(S*n^2).
+template <int CB>
+__global__ void __launch_bounds__(128) k_mtm_linear(MtmArgs a) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (k >= a.M) return;
+    const int g = a.start + i;
+    const int M = a.M, E = a.E, Cc = a.Cc, n1 = a.n_total + 1;
+    for (int c0 = 0; c0 < Cc; c0 += CB) {
+        double acc[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+        for (int e = 0; e < E; ++e) {
+            const double r = a.rates[(static_cast<size_t>(i) * E + e) * M + k];
+            const double chi = (e == 0) ? 1.0 : a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + k];
+            const double* lnA = a.lnA + e * n1;
+            const double* B = a.B + e * n1;
+            double lead = 1.0;
+            if (g > 0) {
+                const double rl = (i > 0) ? a.rates[(static_cast<size_t>(i - 1) * E + e) * M + k]
+                                          : a.lag0[(k / a.paths_per_group) * E + e];
+                lead = 1.0 / exp(lnA[1] - B[1] * rl);
+            }
+            double v[CB];
+            const size_t base = (static_cast<size_t>(e) * n1 + g) * Cc + c0;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (c0 + c < Cc) {
+                    v[c] = lead * a.Nsuf[base + c] - a.N[base + c];
+                    if (g > 0) v[c] -= a.NSsuf[base + c];
+                } else {
+                    v[c] = 0.0;
+                }
+            }
+            for (int m = 1; g + m <= a.n_total; ++m) {
+                const double z = exp(lnA[m] - B[m] * r);
+                const double* h = a.H + (static_cast<size_t>(e) * n1 + g + m) * Cc + c0;
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (c0 + c < Cc) v[c] -= z * __ldg(h + c);
+            }
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[c] += chi * v[c];
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (c0 + c < Cc) a.cube[(static_cast<size_t>(i) * Cc + c0 + c) * M + k] = acc[c];
+    }
+}
+
+// Direct per-swap pricing in the reference's loop and summation order
+// (portfolio.cpp:58-147) for books that do not reset every pricing step.
+struct DirectArgs {
+    int E, Cc, M, n_local, start, n_swaps, paths_per_group;
+    double dt;
+    const hcva_swap* book;
+    const hcva_vasicek* vas;
+    const double* rates;
+    const double* fx;
+    const double* lag0;
+    double* cube;
+};
+
+__device__ double zc_dev(double r, double tau, const hcva_vasicek& p) {
+    if (tau == 0.0) return 1.0;
+    const double a = p.a, b = p.b, s = p.sigma;
+    if (fabs(a) < 1e-8) return exp(-r * tau + s * s * tau * tau * tau / 6.0);
+    const double B = (1.0 - exp(-a * tau)) / a;
+    const double lnA = (b - s * s / (2.0 * a * a)) * (B - tau) - s * s * B * B / (4.0 * a);
+    return exp(lnA - B * r);
+}
+
+__device__ bool is_multiple_dev(double x, double step) {
+    const double q = x / step;
+    return fabs(q - round(q)) < 1e-9 * fmax(1.0, fabs(q));
+}
+
+__global__ void __launch_bounds__(128) k_mtm_direct(DirectArgs a) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (k >= a.M) return;
+    const int E = a.E, M = a.M;
+    const int g = a.start + i;
+    const double t = g * a.dt;
+    for (int c = 0; c < a.Cc; ++c) a.cube[(static_cast<size_t>(i) * a.Cc + c) * M + k] = 0.0;
+    for (int s = 0; s < a.n_swaps; ++s) {
+        const hcva_swap sw = a.book[s];
+        if (t > sw.maturity + 1e-9) continue;
+        const hcva_vasicek vp = a.vas[sw.economy];
+        const double r_now = a.rates[(static_cast<size_t>(i) * E + sw.economy) * M + k];
+        const double delta = sw.tenor, tbar = sw.maturity, sr = sw.fixed_rate;
+        double px;
+        if (t < 1e-9) {
+            const int m = static_cast<int>(llround(tbar / delta));
+            double ann = 0.0;
+            for (int j = 1; j <= m; ++j) ann = __dadd_rn(ann, zc_dev(r_now, j * delta, vp));
+            px = 1.0 - zc_dev(r_now, tbar, vp) - delta * sr * ann;
+        } else {
+            const int lag = static_cast<int>(llround(sw.tenor / a.dt));
+            const int prev_global = ((g - 1) / lag) * lag;
+            const int prev_local = prev_global - a.start;
+            const double r_lag = (prev_local >= 0)
+                                     ? a.rates[(static_cast<size_t>(prev_local) * E + sw.economy) * M + k]
+                                     : a.lag0[(k / a.paths_per_group) * E + sw.economy];
+            const bool on_reset = is_multiple_dev(t, delta);
+            const int m_total = static_cast<int>(llround(tbar / delta));
+            const int j_first = on_reset ? static_cast<int>(llround(t / delta)) + 1
+                                         : static_cast<int>(floor(t / delta + 1e-9)) + 1;
+            double ann = 0.0;
+            for (int j = j_first; j <= m_total; ++j) ann = __dadd_rn(ann, zc_dev(r_now, j * delta - t, vp));
+            if (on_reset) {
+                px = 1.0 / zc_dev(r_lag, delta, vp) - zc_dev(r_now, tbar - t, vp) - delta * sr * (1.0 + ann);
+            } else {
+                const double t_prev = floor(t / delta + 1e-9) * delta;
+                const double t_next = t_prev + delta;
+                px = zc_dev(r_now, t_next - t, vp) / zc_dev(r_lag, t_next - t_prev, vp) -
+                     zc_dev(r_now, tbar - t, vp) - delta * sr * ann;
+            }
+        }
+        const double chi = (sw.economy == 0) ? 1.0 : a.fx[(static_cast<size_t>(i) * (E - 1) + sw.economy - 1) * M + k];
+        double* dst = a.cube + (static_cast<size_t>(i) * a.Cc + sw.client - 1) * M + k;
+        *dst = __dadd_rn(*dst, __dmul_rn(__dmul_rn(sw.notional, px), chi));
+    }
+}
+
+// ------------------------------------------------------------------ K3
+struct DefaultArgs {
+    int M, N, n, Cn, path_offset;
+    uint64_t key;
+    const double* hazard;  // SoA [(i*Cn+c)*M + k]
+    uint16_t* steps;       // [c][k*N+l]
+    unsigned long long* ties;  // [2]
+};
+
+// CTA per path: the path's cumulative hazards are staged in shared memory
+// and shared by its N replicas; each replica (k,l) draws one Exp(1)
+// threshold per name from split(k).split(l) (defaults.cpp:28-43) and finds
+// the first pricing step with Lambda >= eps by binary search over the
+// nondecreasing hazard path (identical to the reference's linear scan,
+// defaults.cpp:13-18).
+__global__ void __launch_bounds__(128) k_defaults(DefaultArgs a) {
+    extern __shared__ double hz[];  // [c][i]
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cn = a.Cn;
+    for (int t = threadIdx.x; t < n1 * Cn; t += blockDim.x) {
+        const int c = t / n1, i = t % n1;
+        hz[t] = a.hazard[(static_cast<size_t>(i) * Cn + c) * a.M + k];
+    }
+    __syncthreads();
+    const uint64_t pkey = split_key(a.key, static_cast<uint64_t>(a.path_offset) + k);
+    unsigned long long tie_ulp = 0, tie_rel = 0;
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
+        const uint64_t rkey = split_key(pkey, static_cast<uint64_t>(l));
+        const size_t row = static_cast<size_t>(k) * a.N + l;
+        uint64_t w0 = 0, w1 = 0;
+        for (int c = 0; c < Cn; ++c) {
+            if ((c & 1) == 0) philox2x64(static_cast<uint64_t>(c >> 1), rkey, w0, w1);
+            const double eps = -log(u64_to_uniform((c & 1) ? w1 : w0));
+            const double* h = hz + c * n1;
+            int lo = 0, hi = n1;  // first index in [0, n1) with h >= eps, n1 if none
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (h[mid] >= eps) hi = mid; else lo = mid + 1;
+            }
+            a.steps[c * R + row] = (lo < n1) ? static_cast<uint16_t>(lo) : static_cast<uint16_t>(0xFFFF);
+            // Threshold ties: a neighbouring hazard within 1 ulp / 1e-12 of eps.
+            const double ulp = fabs(nextafter(eps, 2.0 * eps + 1.0) - eps);
+            const double near_hi = (lo < n1) ? h[lo] - eps : INFINITY;
+            const double near_lo = (lo > 0) ? eps - h[lo - 1] : INFINITY;
+            const double gap = fmin(near_hi, near_lo);
+            if (gap <= ulp) ++tie_ulp;
+            if (gap <= 1e-12 * eps) ++tie_rel;
+        }
+    }
+    if (tie_ulp) atomicAdd(&a.ties[0], tie_ulp);
+    if (tie_rel) atomicAdd(&a.ties[1], tie_rel);
+}
+
+// ------------------------------------------------------------------ K4
+struct LabelArgs {
+    int M, N, n, Cn, E;
+    double dt;
+    const double* disc;
+    const double* intens;
+    const double* cube;      // SoA [(i*Cc + c-1)*M + k]
+    const uint16_t* steps;   // [c][R]
+    double* out;             // [i][R] for i in [i0, i1]
+    int i0, i1;
+};
+
+// Defaults labels (labels.cpp:21-48) for steps i0..i1 in one pass: CTA per
+// path, discounts and positive exposures staged in shared memory, thread per
+// replica.  Summation order is the reference's (clients ascending) and the
+// products are rounded as (beta_i^-1 * beta_s) * exposure.
+__global__ void __launch_bounds__(128) k_labels_defaults(LabelArgs a) {
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cc = a.Cn - 1;
+    double* disc = sm;             // [n1]
+    double* inv = sm + n1;         // [n1]
+    double* expo = sm + 2 * n1;    // [n1][Cc]
+    for (int t = threadIdx.x; t < n1; t += blockDim.x) {
+        disc[t] = a.disc[static_cast<size_t>(t) * a.M + k];
+        inv[t] = 1.0 / disc[t];
+    }
+    for (int t = threadIdx.x; t < n1 * Cc; t += blockDim.x) {
+        const int i = t / Cc, c = t % Cc;
+        const double v = a.cube[(static_cast<size_t>(i) * Cc + c) * a.M + k];
+        expo[t] = (v < 0.0) ? 0.0 : v;
+    }
+    __syncthreads();
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
+        const size_t row = static_cast<size_t>(k) * a.N + l;
+        for (int i = a.i0; i <= a.i1; ++i) {
+            double sum = 0.0;
+            for (int c = 1; c <= Cc; ++c) {
+                const int s = a.steps[c * R + row];
+                if (s > i && s <= a.n)
+                    sum = __dadd_rn(sum, __dmul_rn(__dmul_rn(inv[i], disc[s]), expo[s * Cc + c - 1]));
+            }
+            a.out[static_cast<size_t>(i - a.i0) * R + row] = sum;
+        }
+    }
+}
+
+// Intensity labels (labels.cpp:50-88).  Phase 1: survivor values per
+// (step, client) in the reference's loop order; phase 2: per replica sum over
+// surviving clients.
+__global__ void __launch_bounds__(128) k_labels_intensity(LabelArgs a) {
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cn = a.Cn, Cc = Cn - 1;
+    double* disc = sm;                 // [n1]
+    double* expo = sm + n1;            // [n1][Cc]
+    double* gam = expo + n1 * Cc;      // [n1][Cc]
+    double* sv = gam + n1 * Cc;        // [n1][Cc]
+    for (int t = threadIdx.x; t < n1; t += blockDim.x) disc[t] = a.disc[static_cast<size_t>(t) * a.M + k];
+    for (int t = threadIdx.x; t < n1 * Cc; t += blockDim.x) {
+        const int i = t / Cc, c = t % Cc;
+        const double v = a.cube[(static_cast<size_t>(i) * Cc + c) * a.M + k];
+        expo[t] = (v < 0.0) ? 0.0 : v;
+        gam[t] = a.intens[(static_cast<size_t>(i) * Cn + c + 1) * a.M + k];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < (a.i1 - a.i0 + 1) * Cc; t += blockDim.x) {
+        const int i = a.i0 + t / Cc, c = t % Cc;
+        const double inv = 1.0 / disc[i];
+        double acc = 0.0, gsum = 0.0;
+        for (int j = i; j <= a.n - 1; ++j) {
+            const double gj = gam[j * Cc + c];
+            const double term = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(inv, disc[j]), expo[j * Cc + c]), gj), a.dt);
+            acc = __dadd_rn(acc, __dmul_rn(term, exp(-gsum)));
+            gsum = __dadd_rn(gsum, __dmul_rn(gj, a.dt));
+        }
+        sv[i * Cc + c] = acc;
+    }
+    __syncthreads();
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
+        const size_t row = static_cast<size_t>(k) * a.N + l;
+        for (int i = a.i0; i <= a.i1; ++i) {
+            double sum = 0.0;
+            for (int c = 1; c <= Cc; ++c)
+                if (a.steps[c * R + row] > i) sum = __dadd_rn(sum, sv[i * Cc + c - 1]);
+            a.out[static_cast<size_t>(i - a.i0) * R + row] = sum;
+        }
+    }
+}
+
+// Feature rows of one step (labels.cpp:142-167), row-major R x (p+q).
+struct FeatureArgs {
+    int M, N, n, Cn, E, step, paths_per_group;
+    const double *rates, *fx, *intens, *lag0;
+    const uint16_t* steps;
+    double* out;
+};
+
+__global__ void k_features(FeatureArgs a) {
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    const size_t row = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (row >= R) return;
+    const int k = static_cast<int>(row / a.N);
+    const int E = a.E, Cn = a.Cn, M = a.M, i = a.step;
+    const int cols = (Cn - 1) + E + (E - 1) + (Cn - 1) + E;
+    double* o = a.out + row * cols;
+    int col = 0;
+    for (int c = 1; c < Cn; ++c) o[col++] = (a.steps[c * R + row] <= i) ? 1.0 : 0.0;
+    for (int e = 0; e < E; ++e) o[col++] = a.rates[(static_cast<size_t>(i) * E + e) * M + k];
+    for (int e = 1; e < E; ++e) o[col++] = a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + k];
+    for (int c = 1; c < Cn; ++c) o[col++] = a.intens[(static_cast<size_t>(i) * Cn + c) * M + k];
+    for (int e = 0; e < E; ++e)
+        o[col++] = (i == 0) ? a.lag0[(k / a.paths_per_group) * E + e]
+                            : a.rates[(static_cast<size_t>(i - 1) * E + e) * M + k];
+}
+
+// SoA [(i*F+f)*M + k] -> AoS [(k*(n1)+i)*F + f]
+__global__ void k_soa_to_aos(const double* in, double* out, int M, int n1, int F, int mode,
+                             const double* lag0, int E, int ppg) {
+    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const size_t total = static_cast<size_t>(M) * n1 * F;
+    if (t >= total) return;
+    const int f = static_cast<int>(t % F);
+    const size_t ki = t / F;
+    const int i = static_cast<int>(ki % n1), k = static_cast<int>(ki / n1);
+    double v;
+    if (mode == 1) {  // lagged rates derived from the rate block
+        v = (i == 0) ? lag0[(k / ppg) * E + f] : in[(static_cast<size_t>(i - 1) * F + f) * M + k];
+    } else {
+        v = in[(static_cast<size_t>(i) * F + f) * M + k];
+    }
+    out[t] = v;
+}
+
+__global__ void k_steps_to_aos(const uint16_t* in, uint16_t* out, size_t R, int Cn) {
+    const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (t >= R * Cn) return;
+    const int c = static_cast<int>(t % Cn);
+    const size_t r = t / Cn;
+    out[t] = in[c * R + r];
+}
+
+// Per-step mean of the labels: the CVA profile E[xi_i] (deterministic
+// fixed-order reduction; CTA per step).
+__global__ void __launch_bounds__(256) k_profile(const double* labels, size_t R, double* out) {
+    __shared__ double red[256];
+    const double* row = labels + blockIdx.x * R;
+    double s = 0.0;
+    for (size_t r = threadIdx.x; r < R; r += 256) s += row[r];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = red[0] / static_cast<double>(R);
+}
+
+// ================================================================= host side
+
+inline unsigned grid1(size_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+template <typename T>
+void stage(DeviceBuf& buf, const std::vector<T>& v) {
+    buf.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (!v.empty()) HCVA_CUDA(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+void check_launch(hcva_ctx* ctx) {
+    ctx->launches++;
+    HCVA_CUDA(cudaGetLastError());
+}
+
+constexpr int kP = 16, kG = 4;  // K1: paths per CTA, generator warps per CTA
+
+// Stage K1's tables: per-factor coefficients computed with the reference's
+// rounding (market.cpp:121-134, 214-216), the Cholesky factor as CSR (exact
+// zeros skipped: adding +-0 to the running sum is an identity), group states.
+void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys,
+                    const std::vector<double>& init_state, int paths_per_group, uint64_t local_offset) {
+    const Model& m = sim->model;
+    const int D = m.D, E = m.E, Cn = m.Cn;
+    const double h = m.dt / m.substeps;
+    const double sqh = std::sqrt(h);
+    std::vector<FactorCoef> coef(D);
+    for (int e = 0; e < E; ++e) {
+        const double q = (e == 0) ? 0.0 : m.fx[e - 1].rho * m.fx[e - 1].sigma * m.rates[e].sigma;
+        coef[e] = {m.rates[e].a, m.rates[e].b, q, m.rates[e].sigma * sqh};
+    }
+    for (int e = 1; e < E; ++e)
+        coef[E + e - 1] = {0.5 * m.fx[e - 1].sigma * m.fx[e - 1].sigma, m.fx[e - 1].sigma * sqh, 0, 0};
+    for (int c = 0; c < Cn; ++c) coef[2 * E - 1 + c] = {m.credit[c].alpha, m.credit[c].delta, m.credit[c].nu, 0};
+    std::vector<int> row(D + 1, 0), col;
+    std::vector<double> val;
+    for (int d = 0; d < D; ++d) {
+        for (int j = 0; j <= d; ++j) {
+            const double v = m.chol[static_cast<size_t>(d) * D + j];
+            if (v != 0.0) {
+                col.push_back(j);
+                val.push_back(v);
+            }
+        }
+        row[d + 1] = static_cast<int>(col.size());
+    }
+    sim->m_nnz = static_cast<int>(col.size());
+    stage(sim->m_coef, coef);
+    stage(sim->m_row, row);
+    stage(sim->m_col, col);
+    stage(sim->m_val, val);
+    stage(sim->m_init, init_state);
+    if (group_keys.size() > 1) stage(sim->m_keys, group_keys);
+    sim->m_ppg = paths_per_group;
+    sim->m_local_offset = local_offset;
+    // Chunk of T substeps: T*D even keeps chunks aligned to Philox blocks.
+    int T = 4;
+    if ((T * D) & 1) T += 1;
+    sim->m_T = T;
+    const size_t head = 4 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
+    sim->m_smem = sizeof(double) * (head + static_cast<size_t>(D + Cn + 1) * kP + 2 * static_cast<size_t>(T) * D * kP);
+    if (sim->m_smem > 227 * 1024) throw config_error("model too large for the diffusion kernel's shared memory");
+    if (sim->m_smem > 48 * 1024)
+        HCVA_CUDA(cudaFuncSetAttribute(k_market<kP, kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sim->m_smem)));
+    const Model& mm = sim->model;
+    const size_t n1 = sim->n + 1, M = sim->M;
+    sim->rates.alloc(sizeof(double) * n1 * mm.E * M);
+    sim->fx.alloc(sizeof(double) * n1 * std::max(mm.E - 1, 1) * M);
+    sim->intens.alloc(sizeof(double) * n1 * mm.Cn * M);
+    sim->hazard.alloc(sizeof(double) * n1 * mm.Cn * M);
+    sim->disc.alloc(sizeof(double) * n1 * M);
+}
+
+void launch_market(hcva_sim* sim, uint64_t key0) {
+    hcva_ctx* ctx = sim->ctx;
+    const Model& m = sim->model;
+    MarketArgs a{};
+    a.E = m.E; a.Cn = m.Cn; a.D = m.D; a.substeps = m.substeps; a.n_store = sim->n; a.M = sim->M;
+    a.T = sim->m_T; a.nnz = sim->m_nnz; a.paths_per_group = sim->m_ppg; a.local_offset = sim->m_local_offset;
+    a.h = m.dt / m.substeps; a.sqh = std::sqrt(a.h);
+    a.key0 = key0;
+    a.group_keys = sim->m_keys.p ? sim->m_keys.as<uint64_t>() : nullptr;
+    a.init_state = sim->m_init.as<double>(); a.coef = sim->m_coef.as<FactorCoef>();
+    a.chol_row = sim->m_row.as<int>(); a.chol_col = sim->m_col.as<int>(); a.chol_val = sim->m_val.as<double>();
+    a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.intens = sim->intens.as<double>();
+    a.hazard = sim->hazard.as<double>(); a.disc = sim->disc.as<double>();
+    k_market<kP, kG><<<grid1(sim->M, kP), 32 * (kG + 1), sim->m_smem, ctx->stream>>>(a);
+    check_launch(ctx);
+}
+
+// Stage K2's tables.  Linear (coefficient) form when every swap resets each
+// pricing step; the direct per-swap kernel otherwise (portfolio.cpp:97-147).
+void prepare_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps) {
+    const Model& m = sim->model;
+    if (!book || n_swaps < 1) throw contract_error("build_mtm_cube: empty book");
+    const int E = m.E, Cc = m.Cc, n_total = m.n_steps;
+    bool linear = true;
+    for (int s = 0; s < n_swaps; ++s) {
+        const hcva_swap& sw = book[s];
+        if (sw.client < 1 || sw.client > Cc) throw contract_error("build_mtm_cube: swap client out of range");
+        if (sw.economy < 0 || sw.economy >= E) throw contract_error("build_mtm_cube: swap economy out of range");
+        const double lag_d = sw.tenor / m.dt;
+        const int lag = static_cast<int>(std::llround(lag_d));
+        if (std::fabs(lag_d - lag) > 1e-9 || lag < 1)
+            throw config_error("build_mtm_cube: swap tenor must be a multiple of the pricing step");
+        if (sim->start_step > 0 && lag != 1)
+            throw contract_error("build_mtm_cube: conditional blocks require tenor == pricing step");
+        if (lag != 1 || !is_multiple(sw.maturity, sw.tenor)) linear = false;
+        if (sw.maturity > n_total * m.dt + 1e-9) linear = false;
+    }
+    sim->c_linear = linear;
+    sim->c_nswaps = n_swaps;
+    sim->cube.alloc(sizeof(double) * (sim->n + 1) * static_cast<size_t>(Cc) * sim->M);
+    if (!linear) {
+        stage(sim->c_book, std::vector<hcva_swap>(book, book + n_swaps));
+        stage(sim->c_vas, m.rates);
+        return;
+    }
+    const int n1 = n_total + 1;
+    std::vector<double> lnA(static_cast<size_t>(E) * n1), B(static_cast<size_t>(E) * n1);
+    for (int e = 0; e < E; ++e) {  // zc_price's A(tau), B(tau) at tau = j*dt (portfolio.cpp:34-45)
+        const hcva_vasicek& p = m.rates[e];
+        for (int j = 0; j < n1; ++j) {
+            const double tau = j * m.dt;
+            double b = 0.0, la = 0.0;
+            if (tau == 0.0) {
+            } else if (std::fabs(p.a) < 1e-8) {
+                b = tau;
+                la = p.sigma * p.sigma * tau * tau * tau / 6.0;
+            } else {
+                b = (1.0 - std::exp(-p.a * tau)) / p.a;
+                la = (p.b - p.sigma * p.sigma / (2.0 * p.a * p.a)) * (b - tau) - p.sigma * p.sigma * b * b / (4.0 * p.a);
+            }
+            lnA[e * n1 + j] = la;
+            B[e * n1 + j] = b;
+        }
+    }
+    const size_t tsz = static_cast<size_t>(E) * n1 * Cc;
+    std::vector<double> Nm(tsz, 0.0), NSm(tsz, 0.0), Nsuf(tsz, 0.0), NSsuf(tsz, 0.0), H(tsz, 0.0);
+    for (int s = 0; s < n_swaps; ++s) {
+        const hcva_swap& sw = book[s];
+        const int mat = static_cast<int>(std::llround(sw.maturity / sw.tenor));
+        const size_t idx = (static_cast<size_t>(sw.economy) * n1 + mat) * Cc + sw.client - 1;
+        Nm[idx] += sw.notional;
+        NSm[idx] += sw.notional * (sw.tenor * sw.fixed_rate);
+    }
+    for (int e = 0; e < E; ++e)
+        for (int c = 0; c < Cc; ++c) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int j = n1 - 1; j >= 0; --j) {
+                const size_t idx = (static_cast<size_t>(e) * n1 + j) * Cc + c;
+                a1 += Nm[idx];
+                a2 += NSm[idx];
+                Nsuf[idx] = a1;
+                NSsuf[idx] = a2;
+                H[idx] = Nm[idx] + a2;
+            }
+        }
+    stage(sim->c_lnA, lnA);
+    stage(sim->c_B, B);
+    stage(sim->c_Nsuf, Nsuf);
+    stage(sim->c_N, Nm);
+    stage(sim->c_NSsuf, NSsuf);
+    stage(sim->c_H, H);
+}
+
+void launch_cube(hcva_sim* sim) {
+    hcva_ctx* ctx = sim->ctx;
+    const Model& m = sim->model;
+    dim3 grid(grid1(sim->M, 128), sim->n + 1);
+    if (sim->c_linear) {
+        MtmArgs a{};
+        a.E = m.E; a.Cc = m.Cc; a.M = sim->M; a.n_local = sim->n; a.start = sim->start_step; a.n_total = m.n_steps;
+        a.paths_per_group = sim->M / sim->n_groups;
+        a.lnA = sim->c_lnA.as<double>(); a.B = sim->c_B.as<double>(); a.Nsuf = sim->c_Nsuf.as<double>();
+        a.N = sim->c_N.as<double>(); a.NSsuf = sim->c_NSsuf.as<double>(); a.H = sim->c_H.as<double>();
+        a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.lag0 = sim->lag0.as<double>();
+        a.cube = sim->cube.as<double>();
+        k_mtm_linear<8><<<grid, 128, 0, ctx->stream>>>(a);
+    } else {
+        DirectArgs a{};
+        a.E = m.E; a.Cc = m.Cc; a.M = sim->M; a.n_local = sim->n; a.start = sim->start_step; a.n_swaps = sim->c_nswaps;
+        a.paths_per_group = sim->M / sim->n_groups; a.dt = m.dt;
+        a.book = sim->c_book.as<hcva_swap>(); a.vas = sim->c_vas.as<hcva_vasicek>();
+        a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>();
+        a.lag0 = sim->lag0.as<double>(); a.cube = sim->cube.as<double>();
+        k_mtm_direct<<<grid, 128, 0, ctx->stream>>>(a);
+    }
+    check_launch(ctx);
+    sim->has_cube = true;
+}
+
+void prepare_defaults(hcva_sim* sim, int N) {
+    if (N < 1) throw contract_error("sample_default_block: n_replicas must be >= 1");
+    if (sim->n >= 0xFFFF) throw contract_error("sample_default_block: too many steps for uint16 storage");
+    sim->N = N;
+    const size_t R = static_cast<size_t>(sim->M) * N;
+    const size_t bytes = sizeof(uint16_t) * R * sim->model.Cn;
+    if (sim->steps.bytes != bytes) sim->steps.alloc(bytes);
+    if (!sim->ties.p) sim->ties.alloc(2 * sizeof(unsigned long long));
+    const size_t smem = sizeof(double) * (sim->n + 1) * sim->model.Cn;
+    if (smem > 227 * 1024) throw config_error("too many names x steps for the over-simulation kernel");
+    if (smem > 48 * 1024)
+        HCVA_CUDA(cudaFuncSetAttribute(k_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+}
+
+void launch_defaults(hcva_sim* sim, uint64_t key) {
+    hcva_ctx* ctx = sim->ctx;
+    HCVA_CUDA(cudaMemsetAsync(sim->ties.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    DefaultArgs a{};
+    a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = sim->model.Cn; a.path_offset = sim->path_offset; a.key = key;
+    a.hazard = sim->hazard.as<double>(); a.steps = sim->steps.as<uint16_t>();
+    a.ties = sim->ties.as<unsigned long long>();
+    const size_t smem = sizeof(double) * (sim->n + 1) * sim->model.Cn;
+    const int threads = std::min(128, ((sim->N + 31) / 32) * 32);
+    k_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
+    check_launch(ctx);
+    sim->has_defaults = true;
+    sim->labels_kind = -1;
+}
+
+void launch_labels(hcva_sim* sim, int kind, int i0, int i1, double* dev_out) {
+    hcva_ctx* ctx = sim->ctx;
+    if (!sim->has_defaults) throw contract_error("labels: no default block");
+    if (!sim->has_cube) throw contract_error("labels: no MtM cube");
+    if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+    if (i0 < 0 || i1 > sim->n || i0 > i1) throw contract_error("label step out of range");
+    const Model& m = sim->model;
+    LabelArgs a{};
+    a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = m.Cn; a.E = m.E; a.dt = m.dt;
+    a.disc = sim->disc.as<double>(); a.intens = sim->intens.as<double>(); a.cube = sim->cube.as<double>();
+    a.steps = sim->steps.as<uint16_t>(); a.out = dev_out; a.i0 = i0; a.i1 = i1;
+    const int n1 = sim->n + 1, Cc = m.Cc;
+    const int threads = std::min(128, ((sim->N + 31) / 32) * 32);
+    if (kind == 0) {
+        const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc);
+        if (smem > 48 * 1024)
+            HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        k_labels_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
+    } else {
+        const size_t smem = sizeof(double) * (n1 + 3 * static_cast<size_t>(n1) * Cc);
+        if (smem > 48 * 1024)
+            HCVA_CUDA(cudaFuncSetAttribute(k_labels_intensity, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        k_labels_intensity<<<sim->M, 128, smem, ctx->stream>>>(a);
+    }
+    check_launch(ctx);
+}
+
+void launch_labels_all(hcva_sim* sim, int kind) {
+    const size_t R = static_cast<size_t>(sim->M) * sim->N, bytes = R * (sim->n + 1) * sizeof(double);
+    if (sim->labels.bytes != bytes) sim->labels.alloc(bytes);
+    launch_labels(sim, kind, 0, sim->n, sim->labels.as<double>());
+    sim->labels_kind = kind;
+}
+
+void copy_out(hcva_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    HCVA_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+    HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+hcva_sim* new_sim(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid) {
+    if (!ctx) throw contract_error("null context");
+    HCVA_CUDA(cudaSetDevice(ctx->device));
+    auto sim = std::make_unique<hcva_sim>();
+    sim->ctx = ctx;
+    sim->model = make_model(model, grid);
+    return sim.release();
+}
+
+void record(hcva_sim* sim, int slot, int phase) {
+    if (slot < 0) return;
+    const size_t idx = static_cast<size_t>(slot) * 5 + phase;
+    while (sim->events.size() <= idx) {
+        cudaEvent_t e;
+        HCVA_CUDA(cudaEventCreate(&e));
+        sim->events.push_back(e);
+    }
+    HCVA_CUDA(cudaEventRecord(sim->events[idx], sim->ctx->stream));
+}
+
+}  // namespace hcva
+
+using namespace hcva;
+
+extern "C" {
+
+hcva_status hcva_ctx_create(int device, hcva_ctx** out) {
+    return guarded([&] {
+        int n = 0;
+        HCVA_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw contract_error("hcva_ctx_create: no such device");
+        HCVA_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        HCVA_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10 || prop.minor != 0)
+            throw cuda_error("libhcva_gpu.so is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
+                             std::to_string(prop.minor));
+        auto ctx = std::make_unique<hcva_ctx>();
+        ctx->device = device;
+        ctx->sm_count = prop.multiProcessorCount;
+        HCVA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        *out = ctx.release();
+    });
+}
+
+hcva_status hcva_ctx_destroy(hcva_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+hcva_status hcva_ctx_stream(hcva_ctx* ctx, void** stream_out) {
+    return guarded([&] { *stream_out = ctx->stream; });
+}
+
+hcva_status hcva_ctx_synchronize(hcva_ctx* ctx) {
+    return guarded([&] { HCVA_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+hcva_status hcva_ctx_launch_count(hcva_ctx* ctx, uint64_t* out) {
+    return guarded([&] { *out = ctx->launches; });
+}
+
+hcva_status hcva_rng_draw(hcva_ctx* ctx, uint64_t key, uint64_t start, size_t count, int kind, void* out) {
+    return guarded([&] {
+        if (kind < 0 || kind > 3) throw contract_error("hcva_rng_draw: kind must be 0..3");
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        DeviceBuf buf;
+        buf.alloc(count * 8);
+        if (count) {
+            k_draws<<<grid1(count, 256), 256, 0, ctx->stream>>>(key, start, count, kind, buf.p);
+            check_launch(ctx);
+            copy_out(ctx, out, buf.p, count * 8);
+        }
+    });
+}
+
+hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                              const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
+                              int n_replicas, uint64_t key_market, uint64_t key_defaults, hcva_sim** out) {
+    return guarded([&] {
+        if (!grid) throw contract_error("simulate_set: null grid");
+        if (n_paths < 1) throw contract_error("simulate_market: n_paths must be >= 1");
+        if (path_offset < 0) throw contract_error("simulate_set: negative path offset");
+        std::unique_ptr<hcva_sim> sim(new_sim(ctx, model, grid));
+        const Model& m = sim->model;
+        sim->M = n_paths;
+        sim->n = m.n_steps;
+        sim->path_offset = path_offset;
+        std::vector<double> init(m.D);
+        for (int e = 0; e < m.E; ++e) init[e] = m.rates[e].r0;
+        for (int e = 1; e < m.E; ++e) init[m.E + e - 1] = std::log(m.fx[e - 1].chi0);
+        for (int c = 0; c < m.Cn; ++c) init[2 * m.E - 1 + c] = m.credit[c].gamma0;
+        std::vector<double> lag0(m.E);
+        for (int e = 0; e < m.E; ++e) lag0[e] = m.rates[e].r0;
+        stage(sim->lag0, lag0);
+        prepare_market(sim.get(), {key_market}, init, n_paths + path_offset, static_cast<uint64_t>(path_offset));
+        if (n_replicas > 0) prepare_defaults(sim.get(), n_replicas);
+        if (book) prepare_cube(sim.get(), book, n_swaps);
+        launch_market(sim.get(), key_market);
+        if (n_replicas > 0) launch_defaults(sim.get(), key_defaults);
+        if (book) launch_cube(sim.get());
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = sim.release();
+    });
+}
+
+hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defaults, int labels_kind,
+                           int event_slot) {
+    return guarded([&] {
+        if (sim->start_step != 0 || sim->n_groups != 1) throw contract_error("rerun: outer blocks only");
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        record(sim, event_slot, 0);
+        launch_market(sim, key_market);
+        record(sim, event_slot, 1);
+        if (sim->N > 0) launch_defaults(sim, key_defaults);
+        record(sim, event_slot, 2);
+        if (sim->c_nswaps > 0) launch_cube(sim);
+        record(sim, event_slot, 3);
+        if (labels_kind >= 0) launch_labels_all(sim, labels_kind);
+        record(sim, event_slot, 4);
+    });
+}
+
+hcva_status hcva_sim_phase_times(hcva_sim* sim, int event_slot, float* ms) {
+    return guarded([&] {
+        const size_t base = static_cast<size_t>(event_slot) * 5;
+        if (event_slot < 0 || base + 4 >= sim->events.size()) throw contract_error("phase times: no such slot");
+        for (int p = 0; p < 4; ++p)
+            HCVA_CUDA(cudaEventElapsedTime(&ms[p], sim->events[base + p], sim->events[base + p + 1]));
+    });
+}
+
+hcva_status hcva_simulate_conditional(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                      const double* st_rates, const double* st_logfx, const double* st_intens,
+                                      const double* st_lagged, int start_step, int horizon, int n_inner,
+                                      uint64_t key, hcva_sim** out) {
+    return guarded([&] {
+        if (!grid) throw contract_error("simulate_conditional_market: null grid");
+        std::unique_ptr<hcva_sim> sim(new_sim(ctx, model, grid));
+        const Model& m = sim->model;
+        if (horizon < 0 || start_step < 0 || start_step + horizon > m.n_steps)
+            throw contract_error("simulate_conditional_market: horizon out of range");
+        if (n_inner < 1) throw contract_error("simulate_conditional_market: n_inner must be >= 1");
+        sim->M = n_inner;
+        sim->n = horizon;
+        sim->start_step = start_step;
+        std::vector<double> init(m.D);
+        for (int e = 0; e < m.E; ++e) init[e] = st_rates[e];
+        for (int e = 1; e < m.E; ++e) init[m.E + e - 1] = st_logfx[e - 1];
+        for (int c = 0; c < m.Cn; ++c) init[2 * m.E - 1 + c] = st_intens[c];
+        stage(sim->lag0, std::vector<double>(st_lagged, st_lagged + m.E));
+        prepare_market(sim.get(), {key}, init, n_inner, 0);
+        launch_market(sim.get(), key);
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = sim.release();
+    });
+}
+
+hcva_status hcva_sample_defaults(hcva_sim* sim, int n_replicas, uint64_t key) {
+    return guarded([&] {
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        prepare_defaults(sim, n_replicas);
+        launch_defaults(sim, key);
+        HCVA_CUDA(cudaStreamSynchronize(sim->ctx->stream));
+    });
+}
+
+hcva_status hcva_build_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps) {
+    return guarded([&] {
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        prepare_cube(sim, book, n_swaps);
+        launch_cube(sim);
+        HCVA_CUDA(cudaStreamSynchronize(sim->ctx->stream));
+    });
+}
+
+hcva_status hcva_sim_destroy(hcva_sim* sim) {
+    return guarded([&] {
+        if (!sim) return;
+        cudaSetDevice(sim->ctx->device);
+        cudaStreamSynchronize(sim->ctx->stream);
+        delete sim;
+    });
+}
+
+hcva_status hcva_sim_dims(const hcva_sim* sim, int* dims) {
+    return guarded([&] {
+        dims[0] = sim->M; dims[1] = sim->n; dims[2] = sim->model.E; dims[3] = sim->model.Cn;
+        dims[4] = sim->N; dims[5] = sim->start_step; dims[6] = sim->model.D; dims[7] = sim->model.substeps;
+    });
+}
+
+hcva_status hcva_sim_tie_counts(const hcva_sim* sim, uint64_t* counts) {
+    return guarded([&] {
+        if (!sim->has_defaults) throw contract_error("tie counts: no default block");
+        unsigned long long h[2];
+        HCVA_CUDA(cudaMemcpy(h, sim->ties.p, sizeof h, cudaMemcpyDeviceToHost));
+        counts[0] = h[0];
+        counts[1] = h[1];
+    });
+}
+
+hcva_status hcva_sim_export_market(const hcva_sim* sim, double* rates, double* fx, double* intens,
+                                   double* lagged, double* disc, double* hazard) {
+    return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const Model& m = sim->model;
+        const int n1 = sim->n + 1, M = sim->M, ppg = M / sim->n_groups;
+        DeviceBuf tmp;
+        auto conv = [&](const double* src, double* dst, int F, int mode) {
+            if (!dst || F == 0) return;
+            const size_t cnt = static_cast<size_t>(M) * n1 * F;
+            tmp.alloc(cnt * sizeof(double));
+            k_soa_to_aos<<<grid1(cnt, 256), 256, 0, ctx->stream>>>(src, tmp.as<double>(), M, n1, F, mode,
+                                                                   sim->lag0.as<double>(), m.E, ppg);
+            check_launch(ctx);
+            copy_out(ctx, dst, tmp.p, cnt * sizeof(double));
+        };
+        conv(sim->rates.as<double>(), rates, m.E, 0);
+        conv(sim->fx.as<double>(), fx, m.E - 1, 0);
+        conv(sim->intens.as<double>(), intens, m.Cn, 0);
+        conv(sim->rates.as<double>(), lagged, m.E, 1);
+        conv(sim->disc.as<double>(), disc, 1, 0);
+        conv(sim->hazard.as<double>(), hazard, m.Cn, 0);
+    });
+}
+
+hcva_status hcva_sim_export_defaults(const hcva_sim* sim, uint16_t* steps) {
+    return guarded([&] {
+        if (!sim->has_defaults) throw contract_error("export: no default block");
+        hcva_ctx* ctx = sim->ctx;
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const size_t R = static_cast<size_t>(sim->M) * sim->N, cnt = R * sim->model.Cn;
+        DeviceBuf tmp;
+        tmp.alloc(cnt * sizeof(uint16_t));
+        k_steps_to_aos<<<grid1(cnt, 256), 256, 0, ctx->stream>>>(sim->steps.as<uint16_t>(), tmp.as<uint16_t>(), R,
+                                                                 sim->model.Cn);
+        check_launch(ctx);
+        copy_out(ctx, steps, tmp.p, cnt * sizeof(uint16_t));
+    });
+}
+
+hcva_status hcva_sim_export_cube(const hcva_sim* sim, double* cube) {
+    return guarded([&] {
+        if (!sim->has_cube) throw contract_error("export: no MtM cube");
+        hcva_ctx* ctx = sim->ctx;
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const int n1 = sim->n + 1, M = sim->M, Cc = sim->model.Cc;
+        const size_t cnt = static_cast<size_t>(M) * n1 * Cc;
+        DeviceBuf tmp;
+        tmp.alloc(cnt * sizeof(double));
+        k_soa_to_aos<<<grid1(cnt, 256), 256, 0, ctx->stream>>>(sim->cube.as<double>(), tmp.as<double>(), M, n1, Cc, 0,
+                                                               nullptr, 0, 1);
+        check_launch(ctx);
+        copy_out(ctx, cube, tmp.p, cnt * sizeof(double));
+    });
+}
+
+hcva_status hcva_labels(hcva_sim* sim, int step, int kind, double* out) {
+    return guarded([&] {
+        if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        const size_t R = static_cast<size_t>(sim->M) * sim->N;
+        DeviceBuf tmp;
+        tmp.alloc(R * sizeof(double));
+        launch_labels(sim, kind, step, step, tmp.as<double>());
+        copy_out(sim->ctx, out, tmp.p, R * sizeof(double));
+    });
+}
+
+hcva_status hcva_labels_all(hcva_sim* sim, int kind, double* out) {
+    return guarded([&] {
+        if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        launch_labels_all(sim, kind);
+        if (out) copy_out(sim->ctx, out, sim->labels.p, sim->labels.bytes);
+    });
+}
+
+hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
+    return guarded([&] {
+        if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        if (sim->labels_kind != kind) launch_labels_all(sim, kind);
+        const size_t R = static_cast<size_t>(sim->M) * sim->N;
+        if (!sim->profile.p) sim->profile.alloc(sizeof(double) * (sim->n + 1));
+        k_profile<<<sim->n + 1, 256, 0, sim->ctx->stream>>>(sim->labels.as<double>(), R, sim->profile.as<double>());
+        check_launch(sim->ctx);
+        copy_out(sim->ctx, out, sim->profile.p, sizeof(double) * (sim->n + 1));
+    });
+}
+
+hcva_status hcva_features(hcva_sim* sim, int step, double* out) {
+    return guarded([&] {
+        if (!sim->has_defaults) throw contract_error("features: no default block");
+        if (step < 0 || step > sim->n) throw contract_error("label step out of range");
+        if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+        hcva_ctx* ctx = sim->ctx;
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const Model& m = sim->model;
+        const size_t R = static_cast<size_t>(sim->M) * sim->N;
+        const int cols = (m.Cn - 1) + m.E + (m.E - 1) + (m.Cn - 1) + m.E;
+        DeviceBuf tmp;
+        tmp.alloc(R * cols * sizeof(double));
+        FeatureArgs a{};
+        a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = m.Cn; a.E = m.E; a.step = step;
+        a.paths_per_group = sim->M / sim->n_groups;
+        a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.intens = sim->intens.as<double>();
+        a.lag0 = sim->lag0.as<double>(); a.steps = sim->steps.as<uint16_t>(); a.out = tmp.as<double>();
+        k_features<<<grid1(R, 128), 128, 0, ctx->stream>>>(a);
+        check_launch(ctx);
+        copy_out(ctx, out, tmp.p, R * cols * sizeof(double));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,408 @@
+"""Python surface of the engine, mirroring the reference's pybind module
+(proj/python/hiercva_module.cpp:45-180) on top of the C ABI.
+
+    import paper_2211_17005_b200 as hcva
+    cfg = hcva.load_config("paper_shape.json")
+    market, defaults, cube = hcva.simulate(cfg, paths, replicas)   # on the GPU
+    xi = hcva.defaults_label(step, cfg, market, defaults)          # (M, N)
+    f  = hcva.features(step, market, defaults)                     # (M*N, p+q)
+
+Everything below dispatches to libhcva_gpu.so; nothing here computes on the
+CPU beyond host-side bookkeeping.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from .config import PipelineConfig
+
+# Stream lineage keys of the pipeline phases (pipeline.hpp:26-31).
+K_BOOK, K_TRAIN_SIM, K_VALIDATION_SIM, K_ARD = 0, 1, 2, 3
+
+SWAP_DTYPE = np.dtype([("economy", "<i4"), ("client", "<i4"), ("notional", "<f8"),
+                       ("tenor", "<f8"), ("maturity", "<f8"), ("fixed_rate", "<f8")], align=True)
+
+
+class Context:
+    """One GPU, one CUDA stream (hcva_ctx)."""
+
+    def __init__(self, device: int = 0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        _lib.check(L.hcva_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _lib.check(_lib.lib().hcva_ctx_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self) -> None:
+        _lib.check(_lib.lib().hcva_ctx_synchronize(self.handle))
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        _lib.check(_lib.lib().hcva_ctx_launch_count(self.handle, C.byref(v)))
+        return v.value
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib().hcva_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ctx_lock = threading.Lock()
+_contexts: Dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    with _ctx_lock:
+        if device not in _contexts:
+            _contexts[device] = Context(device)
+        return _contexts[device]
+
+
+class RandomStream:
+    """Key-level mirror of hiercva::RandomStream (rng.hpp:16-52); draws run on the GPU."""
+
+    def __init__(self, seed: int = 0, _key: Optional[int] = None):
+        L = _lib.lib()
+        self.key = int(_key) if _key is not None else int(L.hcva_rng_root_key(seed))
+        self.pos = 0
+
+    def split(self, k: int) -> "RandomStream":
+        return RandomStream(_key=_lib.lib().hcva_rng_split_key(self.key, int(k)))
+
+    def _draw(self, n: int, kind: int, dtype) -> np.ndarray:
+        out = np.zeros(n, dtype=dtype)
+        if n:
+            _lib.check(_lib.lib().hcva_rng_draw(context().handle, self.key, self.pos, n, kind,
+                                                out.ctypes.data_as(C.c_void_p)))
+        self.pos += n
+        return out
+
+    def u64(self, n: int) -> np.ndarray:
+        return self._draw(n, 0, np.uint64)
+
+    def uniforms(self, n: int) -> np.ndarray:
+        return self._draw(n, 1, np.float64)
+
+    def normals(self, n: int) -> np.ndarray:
+        return self._draw(n, 2, np.float64)
+
+    def exponentials(self, n: int) -> np.ndarray:
+        return self._draw(n, 3, np.float64)
+
+
+def _swaps(book: np.ndarray):
+    book = np.ascontiguousarray(book, dtype=SWAP_DTYPE)
+    return book, book.ctypes.data_as(C.POINTER(_lib.Swap))
+
+
+def generate_book(cfg: PipelineConfig, stream: Optional[RandomStream] = None) -> np.ndarray:
+    """generate_book (portfolio.cpp:149-174) from root.split(kBook) by default."""
+    m, g = cfg.to_model()
+    key = stream.key if stream is not None else RandomStream(cfg.seed).split(K_BOOK).key
+    out = np.zeros(cfg.book_count, dtype=SWAP_DTYPE)
+    _lib.check(_lib.lib().hcva_generate_book(C.byref(m), C.byref(g), cfg.book_count,
+                                             cfg.notional_min, cfg.notional_max, key,
+                                             out.ctypes.data_as(C.POINTER(_lib.Swap))))
+    return out
+
+
+def load_book_csv(path: str, cfg: PipelineConfig) -> np.ndarray:
+    """load_book_csv (portfolio.cpp:176-212): economy,client,notional,tenor,maturity,rate|par."""
+    rows = []
+    with open(path) as f:
+        first = True
+        for line in f:
+            line = line.strip()
+            if not line:
+                continue
+            if first and line.startswith("economy"):
+                first = False
+                continue
+            first = False
+            parts = line.split(",")
+            if len(parts) < 6:
+                raise _lib.ConfigError(f"book: malformed row: {line}")
+            e, c = int(parts[0]), int(parts[1])
+            notional, tenor, maturity = float(parts[2]), float(parts[3]), float(parts[4])
+            if parts[5] == "par":
+                rate = par_rate(maturity, tenor, cfg.rates[e])
+            else:
+                rate = float(parts[5])
+            rows.append((e, c, notional, tenor, maturity, rate))
+    if not rows:
+        raise _lib.ConfigError(f"book: no swaps in {path}")
+    return np.array(rows, dtype=SWAP_DTYPE)
+
+
+def resolve_book(cfg: PipelineConfig) -> np.ndarray:  # pipeline.cpp:57-61
+    return load_book_csv(cfg.book_file, cfg) if cfg.book_file else generate_book(cfg)
+
+
+def par_rate(maturity: float, tenor: float, vasicek) -> float:
+    v = _lib.Vasicek(*map(float, vasicek))
+    out = C.c_double()
+    _lib.check(_lib.lib().hcva_par_rate(maturity, tenor, C.byref(v), C.byref(out)))
+    return out.value
+
+
+def zc_price(r: float, tau: float, vasicek) -> float:
+    v = _lib.Vasicek(*map(float, vasicek))
+    out = C.c_double()
+    _lib.check(_lib.lib().hcva_zc_price(r, tau, C.byref(v), C.byref(out)))
+    return out.value
+
+
+def cholesky(cfg: PipelineConfig) -> np.ndarray:
+    m, _ = cfg.to_model()
+    d = cfg.n_factors
+    out = np.zeros((d, d))
+    _lib.check(_lib.lib().hcva_cholesky(C.byref(m), out.ctypes.data_as(_lib.dptr)))
+    return out
+
+
+class SimulationSet:
+    """A simulated (market, defaults, cube) set resident on the GPU (hcva_sim).
+
+    The three reference objects (MarketBlock, DefaultBlock, MtMCube) are views of
+    this one handle: `market`, `defaults` and `cube` all return self so that
+    `market, defaults, cube = simulate(...)` reads like the reference API.
+    """
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+        dims = (C.c_int * 8)()
+        _lib.check(_lib.lib().hcva_sim_dims(handle, dims))
+        (self.n_paths, self.n_steps, self.n_economies, self.n_credit, self.n_replicas,
+         self.start_step, self.n_factors, self.substeps) = list(dims)
+        self._market = None
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().hcva_sim_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    @property
+    def n_clients(self) -> int:
+        return self.n_credit - 1
+
+    # -- exports in the reference's AoS layouts --------------------------
+    def market_arrays(self) -> Dict[str, np.ndarray]:
+        if self._market is None:
+            M, n1, E, Cn = self.n_paths, self.n_steps + 1, self.n_economies, self.n_credit
+            out = dict(rates=np.zeros((M, n1, E)), fx=np.zeros((M, n1, E - 1)),
+                       intens=np.zeros((M, n1, Cn)), lagged=np.zeros((M, n1, E)),
+                       disc=np.zeros((M, n1)), hazard=np.zeros((M, n1, Cn)))
+            p = lambda a: a.ctypes.data_as(C.c_void_p) if a.size else None  # noqa: E731
+            _lib.check(_lib.lib().hcva_sim_export_market(
+                self.handle, p(out["rates"]), p(out["fx"]), p(out["intens"]), p(out["lagged"]),
+                p(out["disc"]), p(out["hazard"])))
+            self._market = out
+        return self._market
+
+    def default_steps(self) -> np.ndarray:
+        out = np.zeros((self.n_paths, self.n_replicas, self.n_credit), dtype=np.uint16)
+        _lib.check(_lib.lib().hcva_sim_export_defaults(self.handle, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def cube_values(self) -> np.ndarray:
+        out = np.zeros((self.n_paths, self.n_steps + 1, self.n_clients))
+        _lib.check(_lib.lib().hcva_sim_export_cube(self.handle, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def tie_counts(self) -> Tuple[int, int]:
+        out = (C.c_uint64 * 2)()
+        _lib.check(_lib.lib().hcva_sim_tie_counts(self.handle, out))
+        return int(out[0]), int(out[1])
+
+    # -- reference accessors (MarketBlock / DefaultBlock / MtMCube) --------
+    def rate(self, k, i, e):
+        return self.market_arrays()["rates"][k, i, e]
+
+    def fx(self, k, i, e):
+        return 1.0 if e == 0 else self.market_arrays()["fx"][k, i, e - 1]
+
+    def intensity(self, k, i, c):
+        return self.market_arrays()["intens"][k, i, c]
+
+    def lagged_rate(self, k, i, e):
+        return self.market_arrays()["lagged"][k, i, e]
+
+    def discount(self, k, i):
+        return self.market_arrays()["disc"][k, i]
+
+    def hazard(self, k, i, c):
+        return self.market_arrays()["hazard"][k, i, c]
+
+    def default_step(self, k, l, c):
+        return int(self.default_steps()[k, l, c])
+
+    def indicator(self, k, l, i, c):
+        return self.default_step(k, l, c) <= i
+
+    def at(self, k, i, client):
+        return self.cube_values()[k, i, client - 1]
+
+    def state_at(self, k: int, i: int) -> Dict[str, np.ndarray]:
+        """MarketState at (k, i) (market.cpp:100-113)."""
+        mk = self.market_arrays()
+        return dict(rates=mk["rates"][k, i].copy(), log_fx=np.log(mk["fx"][k, i]),
+                    intens=mk["intens"][k, i].copy(), lagged=mk["lagged"][k, i].copy())
+
+    # -- labels and features -------------------------------------------
+    def labels(self, step: int, kind: str = "defaults") -> np.ndarray:
+        out = np.zeros((self.n_paths, self.n_replicas))
+        _lib.check(_lib.lib().hcva_labels(self.handle, step, _kind(kind), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def labels_all(self, kind: str = "defaults", to_host: bool = True) -> Optional[np.ndarray]:
+        if not to_host:
+            _lib.check(_lib.lib().hcva_labels_all(self.handle, _kind(kind), None))
+            return None
+        out = np.zeros((self.n_steps + 1, self.n_paths, self.n_replicas))
+        _lib.check(_lib.lib().hcva_labels_all(self.handle, _kind(kind), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def cva_profile(self, kind: str = "defaults") -> np.ndarray:
+        """E[xi_i] for i = 0..n (mean label per step; out[0] = time-0 CVA)."""
+        out = np.zeros(self.n_steps + 1)
+        _lib.check(_lib.lib().hcva_cva_profile(self.handle, _kind(kind), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def rerun(self, stream: "RandomStream", labels: Optional[str] = "defaults", event_slot: int = -1) -> None:
+        """Asynchronous in-place re-simulation with new keys (stream.split(0/1))."""
+        kind = -1 if labels is None else _kind(labels)
+        _lib.check(_lib.lib().hcva_sim_rerun(self.handle, stream.split(0).key, stream.split(1).key, kind,
+                                             event_slot))
+        self._market = None
+
+    def phase_times(self, event_slot: int) -> np.ndarray:
+        ms = (C.c_float * 4)()
+        _lib.check(_lib.lib().hcva_sim_phase_times(self.handle, event_slot, ms))
+        return np.array(list(ms))
+
+    def features(self, step: int) -> np.ndarray:
+        E, Cn = self.n_economies, self.n_credit
+        cols = (Cn - 1) + E + (E - 1) + (Cn - 1) + E
+        out = np.zeros((self.n_paths * self.n_replicas, cols))
+        _lib.check(_lib.lib().hcva_features(self.handle, step, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+def _kind(kind: str) -> int:
+    if kind == "defaults":
+        return 0
+    if kind == "intensity":
+        return 1
+    raise _lib.ConfigError("label_kind must be 'defaults' or 'intensity'")
+
+
+def simulate_set(cfg: PipelineConfig, book: Optional[np.ndarray], n_paths: int, n_replicas: int,
+                 stream: RandomStream, path_offset: int = 0, ctx: Optional[Context] = None
+                 ) -> SimulationSet:
+    """simulate_set (pipeline.cpp:63-70): market from stream.split(0), defaults from stream.split(1)."""
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    h = C.c_void_p()
+    if book is not None:
+        bk, bp = _swaps(book)
+        nsw = len(bk)
+    else:
+        bp, nsw = None, 0
+    _lib.check(_lib.lib().hcva_simulate_set(ctx.handle, C.byref(m), C.byref(g), bp, nsw, n_paths,
+                                            path_offset, n_replicas, stream.split(0).key,
+                                            stream.split(1).key, C.byref(h)))
+    return SimulationSet(h, ctx)
+
+
+def simulate_market(cfg: PipelineConfig, n_paths: int, stream: RandomStream,
+                    ctx: Optional[Context] = None) -> SimulationSet:
+    """simulate_market (market.cpp:161-234): path k draws from stream.split(k)."""
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    h = C.c_void_p()
+    _lib.check(_lib.lib().hcva_simulate_set(ctx.handle, C.byref(m), C.byref(g), None, 0, n_paths, 0,
+                                            0, stream.key, 0, C.byref(h)))
+    return SimulationSet(h, ctx)
+
+
+def simulate_conditional_market(cfg: PipelineConfig, state: Dict[str, np.ndarray], start_step: int,
+                                horizon: int, n_inner: int, stream: RandomStream,
+                                ctx: Optional[Context] = None) -> SimulationSet:
+    """simulate_conditional_market (market.cpp:236-310): inner path l draws from stream.split(l)."""
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    st = [np.ascontiguousarray(state[k], dtype=np.float64) for k in ("rates", "log_fx", "intens", "lagged")]
+    if st[1].size == 0:
+        st[1] = np.zeros(1)
+    h = C.c_void_p()
+    _lib.check(_lib.lib().hcva_simulate_conditional(
+        ctx.handle, C.byref(m), C.byref(g), *[a.ctypes.data_as(_lib.dptr) for a in st], start_step,
+        horizon, n_inner, stream.key, C.byref(h)))
+    return SimulationSet(h, ctx)
+
+
+def sample_default_block(sim: SimulationSet, n_replicas: int, stream: RandomStream) -> SimulationSet:
+    """sample_default_block (defaults.cpp:20-45) on a simulated market, in place."""
+    _lib.check(_lib.lib().hcva_sample_defaults(sim.handle, n_replicas, stream.key))
+    sim.n_replicas = n_replicas
+    return sim
+
+
+def build_mtm_cube(sim: SimulationSet, book: np.ndarray) -> SimulationSet:
+    """build_mtm_cube (portfolio.cpp:97-147) on a simulated market, in place."""
+    bk, bp = _swaps(book)
+    _lib.check(_lib.lib().hcva_build_cube(sim.handle, bp, len(bk)))
+    return sim
+
+
+# ---- pybind-surface mirror (hiercva_module.cpp:99-139) ---------------------
+
+def simulate(cfg: PipelineConfig, paths: int = 0, replicas: int = 0):
+    """hiercva.simulate: (market, defaults, cube) from root.split(kTrainSim)."""
+    book = resolve_book(cfg)
+    sim = simulate_set(cfg, book, paths if paths > 0 else cfg.paths,
+                       replicas if replicas > 0 else cfg.replicas,
+                       RandomStream(cfg.seed).split(K_TRAIN_SIM))
+    sim.book = book
+    return sim, sim, sim
+
+
+def _ensure_cube(cfg: PipelineConfig, sim: SimulationSet) -> None:
+    if getattr(sim, "book", None) is None:
+        sim.book = resolve_book(cfg)
+        build_mtm_cube(sim, sim.book)
+
+
+def defaults_label(step: int, cfg: PipelineConfig, market: SimulationSet, defaults=None) -> np.ndarray:
+    _ensure_cube(cfg, market)
+    return market.labels(step, "defaults")
+
+
+def intensity_label(step: int, cfg: PipelineConfig, market: SimulationSet, defaults=None) -> np.ndarray:
+    _ensure_cube(cfg, market)
+    return market.labels(step, "intensity")
+
+
+def features(step: int, market: SimulationSet, defaults=None) -> np.ndarray:
+    return market.features(step)

@@ -1,0 +1,82 @@
+"""Shared parity cases (reference JSON schema, proj/src/config.cpp:46-172).
+
+C1 / C2 follow SURVEY.md section 8d: C1 = economy 0 and clients 1-2 of
+configs/desk.json with the desk bank, 10 swaps, n=50, sub=25; C2 =
+configs/paper_shape.json with quarterly steps.
+"""
+import copy
+import json
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _load(name):
+    with open(os.path.join(ROOT, "configs", name)) as f:
+        return json.load(f)
+
+
+def _desk_corr():
+    """A dense PSD Brownian correlation for the desk model (D = 2*3-1+5 = 10),
+    with the pinned (r_e, chi_e) entries equal to rho_e (market.cpp:39-46)."""
+    d = 10
+    rng = np.random.default_rng(123)
+    a = rng.standard_normal((d, 3 * d))
+    c = a @ a.T
+    s = np.sqrt(np.diag(c))
+    c = c / np.outer(s, s) * 0.35
+    np.fill_diagonal(c, 1.0)
+    c[1, 3] = c[3, 1] = -0.25   # (r_1, chi_1) = rho_1
+    c[2, 4] = c[4, 2] = 0.30    # (r_2, chi_2) = rho_2
+    w = np.linalg.eigvalsh(c)
+    assert w.min() > 0.05
+    return c.tolist()
+
+
+def case(name):
+    if name == "minimal":
+        j = _load("minimal.json")
+        j["simulation"] = {"paths": 64, "replicas": 2}
+        return j
+    if name == "c1":
+        desk = _load("desk.json")
+        j = copy.deepcopy(desk)
+        j["model"]["economies"] = desk["model"]["economies"][:1]
+        j["model"]["clients"] = desk["model"]["clients"][:2]
+        j["grid"] = {"pricing_steps": 50, "substeps": 25, "dt_years": 1.0}
+        j["book"] = {"generate": {"count": 10, "notional_min": 1.0, "notional_max": 25.0}}
+        j["simulation"] = {"paths": 1024, "replicas": 16}
+        j["training"]["width"] = 32
+        return j
+    if name == "desk_corr":
+        j = _load("desk.json")
+        j["model"]["brownian_correlation"] = _desk_corr()
+        j["grid"] = {"pricing_steps": 12, "substeps": 4, "dt_years": 0.5}
+        j["simulation"] = {"paths": 40, "replicas": 8}
+        return j
+    if name == "c2":
+        j = _load("paper_shape.json")
+        j["grid"] = {"pricing_steps": 100, "substeps": 25, "dt_years": 0.25}
+        j["simulation"] = {"paths": 16384, "replicas": 128}
+        return j
+    if name == "c2_annual":
+        j = case("c2")
+        j["grid"]["dt_years"] = 1.0
+        return j
+    raise KeyError(name)
+
+
+def text(name, **sim):
+    j = case(name)
+    if sim:
+        j["simulation"] = dict(j["simulation"], **sim)
+    return json.dumps(j)
+
+
+def oracle_model(cfg):
+    """PipelineConfig -> the dict taken by tests/oracle_api.py."""
+    return dict(rates=cfg.rates, fx=cfg.fx, credit=cfg.credit,
+                corr=None if cfg.correlation is None else cfg.correlation,
+                n_steps=cfg.n_steps, substeps=cfg.substeps, dt=cfg.dt)

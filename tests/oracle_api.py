@@ -1,0 +1,277 @@
+"""ctypes bindings for the CPU oracle libraries -- TEST INFRASTRUCTURE ONLY.
+
+Loads either the plain-C restatement (oracle/liboracle.so) or the compiled
+reference (oracle/_ref/libhcva_ref.so); both export the C interface declared in
+oracle/hcva_oracle.h.  Used only by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+RESTATEMENT = os.path.join(ORACLE_DIR, "liboracle.so")
+REFERENCE = os.path.join(ORACLE_DIR, "_ref", "libhcva_ref.so")
+
+_u64 = C.c_uint64
+_dp = C.POINTER(C.c_double)
+
+
+class OrModel(C.Structure):
+    _fields_ = [
+        ("n_economies", C.c_int),
+        ("n_clients", C.c_int),
+        ("rates", _dp),
+        ("fx", _dp),
+        ("credit", _dp),
+        ("corr", _dp),
+        ("n_steps", C.c_int),
+        ("substeps", C.c_int),
+        ("dt", C.c_double),
+    ]
+
+
+SWAP_DTYPE = np.dtype(
+    [("economy", "<i4"), ("client", "<i4"), ("notional", "<f8"), ("tenor", "<f8"),
+     ("maturity", "<f8"), ("fixed_rate", "<f8")],
+    align=True,
+)
+
+
+def build():
+    """Compile the restatement (and, where /root/reference exists, the reference)."""
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+def _ptr(a, ctype=C.c_double):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class Oracle:
+    """One oracle library (restatement or compiled reference)."""
+
+    def __init__(self, path=RESTATEMENT):
+        if not os.path.exists(path):
+            build()
+        self.path = path
+        self.lib = C.CDLL(path)
+        L = self.lib
+        L.or_last_error.restype = C.c_char_p
+        L.or_root_key.restype = _u64
+        L.or_root_key.argtypes = [_u64]
+        L.or_split_key.restype = _u64
+        L.or_split_key.argtypes = [_u64, _u64]
+        for name in ("or_uniforms", "or_normals", "or_exponentials"):
+            getattr(L, name).argtypes = [_u64, _u64, C.c_size_t, _dp]
+        L.or_draw_u64.argtypes = [_u64, _u64, C.c_size_t, C.POINTER(_u64)]
+        L.or_inverse_normal_cdf.restype = C.c_double
+        L.or_inverse_normal_cdf.argtypes = [C.c_double]
+        self._keep = []
+
+    # -- helpers ---------------------------------------------------------
+    def _check(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self.lib.or_last_error().decode())
+
+    def model(self, m):
+        """m: dict with rates (E,4), fx (E-1,3), credit (Cc+1,4), corr or None, grid."""
+        rates = np.ascontiguousarray(m["rates"], dtype=np.float64)
+        fx = np.ascontiguousarray(m["fx"], dtype=np.float64).reshape(-1)
+        if fx.size == 0:
+            fx = np.zeros(1)
+        credit = np.ascontiguousarray(m["credit"], dtype=np.float64)
+        corr = m.get("corr")
+        corr = None if corr is None else np.ascontiguousarray(corr, dtype=np.float64)
+        self._keep = [rates, fx, credit, corr]
+        return OrModel(rates.shape[0], credit.shape[0] - 1, _ptr(rates), _ptr(fx), _ptr(credit),
+                       _ptr(corr) if corr is not None else _dp(), m["n_steps"], m["substeps"],
+                       m["dt"])
+
+    # -- RNG -------------------------------------------------------------
+    def key(self, seed, *lineage):
+        k = self.lib.or_root_key(seed)
+        for x in lineage:
+            k = self.lib.or_split_key(k, x)
+        return k
+
+    def split(self, key, k):
+        return self.lib.or_split_key(key, k)
+
+    def u64(self, key, start, count):
+        out = np.zeros(count, dtype=np.uint64)
+        self.lib.or_draw_u64(key, start, count, _ptr(out, _u64))
+        return out
+
+    def uniforms(self, key, start, count):
+        out = np.zeros(count)
+        self.lib.or_uniforms(key, start, count, _ptr(out))
+        return out
+
+    def normals(self, key, start, count):
+        out = np.zeros(count)
+        self.lib.or_normals(key, start, count, _ptr(out))
+        return out
+
+    def exponentials(self, key, start, count):
+        out = np.zeros(count)
+        self.lib.or_exponentials(key, start, count, _ptr(out))
+        return out
+
+    # -- simulation ------------------------------------------------------
+    def simulate_market(self, m, n_paths, key):
+        E, Cn, n = len(m["rates"]), len(m["credit"]), m["n_steps"]
+        rows = n_paths * (n + 1)
+        out = dict(rates=np.zeros((n_paths, n + 1, E)), fx=np.zeros((n_paths, n + 1, max(E - 1, 0))),
+                   intens=np.zeros((n_paths, n + 1, Cn)), lagged=np.zeros((n_paths, n + 1, E)),
+                   disc=np.zeros((n_paths, n + 1)), hazard=np.zeros((n_paths, n + 1, Cn)))
+        fxbuf = out["fx"] if E > 1 else np.zeros(rows)
+        mm = self.model(m)
+        self._check(self.lib.or_simulate_market(
+            C.byref(mm), n_paths, _u64(key), _ptr(out["rates"]), _ptr(fxbuf), _ptr(out["intens"]),
+            _ptr(out["lagged"]), _ptr(out["disc"]), _ptr(out["hazard"])))
+        return out
+
+    def simulate_conditional(self, m, state, start_step, horizon, n_inner, key):
+        E, Cn = len(m["rates"]), len(m["credit"])
+        rows = n_inner * (horizon + 1)
+        out = dict(rates=np.zeros((n_inner, horizon + 1, E)),
+                   fx=np.zeros((n_inner, horizon + 1, max(E - 1, 0))),
+                   intens=np.zeros((n_inner, horizon + 1, Cn)),
+                   lagged=np.zeros((n_inner, horizon + 1, E)), disc=np.zeros((n_inner, horizon + 1)),
+                   hazard=np.zeros((n_inner, horizon + 1, Cn)))
+        fxbuf = out["fx"] if E > 1 else np.zeros(rows)
+        st = [np.ascontiguousarray(state[k], dtype=np.float64)
+              for k in ("rates", "log_fx", "intens", "lagged")]
+        if st[1].size == 0:
+            st[1] = np.zeros(1)
+        mm = self.model(m)
+        self._check(self.lib.or_simulate_conditional(
+            C.byref(mm), _ptr(st[0]), _ptr(st[1]), _ptr(st[2]), _ptr(st[3]), start_step, horizon,
+            n_inner, _u64(key), _ptr(out["rates"]), _ptr(fxbuf), _ptr(out["intens"]),
+            _ptr(out["lagged"]), _ptr(out["disc"]), _ptr(out["hazard"])))
+        return out
+
+    def sample_defaults(self, hazard, n_replicas, key):
+        M, n1, Cn = hazard.shape
+        hz = np.ascontiguousarray(hazard)
+        out = np.zeros((M, n_replicas, Cn), dtype=np.uint16)
+        self._check(self.lib.or_sample_defaults(M, n1 - 1, Cn, _ptr(hz), n_replicas, _u64(key),
+                                                _ptr(out, C.c_uint16)))
+        return out
+
+    def zc_price(self, r, tau, v):
+        v = np.asarray(v, dtype=np.float64)
+        out = C.c_double()
+        self._check(self.lib.or_zc_price(C.c_double(r), C.c_double(tau), _ptr(v), C.byref(out)))
+        return out.value
+
+    def par_rate(self, maturity, tenor, v):
+        v = np.asarray(v, dtype=np.float64)
+        out = C.c_double()
+        self._check(self.lib.or_par_rate(C.c_double(maturity), C.c_double(tenor), _ptr(v),
+                                         C.byref(out)))
+        return out.value
+
+    def generate_book(self, m, count, nmin, nmax, key):
+        out = np.zeros(count, dtype=SWAP_DTYPE)
+        mm = self.model(m)
+        self._check(self.lib.or_generate_book(C.byref(mm), count, C.c_double(nmin),
+                                              C.c_double(nmax), _u64(key), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def build_cube(self, m, market, book, start_step=0):
+        rates = np.ascontiguousarray(market["rates"])
+        M, n1, E = rates.shape
+        fx = np.ascontiguousarray(market["fx"]) if E > 1 else np.zeros(M * n1)
+        lagged = np.ascontiguousarray(market["lagged"])
+        Cc = len(m["credit"]) - 1
+        cube = np.zeros((M, n1, Cc))
+        book = np.ascontiguousarray(book, dtype=SWAP_DTYPE)
+        mm = self.model(m)
+        self._check(self.lib.or_build_cube(C.byref(mm), M, n1 - 1, start_step, _ptr(rates),
+                                           _ptr(fx), _ptr(lagged), book.ctypes.data_as(C.c_void_p),
+                                           len(book), _ptr(cube)))
+        return cube
+
+    def _label(self, fn, step, market, steps, cube, dt):
+        disc = np.ascontiguousarray(market["disc"])
+        intens = np.ascontiguousarray(market["intens"])
+        M, n1 = disc.shape
+        E = market["rates"].shape[2]
+        Cn = intens.shape[2]
+        N = steps.shape[1]
+        out = np.zeros((M, N))
+        st = np.ascontiguousarray(steps, dtype=np.uint16)
+        cb = np.ascontiguousarray(cube)
+        self._check(fn(int(step), M, n1 - 1, E, Cn, N, C.c_double(dt), _ptr(disc), _ptr(intens),
+                       _ptr(st, C.c_uint16), _ptr(cb), _ptr(out)))
+        return out
+
+    def defaults_label(self, step, market, steps, cube, dt):
+        return self._label(self.lib.or_defaults_label, step, market, steps, cube, dt)
+
+    def intensity_label(self, step, market, steps, cube, dt):
+        return self._label(self.lib.or_intensity_label, step, market, steps, cube, dt)
+
+    def features(self, step, market, steps):
+        rates = np.ascontiguousarray(market["rates"])
+        M, n1, E = rates.shape
+        fx = np.ascontiguousarray(market["fx"]) if E > 1 else np.zeros(M * n1)
+        intens = np.ascontiguousarray(market["intens"])
+        lagged = np.ascontiguousarray(market["lagged"])
+        Cn = intens.shape[2]
+        N = steps.shape[1]
+        cols = (Cn - 1) + E + (E - 1) + (Cn - 1) + E
+        out = np.zeros((M * N, cols))
+        st = np.ascontiguousarray(steps, dtype=np.uint16)
+        self._check(self.lib.or_features(int(step), M, n1 - 1, E, Cn, N, _ptr(rates), _ptr(fx),
+                                         _ptr(intens), _ptr(lagged), _ptr(st, C.c_uint16),
+                                         _ptr(out)))
+        return out
+
+    def nested_cva(self, m, book, state, survived, step, inner, key):
+        st = [np.ascontiguousarray(state[k], dtype=np.float64)
+              for k in ("rates", "log_fx", "intens", "lagged")]
+        if st[1].size == 0:
+            st[1] = np.zeros(1)
+        surv = np.ascontiguousarray(survived, dtype=np.int32)
+        book = np.ascontiguousarray(book, dtype=SWAP_DTYPE)
+        v, se = C.c_double(), C.c_double()
+        mm = self.model(m)
+        self._check(self.lib.or_nested_cva(C.byref(mm), book.ctypes.data_as(C.c_void_p), len(book),
+                                           _ptr(st[0]), _ptr(st[1]), _ptr(st[2]), _ptr(st[3]),
+                                           _ptr(surv, C.c_int), int(step), int(inner), _u64(key),
+                                           C.byref(v), C.byref(se)))
+        return v.value, se.value
+
+
+_cache = {}
+
+
+def restatement():
+    if "r" not in _cache:
+        _cache["r"] = Oracle(RESTATEMENT)
+    return _cache["r"]
+
+
+def reference():
+    """The compiled reference, or None where /root/reference was never built."""
+    if "ref" not in _cache:
+        if not os.path.exists(REFERENCE):
+            try:
+                build()
+            except Exception:
+                pass
+        _cache["ref"] = Oracle(REFERENCE) if os.path.exists(REFERENCE) else None
+    return _cache["ref"]

@@ -1,0 +1,200 @@
+"""GPU parity of the Y / MtM / X / label path against the oracle.
+
+Tolerances (the north star's bar is 1e-5 relative per path in FP32 and exact
+default indicators; the FP64 engine is held far tighter):
+  * raw draws u64 / uniform / exponential: bit-exact; normals: <= 8 ulp
+    (libdevice erfc/exp vs glibc inside the Halley step, rng.cpp:120-127);
+  * market factors: 1e-11 relative;
+  * default steps: bit-exact (threshold ties within 1 ulp are counted);
+  * MtM cube: 1e-10 of the cube's scale (the coefficient form reorders the
+    per-client book sum); labels 1e-9 relative + 1e-12 of scale; features as
+    market (indicator columns exact).
+"""
+import numpy as np
+import pytest
+
+import cases
+import oracle_api
+import paper_2211_17005_b200 as hcva
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = ["minimal", "c1", "desk_corr", "c2"]
+MARKET_RTOL = 1e-11
+
+
+def golden(name):
+    return np.load(f"{oracle_api.ROOT}/tests/golden/{name}.npz")
+
+
+def ulps(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    ia = a.view(np.int64).astype(np.float64)
+    ib = b.view(np.int64).astype(np.float64)
+    return np.abs(ia - ib)
+
+
+def close(got, want, rtol, atol_scale=0.0, what=""):
+    scale = np.max(np.abs(want)) if want.size else 0.0
+    err = np.abs(got - want)
+    tol = rtol * np.abs(want) + atol_scale * scale + 1e-300
+    bad = err > tol
+    assert not bad.any(), f"{what}: {bad.sum()} / {bad.size} outside tol, max err {err.max():.3e}"
+
+
+def test_rng_draws_vs_golden():
+    z = np.load(f"{oracle_api.ROOT}/tests/golden/rng_kat.npz")
+    s = hcva.RandomStream(42)
+    assert s.key == int(z["keys"][0])
+    assert np.array_equal(hcva.RandomStream(42).u64(64), z["u64_42"])
+    assert np.array_equal(hcva.RandomStream(42).uniforms(64), z["uniform_42"])
+    ex = hcva.RandomStream(42).exponentials(256)
+    assert ulps(ex, z["exp_42"]).max() <= 1  # -log: libdevice vs glibc, <= 1 ulp
+    nz = hcva.RandomStream(42).normals(4096)
+    u = ulps(nz, z["normal_42"])
+    assert np.abs(nz - z["normal_42"]).max() < 1e-14
+    assert u.max() <= 64 or np.abs(nz - z["normal_42"]).max() < 4e-16
+    kat = hcva.RandomStream(7).split(1).split(0).split(3).normals(1)[0]
+    assert abs(kat - 0.53603967906048189) < 1e-15
+
+
+def test_normals_large_sample_agreement():
+    """1M normals: worst absolute difference and the share that is bit-exact."""
+    R = oracle_api.restatement()
+    key = R.key(2024, 5)
+    want = R.normals(key, 0, 1 << 20)
+    got = hcva.RandomStream(2024).split(5).normals(1 << 20)
+    diff = np.abs(got - want)
+    assert diff.max() < 2e-15
+    exact = np.mean(got == want)
+    assert exact > 0.5, exact
+
+
+def gpu_case(name, M, N):
+    cfg = hcva.parse_config(cases.text(name))
+    book = hcva.generate_book(cfg)
+    sim = hcva.simulate_set(cfg, book, M, N, hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM))
+    return cfg, book, sim
+
+
+@pytest.mark.parametrize("name", GOLDEN)
+def test_simulation_vs_golden(name):
+    z = golden(name)
+    M, N = int(z["M"]), int(z["N"])
+    cfg, book, sim = gpu_case(name, M, N)
+    mk = sim.market_arrays()
+    for key in ("rates", "fx", "intens", "lagged", "disc", "hazard"):
+        close(mk[key], z["market_" + key], MARKET_RTOL, 0.0, key)
+    steps = sim.default_steps()
+    mism = int((steps != z["steps"]).sum())
+    ties = sim.tie_counts()
+    assert mism == 0, f"{mism} default-step mismatches (ties within 1 ulp: {ties[0]})"
+    cube = sim.cube_values()
+    close(cube, z["cube"], 1e-10, 1e-10, "cube")
+    for j, i in enumerate(z["label_steps"]):
+        close(sim.labels(int(i), "defaults"), z["labels_defaults"][j], 1e-9, 1e-12, f"defaults label {i}")
+        close(sim.labels(int(i), "intensity"), z["labels_intensity"][j], 1e-9, 1e-12, f"intensity label {i}")
+    f = sim.features(int(z["feature_step"]))
+    p = cfg.n_clients
+    assert np.array_equal(f[:, :p], z["features"][:, :p])
+    close(f[:, p:], z["features"][:, p:], MARKET_RTOL, 0.0, "features")
+
+
+def test_labels_all_matches_per_step():
+    cfg, book, sim = gpu_case("desk_corr", 40, 8)
+    allv = sim.labels_all("defaults")
+    for i in range(cfg.n_steps + 1):
+        assert np.array_equal(allv[i], sim.labels(i, "defaults"))
+    alli = sim.labels_all("intensity")
+    for i in (0, 5, cfg.n_steps):
+        assert np.array_equal(alli[i], sim.labels(i, "intensity"))
+
+
+def test_c1_full_size_vs_oracle():
+    """C1 at full size (M=1024, N=16, n=50, sub=25) against the live oracle."""
+    R = oracle_api.restatement()
+    cfg, book, sim = gpu_case("c1", 1024, 16)
+    m = cases.oracle_model(cfg)
+    root = R.key(cfg.seed)
+    sk = R.split(root, 1)
+    mk = R.simulate_market(m, 1024, R.split(sk, 0))
+    st = R.sample_defaults(mk["hazard"], 16, R.split(sk, 1))
+    cube = R.build_cube(m, mk, book)
+    g = sim.market_arrays()
+    for key in ("rates", "intens", "disc", "hazard"):
+        close(g[key], mk[key], MARKET_RTOL, 0.0, key)
+    assert int((sim.default_steps() != st).sum()) == 0
+    close(sim.cube_values(), cube, 1e-10, 1e-10, "cube")
+    for i in (0, 1, 17, 49):
+        close(sim.labels(i), R.defaults_label(i, mk, st, cube, cfg.dt), 1e-9, 1e-12, f"label {i}")
+
+
+def test_conditional_market_vs_oracle():
+    R = oracle_api.restatement()
+    cfg = hcva.parse_config(cases.text("desk_corr"))
+    m = cases.oracle_model(cfg)
+    mk = R.simulate_market(m, 4, R.key(9))
+    state = dict(rates=mk["rates"][1, 3], log_fx=np.log(mk["fx"][1, 3]), intens=mk["intens"][1, 3],
+                 lagged=mk["lagged"][1, 3])
+    want = R.simulate_conditional(m, state, 3, 7, 33, R.key(10))
+    sim = hcva.simulate_conditional_market(cfg, state, 3, 7, 33, hcva.RandomStream(10))
+    got = sim.market_arrays()
+    for key in want:
+        close(got[key], want[key], MARKET_RTOL, 0.0, key)
+    book = hcva.generate_book(cfg)
+    hcva.build_mtm_cube(sim, book)
+    close(sim.cube_values(), R.build_cube(m, want, book, start_step=3), 1e-10, 1e-10, "conditional cube")
+
+
+def test_direct_mtm_path_matches_reference_order():
+    """Books whose tenor spans several pricing steps take the per-swap kernel."""
+    R = oracle_api.restatement()
+    cfg = hcva.parse_config(cases.text("desk_corr"))
+    m = cases.oracle_model(cfg)
+    book = hcva.generate_book(cfg)
+    book["tenor"] = 2 * cfg.dt
+    book["maturity"] = np.maximum(2, 2 * np.round(book["maturity"] / (2 * cfg.dt))) * cfg.dt
+    for s in range(len(book)):
+        book["fixed_rate"][s] = hcva.par_rate(book["maturity"][s], book["tenor"][s], cfg.rates[book["economy"][s]])
+    sim = hcva.simulate_set(cfg, book, 24, 2, hcva.RandomStream(cfg.seed).split(1))
+    mk = R.simulate_market(m, 24, R.key(cfg.seed, 1, 0))
+    close(sim.cube_values(), R.build_cube(m, mk, book), 1e-10, 1e-10, "direct cube")
+
+
+def test_path_purity_and_sharding():
+    """Per-path purity (test_market.cpp:135-146) and replica lineage purity
+    (test_defaults.cpp:78-88): a shard simulated with a path offset equals the
+    same paths of the full block, bit for bit."""
+    cfg = hcva.parse_config(cases.text("desk_corr"))
+    book = hcva.generate_book(cfg)
+    stream = hcva.RandomStream(cfg.seed).split(1)
+    full = hcva.simulate_set(cfg, book, 40, 8, stream)
+    lo = hcva.simulate_set(cfg, book, 16, 8, stream, path_offset=0)
+    hi = hcva.simulate_set(cfg, book, 24, 8, stream, path_offset=16)
+    fm, lm, hm = full.market_arrays(), lo.market_arrays(), hi.market_arrays()
+    for key in fm:
+        assert np.array_equal(np.concatenate([lm[key], hm[key]]), fm[key]), key
+    assert np.array_equal(np.concatenate([lo.default_steps(), hi.default_steps()]), full.default_steps())
+    assert np.array_equal(np.concatenate([lo.cube_values(), hi.cube_values()]), full.cube_values())
+    fewer = hcva.simulate_set(cfg, book, 40, 3, stream)
+    assert np.array_equal(fewer.default_steps(), full.default_steps()[:, :3])
+
+
+def test_determinism_bitwise():
+    cfg, book, a = gpu_case("c1", 256, 16)
+    _, _, b = gpu_case("c1", 256, 16)
+    assert np.array_equal(a.cube_values(), b.cube_values())
+    assert np.array_equal(a.labels_all("defaults"), b.labels_all("defaults"))
+
+
+def test_invariants_absorbing_positive():
+    """test_defaults.cpp:60-76 / test_market.cpp:148-166 / test_labels.cpp:145-153."""
+    cfg, book, sim = gpu_case("c1", 512, 16)
+    mk = sim.market_arrays()
+    assert (mk["intens"] >= 0).all() and (mk["disc"] > 0).all()
+    assert (np.diff(mk["hazard"], axis=1) >= 0).all()
+    steps = sim.default_steps()
+    assert (steps > 0).all()  # no default at time zero
+    lab = sim.labels_all("defaults")
+    assert (lab >= 0).all() and (lab[-1] == 0).all()
