@@ -45,6 +45,7 @@ __global__ void k_draws(uint64_t key, uint64_t start, size_t count, int kind, vo
 // ------------------------------------------------------------------ K1
 struct MarketArgs {
     int E, Cn, D, substeps, n_store, M, T, nnz;
+    int mode;  // profiling probe: bit 0 skips normal generation, bit 1 skips the recursion
     int paths_per_group;
     uint64_t local_offset;
     double h, sqh;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(32 * (G + 1)) k_market(MarketArgs a) {
             const int nn = tc * D;
             const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
             double* zb = zbuf + buf * (T * D * P);
-            for (int b = g / P; 2 * b < nn; b += (32 * G) / P) {
+            for (int b = g / P; 2 * b < nn && !(a.mode & 1); b += (32 * G) / P) {
                 uint64_t w0, w1;
                 philox2x64(blk0 + b, pkey, w0, w1);
                 zb[(2 * b) * P + p] = inverse_normal_cdf(u64_to_uniform(w0));
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(32 * (G + 1)) k_market(MarketArgs a) {
         bar_sync(1 + buf, NT);
         const int tc = min(T, total_sub - c * T);
         const double* zb = zbuf + buf * (T * D * P) + lane;
-        if (lane < P) {
+        if (lane < P && !(a.mode & 2)) {
             for (int t = 0; t < tc; ++t) {
                 const double* zt = zb + t * D * P;
                 auto zcorr = [&](int d) {
@@ -635,6 +636,7 @@ void launch_market(hcva_sim* sim, uint64_t key0) {
     a.T = sim->m_T; a.nnz = sim->m_nnz; a.paths_per_group = sim->m_ppg; a.local_offset = sim->m_local_offset;
     a.h = m.dt / m.substeps; a.sqh = std::sqrt(a.h);
     a.key0 = key0;
+    if (const char* env = std::getenv("HCVA_K1_MODE")) a.mode = std::atoi(env);
     a.group_keys = sim->m_keys.p ? sim->m_keys.as<uint64_t>() : nullptr;
     a.init_state = sim->m_init.as<double>(); a.coef = sim->m_coef.as<FactorCoef>();
     a.chol_row = sim->m_row.as<int>(); a.chol_col = sim->m_col.as<int>(); a.chol_val = sim->m_val.as<double>();
