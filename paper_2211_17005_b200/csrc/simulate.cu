@@ -59,29 +59,37 @@ struct MarketArgs {
     double *rates, *fx, *intens, *hazard, *disc;
 };
 
-__device__ __forceinline__ void bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+// K1: Euler diffusion of the exogenous factors Y (market.cpp:161-310).
+//
+// CTA = P paths x (threads per path).  The fine grid is processed in chunks of
+// T substeps.  Per chunk, every thread first generates Philox blocks of its
+// path (the chunk's P*T*D normals are counter-addressable, draw j = (substep,
+// factor) of split(k), rng.cpp:57-67) into a double-buffered shared-memory
+// tile; after one __syncthreads each thread advances the factors it owns for
+// the T substeps with its state in registers:
+//   economy thread e < E : r_e, log chi_e (e > 0) and a private copy of r_0
+//                          (log-FX reads the pre-step r_0 and r_e,
+//                          market.cpp:211-223); thread 0 also carries -ln beta;
+//   credit thread        : two CIR intensities and their cumulative hazards.
+// Every update is rounded as the reference rounds it (no FMA contraction).
+// The correlated increment z = L zraw reads the chunk tile through the CSR of
+// the Cholesky factor (exact zeros skipped).  Stores at pricing steps are
+// coalesced over the path index.
+__device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, double h, double z) {
+    // r + (a(b - r) - q) h + (sigma sqrt h) z     (market.cpp:121-124)
+    return dadd(dadd(r, dmul(dsub(dmul(k.c0, dsub(k.c1, r)), k.c2), h)), dmul(k.c3, z));
 }
 
-// One CTA = P paths.  Warp 0 runs the per-path Euler recursion (one lane per
-// path); warps 1..G generate the chunk's normals cooperatively (the draws are
-// counter-addressable, so the P*T*D normals of a chunk are independent work)
-// into a double-buffered shared-memory ring.  Named barriers hand chunks over:
-// FULL[b] = 1+b, EMPTY[b] = 3+b.
-template <int P, int G>
-__global__ void __launch_bounds__(32 * (G + 1)) k_market(MarketArgs a) {
+template <int P>
+__global__ void __launch_bounds__(512) k_market(MarketArgs a) {
     extern __shared__ double smem[];
-    constexpr int NT = 32 * (G + 1);
     const int E = a.E, Cn = a.Cn, D = a.D, T = a.T;
+    const int NT = blockDim.x;
     FactorCoef* coef = reinterpret_cast<FactorCoef*>(smem);
     double* chol_val = smem + 4 * D;
     int* chol_col = reinterpret_cast<int*>(chol_val + a.nnz);
     int* chol_row = chol_col + a.nnz;
-    double* state = smem + 4 * D + a.nnz + (a.nnz + D + 2) / 2;  // [(D+Cn+1)][P]
-    double* zbuf = state + (D + Cn + 1) * P;                              // [2][T*D][P]
+    double* zs = smem + 4 * D + a.nnz + (a.nnz + D + 2) / 2;  // [2][T*D][P]
 
     for (int t = threadIdx.x; t < D; t += NT) coef[t] = a.coef[t];
     for (int t = threadIdx.x; t < a.nnz; t += NT) {
@@ -89,108 +97,110 @@ __global__ void __launch_bounds__(32 * (G + 1)) k_market(MarketArgs a) {
         chol_col[t] = a.chol_col[t];
     }
     for (int t = threadIdx.x; t <= D; t += NT) chol_row[t] = a.chol_row[t];
-    __syncthreads();
 
-    const int total_sub = a.n_store * a.substeps;
-    const int n_chunks = (total_sub + T - 1) / T;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (warp > 0) {
-        // ---------------- normal generators
-        const int g = threadIdx.x - 32;
-        const int p = g % P;
-        const int kloc = min(static_cast<int>(blockIdx.x) * P + p, a.M - 1);
-        const int grp = kloc / a.paths_per_group;
-        const uint64_t within = static_cast<uint64_t>(kloc - grp * a.paths_per_group) + a.local_offset;
-        const uint64_t pkey = split_key(a.group_keys ? a.group_keys[grp] : a.key0, within);
-        for (int c = 0; c < n_chunks; ++c) {
-            const int buf = c & 1;
-            if (c >= 2) bar_sync(3 + buf, NT);
-            const int tc = min(T, total_sub - c * T);
-            const int nn = tc * D;
-            const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
-            double* zb = zbuf + buf * (T * D * P);
-            for (int b = g / P; 2 * b < nn && !(a.mode & 1); b += (32 * G) / P) {
-                uint64_t w0, w1;
-                philox2x64(blk0 + b, pkey, w0, w1);
-                zb[(2 * b) * P + p] = inverse_normal_cdf(u64_to_uniform(w0));
-                if (2 * b + 1 < nn) zb[(2 * b + 1) * P + p] = inverse_normal_cdf(u64_to_uniform(w1));
-            }
-            bar_arrive(1 + buf, NT);
-        }
-        return;
-    }
-
-    // ---------------- recursion warp
-    const int kloc = static_cast<int>(blockIdx.x) * P + lane;
-    const bool active = lane < P && kloc < a.M;
+    const int p = threadIdx.x % P, w = threadIdx.x / P, TPP = NT / P;
     const int M = a.M;
-    double* st = state + lane;  // slot f at st[f * P]
-    if (lane < P) {
-        const int grp = min(kloc, M - 1) / a.paths_per_group;
-        for (int f = 0; f < D; ++f) st[f * P] = a.init_state[static_cast<size_t>(grp) * D + f];
-        for (int c = 0; c <= Cn; ++c) st[(D + c) * P] = 0.0;  // hazards, log beta
+    const int kloc = static_cast<int>(blockIdx.x) * P + p;
+    const bool valid = kloc < M;
+    const int kk = valid ? kloc : M - 1;
+    const int grp = kk / a.paths_per_group;
+    const uint64_t within = static_cast<uint64_t>(kk - grp * a.paths_per_group) + a.local_offset;
+    const uint64_t pkey = split_key(a.group_keys ? a.group_keys[grp] : a.key0, within);
+
+    const bool econ = w < E;
+    const int c0 = 2 * (w - E), c1 = c0 + 1;
+    const bool cred = !econ && c0 < Cn;
+    const bool has_c1 = cred && c1 < Cn;
+    const double* init = a.init_state + static_cast<size_t>(grp) * D;
+    // Registers: economy (s0 = r_e, s1 = r_0 copy, s2 = log chi_e, s3 = -ln beta);
+    //            credit  (s0, s1 = intensities c0, c1; s2, s3 = their hazards).
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (econ) {
+        s0 = init[w];
+        s1 = init[0];
+        if (w > 0) s2 = init[E + w - 1];
+    } else if (cred) {
+        s0 = init[2 * E - 1 + c0];
+        if (has_c1) s1 = init[2 * E - 1 + c1];
     }
     auto store = [&](int i) {
-        if (!active) return;
-        for (int e = 0; e < E; ++e) a.rates[(static_cast<size_t>(i) * E + e) * M + kloc] = st[e * P];
-        for (int e = 1; e < E; ++e)
-            a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + kloc] = exp(st[(E + e - 1) * P]);
-        for (int c = 0; c < Cn; ++c) {
-            a.intens[(static_cast<size_t>(i) * Cn + c) * M + kloc] = st[(2 * E - 1 + c) * P];
-            a.hazard[(static_cast<size_t>(i) * Cn + c) * M + kloc] = st[(D + c) * P];
-        }
-        a.disc[static_cast<size_t>(i) * M + kloc] = exp(-st[(D + Cn) * P]);
-    };
-    store(0);
-    const double h = a.h, sqh = a.sqh;
-    for (int c = 0; c < n_chunks; ++c) {
-        const int buf = c & 1;
-        bar_sync(1 + buf, NT);
-        const int tc = min(T, total_sub - c * T);
-        const double* zb = zbuf + buf * (T * D * P) + lane;
-        if (lane < P && !(a.mode & 2)) {
-            for (int t = 0; t < tc; ++t) {
-                const double* zt = zb + t * D * P;
-                auto zcorr = [&](int d) {
-                    double acc = 0.0;
-                    for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
-                        acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
-                    return acc;
-                };
-                // Left-endpoint quadrature of -ln beta and the hazards (market.cpp:208-209).
-                const double r0 = st[0];
-                st[(D + Cn) * P] = dadd(st[(D + Cn) * P], dmul(r0, h));
-                for (int cc = 0; cc < Cn; ++cc)
-                    st[(D + cc) * P] = dadd(st[(D + cc) * P], dmul(st[(2 * E - 1 + cc) * P], h));
-                // log-FX first: it reads the pre-step rates (market.cpp:211-223).
-                for (int e = 1; e < E; ++e) {
-                    const FactorCoef k = coef[E + e - 1];  // {half_s2, sig_sqh}
-                    const double lc = st[(E + e - 1) * P];
-                    const double drift = dmul(dsub(dsub(r0, st[e * P]), k.c0), h);
-                    st[(E + e - 1) * P] = dadd(dadd(lc, drift), dmul(k.c1, zcorr(E + e - 1)));
-                }
-                for (int e = 0; e < E; ++e) {
-                    const FactorCoef k = coef[e];  // {a, b, quanto, sig_sqh}
-                    const double r = st[e * P];
-                    const double drift = dmul(dsub(dmul(k.c0, dsub(k.c1, r)), k.c2), h);
-                    st[e * P] = dadd(dadd(r, drift), dmul(k.c3, zcorr(e)));
-                }
-                for (int cc = 0; cc < Cn; ++cc) {
-                    const int f = 2 * E - 1 + cc;
-                    const FactorCoef k = coef[f];  // {alpha, delta, nu}
-                    const double gm = st[f * P];
-                    const double gp = (gm < 0.0) ? 0.0 : gm;
-                    const double drift = dmul(dmul(k.c0, dsub(k.c1, gp)), h);
-                    const double diff = dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(f));
-                    const double nx = dadd(dadd(gm, drift), diff);
-                    st[f * P] = (nx < 0.0) ? 0.0 : nx;
-                }
-                const int s_done = c * T + t + 1;
-                if (s_done % a.substeps == 0) store(s_done / a.substeps);
+        if (!valid) return;
+        if (econ) {
+            a.rates[(static_cast<size_t>(i) * E + w) * M + kloc] = s0;
+            if (w > 0) a.fx[(static_cast<size_t>(i) * (E - 1) + w - 1) * M + kloc] = exp(s2);
+            else a.disc[static_cast<size_t>(i) * M + kloc] = exp(-s3);
+        } else if (cred) {
+            a.intens[(static_cast<size_t>(i) * Cn + c0) * M + kloc] = s0;
+            a.hazard[(static_cast<size_t>(i) * Cn + c0) * M + kloc] = s2;
+            if (has_c1) {
+                a.intens[(static_cast<size_t>(i) * Cn + c1) * M + kloc] = s1;
+                a.hazard[(static_cast<size_t>(i) * Cn + c1) * M + kloc] = s3;
             }
         }
-        if (c + 2 < n_chunks) bar_arrive(3 + buf, NT);
+    };
+    store(0);
+    __syncthreads();
+
+    const double h = a.h, sqh = a.sqh;
+    const int total_sub = a.n_store * a.substeps;
+    const int n_chunks = (total_sub + T - 1) / T;
+    for (int c = 0; c < n_chunks; ++c) {
+        double* zb = zs + (c & 1) * (T * D * P);
+        const int tc = min(T, total_sub - c * T);
+        const int nn = tc * D;
+        const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
+        if (!(a.mode & 1)) {
+            for (int b = w; 2 * b < nn; b += TPP) {
+                uint64_t w0, w1;
+                philox2x64(blk0 + b, pkey, w0, w1);
+                zb[(2 * b) * P + p] = inverse_normal_cdf_dev(u64_to_uniform(w0));
+                if (2 * b + 1 < nn) zb[(2 * b + 1) * P + p] = inverse_normal_cdf_dev(u64_to_uniform(w1));
+            }
+        }
+        __syncthreads();
+        if (!valid || (a.mode & 2) || !(econ || cred)) continue;
+        for (int t = 0; t < tc; ++t) {
+            const double* zt = zb + t * D * P + p;
+            auto zcorr = [&](int d) {
+                double acc = 0.0;
+                for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
+                    acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
+                return acc;
+            };
+            if (econ) {
+                if (w == 0) {
+                    s3 = dadd(s3, dmul(s0, h));  // -ln beta, left endpoint (market.cpp:208)
+                    s0 = vasicek_step(s0, coef[0], h, zcorr(0));
+                } else {
+                    const double r0 = s1, re = s0;
+                    // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z  (market.cpp:126-128)
+                    const FactorCoef kx = coef[E + w - 1];
+                    s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zcorr(E + w - 1)));
+                    s0 = vasicek_step(re, coef[w], h, zcorr(w));
+                    s1 = vasicek_step(r0, coef[0], h, zcorr(0));
+                }
+            } else {
+                // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
+                {
+                    const FactorCoef k = coef[2 * E - 1 + c0];
+                    s2 = dadd(s2, dmul(s0, h));
+                    const double gp = (s0 < 0.0) ? 0.0 : s0;
+                    const double nx = dadd(dadd(s0, dmul(dmul(k.c0, dsub(k.c1, gp)), h)),
+                                           dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(2 * E - 1 + c0)));
+                    s0 = (nx < 0.0) ? 0.0 : nx;
+                }
+                if (has_c1) {
+                    const FactorCoef k = coef[2 * E - 1 + c1];
+                    s3 = dadd(s3, dmul(s1, h));
+                    const double gp = (s1 < 0.0) ? 0.0 : s1;
+                    const double nx = dadd(dadd(s1, dmul(dmul(k.c0, dsub(k.c1, gp)), h)),
+                                           dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(2 * E - 1 + c1)));
+                    s1 = (nx < 0.0) ? 0.0 : nx;
+                }
+            }
+            const int s_done = c * T + t + 1;
+            if (s_done % a.substeps == 0) store(s_done / a.substeps);
+        }
     }
 }
 
@@ -569,7 +579,74 @@ void check_launch(hcva_ctx* ctx) {
     HCVA_CUDA(cudaGetLastError());
 }
 
-constexpr int kP = 16, kG = 4;  // K1: paths per CTA, generator warps per CTA
+template <int P>
+void launch_market_p(const MarketArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+    k_market<P><<<grid, threads, smem, s>>>(a);
+}
+
+using MarketLauncher = void (*)(const MarketArgs&, int, int, size_t, cudaStream_t);
+
+MarketLauncher market_launcher(int P) {
+    switch (P) {
+        case 1: return launch_market_p<1>;
+        case 2: return launch_market_p<2>;
+        case 4: return launch_market_p<4>;
+        case 8: return launch_market_p<8>;
+        case 16: return launch_market_p<16>;
+        default: return launch_market_p<32>;
+    }
+}
+
+const void* market_kernel(int P) {
+    switch (P) {
+        case 1: return reinterpret_cast<const void*>(k_market<1>);
+        case 2: return reinterpret_cast<const void*>(k_market<2>);
+        case 4: return reinterpret_cast<const void*>(k_market<4>);
+        case 8: return reinterpret_cast<const void*>(k_market<8>);
+        case 16: return reinterpret_cast<const void*>(k_market<16>);
+        default: return reinterpret_cast<const void*>(k_market<32>);
+    }
+}
+
+// K1 launch shape: P paths per CTA (P | 32), owner threads per path W =
+// E + ceil(Cn/2), chunk T substeps.  Chosen to minimise the wave-quantisation
+// loss ceil(waves)/waves of M/P equal-cost CTAs over the resident slots.
+void choose_market_shape(hcva_sim* sim) {
+    const Model& m = sim->model;
+    const int D = m.D, W = m.E + (m.Cn + 1) / 2;
+    const size_t head = 4 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
+    double best = -1.0;
+    for (int P : {16, 8, 4, 2, 1}) {
+        const int NT = ((P * W + 31) / 32) * 32;
+        if (NT > 512) continue;
+        const int TPP = NT / P;
+        // T even, ~TPP normal pairs per thread per chunk, bounded by shared memory.
+        int T = std::max(2, ((2 * TPP * 7) / D) & ~1);
+        T = std::min(T, 16);
+        size_t smem = sizeof(double) * (head + 2 * static_cast<size_t>(T) * D * P);
+        while (smem > 100 * 1024 && T > 2) {
+            T -= 2;
+            smem = sizeof(double) * (head + 2 * static_cast<size_t>(T) * D * P);
+        }
+        if (smem > 227 * 1024) continue;
+        HCVA_CUDA(cudaFuncSetAttribute(market_kernel(P), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+        int per_sm = 0;
+        HCVA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, market_kernel(P), NT, smem));
+        if (per_sm < 1) continue;
+        const double ctas = (sim->M + P - 1) / P;
+        const double waves = ctas / (static_cast<double>(per_sm) * sim->ctx->sm_count);
+        const double eff = waves / std::ceil(waves) * std::min(1.0, static_cast<double>(P * W) / NT);
+        if (eff > best + 1e-3) {
+            best = eff;
+            sim->m_P = P;
+            sim->m_NT = NT;
+            sim->m_T = T;
+            sim->m_smem = smem;
+        }
+    }
+    if (best < 0) throw config_error("model too large for the diffusion kernel (shared memory)");
+}
 
 // Stage K1's tables: per-factor coefficients computed with the reference's
 // rounding (market.cpp:121-134, 214-216), the Cholesky factor as CSR (exact
@@ -609,16 +686,7 @@ void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys,
     if (group_keys.size() > 1) stage(sim->m_keys, group_keys);
     sim->m_ppg = paths_per_group;
     sim->m_local_offset = local_offset;
-    // Chunk of T substeps: T*D even keeps chunks aligned to Philox blocks.
-    int T = 4;
-    if ((T * D) & 1) T += 1;
-    sim->m_T = T;
-    const size_t head = 4 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
-    sim->m_smem = sizeof(double) * (head + static_cast<size_t>(D + Cn + 1) * kP + 2 * static_cast<size_t>(T) * D * kP);
-    if (sim->m_smem > 227 * 1024) throw config_error("model too large for the diffusion kernel's shared memory");
-    if (sim->m_smem > 48 * 1024)
-        HCVA_CUDA(cudaFuncSetAttribute(k_market<kP, kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sim->m_smem)));
+    choose_market_shape(sim);
     const Model& mm = sim->model;
     const size_t n1 = sim->n + 1, M = sim->M;
     sim->rates.alloc(sizeof(double) * n1 * mm.E * M);
@@ -642,7 +710,7 @@ void launch_market(hcva_sim* sim, uint64_t key0) {
     a.chol_row = sim->m_row.as<int>(); a.chol_col = sim->m_col.as<int>(); a.chol_val = sim->m_val.as<double>();
     a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.intens = sim->intens.as<double>();
     a.hazard = sim->hazard.as<double>(); a.disc = sim->disc.as<double>();
-    k_market<kP, kG><<<grid1(sim->M, kP), 32 * (kG + 1), sim->m_smem, ctx->stream>>>(a);
+    market_launcher(sim->m_P)(a, grid1(sim->M, sim->m_P), sim->m_NT, sim->m_smem, ctx->stream);
     check_launch(ctx);
 }
 
