@@ -68,7 +68,11 @@ bool is_multiple(double x, double step);
 // Device-side per-launch constants for the diffusion kernel: per-factor
 // coefficient quads staged into shared memory, CSR of the Cholesky factor.
 struct FactorCoef {
-    double c0, c1, c2, c3;
+    double c0, c1, c2, c3;  // Euler coefficients (see prepare_market)
+    double v0, v1;          // Cholesky row, when it has <= 2 nonzeros: z = v0 zraw[col0] + v1 zraw[col1]
+    int col0, col1;
+    int dense;              // row has > 2 nonzeros: use the CSR
+    int pad;
 };
 
 struct DeviceBuf {
@@ -118,7 +122,7 @@ struct hcva_sim {
     // --- execution plan (staged once, reused by every re-run) ---
     // market: per-factor coefficients, Cholesky CSR, initial states, group keys
     hcva::DeviceBuf m_coef, m_row, m_col, m_val, m_init, m_keys;
-    int m_nnz = 0, m_T = 0, m_ppg = 1, m_P = 8, m_NT = 128;
+    int m_nnz = 0, m_T = 0, m_ppg = 1, m_P = 8, m_NT = 128, m_We = 12;
     uint64_t m_local_offset = 0;
     size_t m_smem = 0;
     // MtM: coefficient tables (linear form) or the book (direct form)

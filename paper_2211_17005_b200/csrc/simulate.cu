@@ -45,7 +45,8 @@ __global__ void k_draws(uint64_t key, uint64_t start, size_t count, int kind, vo
 // ------------------------------------------------------------------ K1
 struct MarketArgs {
     int E, Cn, D, substeps, n_store, M, T, nnz;
-    int mode;  // profiling probe: bit 0 skips normal generation, bit 1 skips the recursion
+    int mode;    // profiling probe: bit 0 skips normal generation, bit 1 skips the recursion
+    int W_econ;  // economy-thread slots per path (E rounded up to whole warps)
     int paths_per_group;
     uint64_t local_offset;
     double h, sqh;
@@ -80,16 +81,20 @@ __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, do
     return dadd(dadd(r, dmul(dsub(dmul(k.c0, dsub(k.c1, r)), k.c2), h)), dmul(k.c3, z));
 }
 
+constexpr int kQueueCap = 128;  // per-warp queue of tail draws
+
 template <int P>
 __global__ void __launch_bounds__(512) k_market(MarketArgs a) {
     extern __shared__ double smem[];
     const int E = a.E, Cn = a.Cn, D = a.D, T = a.T;
-    const int NT = blockDim.x;
-    FactorCoef* coef = reinterpret_cast<FactorCoef*>(smem);
-    double* chol_val = smem + 4 * D;
+    const int NT = blockDim.x, NW = NT / 32;
+    FactorCoef* coef = reinterpret_cast<FactorCoef*>(smem);          // [D] (8 doubles each)
+    double* chol_val = smem + 8 * D;
     int* chol_col = reinterpret_cast<int*>(chol_val + a.nnz);
     int* chol_row = chol_col + a.nnz;
-    double* zs = smem + 4 * D + a.nnz + (a.nnz + D + 2) / 2;  // [2][T*D][P]
+    double* qp_all = smem + 8 * D + a.nnz + (a.nnz + D + 2) / 2;      // [NW][cap] tail uniforms
+    int* qs_all = reinterpret_cast<int*>(qp_all + NW * kQueueCap);    // [NW][cap] tail slots
+    double* zs = qp_all + NW * kQueueCap + (NW * kQueueCap) / 2;      // [2][T*D][P]
 
     for (int t = threadIdx.x; t < D; t += NT) coef[t] = a.coef[t];
     for (int t = threadIdx.x; t < a.nnz; t += NT) {
@@ -99,6 +104,10 @@ __global__ void __launch_bounds__(512) k_market(MarketArgs a) {
     for (int t = threadIdx.x; t <= D; t += NT) chol_row[t] = a.chol_row[t];
 
     const int p = threadIdx.x % P, w = threadIdx.x / P, TPP = NT / P;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    double* qp = qp_all + wid * kQueueCap;
+    int* qs = qs_all + wid * kQueueCap;
     const int M = a.M;
     const int kloc = static_cast<int>(blockIdx.x) * P + p;
     const bool valid = kloc < M;
@@ -107,27 +116,34 @@ __global__ void __launch_bounds__(512) k_market(MarketArgs a) {
     const uint64_t within = static_cast<uint64_t>(kk - grp * a.paths_per_group) + a.local_offset;
     const uint64_t pkey = split_key(a.group_keys ? a.group_keys[grp] : a.key0, within);
 
-    const bool econ = w < E;
-    const int c0 = 2 * (w - E), c1 = c0 + 1;
+    // Roles.  Economy threads w < We (We = E rounded up so warps are role-uniform);
+    // credit threads own names c0 = 2(w - We), c1 = c0 + 1.
+    const int We = a.W_econ;
+    const bool econ = w < We;
+    const bool econ_real = w < E;
+    const int c0 = 2 * (w - We), c1 = c0 + 1;
     const bool cred = !econ && c0 < Cn;
     const bool has_c1 = cred && c1 < Cn;
+    const int e = econ_real ? w : 0;
+    const int fr = e, fx = (e > 0) ? E + e - 1 : 0;         // own rate / log-FX factor
+    const int fg0 = cred ? 2 * E - 1 + c0 : 0, fg1 = has_c1 ? 2 * E - 1 + c1 : fg0;
     const double* init = a.init_state + static_cast<size_t>(grp) * D;
     // Registers: economy (s0 = r_e, s1 = r_0 copy, s2 = log chi_e, s3 = -ln beta);
     //            credit  (s0, s1 = intensities c0, c1; s2, s3 = their hazards).
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (econ) {
-        s0 = init[w];
+        s0 = init[fr];
         s1 = init[0];
-        if (w > 0) s2 = init[E + w - 1];
+        s2 = init[fx];
     } else if (cred) {
-        s0 = init[2 * E - 1 + c0];
-        if (has_c1) s1 = init[2 * E - 1 + c1];
+        s0 = init[fg0];
+        s1 = init[fg1];
     }
     auto store = [&](int i) {
         if (!valid) return;
-        if (econ) {
-            a.rates[(static_cast<size_t>(i) * E + w) * M + kloc] = s0;
-            if (w > 0) a.fx[(static_cast<size_t>(i) * (E - 1) + w - 1) * M + kloc] = exp(s2);
+        if (econ_real) {
+            a.rates[(static_cast<size_t>(i) * E + e) * M + kloc] = s0;
+            if (e > 0) a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + kloc] = exp(s2);
             else a.disc[static_cast<size_t>(i) * M + kloc] = exp(-s3);
         } else if (cred) {
             a.intens[(static_cast<size_t>(i) * Cn + c0) * M + kloc] = s0;
@@ -147,14 +163,47 @@ __global__ void __launch_bounds__(512) k_market(MarketArgs a) {
     for (int c = 0; c < n_chunks; ++c) {
         double* zb = zs + (c & 1) * (T * D * P);
         const int tc = min(T, total_sub - c * T);
-        const int nn = tc * D;
+        const int nn = tc * D, nb = (nn + 1) >> 1;
         const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
         if (!(a.mode & 1)) {
-            for (int b = w; 2 * b < nn; b += TPP) {
-                uint64_t w0, w1;
-                philox2x64(blk0 + b, pkey, w0, w1);
-                zb[(2 * b) * P + p] = inverse_normal_cdf_dev(u64_to_uniform(w0));
-                if (2 * b + 1 < nn) zb[(2 * b + 1) * P + p] = inverse_normal_cdf_dev(u64_to_uniform(w1));
+            // Central draws are refined in place; the 4.85% that fall in Acklam's
+            // tails are queued per warp (ballot + popc) and refined afterwards by
+            // full warps, so the log/sqrt tail branch does not serialise ~80% of
+            // the warps.
+            int qn = 0;
+            const int iters = (nb + TPP - 1) / TPP;
+            for (int it = 0; it < iters; ++it) {
+                const int b = w + it * TPP;
+                const bool vb = b < nb;
+                uint64_t w0 = 0, w1 = 0;
+                if (vb) philox2x64(blk0 + b, pkey, w0, w1);
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int j = 2 * b + hf;
+                    const bool v = vb && j < nn;
+                    const double u = u64_to_uniform(hf ? w1 : w0);
+                    const bool tail = v && acklam_tail(u);
+                    const unsigned m = __ballot_sync(0xffffffffu, tail);
+                    if (tail) {
+                        const int pos = qn + __popc(m & lanemask_lt);
+                        qs[pos] = j * P + p;
+                        qp[pos] = u;
+                    }
+                    qn += __popc(m);
+                    if (v && !tail) zb[j * P + p] = halley_refine(acklam_central(u), u);
+                }
+                if (qn > kQueueCap - 64 || it == iters - 1) {
+                    __syncwarp();
+                    for (int base = 0; base < qn; base += 32) {
+                        const int i = base + lane;
+                        if (i < qn) {
+                            const double u = qp[i];
+                            zb[qs[i]] = halley_refine(acklam_tail_seed(u), u);
+                        }
+                    }
+                    qn = 0;
+                    __syncwarp();
+                }
             }
         }
         __syncthreads();
@@ -162,41 +211,36 @@ __global__ void __launch_bounds__(512) k_market(MarketArgs a) {
         for (int t = 0; t < tc; ++t) {
             const double* zt = zb + t * D * P + p;
             auto zcorr = [&](int d) {
+                const FactorCoef& k = coef[d];
+                if (!k.dense) return dadd(dmul(k.v0, zt[k.col0 * P]), dmul(k.v1, zt[k.col1 * P]));
                 double acc = 0.0;
                 for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
                     acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
                 return acc;
             };
             if (econ) {
-                if (w == 0) {
-                    s3 = dadd(s3, dmul(s0, h));  // -ln beta, left endpoint (market.cpp:208)
-                    s0 = vasicek_step(s0, coef[0], h, zcorr(0));
-                } else {
-                    const double r0 = s1, re = s0;
-                    // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z  (market.cpp:126-128)
-                    const FactorCoef kx = coef[E + w - 1];
-                    s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zcorr(E + w - 1)));
-                    s0 = vasicek_step(re, coef[w], h, zcorr(w));
-                    s1 = vasicek_step(r0, coef[0], h, zcorr(0));
-                }
+                const double r0 = s1, re = s0;
+                const double zr = zcorr(fr), z0 = zcorr(0), zx = zcorr(fx);
+                s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
+                // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
+                const FactorCoef& kx = coef[fx];
+                s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zx));
+                s0 = vasicek_step(re, coef[fr], h, zr);
+                s1 = vasicek_step(r0, coef[0], h, z0);
             } else {
                 // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
-                {
-                    const FactorCoef k = coef[2 * E - 1 + c0];
-                    s2 = dadd(s2, dmul(s0, h));
-                    const double gp = (s0 < 0.0) ? 0.0 : s0;
-                    const double nx = dadd(dadd(s0, dmul(dmul(k.c0, dsub(k.c1, gp)), h)),
-                                           dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(2 * E - 1 + c0)));
-                    s0 = (nx < 0.0) ? 0.0 : nx;
-                }
-                if (has_c1) {
-                    const FactorCoef k = coef[2 * E - 1 + c1];
-                    s3 = dadd(s3, dmul(s1, h));
-                    const double gp = (s1 < 0.0) ? 0.0 : s1;
-                    const double nx = dadd(dadd(s1, dmul(dmul(k.c0, dsub(k.c1, gp)), h)),
-                                           dmul(dmul(dmul(k.c2, sqrt(gp)), sqh), zcorr(2 * E - 1 + c1)));
-                    s1 = (nx < 0.0) ? 0.0 : nx;
-                }
+                const double z0 = zcorr(fg0), z1 = zcorr(fg1);
+                const FactorCoef& k0 = coef[fg0];
+                const FactorCoef& k1 = coef[fg1];
+                s2 = dadd(s2, dmul(s0, h));
+                s3 = dadd(s3, dmul(s1, h));
+                const double gp0 = (s0 < 0.0) ? 0.0 : s0, gp1 = (s1 < 0.0) ? 0.0 : s1;
+                const double nx0 = dadd(dadd(s0, dmul(dmul(k0.c0, dsub(k0.c1, gp0)), h)),
+                                        dmul(dmul(dmul(k0.c2, sqrt(gp0)), sqh), z0));
+                const double nx1 = dadd(dadd(s1, dmul(dmul(k1.c0, dsub(k1.c1, gp1)), h)),
+                                        dmul(dmul(dmul(k1.c2, sqrt(gp1)), sqh), z1));
+                s0 = (nx0 < 0.0) ? 0.0 : nx0;
+                s1 = (nx1 < 0.0) ? 0.0 : nx1;
             }
             const int s_done = c * T + t + 1;
             if (s_done % a.substeps == 0) store(s_done / a.substeps);
@@ -613,20 +657,24 @@ const void* market_kernel(int P) {
 // loss ceil(waves)/waves of M/P equal-cost CTAs over the resident slots.
 void choose_market_shape(hcva_sim* sim) {
     const Model& m = sim->model;
-    const int D = m.D, W = m.E + (m.Cn + 1) / 2;
-    const size_t head = 4 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
+    const int D = m.D;
+    const size_t head = 8 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
     double best = -1.0;
     for (int P : {16, 8, 4, 2, 1}) {
+        const int per_warp = 32 / P;
+        const int We = ((m.E + per_warp - 1) / per_warp) * per_warp;
+        const int W = We + (m.Cn + 1) / 2;
         const int NT = ((P * W + 31) / 32) * 32;
         if (NT > 512) continue;
         const int TPP = NT / P;
-        // T even, ~TPP normal pairs per thread per chunk, bounded by shared memory.
+        const size_t queue = static_cast<size_t>(NT / 32) * kQueueCap * 3 / 2;
+        // T even, ~7 normal pairs per thread per chunk, bounded by shared memory.
         int T = std::max(2, ((2 * TPP * 7) / D) & ~1);
         T = std::min(T, 16);
-        size_t smem = sizeof(double) * (head + 2 * static_cast<size_t>(T) * D * P);
+        size_t smem = sizeof(double) * (head + queue + 2 * static_cast<size_t>(T) * D * P);
         while (smem > 100 * 1024 && T > 2) {
             T -= 2;
-            smem = sizeof(double) * (head + 2 * static_cast<size_t>(T) * D * P);
+            smem = sizeof(double) * (head + queue + 2 * static_cast<size_t>(T) * D * P);
         }
         if (smem > 227 * 1024) continue;
         HCVA_CUDA(cudaFuncSetAttribute(market_kernel(P), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -641,6 +689,7 @@ void choose_market_shape(hcva_sim* sim) {
             best = eff;
             sim->m_P = P;
             sim->m_NT = NT;
+            sim->m_We = We;
             sim->m_T = T;
             sim->m_smem = smem;
         }
@@ -660,11 +709,12 @@ void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys,
     std::vector<FactorCoef> coef(D);
     for (int e = 0; e < E; ++e) {
         const double q = (e == 0) ? 0.0 : m.fx[e - 1].rho * m.fx[e - 1].sigma * m.rates[e].sigma;
-        coef[e] = {m.rates[e].a, m.rates[e].b, q, m.rates[e].sigma * sqh};
+        coef[e] = FactorCoef{m.rates[e].a, m.rates[e].b, q, m.rates[e].sigma * sqh};
     }
     for (int e = 1; e < E; ++e)
-        coef[E + e - 1] = {0.5 * m.fx[e - 1].sigma * m.fx[e - 1].sigma, m.fx[e - 1].sigma * sqh, 0, 0};
-    for (int c = 0; c < Cn; ++c) coef[2 * E - 1 + c] = {m.credit[c].alpha, m.credit[c].delta, m.credit[c].nu, 0};
+        coef[E + e - 1] = FactorCoef{0.5 * m.fx[e - 1].sigma * m.fx[e - 1].sigma, m.fx[e - 1].sigma * sqh, 0, 0};
+    for (int c = 0; c < Cn; ++c)
+        coef[2 * E - 1 + c] = FactorCoef{m.credit[c].alpha, m.credit[c].delta, m.credit[c].nu, 0};
     std::vector<int> row(D + 1, 0), col;
     std::vector<double> val;
     for (int d = 0; d < D; ++d) {
@@ -676,6 +726,15 @@ void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys,
             }
         }
         row[d + 1] = static_cast<int>(col.size());
+        // Short rows inline: acc = 0 + v0 z0 (+ v1 z1), a missing second term is
+        // +0 * z1, which leaves the sum unchanged bit for bit.
+        const int nz = row[d + 1] - row[d];
+        FactorCoef& k = coef[d];
+        k.dense = nz > 2;
+        k.v0 = nz >= 1 ? val[row[d]] : 0.0;
+        k.col0 = nz >= 1 ? col[row[d]] : 0;
+        k.v1 = nz == 2 ? val[row[d] + 1] : 0.0;
+        k.col1 = nz == 2 ? col[row[d] + 1] : k.col0;
     }
     sim->m_nnz = static_cast<int>(col.size());
     stage(sim->m_coef, coef);
@@ -704,6 +763,7 @@ void launch_market(hcva_sim* sim, uint64_t key0) {
     a.T = sim->m_T; a.nnz = sim->m_nnz; a.paths_per_group = sim->m_ppg; a.local_offset = sim->m_local_offset;
     a.h = m.dt / m.substeps; a.sqh = std::sqrt(a.h);
     a.key0 = key0;
+    a.W_econ = sim->m_We;
     if (const char* env = std::getenv("HCVA_K1_MODE")) a.mode = std::atoi(env);
     a.group_keys = sim->m_keys.p ? sim->m_keys.as<uint64_t>() : nullptr;
     a.init_state = sim->m_init.as<double>(); a.coef = sim->m_coef.as<FactorCoef>();

@@ -57,14 +57,19 @@ def test_rng_draws_vs_golden():
     assert abs(kat - 0.53603967906048189) < 1e-15
 
 
-# The Halley step of rng.cpp:120-127 makes the result's accuracy that of
-# Phi(x) - p, i.e. of erfc; libdevice and glibc erfc differ by a few ulp, which
-# moves x by ~ulp(p)/phi(x).  The bound is relative to max(1, |x|).
-NORMAL_TOL = 2e-14
+# The Halley step of rng.cpp:120-127 makes the result only as accurate as
+# e = 0.5*erfc(-x/sqrt2) - p: near p -> 1 that difference of two numbers close
+# to 1 carries an absolute error ~ulp(1), so x is known to ~ulp(1)/phi(x) in
+# the reference itself, and libdevice's erfc (vs glibc's) can land one ulp
+# apart there.  The bound is that intrinsic accuracy (4 ulp(1)/phi(x)) plus
+# 2 ulp of x; normal_error() is the largest multiple of it (<= 1 passes).
+NORMAL_TOL = 1.0
 
 
 def normal_error(got, want):
-    return float(np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))))
+    phi = np.exp(-0.5 * want * want) / np.sqrt(2.0 * np.pi)
+    bound = 4 * 2.220446049250313e-16 / phi + 2 * np.spacing(np.abs(want))
+    return float(np.max(np.abs(got - want) / bound))
 
 
 def test_normals_large_sample_agreement():
@@ -77,8 +82,8 @@ def test_normals_large_sample_agreement():
     worst = int(np.argmax(err))
     exact = float(np.mean(got == want))
     print(f"normals: bit-exact {exact:.4f}, worst scaled err {err[worst]:.3e} at x={want[worst]:.6f}, "
-          f"median ulp {np.median(ulps(got, want)):.1f}")
-    assert err.max() <= NORMAL_TOL
+          f"median ulp {np.median(ulps(got, want)):.1f}, worst/bound {normal_error(got, want):.3f}")
+    assert normal_error(got, want) <= NORMAL_TOL
     assert np.mean(err < 1e-15) > 0.99
 
 
