@@ -85,6 +85,9 @@ hcva_status hcva_ctx_launch_count(hcva_ctx* ctx, uint64_t* out);
 /* Diagnostic: measured FP64 FMA throughput of this GPU in TFLOP/s (the
  * roofline denominator of the FP64-bound simulation kernels). */
 hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops);
+/* Diagnostic: the device special functions of the normal transform on host
+ * arguments (fn 0 erfc, 1 exp(z<=0), 2 uniform->normal, 3 exp(-y^2)). */
+hcva_status hcva_diag_special(hcva_ctx* ctx, int fn, const double* x, size_t n, double* out);
 
 /* --- RNG (rng.hpp:16-52, rng.cpp:44-130) --------------------------------- */
 uint64_t hcva_rng_root_key(uint64_t seed);               /* RandomStream(seed) */

@@ -10,7 +10,7 @@ import os
 import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libhcva_gpu.so")
+LIB_PATH = os.environ.get("HCVA_LIB") or os.path.join(PKG, "lib", "libhcva_gpu.so")
 CSRC = os.path.join(PKG, "csrc")
 
 u64 = C.c_uint64
@@ -125,6 +125,7 @@ def lib():
         "hcva_sim_phase_times": [vp, C.c_int, C.POINTER(C.c_float)],
         "hcva_cva_profile": [vp, C.c_int, vp],
         "hcva_diag_fp64_peak": [vp, dptr],
+        "hcva_diag_special": [vp, C.c_int, vp, C.c_size_t, vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -149,5 +150,5 @@ EXPORTED = [
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
-    "hcva_diag_fp64_peak",
+    "hcva_diag_fp64_peak", "hcva_diag_special",
 ]

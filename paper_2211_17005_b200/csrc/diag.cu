@@ -1,5 +1,6 @@
 // diag.cu -- roofline denominators measured on the box (FP64 pipe peak).
 #include "common.cuh"
+#include "normal.cuh"
 
 namespace hcva {
 
@@ -18,9 +19,39 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, doubl
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+__global__ void k_special(int fn, const double* x, size_t n, double* out) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double E = 0.0;
+    switch (fn) {
+        case 0: out[i] = erfc_fast(x[i], E); break;
+        case 1: out[i] = exp_neg(x[i]); break;
+        case 2: out[i] = normal_from_uniform(x[i]); break;
+        default: (void)erfc_fast(x[i], E); out[i] = E; break;
+    }
+}
+
 }  // namespace hcva
 
 using namespace hcva;
+
+// Device special functions on host-provided arguments (test hook):
+// fn 0 = erfc, 1 = exp (z <= 0), 2 = uniform -> normal, 3 = exp(-y^2) from erfc.
+extern "C" hcva_status hcva_diag_special(hcva_ctx* ctx, int fn, const double* x, size_t n, double* out) {
+    return guarded([&] {
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        DeviceBuf dx, dy;
+        dx.alloc(n * 8);
+        dy.alloc(n * 8);
+        HCVA_CUDA(cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+        k_special<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(fn, dx.as<double>(), n,
+                                                                                  dy.as<double>());
+        ctx->launches++;
+        HCVA_CUDA(cudaGetLastError());
+        HCVA_CUDA(cudaMemcpyAsync(out, dy.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
 
 extern "C" hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops) {
     return guarded([&] {

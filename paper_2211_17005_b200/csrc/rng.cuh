@@ -107,56 +107,6 @@ HCVA_HD double draw_normal(uint64_t key, uint64_t j) {
     return inverse_normal_cdf(u64_to_uniform(draw_u64(key, j)));
 }
 
-#ifdef __CUDACC__
-// Device form used by the kernels.  The Acklam seed and the erfc argument are
-// kept in FP64 exactly as the reference forms them: near p -> 1 the
-// refinement's accuracy is ulp(1)/phi(x) (0.5*erfc(-x/sqrt2) - p cancels), so
-// any change of seed re-rolls that rounding and moves x by ~1e-12; with the
-// reference's seed the result tracks glibc to the accuracy of erfc.  Only the
-// final Halley divide u/(1+v) is replaced by u(1 - v + v^2), v = x u/2 ~ 1e-9
-// (difference O(u v^3) ~ 1e-36, below any rounding of x - u/(1+v)).
-constexpr double kAcklamLow = 0.02425;
-
-__device__ __forceinline__ bool acklam_tail(double p) { return p < kAcklamLow || p > 1.0 - kAcklamLow; }
-
-// Acklam seed, central region (rng.cpp:103-107).
-__device__ __forceinline__ double acklam_central(double p) {
-    const double q = p - 0.5;
-    const double r = q * q;
-    const double num =
-        (((((-3.969683028665376e+01 * r + 2.209460984245205e+02) * r + -2.759285104469687e+02) * r +
-           1.383577518672690e+02) * r + -3.066479806614716e+01) * r + 2.506628277459239e+00) * q;
-    const double den =
-        ((((-5.447609879822406e+01 * r + 1.615858368580409e+02) * r + -1.556989798598866e+02) * r +
-          6.680131188771972e+01) * r + -1.328068155288572e+01) * r + 1.0;
-    return num / den;
-}
-
-// Acklam seed, tails (rng.cpp:99-102, 108-112).
-__device__ __forceinline__ double acklam_tail_seed(double p) {
-    const bool upper = p > 0.5;
-    const double q = sqrt(-2.0 * log(upper ? 1.0 - p : p));
-    const double num =
-        ((((-7.784894002430293e-03 * q + -3.223964580411365e-01) * q + -2.400758277161838e+00) * q +
-          -2.549732539343734e+00) * q + 4.374664141464968e+00) * q + 2.938163982698783e+00;
-    const double den =
-        (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q + 2.445134137142996e+00) * q +
-         3.754408661907416e+00) * q + 1.0;
-    return upper ? -num / den : num / den;
-}
-
-// One Halley step against erfc (rng.cpp:120-127).
-__device__ __forceinline__ double halley_refine(double x, double p) {
-    const double e = 0.5 * erfc(-x / 1.4142135623730951) - p;
-    const double u = e * 2.5066282746310002 * exp(x * x * 0.5);
-    const double v = x * u * 0.5;
-    return x - u * (1.0 - v * (1.0 - v));
-}
-
-__device__ __forceinline__ double inverse_normal_cdf_dev(double p) {
-    return halley_refine(acklam_tail(p) ? acklam_tail_seed(p) : acklam_central(p), p);
-}
-#endif
 
 HCVA_HD double draw_exponential(uint64_t key, uint64_t j) {
     return -log(u64_to_uniform(draw_u64(key, j)));

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "rng.cuh"
+#include "normal.cuh"
 
 namespace hcva {
 
@@ -37,7 +38,7 @@ __global__ void k_draws(uint64_t key, uint64_t start, size_t count, int kind, vo
     }
     const double u = u64_to_uniform(x);
     double v = u;
-    if (kind == 2) v = inverse_normal_cdf(u);
+    if (kind == 2) v = normal_from_uniform(u);
     if (kind == 3) v = -log(u);
     static_cast<double*>(out)[t] = v;
 }
@@ -84,7 +85,10 @@ __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, do
 constexpr int kQueueCap = 128;  // per-warp queue of tail draws
 
 template <int P>
-__global__ void __launch_bounds__(512) k_market(MarketArgs a) {
+#ifndef HCVA_K1_MAXNREG
+#define HCVA_K1_MAXNREG 128  // <= 128 keeps 512-thread CTAs launchable
+#endif
+__global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     extern __shared__ double smem[];
     const int E = a.E, Cn = a.Cn, D = a.D, T = a.T;
     const int NT = blockDim.x, NW = NT / 32;
