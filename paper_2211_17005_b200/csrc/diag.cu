@@ -27,6 +27,14 @@ __global__ void k_special(int fn, const double* x, size_t n, double* out) {
         case 0: out[i] = erfc_fast(x[i], E); break;
         case 1: out[i] = exp_neg(x[i]); break;
         case 2: out[i] = normal_from_uniform(x[i]); break;
+        case 4: out[i] = rcp_nr(x[i]); break;
+        case 5: out[i] = rcp_approx(x[i]); break;
+        case 6: {
+            double P = kErfcP[21];
+            for (int j = 20; j >= 0; --j) P = fma(P, x[i], kErfcP[j]);
+            out[i] = P;
+            break;
+        }
         default: (void)erfc_fast(x[i], E); out[i] = E; break;
     }
 }

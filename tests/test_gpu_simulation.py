@@ -30,9 +30,7 @@ def golden(name):
 def ulps(a, b):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
-    ia = a.view(np.int64).astype(np.float64)
-    ib = b.view(np.int64).astype(np.float64)
-    return np.abs(ia - ib)
+    return np.abs(a - b) / np.spacing(np.abs(b))
 
 
 def close(got, want, rtol, atol_scale=0.0, what=""):

@@ -23,7 +23,7 @@ def special(fn, x):
 
 
 def ulps(a, b):
-    return np.abs(a.view(np.int64).astype(np.float64) - b.view(np.int64).astype(np.float64))
+    return np.abs(a - b) / np.spacing(np.abs(b))
 
 
 def test_erfc_fast_within_4_ulp():
@@ -41,8 +41,8 @@ def test_exp_neg_within_2_ulp():
     print(f"exp: max {u.max():.0f} ulp, mean {u.mean():.3f}")
     assert u.max() <= 2
     e = special(3, z["erfc_x"])
-    want = np.exp(-z["erfc_x"] ** 2)
-    assert np.max(np.abs(e / want - 1)) < 2e-15
+    want = np.exp(-z["erfc_x"] ** 2)  # numpy rounds x^2 first: ~|x|^2 ulp of slack
+    assert np.max(np.abs(e / want - 1)) < 1e-14
 
 
 def test_normal_transform_matches_k0():
