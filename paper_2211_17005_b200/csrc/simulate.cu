@@ -164,91 +164,114 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     const double h = a.h, sqh = a.sqh;
     const int total_sub = a.n_store * a.substeps;
     const int n_chunks = (total_sub + T - 1) / T;
-    for (int c = 0; c < n_chunks; ++c) {
-        double* zb = zs + (c & 1) * (T * D * P);
-        const int tc = min(T, total_sub - c * T);
-        const int nn = tc * D, nb = (nn + 1) >> 1;
-        const uint64_t blk0 = (static_cast<uint64_t>(c) * T * D) >> 1;
-        if (!(a.mode & 1)) {
-            // Central draws are refined in place; the 4.85% that fall in Acklam's
-            // tails are queued per warp (ballot + popc) and refined afterwards by
-            // full warps, so the log/sqrt tail branch does not serialise ~80% of
-            // the warps.
-            int qn = 0;
-            const int iters = (nb + TPP - 1) / TPP;
-            for (int it = 0; it < iters; ++it) {
-                const int b = w + it * TPP;
-                const bool vb = b < nb;
-                uint64_t w0 = 0, w1 = 0;
-                if (vb) philox2x64(blk0 + b, pkey, w0, w1);
+    const bool do_gen = !(a.mode & 1);
+    const bool do_rec = valid && !(a.mode & 2) && (econ || cred);
+
+    // Generation of chunk c, iteration it (one Philox block -> 2 draws per
+    // thread).  Central draws are refined in place; the 4.85% in Acklam's tails
+    // are queued per warp (ballot + popc) and refined by full warps at the end
+    // of the chunk, so the log/sqrt branch does not serialise ~80% of warps.
+    // it, iters and qn are warp-uniform.
+    auto gen_iter = [&](int cc, int it, int iters, int& qn) {
+        double* zb = zs + (cc & 1) * (T * D * P);
+        const int nn = min(T, total_sub - cc * T) * D, nb = (nn + 1) >> 1;
+        const uint64_t blk0 = (static_cast<uint64_t>(cc) * T * D) >> 1;
+        const int b = w + it * TPP;
+        const bool vb = b < nb;
+        uint64_t w0 = 0, w1 = 0;
+        if (vb) philox2x64(blk0 + b, pkey, w0, w1);
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    const int j = 2 * b + hf;
-                    const bool v = vb && j < nn;
-                    const double u = u64_to_uniform(hf ? w1 : w0);
-                    const bool tail = v && acklam_tail(u);
-                    const unsigned m = __ballot_sync(0xffffffffu, tail);
-                    if (tail) {
-                        const int pos = qn + __popc(m & lanemask_lt);
-                        qs[pos] = j * P + p;
-                        qp[pos] = u;
-                    }
-                    qn += __popc(m);
-                    if (v && !tail) zb[j * P + p] = halley_refine(acklam_central(u), u);
-                }
-                if (qn > kQueueCap - 64 || it == iters - 1) {
-                    __syncwarp();
-                    for (int base = 0; base < qn; base += 32) {
-                        const int i = base + lane;
-                        if (i < qn) {
-                            const double u = qp[i];
-                            zb[qs[i]] = halley_refine(acklam_tail_seed(u), u);
-                        }
-                    }
-                    qn = 0;
-                    __syncwarp();
+        for (int hf = 0; hf < 2; ++hf) {
+            const int j = 2 * b + hf;
+            const bool v = vb && j < nn;
+            const double u = u64_to_uniform(hf ? w1 : w0);
+            const bool tail = v && acklam_tail(u);
+            const unsigned m = __ballot_sync(0xffffffffu, tail);
+            if (tail) {
+                const int pos = qn + __popc(m & lanemask_lt);
+                qs[pos] = j * P + p;
+                qp[pos] = u;
+            }
+            qn += __popc(m);
+            if (v && !tail) zb[j * P + p] = halley_refine(acklam_central(u), u);
+        }
+        if (qn > kQueueCap - 64 || it == iters - 1) {
+            __syncwarp();
+            for (int base = 0; base < qn; base += 32) {
+                const int i = base + lane;
+                if (i < qn) {
+                    const double u = qp[i];
+                    zb[qs[i]] = halley_refine(acklam_tail_seed(u), u);
                 }
             }
+            qn = 0;
+            __syncwarp();
+        }
+    };
+    auto gen_iters = [&](int cc) {
+        const int nb = (min(T, total_sub - cc * T) * D + 1) >> 1;
+        return (nb + TPP - 1) / TPP;
+    };
+
+    // Recursion: substep t of chunk c for the factors this thread owns.
+    auto rec_step = [&](int cc, int t) {
+        const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
+        auto zcorr = [&](int d) {
+            const FactorCoef& k = coef[d];
+            if (!k.dense) return dadd(dmul(k.v0, zt[k.col0 * P]), dmul(k.v1, zt[k.col1 * P]));
+            double acc = 0.0;
+            for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
+                acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
+            return acc;
+        };
+        if (econ) {
+            const double r0 = s1, re = s0;
+            const double zr = zcorr(fr), z0 = zcorr(0), zx = zcorr(fx);
+            s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
+            // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
+            const FactorCoef& kx = coef[fx];
+            s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zx));
+            s0 = vasicek_step(re, coef[fr], h, zr);
+            s1 = vasicek_step(r0, coef[0], h, z0);
+        } else {
+            // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
+            const double z0 = zcorr(fg0), z1 = zcorr(fg1);
+            const FactorCoef& k0 = coef[fg0];
+            const FactorCoef& k1 = coef[fg1];
+            s2 = dadd(s2, dmul(s0, h));
+            s3 = dadd(s3, dmul(s1, h));
+            const double gp0 = (s0 < 0.0) ? 0.0 : s0, gp1 = (s1 < 0.0) ? 0.0 : s1;
+            const double nx0 = dadd(dadd(s0, dmul(dmul(k0.c0, dsub(k0.c1, gp0)), h)),
+                                    dmul(dmul(dmul(k0.c2, sqrt(gp0)), sqh), z0));
+            const double nx1 = dadd(dadd(s1, dmul(dmul(k1.c0, dsub(k1.c1, gp1)), h)),
+                                    dmul(dmul(dmul(k1.c2, sqrt(gp1)), sqh), z1));
+            s0 = (nx0 < 0.0) ? 0.0 : nx0;
+            s1 = (nx1 < 0.0) ? 0.0 : nx1;
+        }
+        const int s_done = cc * T + t + 1;
+        if (s_done % a.substeps == 0) store(s_done / a.substeps);
+    };
+
+    // Software pipeline: generation of chunk c+1 (into the other buffer) is
+    // interleaved with the recursion of chunk c, so the recursion's short
+    // dependent chains hide under the generator's FP64 throughput.  One
+    // __syncthreads per chunk publishes the next buffer.
+    if (do_gen) {
+        int qn = 0;
+        const int iters = gen_iters(0);
+        for (int it = 0; it < iters; ++it) gen_iter(0, it, iters, qn);
+    }
+    __syncthreads();
+    for (int c = 0; c < n_chunks; ++c) {
+        const int iters = (do_gen && c + 1 < n_chunks) ? gen_iters(c + 1) : 0;
+        const int tc = min(T, total_sub - c * T);
+        const int steps = max(iters, tc);
+        int qn = 0;
+        for (int s = 0; s < steps; ++s) {
+            if (s < iters) gen_iter(c + 1, s, iters, qn);
+            if (s < tc && do_rec) rec_step(c, s);
         }
         __syncthreads();
-        if (!valid || (a.mode & 2) || !(econ || cred)) continue;
-        for (int t = 0; t < tc; ++t) {
-            const double* zt = zb + t * D * P + p;
-            auto zcorr = [&](int d) {
-                const FactorCoef& k = coef[d];
-                if (!k.dense) return dadd(dmul(k.v0, zt[k.col0 * P]), dmul(k.v1, zt[k.col1 * P]));
-                double acc = 0.0;
-                for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
-                    acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
-                return acc;
-            };
-            if (econ) {
-                const double r0 = s1, re = s0;
-                const double zr = zcorr(fr), z0 = zcorr(0), zx = zcorr(fx);
-                s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
-                // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
-                const FactorCoef& kx = coef[fx];
-                s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zx));
-                s0 = vasicek_step(re, coef[fr], h, zr);
-                s1 = vasicek_step(r0, coef[0], h, z0);
-            } else {
-                // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
-                const double z0 = zcorr(fg0), z1 = zcorr(fg1);
-                const FactorCoef& k0 = coef[fg0];
-                const FactorCoef& k1 = coef[fg1];
-                s2 = dadd(s2, dmul(s0, h));
-                s3 = dadd(s3, dmul(s1, h));
-                const double gp0 = (s0 < 0.0) ? 0.0 : s0, gp1 = (s1 < 0.0) ? 0.0 : s1;
-                const double nx0 = dadd(dadd(s0, dmul(dmul(k0.c0, dsub(k0.c1, gp0)), h)),
-                                        dmul(dmul(dmul(k0.c2, sqrt(gp0)), sqh), z0));
-                const double nx1 = dadd(dadd(s1, dmul(dmul(k1.c0, dsub(k1.c1, gp1)), h)),
-                                        dmul(dmul(dmul(k1.c2, sqrt(gp1)), sqh), z1));
-                s0 = (nx0 < 0.0) ? 0.0 : nx0;
-                s1 = (nx1 < 0.0) ? 0.0 : nx1;
-            }
-            const int s_done = c * T + t + 1;
-            if (s_done % a.substeps == 0) store(s_done / a.substeps);
-        }
     }
 }
 
