@@ -75,16 +75,30 @@ struct FactorCoef {
     int pad;
 };
 
+// Stream the calling C-ABI entry point works on (set by StreamScope); device
+// buffers are stream-ordered allocations from the device's memory pool, whose
+// release threshold the context raises so repeated runs reuse the memory
+// instead of paying cudaMalloc/cudaFree for gigabyte buffers.
+cudaStream_t& alloc_stream();
+
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+    ~StreamScope() { alloc_stream() = prev; }
+};
+
 struct DeviceBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t stream = nullptr;
     void alloc(size_t b) {
         release();
-        if (b) HCVA_CUDA(cudaMalloc(&p, b));
+        stream = alloc_stream();
+        if (b) HCVA_CUDA(cudaMallocAsync(&p, b, stream));
         bytes = b;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, stream);
         p = nullptr;
         bytes = 0;
     }

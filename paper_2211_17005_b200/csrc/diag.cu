@@ -47,11 +47,12 @@ using namespace hcva;
 // fn 0 = erfc, 1 = exp (z <= 0), 2 = uniform -> normal, 3 = exp(-y^2) from erfc.
 extern "C" hcva_status hcva_diag_special(hcva_ctx* ctx, int fn, const double* x, size_t n, double* out) {
     return guarded([&] {
+        StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
         DeviceBuf dx, dy;
         dx.alloc(n * 8);
         dy.alloc(n * 8);
-        HCVA_CUDA(cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+        HCVA_CUDA(cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
         k_special<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(fn, dx.as<double>(), n,
                                                                                   dy.as<double>());
         ctx->launches++;
@@ -63,6 +64,7 @@ extern "C" hcva_status hcva_diag_special(hcva_ctx* ctx, int fn, const double* x,
 
 extern "C" hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops) {
     return guarded([&] {
+        StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
         DeviceBuf out;
         out.alloc(8);

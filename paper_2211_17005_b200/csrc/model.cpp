@@ -18,6 +18,11 @@ constexpr double kGridTol = 1e-9;  // portfolio.cpp:14
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+cudaStream_t& alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
 bool is_multiple(double x, double step) {  // portfolio.cpp:16-19
     const double q = x / step;
     return std::fabs(q - std::round(q)) < kGridTol * std::max(1.0, std::fabs(q));

@@ -642,7 +642,10 @@ inline unsigned grid1(size_t n, int b) { return static_cast<unsigned>((n + b - 1
 template <typename T>
 void stage(DeviceBuf& buf, const std::vector<T>& v) {
     buf.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
-    if (!v.empty()) HCVA_CUDA(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!v.empty()) {
+        HCVA_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, buf.stream));
+        HCVA_CUDA(cudaStreamSynchronize(buf.stream));
+    }
 }
 
 void check_launch(hcva_ctx* ctx) {
@@ -1012,6 +1015,12 @@ hcva_status hcva_ctx_create(int device, hcva_ctx** out) {
         ctx->device = device;
         ctx->sm_count = prop.multiProcessorCount;
         HCVA_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        // Keep freed pool memory reserved: repeated simulate/label calls then
+        // re-use it instead of returning gigabytes to the driver each time.
+        cudaMemPool_t pool;
+        HCVA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t threshold = UINT64_MAX;
+        HCVA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
         *out = ctx.release();
     });
 }
@@ -1040,6 +1049,7 @@ hcva_status hcva_ctx_launch_count(hcva_ctx* ctx, uint64_t* out) {
 
 hcva_status hcva_rng_draw(hcva_ctx* ctx, uint64_t key, uint64_t start, size_t count, int kind, void* out) {
     return guarded([&] {
+        StreamScope sc__(ctx->stream);
         if (kind < 0 || kind > 3) throw contract_error("hcva_rng_draw: kind must be 0..3");
         HCVA_CUDA(cudaSetDevice(ctx->device));
         DeviceBuf buf;
@@ -1056,6 +1066,7 @@ hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva
                               const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
                               int n_replicas, uint64_t key_market, uint64_t key_defaults, hcva_sim** out) {
     return guarded([&] {
+        StreamScope sc__(ctx->stream);
         if (!grid) throw contract_error("simulate_set: null grid");
         if (n_paths < 1) throw contract_error("simulate_market: n_paths must be >= 1");
         if (path_offset < 0) throw contract_error("simulate_set: negative path offset");
@@ -1085,6 +1096,7 @@ hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva
 hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defaults, int labels_kind,
                            int event_slot) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (sim->start_step != 0 || sim->n_groups != 1) throw contract_error("rerun: outer blocks only");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         record(sim, event_slot, 0);
@@ -1101,6 +1113,7 @@ hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defa
 
 hcva_status hcva_sim_phase_times(hcva_sim* sim, int event_slot, float* ms) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         const size_t base = static_cast<size_t>(event_slot) * 5;
         if (event_slot < 0 || base + 4 >= sim->events.size()) throw contract_error("phase times: no such slot");
         for (int p = 0; p < 4; ++p)
@@ -1113,6 +1126,7 @@ hcva_status hcva_simulate_conditional(hcva_ctx* ctx, const hcva_model* model, co
                                       const double* st_lagged, int start_step, int horizon, int n_inner,
                                       uint64_t key, hcva_sim** out) {
     return guarded([&] {
+        StreamScope sc__(ctx->stream);
         if (!grid) throw contract_error("simulate_conditional_market: null grid");
         std::unique_ptr<hcva_sim> sim(new_sim(ctx, model, grid));
         const Model& m = sim->model;
@@ -1136,6 +1150,7 @@ hcva_status hcva_simulate_conditional(hcva_ctx* ctx, const hcva_model* model, co
 
 hcva_status hcva_sample_defaults(hcva_sim* sim, int n_replicas, uint64_t key) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         prepare_defaults(sim, n_replicas);
         launch_defaults(sim, key);
@@ -1145,6 +1160,7 @@ hcva_status hcva_sample_defaults(hcva_sim* sim, int n_replicas, uint64_t key) {
 
 hcva_status hcva_build_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         prepare_cube(sim, book, n_swaps);
         launch_cube(sim);
@@ -1154,6 +1170,7 @@ hcva_status hcva_build_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps) {
 
 hcva_status hcva_sim_destroy(hcva_sim* sim) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (!sim) return;
         cudaSetDevice(sim->ctx->device);
         cudaStreamSynchronize(sim->ctx->stream);
@@ -1163,6 +1180,7 @@ hcva_status hcva_sim_destroy(hcva_sim* sim) {
 
 hcva_status hcva_sim_dims(const hcva_sim* sim, int* dims) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         dims[0] = sim->M; dims[1] = sim->n; dims[2] = sim->model.E; dims[3] = sim->model.Cn;
         dims[4] = sim->N; dims[5] = sim->start_step; dims[6] = sim->model.D; dims[7] = sim->model.substeps;
     });
@@ -1170,9 +1188,10 @@ hcva_status hcva_sim_dims(const hcva_sim* sim, int* dims) {
 
 hcva_status hcva_sim_tie_counts(const hcva_sim* sim, uint64_t* counts) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (!sim->has_defaults) throw contract_error("tie counts: no default block");
         unsigned long long h[2];
-        HCVA_CUDA(cudaMemcpy(h, sim->ties.p, sizeof h, cudaMemcpyDeviceToHost));
+        copy_out(sim->ctx, h, sim->ties.p, sizeof h);
         counts[0] = h[0];
         counts[1] = h[1];
     });
@@ -1181,6 +1200,7 @@ hcva_status hcva_sim_tie_counts(const hcva_sim* sim, uint64_t* counts) {
 hcva_status hcva_sim_export_market(const hcva_sim* sim, double* rates, double* fx, double* intens,
                                    double* lagged, double* disc, double* hazard) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         hcva_ctx* ctx = sim->ctx;
         HCVA_CUDA(cudaSetDevice(ctx->device));
         const Model& m = sim->model;
@@ -1206,6 +1226,7 @@ hcva_status hcva_sim_export_market(const hcva_sim* sim, double* rates, double* f
 
 hcva_status hcva_sim_export_defaults(const hcva_sim* sim, uint16_t* steps) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (!sim->has_defaults) throw contract_error("export: no default block");
         hcva_ctx* ctx = sim->ctx;
         HCVA_CUDA(cudaSetDevice(ctx->device));
@@ -1221,6 +1242,7 @@ hcva_status hcva_sim_export_defaults(const hcva_sim* sim, uint16_t* steps) {
 
 hcva_status hcva_sim_export_cube(const hcva_sim* sim, double* cube) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (!sim->has_cube) throw contract_error("export: no MtM cube");
         hcva_ctx* ctx = sim->ctx;
         HCVA_CUDA(cudaSetDevice(ctx->device));
@@ -1237,6 +1259,7 @@ hcva_status hcva_sim_export_cube(const hcva_sim* sim, double* cube) {
 
 hcva_status hcva_labels(hcva_sim* sim, int step, int kind, double* out) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         const size_t R = static_cast<size_t>(sim->M) * sim->N;
@@ -1249,6 +1272,7 @@ hcva_status hcva_labels(hcva_sim* sim, int step, int kind, double* out) {
 
 hcva_status hcva_labels_all(hcva_sim* sim, int kind, double* out) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         launch_labels_all(sim, kind);
@@ -1258,6 +1282,7 @@ hcva_status hcva_labels_all(hcva_sim* sim, int kind, double* out) {
 
 hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         if (sim->labels_kind != kind) launch_labels_all(sim, kind);
@@ -1271,6 +1296,7 @@ hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
 
 hcva_status hcva_features(hcva_sim* sim, int step, double* out) {
     return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
         if (!sim->has_defaults) throw contract_error("features: no default block");
         if (step < 0 || step > sim->n) throw contract_error("label step out of range");
         if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
