@@ -165,6 +165,19 @@ hcva_status hcva_labels_all(hcva_sim* sim, int kind, double* out);
 /* CVA profile: out[i] = mean over (k,l) of the step-i labels, i = 0..n (the
  * pathwise CVA estimator E[xi_i]; out[0] is the time-0 CVA).  Host or device. */
 hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out /* [n+1] */);
+/* --- nested Monte Carlo benchmark (validation.cpp:123-179) ---------------- */
+/* nested_cva for n_states outer states at pricing step `step`, batched:
+ * state s = states[s*(3E-1+Cn) ...] laid out as rates[E], log_fx[E-1],
+ * intensities[Cn], lagged_rates[E] (MarketState, market.hpp:58-63);
+ * survived[s*Cc + c-1] != 0 when client c survived to `step`.  Inner path l of
+ * state s draws from split(split(parent_key, s), l) -- parent_key is the key
+ * of the reference's nstream (pipeline.cpp:284-288).  value/std_error[s]
+ * are EstimateWithError (validation.hpp:17-20). */
+hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                  const hcva_swap* book, int n_swaps, const double* states,
+                                  const int* survived, int n_states, int step, int inner,
+                                  uint64_t parent_key, double* value, double* std_error);
+
 /* features_at: row-major (M*N) x (p+q) FP64. */
 hcva_status hcva_features(hcva_sim* sim, int step, double* out);
 

@@ -126,6 +126,8 @@ def lib():
         "hcva_cva_profile": [vp, C.c_int, vp],
         "hcva_diag_fp64_peak": [vp, dptr],
         "hcva_diag_special": [vp, C.c_int, vp, C.c_size_t, vp],
+        "hcva_nested_cva_batch": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
+                                  C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, u64, dptr, dptr],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -150,5 +152,5 @@ EXPORTED = [
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
-    "hcva_diag_fp64_peak", "hcva_diag_special",
+    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch",
 ]

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -149,3 +150,29 @@ struct hcva_sim {
         for (auto e : events) cudaEventDestroy(e);
     }
 };
+
+namespace hcva {
+
+inline unsigned grid1(size_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+// Small host table -> device buffer (stream-ordered, synchronised).
+template <typename T>
+void stage(DeviceBuf& buf, const std::vector<T>& v) {
+    buf.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (!v.empty()) {
+        HCVA_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, buf.stream));
+        HCVA_CUDA(cudaStreamSynchronize(buf.stream));
+    }
+}
+
+// Launch helpers shared by the C-ABI translation units (simulate.cu).
+void check_launch(hcva_ctx* ctx);
+hcva_sim* new_sim(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid);
+void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys, const std::vector<double>& init_state,
+                    int paths_per_group, uint64_t local_offset);
+void launch_market(hcva_sim* sim, uint64_t key0);
+void prepare_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps);
+void launch_cube(hcva_sim* sim);
+void copy_out(hcva_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+}  // namespace hcva

@@ -637,17 +637,6 @@ __global__ void __launch_bounds__(256) k_profile(const double* labels, size_t R,
 
 // ================================================================= host side
 
-inline unsigned grid1(size_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
-
-template <typename T>
-void stage(DeviceBuf& buf, const std::vector<T>& v) {
-    buf.alloc(std::max<size_t>(v.size(), 1) * sizeof(T));
-    if (!v.empty()) {
-        HCVA_CUDA(cudaMemcpyAsync(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, buf.stream));
-        HCVA_CUDA(cudaStreamSynchronize(buf.stream));
-    }
-}
-
 void check_launch(hcva_ctx* ctx) {
     ctx->launches++;
     HCVA_CUDA(cudaGetLastError());

@@ -376,6 +376,48 @@ def build_mtm_cube(sim: SimulationSet, book: np.ndarray) -> SimulationSet:
     return sim
 
 
+def nested_cva(cfg: PipelineConfig, book: np.ndarray, states: Dict[str, np.ndarray], survived: np.ndarray,
+               step: int, inner: int, parent: RandomStream, ctx: Optional[Context] = None):
+    """nested_cva (validation.cpp:123-179) for a batch of outer states.
+
+    states: dict of arrays rates (S,E), log_fx (S,E-1), intens (S,Cn), lagged (S,E);
+    survived: (S, Cc) bool; state s uses parent.split(s) (pipeline.cpp:284-288).
+    Returns (value[S], std_error[S]).
+    """
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    S = states["rates"].shape[0]
+    packed = np.ascontiguousarray(np.concatenate(
+        [states["rates"], states["log_fx"].reshape(S, -1), states["intens"], states["lagged"]], axis=1),
+        dtype=np.float64)
+    surv = np.ascontiguousarray(survived, dtype=np.int32)
+    bk, bp = _swaps(book)
+    val, se = np.zeros(S), np.zeros(S)
+    _lib.check(_lib.lib().hcva_nested_cva_batch(
+        ctx.handle, C.byref(m), C.byref(g), bp, len(bk), packed.ctypes.data_as(_lib.dptr),
+        surv.ctypes.data_as(C.POINTER(C.c_int)), S, step, inner, parent.key, val.ctypes.data_as(_lib.dptr),
+        se.ctypes.data_as(_lib.dptr)))
+    return val, se
+
+
+def nested_relative_rmse(predictions: np.ndarray, nested: np.ndarray):
+    """nested_relative_rmse (validation.cpp:181-210): (value, std_error, excluded_zero, used)."""
+    pred = np.asarray(predictions, dtype=np.float64)
+    nest = np.asarray(nested, dtype=np.float64)
+    if pred.shape != nest.shape or pred.size == 0:
+        raise _lib.ContractError("nested_relative_rmse: size mismatch or empty input")
+    keep = nest != 0.0
+    if not keep.any():
+        raise _lib.NumericError("nested_relative_rmse: all benchmarks are zero")
+    sq = ((pred[keep] - nest[keep]) / nest[keep]) ** 2
+    m = float(np.mean(sq))
+    value = float(np.sqrt(m))
+    se = 0.0
+    if sq.size > 1 and m > 0.0:
+        se = float(np.sqrt(np.var(sq, ddof=1) / sq.size) / (2.0 * value))
+    return value, se, int((~keep).sum()), int(keep.sum())
+
+
 # ---- pybind-surface mirror (hiercva_module.cpp:99-139) ---------------------
 
 def simulate(cfg: PipelineConfig, paths: int = 0, replicas: int = 0):
