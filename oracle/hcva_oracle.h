@@ -108,6 +108,27 @@ int or_nested_cva(const or_model* m, const or_swap* book, int n_swaps, const dou
                   const int* survived, int step, int inner, uint64_t key, double* value,
                   double* std_error);
 
+/* --- regression (regressor.cpp, restated in regress_oracle.c) ---
+ * activation: 0 tanh, 1 sigmoid, 2 softplus, 3 relu.  Flat parameters: for
+ * l = 0..hidden, W_l [fan_out][fan_in] then b_l [fan_out]; then mu. */
+typedef struct {
+    int input_dim;
+    int hidden;
+    int width;
+    int activation;
+} or_net_shape;
+
+size_t or_net_size(const or_net_shape* s);
+void or_init_network(const or_net_shape* s, uint64_t key, double* params);
+int or_fit_scaler(const double* x, int rows, int cols, int passthrough, double* mean, double* scale);
+void or_forward(const or_net_shape* s, const double* params, int head, const double* x, int rows, double* out);
+double or_quadratic_loss(const or_net_shape* s, const double* params, int head, const double* x,
+                         const double* y, int rows, double* grads);
+int or_refit(const or_net_shape* s, double* params, const double* x, const double* y, int rows, double ridge);
+int or_train_base(const or_net_shape* s, const double* x, const double* y, int rows, int n_batches,
+                  int epochs, double lr, int adam, double ridge, const double* init, double* best,
+                  double* epoch_losses, double* best_loss, int* best_epoch);
+
 /* --- timed CPU baseline of the scenario pipeline ---
  * simulate_set (pipeline.cpp:63-70) with market = split(0), defaults =
  * split(1) of `key_sim`, then for every step i = n..1 the label source

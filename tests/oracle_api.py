@@ -256,6 +256,87 @@ class Oracle:
         return v.value, se.value
 
 
+    # -- regression (regressor.cpp restated) -------------------------------
+    def _shape(self, d, hidden, width, activation=0):
+        class S(C.Structure):
+            _fields_ = [("input_dim", C.c_int), ("hidden", C.c_int), ("width", C.c_int), ("activation", C.c_int)]
+        return S(d, hidden, width, activation)
+
+    def net_size(self, d, hidden, width):
+        self.lib.or_net_size.restype = C.c_size_t
+        return self.lib.or_net_size(C.byref(self._shape(d, hidden, width)))
+
+    def init_network(self, d, hidden, width, key):
+        p = np.zeros(self.net_size(d, hidden, width))
+        self.lib.or_init_network(C.byref(self._shape(d, hidden, width)), _u64(key), _ptr(p))
+        return p
+
+    def fit_scaler(self, x, passthrough):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        mean, scale = np.zeros(x.shape[1]), np.zeros(x.shape[1])
+        self.lib.or_fit_scaler(_ptr(x), x.shape[0], x.shape[1], passthrough, _ptr(mean), _ptr(scale))
+        return mean, scale
+
+    def forward(self, p, x, hidden, width, activation=0, head=True):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        out = np.zeros(x.shape[0])
+        self.lib.or_forward(C.byref(self._shape(x.shape[1], hidden, width, activation)), _ptr(p), int(head),
+                            _ptr(x), x.shape[0], _ptr(out))
+        return out
+
+    def loss(self, p, x, y, hidden, width, activation=0, head=False, grads=True):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        g = np.zeros_like(p) if grads else None
+        self.lib.or_quadratic_loss.restype = C.c_double
+        v = self.lib.or_quadratic_loss(C.byref(self._shape(x.shape[1], hidden, width, activation)), _ptr(p),
+                                       int(head), _ptr(x), _ptr(y), x.shape[0], _ptr(g) if grads else _dp())
+        return (v, g) if grads else v
+
+    def refit(self, p, x, y, hidden, width, ridge=1e-8, activation=0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        p = np.array(p, dtype=np.float64)
+        self.lib.or_refit(C.byref(self._shape(x.shape[1], hidden, width, activation)), _ptr(p), _ptr(x), _ptr(y),
+                          x.shape[0], C.c_double(ridge))
+        return p
+
+    def train_base(self, x, y, init, hidden, width, n_batches, epochs, lr=1e-3, adam=True, ridge=1e-8,
+                   activation=0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        init = np.ascontiguousarray(init, dtype=np.float64)
+        best = np.zeros_like(init)
+        losses = np.zeros(epochs)
+        bl, be = C.c_double(), C.c_int()
+        self._check(self.lib.or_train_base(
+            C.byref(self._shape(x.shape[1], hidden, width, activation)), _ptr(x), _ptr(y), x.shape[0], n_batches,
+            epochs, C.c_double(lr), int(adam), C.c_double(ridge), _ptr(init), _ptr(best), _ptr(losses),
+            C.byref(bl), C.byref(be)))
+        return best, dict(epoch_losses=losses, best_loss=bl.value, best_epoch=be.value)
+
+    def backward_learn(self, n_steps, source, seed, hidden, width, n_batches, epochs, lr=1e-3, adam=True,
+                       ridge=1e-8, activation=0):
+        """regressor.cpp:354-395 (Alg. 2): i = n..1, fit_scaler, init at n (mu = label mean)
+        else warm start from step i+1's best; returns {i: (params, mean, scale, report)}."""
+        out, carry = {}, None
+        for i in range(n_steps, 0, -1):
+            x, y, passthrough = source(i)
+            mean, scale = self.fit_scaler(x, passthrough)
+            xs = (x - mean) / scale
+            if i == n_steps:
+                start = self.init_network(x.shape[1], hidden, width, self.key(seed, 0xBEEF, i))
+                start[-1] = float(np.mean(y))
+            else:
+                start = carry
+            best, rep = self.train_base(xs, y, start, hidden, width, n_batches, epochs, lr, adam, ridge, activation)
+            carry = best
+            out[i] = (best, mean, scale, rep)
+        return out
+
+
 _cache = {}
 
 
