@@ -178,6 +178,46 @@ hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const 
                                   const int* survived, int n_states, int step, int inner,
                                   uint64_t parent_key, double* value, double* std_error);
 
+/* --- regression (regressor.hpp:33-139) ----------------------------------- */
+typedef struct {              /* TrainConfig, regressor.hpp:33-44 */
+    int epochs;               /* >= 2, head switch at floor(epochs/2)  */
+    int n_batches;            /* must divide the row count             */
+    int hidden_layers;        /* 1..4                                   */
+    int width;                /* 1..128                                 */
+    int activation;           /* 0 tanh, 1 sigmoid, 2 softplus, 3 relu  */
+    int adam;                 /* 1 Adam, 0 plain SGD                    */
+    double learning_rate;
+    double ridge;
+    uint64_t seed;            /* init stream RandomStream(seed).split(0xBEEF).split(n) */
+} hcva_train_cfg;
+typedef struct hcva_models hcva_models; /* TrainedModelSequence, device resident */
+
+/* Flat parameter layout: for l = 0..hidden, W_l [fan_out][fan_in] row-major
+ * then b_l [fan_out]; then mu (NetworkParams, regressor.hpp:21-31). */
+hcva_status hcva_net_size(const hcva_train_cfg* cfg, int input_dim, int* n_params);
+/* init_network (regressor.cpp:172-189) from a stream key; mu = 0. */
+hcva_status hcva_init_network(const hcva_train_cfg* cfg, int input_dim, uint64_t key, double* params);
+/* quadratic_loss (regressor.cpp:115-158) on host rows x [rows][input_dim];
+ * grads may be NULL. */
+hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                                int head, const double* x, const double* y, int rows, double* loss, double* grads);
+/* train_base (regressor.cpp:265-347) on host rows, contiguous batches. */
+hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
+                            const double* y, int rows, const double* init, double* best, double* epoch_losses,
+                            double* best_loss, int* best_epoch);
+/* backward_learn (regressor.cpp:354-395) fed by the label source of
+ * make_label_source (pipeline.cpp:72-111) on a simulated set; label_kind 0 =
+ * defaults, 1 = intensity.  Everything stays on the GPU. */
+hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out);
+/* info: [0] n_steps [1] input_dim [2] n_params [3] epochs */
+hcva_status hcva_models_info(const hcva_models* m, int* info /* [4] */);
+/* Per-step model (steps[i-1]): params, scaler mean/scale, report.  NULL skips. */
+hcva_status hcva_models_get(const hcva_models* m, int step, double* params, double* mean, double* scale,
+                            double* epoch_losses, double* best_loss, int* best_epoch);
+/* TrainedModelSequence::predict (regressor.cpp:349-352) on sim's features at step. */
+hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* out /* [M*N] */);
+hcva_status hcva_models_destroy(hcva_models* m);
+
 /* features_at: row-major (M*N) x (p+q) FP64. */
 hcva_status hcva_features(hcva_sim* sim, int step, double* out);
 

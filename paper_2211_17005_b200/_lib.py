@@ -43,6 +43,12 @@ class Swap(C.Structure):
                 ("tenor", C.c_double), ("maturity", C.c_double), ("fixed_rate", C.c_double)]
 
 
+class TrainCfg(C.Structure):
+    _fields_ = [("epochs", C.c_int), ("n_batches", C.c_int), ("hidden_layers", C.c_int), ("width", C.c_int),
+                ("activation", C.c_int), ("adam", C.c_int), ("learning_rate", C.c_double), ("ridge", C.c_double),
+                ("seed", u64)]
+
+
 # Status codes (include/hcva_gpu.h) -> exception types of the reference
 # (proj/include/hiercva/errors.hpp:9-25, hiercva_module.cpp:49-50).
 class HcvaError(RuntimeError):
@@ -128,6 +134,16 @@ def lib():
         "hcva_diag_special": [vp, C.c_int, vp, C.c_size_t, vp],
         "hcva_nested_cva_batch": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
                                   C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, u64, dptr, dptr],
+        "hcva_net_size": [C.POINTER(TrainCfg), C.c_int, C.POINTER(C.c_int)],
+        "hcva_init_network": [C.POINTER(TrainCfg), C.c_int, u64, dptr],
+        "hcva_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, dptr, dptr],
+        "hcva_train_base": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr, dptr, dptr, dptr,
+                            C.POINTER(C.c_int)],
+        "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
+        "hcva_models_info": [vp, C.POINTER(C.c_int)],
+        "hcva_models_get": [vp, C.c_int, dptr, dptr, dptr, dptr, dptr, C.POINTER(C.c_int)],
+        "hcva_predict": [vp, vp, C.c_int, dptr],
+        "hcva_models_destroy": [vp],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)
@@ -152,5 +168,7 @@ EXPORTED = [
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
-    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch",
+    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch", "hcva_net_size",
+    "hcva_init_network", "hcva_quadratic_loss", "hcva_train_base", "hcva_backward_learn", "hcva_models_info",
+    "hcva_models_get", "hcva_predict", "hcva_models_destroy",
 ]

@@ -174,5 +174,6 @@ void launch_market(hcva_sim* sim, uint64_t key0);
 void prepare_cube(hcva_sim* sim, const hcva_swap* book, int n_swaps);
 void launch_cube(hcva_sim* sim);
 void copy_out(hcva_ctx* ctx, void* dst, const void* src, size_t bytes);
+void launch_labels_all(hcva_sim* sim, int kind);
 
 }  // namespace hcva

@@ -1,0 +1,936 @@
+// regress.cu -- K5: the backward MLP regression of the conditional CVA
+// (proj/src/regressor.cpp, Alg. 1 train_base :265-347, Alg. 2 backward_learn
+// :354-395), device-resident end to end.
+//
+// Per pricing step i = n..1: the feature rows of every replica (k,l)
+// (labels.cpp:142-167) are built on the device and standardised with the
+// scaler fitted over all rows (regressor.cpp:84-95); the network starts from
+// Glorot init at i = n (host RNG, same stream as the reference) or from step
+// i+1's best; train_base runs E epochs of |B| contiguous batches with Adam,
+// the closed-form ridge refit and head switch at epoch floor(E/2), full-sample
+// evaluation and best tracking each epoch -- all without host round trips.
+//
+// Kernels:
+//   k_sgd       forward + backward of one batch tile (TR rows per CTA):
+//               activations in shared memory, FP32 FMA tiles, per-CTA partial
+//               gradients (FP32) and loss (FP64)
+//   k_adam      fixed-order FP64 reduction of the partials + Adam (:236-261)
+//               on the FP64 master parameters, FP32 compute copy
+//   k_eval      full-sample forward: loss with the positive head, min of the
+//               plain-head fit (head switch), predictions
+//   k_gram      Gram matrix and rhs of [z_h, 1] (refit, :191-213), FP64
+//   k_refit     one-CTA reduction + ridge + LDL^T solve of the (u+1)^2 system
+//   k_switch / k_track   head switch (:299-314) and best tracking (:316-327)
+// Reductions are over fixed CTA partitions in fixed order: results are
+// deterministic and independent of scheduling.
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace hcva {
+
+constexpr int kMaxLayers = 5;  // hidden layers <= 4
+
+struct NetDims {
+    int d, h, u, act, P;
+    int off[kMaxLayers + 1];  // W_l offset; b_l = off[l] + fout*fin
+    int fin[kMaxLayers + 1], fout[kMaxLayers + 1];
+};
+
+NetDims make_dims(int d, int h, int u, int act) {
+    if (h < 1 || h > kMaxLayers - 1) throw config_error("training: hidden_layers must be in 1..4");
+    if (u < 1 || u > 128) throw config_error("training: width must be in 1..128");
+    NetDims n{};
+    n.d = d;
+    n.h = h;
+    n.u = u;
+    n.act = act;
+    int off = 0, fin = d;
+    for (int l = 0; l <= h; ++l) {
+        const int fout = (l == h) ? 1 : u;
+        n.off[l] = off;
+        n.fin[l] = fin;
+        n.fout[l] = fout;
+        off += fout * fin + fout;
+        fin = fout;
+    }
+    n.P = off + 1;  // + mu
+    return n;
+}
+
+// regressor.cpp:35-57.  Derivatives from the activation value: tanh 1-a^2,
+// sigmoid a(1-a), softplus sigma(z) = 1 - exp(-a), relu 1{a>0}.
+__device__ __forceinline__ float act_fwd(int a, float z) {
+    switch (a) {
+        case 0: return tanhf(z);
+        case 1: return 1.0f / (1.0f + expf(-z));
+        case 2: return fmaxf(z, 0.0f) + log1pf(expf(-fabsf(z)));
+        default: return fmaxf(z, 0.0f);
+    }
+}
+__device__ __forceinline__ float act_der(int a, float v) {
+    switch (a) {
+        case 0: return 1.0f - v * v;
+        case 1: return v * (1.0f - v);
+        case 2: return -expm1f(-v);
+        default: return v > 0.0f ? 1.0f : 0.0f;
+    }
+}
+
+// Shared-memory plan of one tile: params (P floats), x tile [TR][d+1],
+// h activation buffers [TR][u+1] (reused in place as gradient buffers).
+__host__ __device__ inline size_t tile_smem(const NetDims& n, int TR) {
+    return sizeof(float) * (static_cast<size_t>(n.P) + 1 + static_cast<size_t>(TR) * (n.d + 1) +
+                            static_cast<size_t>(n.h) * TR * (n.u + 1)) + 64 * sizeof(double);
+}
+
+// Forward of the rows of a tile: thread r owns row r.  Returns f (pre-head output).
+__device__ float tile_forward(const NetDims& n, const float* W, const float* xs, float* acts, int TR, int r) {
+    const int ld_in0 = n.d + 1, ld = n.u + 1;
+    for (int l = 0; l < n.h; ++l) {
+        const float* in = (l == 0) ? xs + r * ld_in0 : acts + (l - 1) * TR * ld + r * ld;
+        float* out = acts + l * TR * ld + r * ld;
+        const float* Wl = W + n.off[l];
+        const int fin = n.fin[l], fout = n.fout[l];
+        const float* bl = Wl + fout * fin;
+        for (int o0 = 0; o0 < fout; o0 += 8) {
+            float acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = (o0 + q < fout) ? bl[o0 + q] : 0.0f;
+            for (int j = 0; j < fin; ++j) {
+                const float v = in[j];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (o0 + q < fout) acc[q] = fmaf(v, Wl[(o0 + q) * fin + j], acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (o0 + q < fout) out[o0 + q] = act_fwd(n.act, acc[q]);
+        }
+    }
+    const float* top = acts + (n.h - 1) * TR * ld + r * ld;
+    const float* w = W + n.off[n.h];
+    float f = w[n.u];
+    for (int j = 0; j < n.u; ++j) f = fmaf(top[j], w[j], f);
+    return f;
+}
+
+// Partial gradient of W_l over the tile rows: sum_r g[r][o] in[r][j], 4x4 blocks per thread.
+__device__ void tile_outer(const float* g, int ldg, const float* in, int ldi, int TR, int rows, int fout, int fin,
+                           float* gW, float* gb) {
+    const int bo = (fout + 3) / 4, bj = (fin + 3) / 4;
+    for (int blk = threadIdx.x; blk < bo * bj; blk += blockDim.x) {
+        const int o0 = (blk / bj) * 4, j0 = (blk % bj) * 4;
+        float acc[4][4] = {};
+        for (int r = 0; r < rows; ++r) {
+            float gv[4], iv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                gv[q] = (o0 + q < fout) ? g[r * ldg + o0 + q] : 0.0f;
+                iv[q] = (j0 + q < fin) ? in[r * ldi + j0 + q] : 0.0f;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(gv[a], iv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (o0 + a < fout && j0 + b < fin) gW[(o0 + a) * fin + j0 + b] = acc[a][b];
+    }
+    for (int o = threadIdx.x; o < fout; o += blockDim.x) {
+        float s = 0.0f;
+        for (int r = 0; r < rows; ++r) s += g[r * ldg + o];
+        gb[o] = s;
+    }
+}
+
+__device__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    return s;  // valid in thread 0
+}
+
+// One batch tile: rows [row0 + blockIdx.x*TR, min(+TR, row_end)).  Writes the
+// CTA's partial gradient (FP32, parameter layout incl. mu) and partial
+// sum of squared residuals (FP64).  nb = batch size (loss normaliser).
+__global__ void k_sgd(NetDims n, const float* X, const double* y, long row0, long row_end, const float* params,
+                      int head, double nb, float* gpart, double* lpart, int TR) {
+    extern __shared__ double smd[];
+    float* W = reinterpret_cast<float*>(smd);
+    float* xs = W + n.P + 1;
+    float* acts = xs + TR * (n.d + 1);
+    double* red = reinterpret_cast<double*>(acts + n.h * TR * (n.u + 1) + 1);
+    red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
+    const long base = row0 + static_cast<long>(blockIdx.x) * TR;
+    const int rows = static_cast<int>(min(static_cast<long>(TR), row_end - base));
+    for (int i = threadIdx.x; i < n.P; i += blockDim.x) W[i] = params[i];
+    for (int i = threadIdx.x; i < rows * n.d; i += blockDim.x) {
+        const int r = i / n.d, c = i % n.d;
+        xs[r * (n.d + 1) + c] = X[(base + r) * n.d + c];
+    }
+    __syncthreads();
+    const int r = threadIdx.x;
+    const int ld = n.u + 1;
+    const float mu = W[n.P - 1];
+    double resid2 = 0.0, dmu = 0.0;
+    float dd = 0.0f;
+    if (r < rows) {
+        const float f = tile_forward(n, W, xs, acts, TR, r);
+        const float pred = ((head && f < 0.0f) ? 0.0f : f) + mu;
+        const double resid = static_cast<double>(pred) - y[base + r];
+        resid2 = resid * resid;
+        dmu = 2.0 * resid / nb;
+        dd = static_cast<float>(dmu);
+        if (head && !(f > 0.0f)) dd = 0.0f;
+    }
+    const double lsum = block_sum(resid2, red);
+    const double msum = block_sum(dmu, red);
+    float* gout = gpart + static_cast<size_t>(blockIdx.x) * n.P;
+    if (threadIdx.x == 0) {
+        lpart[blockIdx.x] = lsum;
+        gout[n.P - 1] = static_cast<float>(msum);
+    }
+    // Output layer: gw[j] = sum_r dd_r z_r[j], gb = sum_r dd_r; stash dd in xs[r][d].
+    if (r < rows) xs[r * (n.d + 1) + n.d] = dd;
+    __syncthreads();
+    {
+        const float* top = acts + (n.h - 1) * TR * ld;
+        float* gw = gout + n.off[n.h];
+        for (int j = threadIdx.x; j <= n.u; j += blockDim.x) {
+            float s = 0.0f;
+            for (int rr = 0; rr < rows; ++rr) s = fmaf(xs[rr * (n.d + 1) + n.d], (j < n.u) ? top[rr * ld + j] : 1.0f, s);
+            gw[j] = s;
+        }
+    }
+    __syncthreads();
+    // g = dd w (x) act'(z_{h}) in place of the top activations.
+    if (r < rows) {
+        float* top = acts + (n.h - 1) * TR * ld + r * ld;
+        const float* w = W + n.off[n.h];
+        for (int j = 0; j < n.u; ++j) top[j] = dd * w[j] * act_der(n.act, top[j]);
+    }
+    __syncthreads();
+    for (int l = n.h - 1; l >= 0; --l) {
+        const float* g = acts + l * TR * ld;
+        const float* in = (l == 0) ? xs : acts + (l - 1) * TR * ld;
+        const int ldi = (l == 0) ? n.d + 1 : ld;
+        float* gW = gout + n.off[l];
+        tile_outer(g, ld, in, ldi, TR, rows, n.fout[l], n.fin[l], gW, gW + n.fout[l] * n.fin[l]);
+        if (l > 0) {
+            // g_prev[j] = sum_o g[o] W_l[o][j], times act'(z_{l}) -- in place of act[l-1].
+            __syncthreads();
+            if (r < rows) {
+                const float* Wl = W + n.off[l];
+                float* prev = acts + (l - 1) * TR * ld + r * ld;
+                const float* gr = g + r * ld;
+                for (int j = 0; j < n.u; ++j) {
+                    float s = 0.0f;
+                    for (int o = 0; o < n.u; ++o) s = fmaf(gr[o], Wl[o * n.u + j], s);
+                    prev[j] = s * act_der(n.act, prev[j]);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Fixed-order reduction of the tile partials + optimiser step (regressor.cpp:236-261).
+__global__ void k_adam(int P, const float* gpart, int nct, const double* lpart, double nb, double* p64, float* p32,
+                       double* m, double* v, long t, double lr, int adam, int* nonfinite) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        double s = 0.0;
+        for (int c = 0; c < nct; ++c) s += lpart[c];
+        if (!isfinite(s / nb)) atomicExch(nonfinite, 1);
+    }
+    if (i >= P) return;
+    double g = 0.0;
+    for (int c = 0; c < nct; ++c) g += static_cast<double>(gpart[static_cast<size_t>(c) * P + i]);
+    double w = p64[i];
+    if (adam) {
+        const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+        const double c1 = 1.0 - pow(b1, static_cast<double>(t)), c2 = 1.0 - pow(b2, static_cast<double>(t));
+        const double mi = b1 * m[i] + (1.0 - b1) * g;
+        const double vi = b2 * v[i] + (1.0 - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        w -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+    } else {
+        w -= lr * g;
+    }
+    p64[i] = w;
+    p32[i] = static_cast<float>(w);
+}
+
+// Full-sample forward over tiles (grid-stride, fixed tile->CTA map).
+// mode bit 0: loss with the positive head -> lpart; bit 1: min of the plain
+// fit f + mu -> mpart; bit 2: predictions (head on) -> pred.
+__global__ void k_eval(NetDims n, const float* X, const double* y, long R, const float* params, int mode,
+                       double* lpart, double* mpart, double* pred, int TR) {
+    extern __shared__ double smd[];
+    float* W = reinterpret_cast<float*>(smd);
+    float* xs = W + n.P + 1;
+    float* acts = xs + TR * (n.d + 1);
+    double* red = reinterpret_cast<double*>(acts + n.h * TR * (n.u + 1) + 1);
+    red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
+    for (int i = threadIdx.x; i < n.P; i += blockDim.x) W[i] = params[i];
+    const float mu = params[n.P - 1];
+    double lacc = 0.0, macc = INFINITY;
+    const long ntiles = (R + TR - 1) / TR;
+    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long base = tile * TR;
+        const int rows = static_cast<int>(min(static_cast<long>(TR), R - base));
+        __syncthreads();
+        for (int i = threadIdx.x; i < rows * n.d; i += blockDim.x) {
+            const int r = i / n.d, c = i % n.d;
+            xs[r * (n.d + 1) + c] = X[(base + r) * n.d + c];
+        }
+        __syncthreads();
+        const int r = threadIdx.x;
+        if (r < rows) {
+            const float f = tile_forward(n, W, xs, acts, TR, r);
+            const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
+            if (mode & 1) {
+                const double res = ph - y[base + r];
+                lacc += res * res;
+            }
+            if (mode & 2) macc = fmin(macc, static_cast<double>(f + mu));
+            if (mode & 4) pred[base + r] = ph;
+        }
+    }
+    if (mode & 1) {
+        const double s = block_sum(lacc, red);
+        if (threadIdx.x == 0) lpart[blockIdx.x] = s;
+    }
+    if (mode & 2) {
+        for (int o = 16; o > 0; o >>= 1) macc = fmin(macc, __shfl_down_sync(0xffffffffu, macc, o));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = macc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double mn = INFINITY;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mn = fmin(mn, red[i]);
+            mpart[blockIdx.x] = mn;
+        }
+    }
+}
+
+// Gram of [z_h, 1] (upper triangle, row-major) and rhs sum z (y - mu) over the
+// CTA's tiles, accumulated in FP64 into the CTA's own partial slot.
+// gpart[cta][(u+1)(u+2)/2 + (u+1)].
+__global__ void k_gram(NetDims n, const float* X, const double* y, long R, const float* params, double* gpart,
+                       int TR) {
+    extern __shared__ double smd[];
+    float* W = reinterpret_cast<float*>(smd);
+    float* xs = W + n.P + 1;
+    float* acts = xs + TR * (n.d + 1);
+    const int ld = n.u + 1, m = n.u + 1, tri = m * (m + 1) / 2, npair = tri + m;
+    for (int i = threadIdx.x; i < n.P; i += blockDim.x) W[i] = params[i];
+    const double mu = params[n.P - 1];
+    double* out = gpart + static_cast<size_t>(blockIdx.x) * npair;
+    for (int idx = threadIdx.x; idx < npair; idx += blockDim.x) out[idx] = 0.0;
+    const long ntiles = (R + TR - 1) / TR;
+    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long base = tile * TR;
+        const int rows = static_cast<int>(min(static_cast<long>(TR), R - base));
+        __syncthreads();
+        for (int i = threadIdx.x; i < rows * n.d; i += blockDim.x) {
+            const int r = i / n.d, c = i % n.d;
+            xs[r * (n.d + 1) + c] = X[(base + r) * n.d + c];
+        }
+        __syncthreads();
+        if (static_cast<int>(threadIdx.x) < rows) {
+            const int r = threadIdx.x;
+            (void)tile_forward(n, W, xs, acts, TR, r);
+            acts[(n.h - 1) * TR * ld + r * ld + n.u] = 1.0f;
+        }
+        __syncthreads();
+        const float* top = acts + (n.h - 1) * TR * ld;
+        int a = 0, rem = threadIdx.x;  // idx -> (a, b) walk, advanced by blockDim each step
+        for (int idx = threadIdx.x; idx < npair; idx += blockDim.x) {
+            double s = 0.0;
+            if (idx < tri) {
+                while (rem >= m - a) {
+                    rem -= m - a;
+                    ++a;
+                }
+                const int b = a + rem;
+                for (int rr = 0; rr < rows; ++rr) s += static_cast<double>(top[rr * ld + a]) * top[rr * ld + b];
+                rem += blockDim.x;
+            } else {
+                const int c = idx - tri;
+                for (int rr = 0; rr < rows; ++rr) s += static_cast<double>(top[rr * ld + c]) * (y[base + rr] - mu);
+            }
+            out[idx] += s;
+        }
+    }
+}
+
+// One CTA: reduce the Gram partials (fixed order), ridge lam = max(ridge tr/(u+1), 1e-300),
+// LDL^T solve, write the output layer (regressor.cpp:191-213).
+__global__ void k_refit(NetDims n, const double* gpart, int nct, double ridge, double* p64, float* p32) {
+    extern __shared__ double sm[];
+    const int m = n.u + 1, tri = m * (m + 1) / 2, stride = tri + m;
+    double* G = sm;           // [m][m]
+    double* rhs = G + m * m;  // [m]
+    double* D = rhs + m;      // [m]
+    for (int idx = threadIdx.x; idx < stride; idx += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nct; ++c) s += gpart[static_cast<size_t>(c) * stride + idx];
+        if (idx < tri) {
+            int a = 0, rem = idx;
+            while (rem >= m - a) {
+                rem -= m - a;
+                ++a;
+            }
+            const int b = a + rem;
+            G[a * m + b] = s;
+            G[b * m + a] = s;
+        } else {
+            rhs[idx - tri] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tr = 0.0;
+        for (int a = 0; a < m; ++a) tr += G[a * m + a];
+        const double lam = fmax(ridge * tr / m, 1e-300);
+        for (int a = 0; a < m; ++a) G[a * m + a] += lam;
+    }
+    __syncthreads();
+    // LDL^T in place (lower part of G holds L), column by column.
+    for (int j = 0; j < m; ++j) {
+        if (threadIdx.x == 0) {
+            double dj = G[j * m + j];
+            for (int k = 0; k < j; ++k) dj -= G[j * m + k] * G[j * m + k] * D[k];
+            D[j] = dj;
+        }
+        __syncthreads();
+        for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
+            double v = G[i * m + j];
+            for (int k = 0; k < j; ++k) v -= G[i * m + k] * G[j * m + k] * D[k];
+            G[i * m + j] = v / D[j];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < m; ++i) {
+            double v = rhs[i];
+            for (int k = 0; k < i; ++k) v -= G[i * m + k] * rhs[k];
+            rhs[i] = v;
+        }
+        for (int i = 0; i < m; ++i) rhs[i] /= D[i];
+        for (int i = m - 1; i >= 0; --i) {
+            double v = rhs[i];
+            for (int k = i + 1; k < m; ++k) v -= G[k * m + i] * rhs[k];
+            rhs[i] = v;
+        }
+        const int o = n.off[n.h];
+        for (int c = 0; c < m; ++c) {
+            p64[o + c] = rhs[c];
+            p32[o + c] = static_cast<float>(rhs[c]);
+        }
+    }
+}
+
+// Head switch (regressor.cpp:299-314): mu_new = max(0, min fit), output bias += mu - mu_new,
+// Adam state reset.
+__global__ void k_switch(NetDims n, const double* mpart, int nct, double* p64, float* p32, double* m, double* v) {
+    for (int i = threadIdx.x; i < n.P; i += blockDim.x) {
+        m[i] = 0.0;
+        v[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        double mn = INFINITY;
+        for (int c = 0; c < nct; ++c) mn = fmin(mn, mpart[c]);
+        const double mu_new = fmax(0.0, mn);
+        const int bo = n.off[n.h] + n.u;
+        p64[bo] += p64[n.P - 1] - mu_new;
+        p64[n.P - 1] = mu_new;
+        p32[bo] = static_cast<float>(p64[bo]);
+        p32[n.P - 1] = static_cast<float>(mu_new);
+    }
+}
+
+// Epoch bookkeeping (regressor.cpp:316-327): record the full-sample loss,
+// keep the best parameters on a strict improvement.
+__global__ void k_track(int P, const double* lpart, int nct, double R, int epoch, const double* p64, double* best,
+                        double* losses, double* best_loss, int* best_epoch, int* nonfinite) {
+    __shared__ int improved;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int c = 0; c < nct; ++c) s += lpart[c];
+        const double ev = s / R;
+        losses[epoch - 1] = ev;
+        if (!isfinite(ev)) *nonfinite = 1;
+        improved = ev < *best_loss;
+        if (improved) {
+            *best_loss = ev;
+            *best_epoch = epoch;
+        }
+    }
+    __syncthreads();
+    if (improved)
+        for (int i = threadIdx.x; i < P; i += blockDim.x) best[i] = p64[i];
+}
+
+__global__ void k_to_f32(const double* a, float* b, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = static_cast<float>(a[i]);
+}
+
+__global__ void k_set_mu_mean(const double* y, long R, double* p64, float* p32, int P) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long r = threadIdx.x; r < R; r += blockDim.x) s += y[r];
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        p64[P - 1] = t / static_cast<double>(R);
+        p32[P - 1] = static_cast<float>(t / static_cast<double>(R));
+    }
+}
+
+// ---------------------------------------------------------------- trainer
+
+struct Trainer {
+    hcva_ctx* ctx;
+    NetDims n;
+    int TR = 128, eval_ctas = 0;
+    DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
+    int max_tiles = 0;
+
+    Trainer(hcva_ctx* c, const NetDims& dims, long max_batch) : ctx(c), n(dims) {
+        while (TR > 32 && tile_smem(n, TR) > 200 * 1024) TR /= 2;
+        if (tile_smem(n, TR) > 227 * 1024) throw config_error("training: network too wide for the tile kernel");
+        const size_t smem = tile_smem(n, TR);
+        HCVA_CUDA(cudaFuncSetAttribute(k_sgd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        HCVA_CUDA(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        HCVA_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 1;
+        HCVA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval, TR, smem));
+        eval_ctas = std::max(1, per_sm) * ctx->sm_count;
+        max_tiles = static_cast<int>((max_batch + TR - 1) / TR);
+        const size_t P = n.P;
+        p64.alloc(P * 8);
+        p32.alloc(P * 4);
+        m.alloc(P * 8);
+        v.alloc(P * 8);
+        best.alloc(P * 8);
+        gpart.alloc(static_cast<size_t>(std::max(max_tiles, 1)) * P * 4);
+        lpart.alloc(static_cast<size_t>(std::max(max_tiles, eval_ctas)) * 8);
+        mpart.alloc(static_cast<size_t>(eval_ctas) * 8);
+        const size_t mm = n.u + 1;
+        gram.alloc(static_cast<size_t>(eval_ctas) * (mm * (mm + 1) / 2 + mm) * 8);
+        flag.alloc(4);
+        best_loss.alloc(8);
+        best_epoch.alloc(4);
+    }
+
+    size_t smem() const { return tile_smem(n, TR); }
+
+    void set_params(const double* host_or_dev) {
+        HCVA_CUDA(cudaMemcpyAsync(p64.p, host_or_dev, n.P * 8, cudaMemcpyDefault, ctx->stream));
+        k_to_f32<<<grid1(n.P, 256), 256, 0, ctx->stream>>>(p64.as<double>(), p32.as<float>(), n.P);
+        check_launch(ctx);
+    }
+
+    void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
+        const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);
+        k_sgd<<<tiles, TR, smem(), ctx->stream>>>(n, X, y, b0, b1, p32.as<float>(), head, static_cast<double>(b1 - b0),
+                                                 gpart.as<float>(), lpart.as<double>(), TR);
+        check_launch(ctx);
+        k_adam<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, lpart.as<double>(),
+                                                         static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
+                                                         m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>());
+        check_launch(ctx);
+    }
+
+    void eval(const float* X, const double* y, long R, int mode, double* pred) {
+        k_eval<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), mode, lpart.as<double>(),
+                                                      mpart.as<double>(), pred, TR);
+        check_launch(ctx);
+    }
+
+    void refit(const float* X, const double* y, long R, double ridge) {
+        k_gram<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), gram.as<double>(), TR);
+        check_launch(ctx);
+        const int mm = n.u + 1;
+        const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
+        HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        k_refit<<<1, 128, sm, ctx->stream>>>(n, gram.as<double>(), eval_ctas, ridge, p64.as<double>(), p32.as<float>());
+        check_launch(ctx);
+    }
+
+    // train_base (regressor.cpp:265-347) on device-resident X [R][d] (FP32), y [R] (FP64).
+    // losses_dev: [epochs] (device).  Parameters start in p64/p32; the best end in `best`.
+    void train_base(const float* X, const double* y, long R, int epochs, int n_batches, double lr, int adam,
+                    double ridge, double* losses_dev) {
+        if (epochs < 2) throw config_error("training: epochs must be >= 2 (head switch at E/2)");
+        if (n_batches < 1 || R % n_batches != 0) throw config_error("make_batches: batch count must divide M*N");
+        const long bs = R / n_batches;
+        const double inf = INFINITY;
+        HCVA_CUDA(cudaMemcpyAsync(best_loss.p, &inf, 8, cudaMemcpyHostToDevice, ctx->stream));
+        HCVA_CUDA(cudaMemsetAsync(best_epoch.p, 0, 4, ctx->stream));
+        HCVA_CUDA(cudaMemsetAsync(m.p, 0, n.P * 8, ctx->stream));
+        HCVA_CUDA(cudaMemsetAsync(v.p, 0, n.P * 8, ctx->stream));
+        HCVA_CUDA(cudaMemcpyAsync(best.p, p64.p, n.P * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));  // &inf lives on this frame
+        int head = 0;
+        long t = 0;
+        const int sw = epochs / 2;
+        for (int e = 1; e <= epochs; ++e) {
+            for (int b = 0; b < n_batches; ++b) sgd_step(X, y, b * bs, (b + 1) * bs, head, ++t, lr, adam);
+            if (e == sw) {
+                refit(X, y, R, ridge);
+                eval(X, y, R, 2, nullptr);
+                k_switch<<<1, 256, 0, ctx->stream>>>(n, mpart.as<double>(), eval_ctas, p64.as<double>(),
+                                                      p32.as<float>(), m.as<double>(), v.as<double>());
+                check_launch(ctx);
+                head = 1;
+                t = 0;
+            }
+            eval(X, y, R, 1, nullptr);
+            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lpart.as<double>(), eval_ctas, static_cast<double>(R), e,
+                                                 p64.as<double>(), best.as<double>(), losses_dev,
+                                                 best_loss.as<double>(), best_epoch.as<int>(), flag.as<int>());
+            check_launch(ctx);
+        }
+    }
+
+    void check_finite() {
+        int f = 0;
+        copy_out(ctx, &f, flag.p, 4);
+        if (f) throw numeric_error("training diverged (non-finite loss); try a smaller learning rate");
+    }
+};
+
+// Features of step i for every replica row, standardised (labels.cpp:142-167,
+// regressor.cpp:76-95): [indicators 1{s_c <= i}, rates, fx, client intensities, lagged].
+struct FeatArgs {
+    int M, N, E, Cn, step;
+    const double *rates, *fx, *intens, *lag0;
+    const uint16_t* steps;
+    const double* mean;
+    const double* scale;
+    float* X;
+};
+
+__device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
+    const int E = a.E, Cc = a.Cn - 1, M = a.M, i = a.step;
+    if (j < E) return a.rates[(static_cast<size_t>(i) * E + j) * M + k];
+    j -= E;
+    if (j < E - 1) return a.fx[(static_cast<size_t>(i) * (E - 1) + j) * M + k];
+    j -= E - 1;
+    if (j < Cc) return a.intens[(static_cast<size_t>(i) * a.Cn + j + 1) * M + k];
+    j -= Cc;
+    return (i == 0) ? a.lag0[j] : a.rates[(static_cast<size_t>(i - 1) * E + j) * M + k];
+}
+
+__global__ void k_build_x(FeatArgs a) {
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    const size_t row = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (row >= R) return;
+    const int k = static_cast<int>(row / a.N);
+    const int Cc = a.Cn - 1, q = 3 * a.E - 1 + Cc, d = Cc + q;
+    float* o = a.X + row * d;
+    for (int c = 1; c <= Cc; ++c) o[c - 1] = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
+    for (int j = 0; j < q; ++j)
+        o[Cc + j] = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
+}
+
+// Scaler (regressor.cpp:84-95) over the rows: the state columns repeat per path,
+// so mean / population variance over rows equal those over paths.  One CTA per
+// column, fixed-order FP64 reduction; indicator columns pass through.
+__global__ void k_scaler(FeatArgs a, double* mean, double* scale) {
+    __shared__ double red[32];
+    const int Cc = a.Cn - 1, j = blockIdx.x;
+    if (j < Cc) {
+        if (threadIdx.x == 0) {
+            mean[j] = 0.0;
+            scale[j] = 1.0;
+        }
+        return;
+    }
+    const int js = j - Cc;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < a.M; k += blockDim.x) s += state_col(a, k, js);
+    const double tot = block_sum(s, red);
+    __shared__ double m_sh;
+    if (threadIdx.x == 0) m_sh = tot / a.M;
+    __syncthreads();
+    const double mu = m_sh;
+    double v = 0.0;
+    for (int k = threadIdx.x; k < a.M; k += blockDim.x) {
+        const double dlt = state_col(a, k, js) - mu;
+        v += dlt * dlt;
+    }
+    const double vt = block_sum(v, red);
+    if (threadIdx.x == 0) {
+        const double sd = sqrt(vt / a.M);
+        mean[j] = mu;
+        scale[j] = (sd > 1e-12) ? sd : 1.0;
+    }
+}
+
+}  // namespace hcva
+
+// Trained model sequence (regressor.hpp:120-131), device resident.
+struct hcva_models {
+    hcva_ctx* ctx = nullptr;
+    hcva::NetDims n{};
+    int n_steps = 0, epochs = 0;
+    hcva::DeviceBuf params, mean, scale, losses, best_loss, best_epoch;  // [n][...]
+};
+
+using namespace hcva;
+
+namespace {
+
+NetDims dims_from(const hcva_train_cfg* cfg, int d) {
+    if (!cfg) throw contract_error("training: null config");
+    return make_dims(d, cfg->hidden_layers, cfg->width, cfg->activation);
+}
+
+// Glorot-uniform init (regressor.cpp:172-189) from stream key, mu = 0.
+std::vector<double> init_params(const NetDims& n, uint64_t key) {
+    std::vector<double> p(n.P, 0.0);
+    uint64_t j = 0;
+    for (int l = 0; l <= n.h; ++l) {
+        const double limit = std::sqrt(6.0 / (n.fin[l] + n.fout[l]));
+        for (int r = 0; r < n.fout[l]; ++r)
+            for (int c = 0; c < n.fin[l]; ++c)
+                p[n.off[l] + r * n.fin[l] + c] = limit * (2.0 * u64_to_uniform(draw_u64(key, j++)) - 1.0);
+    }
+    return p;
+}
+
+FeatArgs feat_args(hcva_sim* sim, int step) {
+    FeatArgs a{};
+    a.M = sim->M;
+    a.N = sim->N;
+    a.E = sim->model.E;
+    a.Cn = sim->model.Cn;
+    a.step = step;
+    a.rates = sim->rates.as<double>();
+    a.fx = sim->fx.as<double>();
+    a.intens = sim->intens.as<double>();
+    a.lag0 = sim->lag0.as<double>();
+    a.steps = sim->steps.as<uint16_t>();
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+hcva_status hcva_net_size(const hcva_train_cfg* cfg, int input_dim, int* n_params) {
+    return guarded([&] { *n_params = dims_from(cfg, input_dim).P; });
+}
+
+hcva_status hcva_init_network(const hcva_train_cfg* cfg, int input_dim, uint64_t key, double* params) {
+    return guarded([&] {
+        const auto p = init_params(dims_from(cfg, input_dim), key);
+        std::memcpy(params, p.data(), p.size() * 8);
+    });
+}
+
+hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                                int head, const double* x, const double* y, int rows, double* loss, double* grads) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const NetDims n = dims_from(cfg, input_dim);
+        Trainer tr(ctx, n, rows);
+        std::vector<float> xf(static_cast<size_t>(rows) * input_dim);
+        for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
+        DeviceBuf dX, dy;
+        stage(dX, xf);
+        stage(dy, std::vector<double>(y, y + rows));
+        tr.set_params(params);
+        const int tiles = (rows + tr.TR - 1) / tr.TR;
+        k_sgd<<<tiles, tr.TR, tr.smem(), ctx->stream>>>(n, dX.as<float>(), dy.as<double>(), 0, rows, tr.p32.as<float>(),
+                                                       head, static_cast<double>(rows), tr.gpart.as<float>(),
+                                                       tr.lpart.as<double>(), tr.TR);
+        check_launch(ctx);
+        std::vector<float> gp(static_cast<size_t>(tiles) * n.P);
+        std::vector<double> lp(tiles);
+        copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);
+        copy_out(ctx, lp.data(), tr.lpart.p, lp.size() * 8);
+        double l = 0.0;
+        for (double v : lp) l += v;
+        *loss = l / rows;
+        if (grads)
+            for (int i = 0; i < n.P; ++i) {
+                double g = 0.0;
+                for (int c = 0; c < tiles; ++c) g += gp[static_cast<size_t>(c) * n.P + i];
+                grads[i] = g;
+            }
+    });
+}
+
+hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
+                            const double* y, int rows, const double* init, double* best, double* epoch_losses,
+                            double* best_loss, int* best_epoch) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        const NetDims n = dims_from(cfg, input_dim);
+        if (cfg->n_batches < 1 || rows % cfg->n_batches != 0)
+            throw config_error("make_batches: batch count must divide M*N");
+        Trainer tr(ctx, n, rows / cfg->n_batches);
+        std::vector<float> xf(static_cast<size_t>(rows) * input_dim);
+        for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
+        DeviceBuf dX, dy, dl;
+        stage(dX, xf);
+        stage(dy, std::vector<double>(y, y + rows));
+        dl.alloc(sizeof(double) * std::max(cfg->epochs, 1));
+        tr.set_params(init);
+        tr.train_base(dX.as<float>(), dy.as<double>(), rows, cfg->epochs, cfg->n_batches, cfg->learning_rate,
+                      cfg->adam, cfg->ridge, dl.as<double>());
+        tr.check_finite();
+        copy_out(ctx, best, tr.best.p, n.P * 8);
+        copy_out(ctx, epoch_losses, dl.p, cfg->epochs * 8);
+        copy_out(ctx, best_loss, tr.best_loss.p, 8);
+        copy_out(ctx, best_epoch, tr.best_epoch.p, 4);
+    });
+}
+
+// backward_learn (regressor.cpp:354-395) over a simulated set with the label
+// source of pipeline.cpp:72-111 (features_at + defaults_/intensity_label).
+hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out) {
+    return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (!sim->has_defaults || !sim->has_cube) throw contract_error("backward_learn: simulate a full set first");
+        if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+        if (label_kind != 0 && label_kind != 1) throw config_error("config: label_kind must be 'defaults' or 'intensity'");
+        const int Cc = sim->model.Cc, E = sim->model.E, nsteps = sim->n;
+        const int d = Cc + 3 * E - 1 + Cc;
+        const NetDims n = dims_from(cfg, d);
+        const long R = static_cast<long>(sim->M) * sim->N;
+        if (cfg->n_batches < 1 || R % cfg->n_batches != 0) throw config_error("make_batches: batch count must divide M*N");
+        auto models = std::make_unique<hcva_models>();
+        models->ctx = ctx;
+        models->n = n;
+        models->n_steps = nsteps;
+        models->epochs = cfg->epochs;
+        models->params.alloc(static_cast<size_t>(nsteps) * n.P * 8);
+        models->mean.alloc(static_cast<size_t>(nsteps) * d * 8);
+        models->scale.alloc(static_cast<size_t>(nsteps) * d * 8);
+        models->losses.alloc(static_cast<size_t>(nsteps) * std::max(cfg->epochs, 1) * 8);
+        models->best_loss.alloc(static_cast<size_t>(nsteps) * 8);
+        models->best_epoch.alloc(static_cast<size_t>(nsteps) * 4);
+        if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
+        Trainer tr(ctx, n, R / cfg->n_batches);
+        HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
+        DeviceBuf X;
+        X.alloc(sizeof(float) * R * d);
+        for (int i = nsteps; i >= 1; --i) {
+            FeatArgs fa = feat_args(sim, i);
+            double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
+            double* scale = models->scale.as<double>() + static_cast<size_t>(i - 1) * d;
+            k_scaler<<<d, 256, 0, ctx->stream>>>(fa, mean, scale);
+            check_launch(ctx);
+            fa.mean = mean;
+            fa.scale = scale;
+            fa.X = X.as<float>();
+            k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
+            check_launch(ctx);
+            const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
+            if (i == nsteps) {
+                const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));
+                tr.set_params(p.data());
+                HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+                k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
+                check_launch(ctx);
+            } else {
+                tr.set_params(tr.best.as<double>());  // warm start from step i+1's best
+            }
+            tr.train_base(X.as<float>(), y, R, cfg->epochs, cfg->n_batches, cfg->learning_rate, cfg->adam, cfg->ridge,
+                          models->losses.as<double>() + static_cast<size_t>(i - 1) * cfg->epochs);
+            HCVA_CUDA(cudaMemcpyAsync(models->params.as<double>() + static_cast<size_t>(i - 1) * n.P, tr.best.p, n.P * 8,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+            HCVA_CUDA(cudaMemcpyAsync(models->best_loss.as<double>() + (i - 1), tr.best_loss.p, 8,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+            HCVA_CUDA(cudaMemcpyAsync(models->best_epoch.as<int>() + (i - 1), tr.best_epoch.p, 4,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        tr.check_finite();
+        *out = models.release();
+    });
+}
+
+hcva_status hcva_models_info(const hcva_models* m, int* info) {
+    return guarded([&] {
+        info[0] = m->n_steps;
+        info[1] = m->n.d;
+        info[2] = m->n.P;
+        info[3] = m->epochs;
+    });
+}
+
+hcva_status hcva_models_get(const hcva_models* m, int step, double* params, double* mean, double* scale,
+                            double* epoch_losses, double* best_loss, int* best_epoch) {
+    return guarded([&] {
+        StreamScope sc__(m->ctx->stream);
+        if (step < 1 || step > m->n_steps) throw contract_error("models: step out of range");
+        const size_t s = step - 1;
+        if (params) copy_out(m->ctx, params, m->params.as<double>() + s * m->n.P, m->n.P * 8);
+        if (mean) copy_out(m->ctx, mean, m->mean.as<double>() + s * m->n.d, m->n.d * 8);
+        if (scale) copy_out(m->ctx, scale, m->scale.as<double>() + s * m->n.d, m->n.d * 8);
+        if (epoch_losses) copy_out(m->ctx, epoch_losses, m->losses.as<double>() + s * m->epochs, m->epochs * 8);
+        if (best_loss) copy_out(m->ctx, best_loss, m->best_loss.as<double>() + s, 8);
+        if (best_epoch) copy_out(m->ctx, best_epoch, m->best_epoch.as<int>() + s, 4);
+    });
+}
+
+// TrainedModelSequence::predict (regressor.cpp:349-352) on a simulated set's
+// features at `step` (e.g. the validation set, pipeline.cpp:138-156).
+hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* out) {
+    return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (step < 1 || step > m->n_steps) throw contract_error("models: step out of range");
+        if (!sim->has_defaults) throw contract_error("predict: no default block");
+        const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
+        if (d != m->n.d) throw contract_error("forward: feature dimension mismatch");
+        const long R = static_cast<long>(sim->M) * sim->N;
+        Trainer tr(ctx, m->n, 1);
+        tr.set_params(m->params.as<double>() + static_cast<size_t>(step - 1) * m->n.P);
+        FeatArgs fa = feat_args(sim, step);
+        fa.mean = m->mean.as<double>() + static_cast<size_t>(step - 1) * d;
+        fa.scale = m->scale.as<double>() + static_cast<size_t>(step - 1) * d;
+        DeviceBuf X, pred;
+        X.alloc(sizeof(float) * R * d);
+        pred.alloc(sizeof(double) * R);
+        fa.X = X.as<float>();
+        k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
+        check_launch(ctx);
+        tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
+        copy_out(ctx, out, pred.p, R * 8);
+    });
+}
+
+hcva_status hcva_models_destroy(hcva_models* m) {
+    return guarded([&] {
+        if (!m) return;
+        cudaStreamSynchronize(m->ctx->stream);
+        delete m;
+    });
+}
+
+}  // extern "C"

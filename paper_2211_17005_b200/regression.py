@@ -1,0 +1,128 @@
+"""Backward MLP regression (regressor.hpp:33-139) on the GPU, over the C ABI.
+
+    models = backward_learn(sim, cfg)            # Alg. 2 over every pricing step
+    params, mean, scale, report = models.get(5)  # StepModel of step 5
+    pred = models.predict(5, validation_sim)     # TrainedModelSequence::predict
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from .config import PipelineConfig, TrainConfig
+from .engine import Context, SimulationSet, context
+
+ACTIVATIONS = {"tanh": 0, "sigmoid": 1, "softplus": 2, "relu": 3}
+
+
+def train_cfg(t: TrainConfig) -> _lib.TrainCfg:
+    if t.activation not in ACTIVATIONS:
+        raise _lib.ConfigError(f"unknown activation: {t.activation}")
+    return _lib.TrainCfg(t.epochs, t.n_batches, t.hidden_layers, t.width, ACTIVATIONS[t.activation],
+                         int(bool(t.adam)), t.learning_rate, t.ridge, t.seed)
+
+
+def net_size(t: TrainConfig, input_dim: int) -> int:
+    n = C.c_int()
+    _lib.check(_lib.lib().hcva_net_size(C.byref(train_cfg(t)), input_dim, C.byref(n)))
+    return n.value
+
+
+def init_network(t: TrainConfig, input_dim: int, key: int) -> np.ndarray:
+    """init_network (regressor.cpp:172-189) from a stream key (mu = 0)."""
+    p = np.zeros(net_size(t, input_dim))
+    _lib.check(_lib.lib().hcva_init_network(C.byref(train_cfg(t)), input_dim, key, p.ctypes.data_as(_lib.dptr)))
+    return p
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def quadratic_loss(t: TrainConfig, params: np.ndarray, x: np.ndarray, y: np.ndarray, head: bool = False,
+                   ctx: Optional[Context] = None) -> Tuple[float, np.ndarray]:
+    """quadratic_loss (regressor.cpp:115-158): (loss, gradients in the flat layout)."""
+    ctx = ctx or context()
+    x, y, params = _f64(x), _f64(y), _f64(params)
+    g = np.zeros_like(params)
+    loss = C.c_double()
+    _lib.check(_lib.lib().hcva_quadratic_loss(ctx.handle, C.byref(train_cfg(t)), x.shape[1],
+                                              params.ctypes.data_as(_lib.dptr), int(head),
+                                              x.ctypes.data_as(_lib.dptr), y.ctypes.data_as(_lib.dptr),
+                                              x.shape[0], C.byref(loss), g.ctypes.data_as(_lib.dptr)))
+    return loss.value, g
+
+
+def train_base(t: TrainConfig, x: np.ndarray, y: np.ndarray, init: np.ndarray, ctx: Optional[Context] = None):
+    """train_base (regressor.cpp:265-347) with contiguous batches: (best params, report)."""
+    ctx = ctx or context()
+    x, y, init = _f64(x), _f64(y), _f64(init)
+    best = np.zeros_like(init)
+    losses = np.zeros(t.epochs)
+    bl, be = C.c_double(), C.c_int()
+    _lib.check(_lib.lib().hcva_train_base(ctx.handle, C.byref(train_cfg(t)), x.shape[1], x.ctypes.data_as(_lib.dptr),
+                                          y.ctypes.data_as(_lib.dptr), x.shape[0], init.ctypes.data_as(_lib.dptr),
+                                          best.ctypes.data_as(_lib.dptr), losses.ctypes.data_as(_lib.dptr),
+                                          C.byref(bl), C.byref(be)))
+    return best, dict(epoch_losses=losses, best_loss=bl.value, best_epoch=be.value)
+
+
+class Models:
+    """TrainedModelSequence (regressor.hpp:120-131), device resident."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle, self.ctx = handle, ctx
+        info = (C.c_int * 4)()
+        _lib.check(_lib.lib().hcva_models_info(handle, info))
+        self.n_steps, self.input_dim, self.n_params, self.epochs = list(info)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().hcva_models_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def get(self, step: int):
+        p, mean, scale = np.zeros(self.n_params), np.zeros(self.input_dim), np.zeros(self.input_dim)
+        losses = np.zeros(self.epochs)
+        bl, be = C.c_double(), C.c_int()
+        d = lambda a: a.ctypes.data_as(_lib.dptr)  # noqa: E731
+        _lib.check(_lib.lib().hcva_models_get(self.handle, step, d(p), d(mean), d(scale), d(losses), C.byref(bl),
+                                              C.byref(be)))
+        return p, mean, scale, dict(epoch_losses=losses, best_loss=bl.value, best_epoch=be.value)
+
+    def predict(self, step: int, sim: SimulationSet) -> np.ndarray:
+        out = np.zeros(sim.n_paths * sim.n_replicas)
+        _lib.check(_lib.lib().hcva_predict(self.handle, sim.handle, step, out.ctypes.data_as(_lib.dptr)))
+        return out
+
+
+def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults") -> Models:
+    """backward_learn (regressor.cpp:354-395) over the label source of make_label_source."""
+    kind = {"defaults": 0, "intensity": 1}.get(label_kind)
+    if kind is None:
+        raise _lib.ConfigError("config: label_kind must be 'defaults' or 'intensity'")
+    h = C.c_void_p()
+    _lib.check(_lib.lib().hcva_backward_learn(sim.handle, C.byref(train_cfg(t)), kind, C.byref(h)))
+    return Models(h, sim.ctx)
+
+
+def percentile_table(models: Models, validation: SimulationSet) -> Dict[int, Dict[str, float]]:
+    """percentile_table (pipeline.cpp:138-156): out-of-sample mean and percentile bands per step."""
+    rows = {}
+    for i in range(1, models.n_steps + 1):
+        v = np.sort(models.predict(i, validation))
+
+        def pct(q):
+            pos = q * (v.size - 1)
+            idx = int(pos)
+            frac = pos - idx
+            return v[idx] * (1 - frac) + v[idx + 1] * frac if idx + 1 < v.size else v[idx]
+
+        rows[i] = dict(mean=float(np.sum(v) / v.size), p1=pct(0.01), p2_5=pct(0.025), p97_5=pct(0.975), p99=pct(0.99))
+    return rows
