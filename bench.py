@@ -40,7 +40,7 @@ UNIT = "scenarios/s"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--cpu-baseline-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-learning", action="store_true", help="skip metric 2 (CVA learning time)")
+    ap.add_argument("--learning-steps", type=int, default=0, help="pricing steps for metric 2 (default: all)")
     return ap.parse_args()
 
 
@@ -169,7 +171,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -282,6 +284,9 @@ def ours_arm(args):
     e2e = None
     if not args.no_e2e:
         e2e = e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args)
+    learning = None
+    if not args.no_learning and world == 1:
+        learning = learning_leg(hcva, cfg, book, ctx, args)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
@@ -305,6 +310,7 @@ def ours_arm(args):
                          "k1_share_of_step": k1_ms / ms_step},
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
+            "cva_learning": learning,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -351,6 +357,66 @@ def e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args):
             "d2h_bytes_per_step": int(prof.nbytes), "ms_per_step": dt * 1e3,
             "path": "hcva.simulate_set (hcva_simulate_set: stage + K1/K3/K2) + cva_profile (K4 + reduction)",
             "cva0": float(prof[0])}
+
+
+def learning_leg(hcva, cfg, book, ctx, args):
+    """BASELINE metric 2: end-to-end CVA learning time on the same workload --
+    host config -> simulate_set -> labels -> backward_learn over every pricing
+    step (Alg. 2, E epochs x |B| batches, refit, best tracking) -> the time-0
+    CVA estimate back on the host.  One run, wall clock around a synchronised
+    device pipeline (the regression is a dependent chain of ~100*(E|B|+E)
+    phases, so there is no batch of independent steps to average)."""
+    from paper_2211_17005_b200 import regression as rg
+
+    t = cfg.training
+    steps = args.learning_steps or cfg.n_steps
+    if steps != cfg.n_steps:
+        import json as _json
+
+        import cases
+
+        j = cases.case(args.config)
+        j["grid"]["pricing_steps"] = steps
+        cfg = hcva.parse_config(_json.dumps(j))
+        book = hcva.generate_book(cfg)
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    sim = hcva.simulate_set(cfg, book, cfg.paths, cfg.replicas, root, ctx=ctx)
+    sim.labels_all(cfg.label_kind, to_host=False)
+    ctx.synchronize()
+    t1 = time.perf_counter()
+    models = rg.backward_learn(sim, t, cfg.label_kind)
+    p, mean, scale, rep = models.get(1)
+    t2 = time.perf_counter()
+    cpu = None
+    if not args.no_cpu_baseline:
+        # CPU reference of the regression: the FP64 restatement of regressor.cpp
+        # (the reference's own regressor needs Eigen, absent) timed on a bounded
+        # sample -- one train_base of step n on the first rows of its data --
+        # and extrapolated linearly in rows and steps (train_base is linear in both).
+        import oracle_api
+
+        R = oracle_api.restatement()
+        rows = min(cfg.paths * cfg.replicas, max(t.n_batches * 64, 4096))
+        rows -= rows % t.n_batches
+        x = sim.features(cfg.n_steps)[:rows]
+        y = sim.labels(cfg.n_steps, cfg.label_kind).reshape(-1)[:rows]
+        mean, scale = R.fit_scaler(x, cfg.n_clients)
+        init = R.init_network(x.shape[1], t.hidden_layers, t.width, R.key(cfg.seed, 0xBEEF, cfg.n_steps))
+        init[-1] = float(np.mean(y))
+        c0 = time.perf_counter()
+        R.train_base((x - mean) / scale, y, init, t.hidden_layers, t.width, t.n_batches, t.epochs, t.learning_rate)
+        sec = time.perf_counter() - c0
+        full = sec * (cfg.paths * cfg.replicas / rows) * steps
+        cpu = {"value": full, "unit": "s (extrapolated)", "cores": 1, "kind": "port",
+               "sample": f"train_base of step {cfg.n_steps} on {rows} rows: {sec:.2f} s, x{cfg.paths * cfg.replicas // rows}"
+                         f" rows x {steps} steps (FP64 restatement of regressor.cpp; simulation not included)"}
+    return {"value": t2 - t0, "unit": "s", "higher_is_better": False, "pricing_steps": steps, "cpu_baseline": cpu,
+            "simulate_and_labels_s": t1 - t0, "backward_learn_s": t2 - t1,
+            "sgd_steps": steps * t.epochs * t.n_batches, "rows": cfg.paths * cfg.replicas,
+            "net": f"{t.hidden_layers}x{t.width} {t.activation}", "best_loss_step1": rep["best_loss"],
+            "path": "hcva_simulate_set + hcva_labels_all + hcva_backward_learn (K1-K5, device resident)"}
 
 
 def main():
