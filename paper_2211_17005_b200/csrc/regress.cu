@@ -34,6 +34,12 @@ namespace hcva {
 
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
+// Tensor-core SGD tile (regress_tc.cu) for the paper's network shape.
+bool tc_eligible(int d, int h, int u);
+void launch_sgd_tc(int d, int u, int act, int P, int off0, int off1, int off2, const float* X, const double* y,
+                   long row0, long row_end, const float* params, int head, double nb, float* gpart, double* lpart,
+                   cudaStream_t s);
+
 struct NetDims {
     int d, h, u, act, P;
     int off[kMaxLayers + 1];  // W_l offset; b_l = off[l] + fout*fin
@@ -510,8 +516,10 @@ struct Trainer {
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
     int max_tiles = 0;
+    bool use_tc = false;
 
     Trainer(hcva_ctx* c, const NetDims& dims, long max_batch) : ctx(c), n(dims) {
+        use_tc = tc_eligible(n.d, n.h, n.u);
         while (TR > 32 && tile_smem(n, TR) > 200 * 1024) TR /= 2;
         if (tile_smem(n, TR) > 227 * 1024) throw config_error("training: network too wide for the tile kernel");
         const size_t smem = tile_smem(n, TR);
@@ -546,11 +554,23 @@ struct Trainer {
         check_launch(ctx);
     }
 
-    void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
+    // Gradient partials of rows [b0, b1) (one per tile); returns the tile count.
+    int grad_tiles(const float* X, const double* y, long b0, long b1, int head, double nb) {
+        if (use_tc) {
+            launch_sgd_tc(n.d, n.u, n.act, n.P, n.off[0], n.off[1], n.off[2], X, y, b0, b1, p32.as<float>(), head, nb,
+                          gpart.as<float>(), lpart.as<double>(), ctx->stream);
+            check_launch(ctx);
+            return static_cast<int>((b1 - b0 + 127) / 128);
+        }
         const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);
-        k_sgd<<<tiles, TR, smem(), ctx->stream>>>(n, X, y, b0, b1, p32.as<float>(), head, static_cast<double>(b1 - b0),
-                                                 gpart.as<float>(), lpart.as<double>(), TR);
+        k_sgd<<<tiles, TR, smem(), ctx->stream>>>(n, X, y, b0, b1, p32.as<float>(), head, nb, gpart.as<float>(),
+                                                 lpart.as<double>(), TR);
         check_launch(ctx);
+        return tiles;
+    }
+
+    void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
+        const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0));
         k_adam<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>());
@@ -759,11 +779,7 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         stage(dX, xf);
         stage(dy, std::vector<double>(y, y + rows));
         tr.set_params(params);
-        const int tiles = (rows + tr.TR - 1) / tr.TR;
-        k_sgd<<<tiles, tr.TR, tr.smem(), ctx->stream>>>(n, dX.as<float>(), dy.as<double>(), 0, rows, tr.p32.as<float>(),
-                                                       head, static_cast<double>(rows), tr.gpart.as<float>(),
-                                                       tr.lpart.as<double>(), tr.TR);
-        check_launch(ctx);
+        const int tiles = tr.grad_tiles(dX.as<float>(), dy.as<double>(), 0, rows, head, static_cast<double>(rows));
         std::vector<float> gp(static_cast<size_t>(tiles) * n.P);
         std::vector<double> lp(tiles);
         copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);

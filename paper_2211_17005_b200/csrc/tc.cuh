@@ -1,0 +1,151 @@
+// tc.cuh -- thin sm_100a tensor-core layer: tcgen05 MMA (kind::tf32), TMEM,
+// mbarriers, shared-memory operand tiles.
+//
+// Operand tiles use the canonical no-swizzle "core matrix" layout: a logical
+// R x C FP32 tile (R % 8 == 0, C % 4 == 0) stores element (r, c) at byte
+//   ((c/4) * (R/8) + r/8) * 128 + (r%8) * 16 + (c%4) * 4,
+// i.e. 8x4 core matrices of 128 contiguous bytes, consecutive along r.  The
+// same bytes are a K-major operand (rows = M/N, cols = K: SBO = 128,
+// LBO = R/8*128) and an MN-major operand (rows = K, cols = M/N:
+// SBO = R/8*128, LBO = 128), so activations written once serve the forward
+// GEMM (K-major) and the weight-gradient GEMM (MN-major).
+//
+// 3xTF32: every FP32 operand is stored as hi = rna_tf32(a) and lo = a - hi;
+// D += A_hi B_hi + A_lo B_hi + A_hi B_lo gives ~FP32 products with FP32
+// accumulation in TMEM.
+#pragma once
+#include <cstdint>
+
+namespace hcva {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t core_off(int r, int c, int R) {
+    return (static_cast<uint32_t>((c >> 2) * (R >> 3) + (r >> 3)) << 7) + ((r & 7) << 4) + ((c & 3) << 2);
+}
+
+__device__ __forceinline__ float tf32_rna(float a) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
+    return __uint_as_float(r);
+}
+
+// Store a into the hi / lo tiles (same layout, `lo_bytes` apart).
+__device__ __forceinline__ void put_split(uint8_t* tile, uint32_t lo_bytes, int r, int c, int R, float a) {
+    const float hi = tf32_rna(a);
+    const uint32_t o = core_off(r, c, R);
+    *reinterpret_cast<float*>(tile + o) = hi;
+    *reinterpret_cast<float*>(tile + lo_bytes + o) = a - hi;
+}
+
+__device__ __forceinline__ float get_split(const uint8_t* tile, uint32_t lo_bytes, int r, int c, int R) {
+    const uint32_t o = core_off(r, c, R);
+    return *reinterpret_cast<const float*>(tile + o) + *reinterpret_cast<const float*>(tile + lo_bytes + o);
+}
+
+// UMMA shared-memory descriptor, no swizzle (SmemDescriptor, mma_sm100_desc.hpp).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor kind::tf32, D = F32 (InstrDescriptor, mma_sm100_desc.hpp).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn_major) << 15) |
+           (static_cast<uint32_t>(b_mn_major) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, int accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// Warp-wide TMEM allocation of `cols` columns; the base address lands in *dst.
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols) : "memory");
+}
+
+// 16 consecutive FP32 columns of this thread's TMEM lane (warp-collective).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// D[tmem] (+)= A B^T over K (multiple of 8) in 3xTF32, issued by one thread.
+// A: M x K tile, B: N x K tile, each given by its hi base address, the byte
+// offset of its lo copy, and (for the K walk) whether it is read K-major
+// (advance 2 core columns = 2*lbo per K-step) or MN-major (advance one core
+// row block = 128 B per K-step).
+struct Operand {
+    uint32_t hi, lo_off, lbo, sbo;
+    int mn_major;
+    __device__ __forceinline__ uint64_t desc(int part, int ks) const {
+        const uint32_t base = hi + (part ? lo_off : 0u);
+        const uint32_t step = mn_major ? 128u * ks : 2u * lbo * ks;
+        return sdesc(base + step, lbo, sbo);
+    }
+};
+
+__device__ __forceinline__ void gemm3(uint32_t d_tmem, const Operand& A, const Operand& B, int K, uint32_t idesc,
+                                      int accumulate) {
+    for (int ks = 0; ks < K / 8; ++ks) {
+        mma_tf32(d_tmem, A.desc(0, ks), B.desc(0, ks), idesc, (ks > 0 || accumulate) ? 1 : 0);
+        mma_tf32(d_tmem, A.desc(1, ks), B.desc(0, ks), idesc, 1);
+        mma_tf32(d_tmem, A.desc(0, ks), B.desc(1, ks), idesc, 1);
+    }
+}
+
+// K-major view of a core tile with R rows; MN-major view of a core tile with R rows.
+__device__ __forceinline__ Operand kmajor(const void* hi, uint32_t lo_off, int R) {
+    return Operand{smem_u32(hi), lo_off, static_cast<uint32_t>(R / 8) * 128u, 128u, 0};
+}
+__device__ __forceinline__ Operand mnmajor(const void* hi, uint32_t lo_off, int R) {
+    return Operand{smem_u32(hi), lo_off, 128u, static_cast<uint32_t>(R / 8) * 128u, 1};
+}
+
+}  // namespace tc
+}  // namespace hcva
