@@ -279,6 +279,53 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_sgd_tc(TcArgs a) {
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
+// Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T with the operands laid out
+// K-major or MN-major in core tiles (test hook for the descriptor conventions).
+__global__ void k_tc_gemm_diag(int M, int N, int K, int amn, int bmn, const float* A, const float* B, float* D) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int R_A = amn ? K : M, C_A = amn ? M : K, R_B = bmn ? K : N, C_B = bmn ? N : K;
+    const uint32_t abytes = R_A * C_A * 4, bbytes = R_B * C_B * 4;
+    uint8_t* ta = sm;
+    uint8_t* tb = sm + 2 * abytes;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(tb + 2 * bbytes);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
+    const int t = threadIdx.x, warp = t >> 5;
+    if (t == 0) tc::mbar_init(mbar, 1);
+    if (warp == 0) tc::tmem_alloc(tbase, 256);
+    for (int i = t; i < M * K; i += blockDim.x) {
+        const int m = i / K, k = i % K;
+        if (amn) tc::put_split(ta, abytes, k, m, R_A, A[i]); else tc::put_split(ta, abytes, m, k, R_A, A[i]);
+    }
+    for (int i = t; i < N * K; i += blockDim.x) {
+        const int n = i / K, k = i % K;
+        if (bmn) tc::put_split(tb, bbytes, k, n, R_B, B[i]); else tc::put_split(tb, bbytes, n, k, R_B, B[i]);
+    }
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = *tbase;
+    if (t == 0) {
+        const tc::Operand oa = amn ? tc::mnmajor(ta, abytes, R_A) : tc::kmajor(ta, abytes, R_A);
+        const tc::Operand ob = bmn ? tc::mnmajor(tb, bbytes, R_B) : tc::kmajor(tb, bbytes, R_B);
+        tc::gemm3(tm, oa, ob, K, tc::idesc_tf32(M, N, amn, bmn), 0);
+        tc::commit(mbar);
+    }
+    tc::mbar_wait(mbar, 0);
+    tc::fence_after_sync();
+    for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tm + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+        const int lane = t & 31;
+        const int row = (M == 128) ? t : ((lane < 16) ? warp * 16 + lane : -1);
+        if (row >= 0)
+            for (int q = 0; q < 16 && c0 + q < N; ++q) D[row * N + c0 + q] = v[q];
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
@@ -324,3 +371,25 @@ void launch_sgd_tc(int d, int u, int act, int P, int off0, int off1, int off2, c
 }
 
 }  // namespace hcva
+
+using namespace hcva;
+
+extern "C" hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int a_mn_major, int b_mn_major,
+                                         const float* A, const float* B, float* D) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if ((M != 64 && M != 128) || N % 16 || N > 128 || K % 8 || K > 128)
+            throw contract_error("diag gemm: M in {64,128}, N % 16 == 0 <= 128, K % 8 == 0 <= 128");
+        DeviceBuf dA, dB, dD;
+        stage(dA, std::vector<float>(A, A + M * K));
+        stage(dB, std::vector<float>(B, B + N * K));
+        dD.alloc(sizeof(float) * M * N);
+        const size_t smem = 2 * 4 * (static_cast<size_t>(M) * K + static_cast<size_t>(N) * K) + 64;
+        HCVA_CUDA(cudaFuncSetAttribute(k_tc_gemm_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tc_gemm_diag<<<1, 128, smem, ctx->stream>>>(M, N, K, a_mn_major, b_mn_major, dA.as<float>(), dB.as<float>(),
+                                                      dD.as<float>());
+        check_launch(ctx);
+        copy_out(ctx, D, dD.p, sizeof(float) * M * N);
+    });
+}
