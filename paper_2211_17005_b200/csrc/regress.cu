@@ -34,11 +34,9 @@ namespace hcva {
 
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
-// Tensor-core SGD tile (regress_tc.cu) for the paper's network shape.
-bool tc_eligible(int d, int h, int u);
-void launch_sgd_tc(int d, int u, int act, int P, int off0, int off1, int off2, const float* X, const double* y,
-                   long row0, long row_end, const float* params, int head, double nb, float* gpart, double* lpart,
-                   cudaStream_t s);
+}  // namespace hcva
+#include "regress_tc.cuh"  // tensor-core tiles for the paper's network shape
+namespace hcva {
 
 struct NetDims {
     int d, h, u, act, P;
@@ -253,8 +251,16 @@ __global__ void k_sgd(NetDims n, const float* X, const double* y, long row0, lon
 }
 
 // Fixed-order reduction of the tile partials + optimiser step (regressor.cpp:236-261).
-__global__ void k_adam(int P, const float* gpart, int nct, const double* lpart, double nb, double* p64, float* p32,
-                       double* m, double* v, long t, double lr, int adam, int* nonfinite) {
+// Parameters whose gradient partials come from the weight-gradient kernel
+// (tensor-core path: W0 and W1) instead of the per-tile kernel.
+struct SplitPartials {
+    const float* gpartB = nullptr;
+    int nB = 0;
+    int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // [lo, hi) index ranges served by gpartB
+};
+
+__global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
+                       double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
         double s = 0.0;
@@ -263,7 +269,11 @@ __global__ void k_adam(int P, const float* gpart, int nct, const double* lpart, 
     }
     if (i >= P) return;
     double g = 0.0;
-    for (int c = 0; c < nct; ++c) g += static_cast<double>(gpart[static_cast<size_t>(c) * P + i]);
+    if (sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1))) {
+        for (int c = 0; c < sp.nB; ++c) g += static_cast<double>(sp.gpartB[static_cast<size_t>(c) * P + i]);
+    } else {
+        for (int c = 0; c < nct; ++c) g += static_cast<double>(gpart[static_cast<size_t>(c) * P + i]);
+    }
     double w = p64[i];
     if (adam) {
         const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
@@ -515,10 +525,13 @@ struct Trainer {
     NetDims n;
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
-    int max_tiles = 0;
+    DeviceBuf gpartB, h1t, g2t, g1t;  // tensor-core path: weight-gradient partials, transposed activations
+    int max_tiles = 0, last_parts = 0, dp = 0;
     bool use_tc = false;
+    const float* Xt = nullptr;  // transposed features [dp][ld_x] (tensor-core weight gradients)
+    long ld_x = 0;
 
-    Trainer(hcva_ctx* c, const NetDims& dims, long max_batch) : ctx(c), n(dims) {
+    Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0) : ctx(c), n(dims) {
         use_tc = tc_eligible(n.d, n.h, n.u);
         while (TR > 32 && tile_smem(n, TR) > 200 * 1024) TR /= 2;
         if (tile_smem(n, TR) > 227 * 1024) throw config_error("training: network too wide for the tile kernel");
@@ -531,14 +544,24 @@ struct Trainer {
         eval_ctas = std::max(1, per_sm) * ctx->sm_count;
         max_tiles = static_cast<int>((max_batch + TR - 1) / TR);
         const size_t P = n.P;
+        long parts = std::max<long>(max_tiles, eval_ctas);
+        if (use_tc) {
+            dp = tc_dp(n.d);
+            parts = std::max<long>(parts, (std::max(max_rows, max_batch) + 127) / 128);
+            const size_t tsz = static_cast<size_t>(n.u) * std::max<long>(max_batch, 1) * 4;
+            h1t.alloc(tsz);
+            g2t.alloc(tsz);
+            g1t.alloc(tsz);
+            gpartB.alloc(static_cast<size_t>(ctx->sm_count) * P * 4);
+        }
         p64.alloc(P * 8);
         p32.alloc(P * 4);
         m.alloc(P * 8);
         v.alloc(P * 8);
         best.alloc(P * 8);
-        gpart.alloc(static_cast<size_t>(std::max(max_tiles, 1)) * P * 4);
-        lpart.alloc(static_cast<size_t>(std::max(max_tiles, eval_ctas)) * 8);
-        mpart.alloc(static_cast<size_t>(eval_ctas) * 8);
+        gpart.alloc(static_cast<size_t>(std::max<long>(parts, 1)) * P * 4);
+        lpart.alloc(static_cast<size_t>(parts) * 8);
+        mpart.alloc(static_cast<size_t>(parts) * 8);
         const size_t mm = n.u + 1;
         gram.alloc(static_cast<size_t>(eval_ctas) * (mm * (mm + 1) / 2 + mm) * 8);
         flag.alloc(4);
@@ -554,33 +577,63 @@ struct Trainer {
         check_launch(ctx);
     }
 
-    // Gradient partials of rows [b0, b1) (one per tile); returns the tile count.
-    int grad_tiles(const float* X, const double* y, long b0, long b1, int head, double nb) {
+    TileArgs tile_args(const float* X, const double* y, long b0, long b1, int head, int mode, double nb, double* pred) {
+        TileArgs ta{};
+        ta.d = n.d; ta.dp = dp; ta.act = n.act; ta.P = n.P;
+        ta.off0 = n.off[0]; ta.off1 = n.off[1]; ta.off2 = n.off[2];
+        ta.X = X; ta.y = y; ta.row0 = b0; ta.row_end = b1; ta.params = p32.as<float>();
+        ta.head = head; ta.mode = mode; ta.nb = nb;
+        ta.gpart = gpart.as<float>(); ta.lpart = lpart.as<double>(); ta.mpart = mpart.as<double>(); ta.pred = pred;
+        ta.H1t = h1t.as<float>(); ta.G2t = g2t.as<float>(); ta.G1t = g1t.as<float>(); ta.ld_t = b1 - b0;
+        return ta;
+    }
+
+    // Gradient partials of rows [b0, b1): per-tile partials (+ weight-gradient
+    // partials on the tensor-core path, described by sp); returns the tile count.
+    int grad_tiles(const float* X, const double* y, long b0, long b1, int head, double nb, SplitPartials* sp) {
         if (use_tc) {
-            launch_sgd_tc(n.d, n.u, n.act, n.P, n.off[0], n.off[1], n.off[2], X, y, b0, b1, p32.as<float>(), head, nb,
-                          gpart.as<float>(), lpart.as<double>(), ctx->stream);
+            if (!Xt) throw contract_error("training: transposed features missing for the tensor-core path");
+            launch_tile_tc(n.u, tile_args(X, y, b0, b1, head, 0, nb, nullptr), ctx->stream);
             check_launch(ctx);
+            WgradArgs wa{};
+            wa.d = n.d; wa.dp = dp; wa.P = n.P; wa.off0 = n.off[0]; wa.off1 = n.off[1];
+            wa.G2t = g2t.as<float>(); wa.H1t = h1t.as<float>(); wa.G1t = g1t.as<float>(); wa.ld_t = b1 - b0;
+            wa.Xt = Xt; wa.ld_x = ld_x; wa.row0 = b0; wa.rows = b1 - b0; wa.gpart = gpartB.as<float>();
+            const int nB = launch_wgrad_tc(n.u, wa, ctx->sm_count, ctx->stream);
+            check_launch(ctx);
+            if (sp) *sp = SplitPartials{gpartB.as<float>(), nB, n.off[0], n.off[0] + n.u * n.d, n.off[1],
+                                        n.off[1] + n.u * n.u};
             return static_cast<int>((b1 - b0 + 127) / 128);
         }
         const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);
         k_sgd<<<tiles, TR, smem(), ctx->stream>>>(n, X, y, b0, b1, p32.as<float>(), head, nb, gpart.as<float>(),
                                                  lpart.as<double>(), TR);
         check_launch(ctx);
+        if (sp) *sp = SplitPartials{};
         return tiles;
     }
 
     void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
-        const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0));
-        k_adam<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, lpart.as<double>(),
+        SplitPartials sp;
+        const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
+        k_adam<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>());
         check_launch(ctx);
     }
 
+    // Full-sample forward; sets last_parts = number of loss / min partials written.
     void eval(const float* X, const double* y, long R, int mode, double* pred) {
+        if (use_tc) {
+            launch_tile_tc(n.u, tile_args(X, y, 0, R, 1, mode, 1.0, pred), ctx->stream);
+            check_launch(ctx);
+            last_parts = static_cast<int>((R + 127) / 128);
+            return;
+        }
         k_eval<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), mode, lpart.as<double>(),
                                                       mpart.as<double>(), pred, TR);
         check_launch(ctx);
+        last_parts = eval_ctas;
     }
 
     void refit(const float* X, const double* y, long R, double ridge) {
@@ -615,14 +668,14 @@ struct Trainer {
             if (e == sw) {
                 refit(X, y, R, ridge);
                 eval(X, y, R, 2, nullptr);
-                k_switch<<<1, 256, 0, ctx->stream>>>(n, mpart.as<double>(), eval_ctas, p64.as<double>(),
+                k_switch<<<1, 256, 0, ctx->stream>>>(n, mpart.as<double>(), last_parts, p64.as<double>(),
                                                       p32.as<float>(), m.as<double>(), v.as<double>());
                 check_launch(ctx);
                 head = 1;
                 t = 0;
             }
             eval(X, y, R, 1, nullptr);
-            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lpart.as<double>(), eval_ctas, static_cast<double>(R), e,
+            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lpart.as<double>(), last_parts, static_cast<double>(R), e,
                                                  p64.as<double>(), best.as<double>(), losses_dev,
                                                  best_loss.as<double>(), best_epoch.as<int>(), flag.as<int>());
             check_launch(ctx);
@@ -645,6 +698,7 @@ struct FeatArgs {
     const double* mean;
     const double* scale;
     float* X;
+    float* Xt;  // optional transposed copy [d][M*N] (tensor-core weight gradients)
 };
 
 __device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
@@ -665,9 +719,16 @@ __global__ void k_build_x(FeatArgs a) {
     const int k = static_cast<int>(row / a.N);
     const int Cc = a.Cn - 1, q = 3 * a.E - 1 + Cc, d = Cc + q;
     float* o = a.X + row * d;
-    for (int c = 1; c <= Cc; ++c) o[c - 1] = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
-    for (int j = 0; j < q; ++j)
-        o[Cc + j] = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
+    for (int c = 1; c <= Cc; ++c) {
+        const float v = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
+        o[c - 1] = v;
+        if (a.Xt) a.Xt[(c - 1) * R + row] = v;
+    }
+    for (int j = 0; j < q; ++j) {
+        const float v = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
+        o[Cc + j] = v;
+        if (a.Xt) a.Xt[(Cc + j) * R + row] = v;
+    }
 }
 
 // Scaler (regressor.cpp:84-95) over the rows: the state columns repeat per path,
@@ -751,6 +812,22 @@ FeatArgs feat_args(hcva_sim* sim, int step) {
     return a;
 }
 
+// Stage host features (FP64 [rows][d]) as FP32 X and, for the tensor-core
+// path, the zero-padded transpose Xt [dp][rows].
+void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX, DeviceBuf& dXt) {
+    std::vector<float> xf(static_cast<size_t>(rows) * d);
+    for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
+    stage(dX, xf);
+    if (tr.use_tc) {
+        std::vector<float> xt(static_cast<size_t>(tr.dp) * rows, 0.0f);
+        for (int r = 0; r < rows; ++r)
+            for (int j = 0; j < d; ++j) xt[static_cast<size_t>(j) * rows + r] = xf[static_cast<size_t>(r) * d + j];
+        stage(dXt, xt);
+        tr.Xt = dXt.as<float>();
+        tr.ld_x = rows;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -773,24 +850,28 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         HCVA_CUDA(cudaSetDevice(ctx->device));
         const NetDims n = dims_from(cfg, input_dim);
         Trainer tr(ctx, n, rows);
-        std::vector<float> xf(static_cast<size_t>(rows) * input_dim);
-        for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
-        DeviceBuf dX, dy;
-        stage(dX, xf);
+        DeviceBuf dX, dXt, dy;
+        stage_features(tr, x, rows, input_dim, dX, dXt);
         stage(dy, std::vector<double>(y, y + rows));
         tr.set_params(params);
-        const int tiles = tr.grad_tiles(dX.as<float>(), dy.as<double>(), 0, rows, head, static_cast<double>(rows));
-        std::vector<float> gp(static_cast<size_t>(tiles) * n.P);
+        SplitPartials sp;
+        const int tiles =
+            tr.grad_tiles(dX.as<float>(), dy.as<double>(), 0, rows, head, static_cast<double>(rows), &sp);
+        std::vector<float> gp(static_cast<size_t>(tiles) * n.P), gb(static_cast<size_t>(sp.nB) * n.P);
         std::vector<double> lp(tiles);
         copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);
+        if (sp.nB) copy_out(ctx, gb.data(), sp.gpartB, gb.size() * 4);
         copy_out(ctx, lp.data(), tr.lpart.p, lp.size() * 8);
         double l = 0.0;
         for (double v : lp) l += v;
         *loss = l / rows;
         if (grads)
             for (int i = 0; i < n.P; ++i) {
+                const bool split = (i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1);
+                const std::vector<float>& src = (split && sp.nB) ? gb : gp;
+                const int cnt = (split && sp.nB) ? sp.nB : tiles;
                 double g = 0.0;
-                for (int c = 0; c < tiles; ++c) g += gp[static_cast<size_t>(c) * n.P + i];
+                for (int c = 0; c < cnt; ++c) g += src[static_cast<size_t>(c) * n.P + i];
                 grads[i] = g;
             }
     });
@@ -805,11 +886,9 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
         const NetDims n = dims_from(cfg, input_dim);
         if (cfg->n_batches < 1 || rows % cfg->n_batches != 0)
             throw config_error("make_batches: batch count must divide M*N");
-        Trainer tr(ctx, n, rows / cfg->n_batches);
-        std::vector<float> xf(static_cast<size_t>(rows) * input_dim);
-        for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
-        DeviceBuf dX, dy, dl;
-        stage(dX, xf);
+        Trainer tr(ctx, n, rows / cfg->n_batches, rows);
+        DeviceBuf dX, dXt, dy, dl;
+        stage_features(tr, x, rows, input_dim, dX, dXt);
         stage(dy, std::vector<double>(y, y + rows));
         dl.alloc(sizeof(double) * std::max(cfg->epochs, 1));
         tr.set_params(init);
@@ -850,10 +929,16 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
         models->best_loss.alloc(static_cast<size_t>(nsteps) * 8);
         models->best_epoch.alloc(static_cast<size_t>(nsteps) * 4);
         if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
-        Trainer tr(ctx, n, R / cfg->n_batches);
+        Trainer tr(ctx, n, R / cfg->n_batches, R);
         HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
-        DeviceBuf X;
+        DeviceBuf X, Xt;
         X.alloc(sizeof(float) * R * d);
+        if (tr.use_tc) {
+            Xt.alloc(sizeof(float) * R * tr.dp);
+            HCVA_CUDA(cudaMemsetAsync(Xt.p, 0, sizeof(float) * R * tr.dp, ctx->stream));  // pad rows stay 0
+            tr.Xt = Xt.as<float>();
+            tr.ld_x = R;
+        }
         for (int i = nsteps; i >= 1; --i) {
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
@@ -863,6 +948,7 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
             fa.mean = mean;
             fa.scale = scale;
             fa.X = X.as<float>();
+            fa.Xt = tr.use_tc ? Xt.as<float>() : nullptr;
             k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
             check_launch(ctx);
             const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
@@ -925,7 +1011,7 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
         if (d != m->n.d) throw contract_error("forward: feature dimension mismatch");
         const long R = static_cast<long>(sim->M) * sim->N;
-        Trainer tr(ctx, m->n, 1);
+        Trainer tr(ctx, m->n, 1, R);
         tr.set_params(m->params.as<double>() + static_cast<size_t>(step - 1) * m->n.P);
         FeatArgs fa = feat_args(sim, step);
         fa.mean = m->mean.as<double>() + static_cast<size_t>(step - 1) * d;

@@ -139,6 +139,55 @@ __device__ __forceinline__ void gemm3(uint32_t d_tmem, const Operand& A, const O
     }
 }
 
+// ---- 128-byte swizzled tiles (SWIZZLE_128B): rows of 32 FP32 (128 B) in
+// 8-row atoms of 1 KB, 16-byte chunk index XOR-ed with the row within the atom.
+// Atoms run along the rows first: atom (r/8, c/32) at ((c/32)*(R/8) + r/8)*1024.
+// K-major view (rows = M/N, cols = K): SBO = 1024 (next 8 rows), K-step of 8
+// FP32 = +32 B inside the atom, +R/8*1024 past each 32 columns.
+// MN-major view (rows = K, cols = M/N): SBO = 1024 (next 8 K rows), LBO =
+// R/8*1024 (next 32 M/N columns), K-step of 8 = +1024.
+__device__ __forceinline__ uint32_t sw_off(int r, int c, int R) {
+    const uint32_t atom = static_cast<uint32_t>((c >> 5) * (R >> 3) + (r >> 3)) << 10;
+    const uint32_t row = r & 7, chunk = (c & 31) >> 2;
+    return atom + (row << 7) + ((chunk ^ row) << 4) + ((c & 3) << 2);
+}
+
+__device__ __forceinline__ void put_split_sw(uint8_t* tile, uint32_t lo_bytes, int r, int c, int R, float a) {
+    const float hi = tf32_rna(a);
+    const uint32_t o = sw_off(r, c, R);
+    *reinterpret_cast<float*>(tile + o) = hi;
+    *reinterpret_cast<float*>(tile + lo_bytes + o) = a - hi;
+}
+
+__device__ __forceinline__ float get_split_sw(const uint8_t* tile, uint32_t lo_bytes, int r, int c, int R) {
+    const uint32_t o = sw_off(r, c, R);
+    return *reinterpret_cast<const float*>(tile + o) + *reinterpret_cast<const float*>(tile + lo_bytes + o);
+}
+
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return sdesc(addr, lbo, sbo) | (2ull << 61);
+}
+
+struct OperandSW {
+    uint32_t hi, lo_off, R;
+    int mn_major;
+    __device__ __forceinline__ uint64_t desc(int part, int ks) const {
+        const uint32_t base = hi + (part ? lo_off : 0u);
+        if (mn_major) return sdesc_sw128(base + 1024u * ks, (R / 8) * 1024u, 1024u);
+        const uint32_t col = 8 * ks;  // first K column of this step
+        return sdesc_sw128(base + (col >> 5) * (R / 8) * 1024u + (col & 31) * 4u, 16u, 1024u);
+    }
+};
+
+__device__ __forceinline__ void gemm3_sw(uint32_t d_tmem, const OperandSW& A, const OperandSW& B, int K,
+                                         uint32_t idesc, int accumulate) {
+    for (int ks = 0; ks < K / 8; ++ks) {
+        mma_tf32(d_tmem, A.desc(0, ks), B.desc(0, ks), idesc, (ks > 0 || accumulate) ? 1 : 0);
+        mma_tf32(d_tmem, A.desc(1, ks), B.desc(0, ks), idesc, 1);
+        mma_tf32(d_tmem, A.desc(0, ks), B.desc(1, ks), idesc, 1);
+    }
+}
+
 // K-major view of a core tile with R rows; MN-major view of a core tile with R rows.
 __device__ __forceinline__ Operand kmajor(const void* hi, uint32_t lo_off, int R) {
     return Operand{smem_u32(hi), lo_off, static_cast<uint32_t>(R / 8) * 128u, 128u, 0};

@@ -1,4 +1,4 @@
-"""Exercise hcva_diag_tc_gemm over operand major-ness combinations (debug aid)."""
+"""Exercise hcva_diag_tc_gemm (K-major operands, no-swizzle and SW128) (debug aid)."""
 import ctypes as C
 import os
 import sys
@@ -11,15 +11,14 @@ import paper_2211_17005_b200 as hcva  # noqa: E402
 from paper_2211_17005_b200 import _lib  # noqa: E402
 
 L = _lib.lib()
-L.hcva_diag_tc_gemm.argtypes = [C.c_void_p] + [C.c_int] * 5 + [C.c_void_p] * 3
+L.hcva_diag_tc_gemm.argtypes = [C.c_void_p] + [C.c_int] * 4 + [C.c_void_p] * 3
 rng = np.random.default_rng(0)
 for M, N, K in ((128, 32, 16), (64, 32, 128), (128, 64, 64), (64, 48, 128)):
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
-    for am in (0, 1):
-        for bm in (0, 1):
-            D = np.zeros((M, N), dtype=np.float32)
-            rc = L.hcva_diag_tc_gemm(hcva.context().handle, M, N, K, am, bm, A.ctypes.data, B.ctypes.data, D.ctypes.data)
-            err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
-            print(M, N, K, "a_mn", am, "b_mn", bm, "rc", rc, "relerr %.2e" % err, "D[0,:3]", D[0, :3], "ref", ref[0, :3])
+    for swz in (0, 1):
+        D = np.zeros((M, N), dtype=np.float32)
+        rc = L.hcva_diag_tc_gemm(hcva.context().handle, M, N, K, swz, A.ctypes.data, B.ctypes.data, D.ctypes.data)
+        err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
+        print(M, N, K, "sw128", swz, "rc", rc, "relerr %.2e" % err, "D[0,:3]", D[0, :3], "ref", ref[0, :3])

@@ -35,4 +35,7 @@ def main(d=12, u=32, rows=700, head=False):
 
 
 if __name__ == "__main__":
-    main()
+    for d, u, rows, head in ((12, 32, 700, False), (12, 32, 700, True), (21, 64, 1000, False), (5, 16, 130, True),
+                             (64, 64, 4096, False)):
+        print(f"--- d={d} u={u} rows={rows} head={head}")
+        main(d, u, rows, head)
