@@ -525,11 +525,11 @@ struct Trainer {
     NetDims n;
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
-    DeviceBuf gpartB, h1t, g2t, g1t;  // tensor-core path: weight-gradient partials, transposed activations
+    // Tensor-core path: weight-gradient partials, transposed activations, packed operand images.
+    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt;
     int max_tiles = 0, last_parts = 0, dp = 0;
     bool use_tc = false;
-    const float* Xt = nullptr;  // transposed features [dp][ld_x] (tensor-core weight gradients)
-    long ld_x = 0;
+    long ld_x = 0, ld_tmax = 0, x_rows = 0;
 
     Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0) : ctx(c), n(dims) {
         use_tc = tc_eligible(n.d, n.h, n.u);
@@ -547,12 +547,18 @@ struct Trainer {
         long parts = std::max<long>(max_tiles, eval_ctas);
         if (use_tc) {
             dp = tc_dp(n.d);
-            parts = std::max<long>(parts, (std::max(max_rows, max_batch) + 127) / 128);
-            const size_t tsz = static_cast<size_t>(n.u) * std::max<long>(max_batch, 1) * 4;
+            parts = std::max<long>(parts, ctx->sm_count);
+            ld_tmax = ((std::max<long>(max_batch, 1) + 63) / 64) * 64;
+            const size_t tsz = static_cast<size_t>(n.u) * ld_tmax * 4;
             h1t.alloc(tsz);
             g2t.alloc(tsz);
             g1t.alloc(tsz);
             gpartB.alloc(static_cast<size_t>(ctx->sm_count) * P * 4);
+            wimg.alloc(tc_weight_image_bytes(n.u, dp));
+            x_rows = std::max(max_rows, max_batch);
+            ld_x = ((x_rows + 64 + 3) / 4) * 4;  // slack for the 64-row chunk loads
+            ximg.alloc(static_cast<size_t>((x_rows + 127) / 128) * tc_x_tile_bytes(dp));
+            xt.alloc(static_cast<size_t>(dp) * ld_x * 4);
         }
         p64.alloc(P * 8);
         p32.alloc(P * 4);
@@ -577,33 +583,47 @@ struct Trainer {
         check_launch(ctx);
     }
 
-    TileArgs tile_args(const float* X, const double* y, long b0, long b1, int head, int mode, double nb, double* pred) {
+    // Features of the sample (X [R][d], device) -> the tensor-core operand images.
+    void prepare_x(const float* X, long R) {
+        if (!use_tc) return;
+        if (R > x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
+        launch_pack_x(X, R, n.d, dp, ximg.as<uint8_t>(), xt.as<float>(), ld_x, ctx->stream);
+        check_launch(ctx);
+    }
+
+    // Launch the persistent tile kernel over rows [b0, b1); returns the partial count.
+    int tile_launch(const double* y, long b0, long b1, int head, int mode, double nb, double* pred) {
+        launch_pack_w(n.u, n.d, dp, n.off[0], n.off[1], n.off[2], n.P, p32.as<float>(), wimg.as<uint8_t>(),
+                      ctx->stream);
+        check_launch(ctx);
         TileArgs ta{};
         ta.d = n.d; ta.dp = dp; ta.act = n.act; ta.P = n.P;
         ta.off0 = n.off[0]; ta.off1 = n.off[1]; ta.off2 = n.off[2];
-        ta.X = X; ta.y = y; ta.row0 = b0; ta.row_end = b1; ta.params = p32.as<float>();
+        ta.wimg = wimg.as<uint8_t>(); ta.ximg = ximg.as<uint8_t>(); ta.y = y; ta.b0 = b0; ta.b1 = b1;
         ta.head = head; ta.mode = mode; ta.nb = nb;
         ta.gpart = gpart.as<float>(); ta.lpart = lpart.as<double>(); ta.mpart = mpart.as<double>(); ta.pred = pred;
-        ta.H1t = h1t.as<float>(); ta.G2t = g2t.as<float>(); ta.G1t = g1t.as<float>(); ta.ld_t = b1 - b0;
-        return ta;
+        ta.H1t = h1t.as<float>(); ta.G2t = g2t.as<float>(); ta.G1t = g1t.as<float>();
+        ta.ld_t = ((b1 - b0 + 63) / 64) * 64;
+        const int ctas = launch_tile_tc(n.u, ta, ctx->sm_count, ctx->stream);
+        check_launch(ctx);
+        return ctas;
     }
 
     // Gradient partials of rows [b0, b1): per-tile partials (+ weight-gradient
     // partials on the tensor-core path, described by sp); returns the tile count.
     int grad_tiles(const float* X, const double* y, long b0, long b1, int head, double nb, SplitPartials* sp) {
         if (use_tc) {
-            if (!Xt) throw contract_error("training: transposed features missing for the tensor-core path");
-            launch_tile_tc(n.u, tile_args(X, y, b0, b1, head, 0, nb, nullptr), ctx->stream);
-            check_launch(ctx);
+            const int ctas = tile_launch(y, b0, b1, head, 0, nb, nullptr);
             WgradArgs wa{};
             wa.d = n.d; wa.dp = dp; wa.P = n.P; wa.off0 = n.off[0]; wa.off1 = n.off[1];
-            wa.G2t = g2t.as<float>(); wa.H1t = h1t.as<float>(); wa.G1t = g1t.as<float>(); wa.ld_t = b1 - b0;
-            wa.Xt = Xt; wa.ld_x = ld_x; wa.row0 = b0; wa.rows = b1 - b0; wa.gpart = gpartB.as<float>();
+            wa.G2t = g2t.as<float>(); wa.H1t = h1t.as<float>(); wa.G1t = g1t.as<float>();
+            wa.ld_t = ((b1 - b0 + 63) / 64) * 64;
+            wa.Xt = xt.as<float>(); wa.ld_x = ld_x; wa.row0 = b0; wa.rows = b1 - b0; wa.gpart = gpartB.as<float>();
             const int nB = launch_wgrad_tc(n.u, wa, ctx->sm_count, ctx->stream);
             check_launch(ctx);
             if (sp) *sp = SplitPartials{gpartB.as<float>(), nB, n.off[0], n.off[0] + n.u * n.d, n.off[1],
                                         n.off[1] + n.u * n.u};
-            return static_cast<int>((b1 - b0 + 127) / 128);
+            return ctas;
         }
         const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);
         k_sgd<<<tiles, TR, smem(), ctx->stream>>>(n, X, y, b0, b1, p32.as<float>(), head, nb, gpart.as<float>(),
@@ -625,9 +645,7 @@ struct Trainer {
     // Full-sample forward; sets last_parts = number of loss / min partials written.
     void eval(const float* X, const double* y, long R, int mode, double* pred) {
         if (use_tc) {
-            launch_tile_tc(n.u, tile_args(X, y, 0, R, 1, mode, 1.0, pred), ctx->stream);
-            check_launch(ctx);
-            last_parts = static_cast<int>((R + 127) / 128);
+            last_parts = tile_launch(y, 0, R, 1, mode, 1.0, pred);
             return;
         }
         k_eval<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), mode, lpart.as<double>(),
@@ -698,7 +716,6 @@ struct FeatArgs {
     const double* mean;
     const double* scale;
     float* X;
-    float* Xt;  // optional transposed copy [d][M*N] (tensor-core weight gradients)
 };
 
 __device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
@@ -719,16 +736,9 @@ __global__ void k_build_x(FeatArgs a) {
     const int k = static_cast<int>(row / a.N);
     const int Cc = a.Cn - 1, q = 3 * a.E - 1 + Cc, d = Cc + q;
     float* o = a.X + row * d;
-    for (int c = 1; c <= Cc; ++c) {
-        const float v = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
-        o[c - 1] = v;
-        if (a.Xt) a.Xt[(c - 1) * R + row] = v;
-    }
-    for (int j = 0; j < q; ++j) {
-        const float v = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
-        o[Cc + j] = v;
-        if (a.Xt) a.Xt[(Cc + j) * R + row] = v;
-    }
+    for (int c = 1; c <= Cc; ++c) o[c - 1] = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
+    for (int j = 0; j < q; ++j)
+        o[Cc + j] = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
 }
 
 // Scaler (regressor.cpp:84-95) over the rows: the state columns repeat per path,
@@ -812,20 +822,12 @@ FeatArgs feat_args(hcva_sim* sim, int step) {
     return a;
 }
 
-// Stage host features (FP64 [rows][d]) as FP32 X and, for the tensor-core
-// path, the zero-padded transpose Xt [dp][rows].
-void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX, DeviceBuf& dXt) {
+// Stage host features (FP64 [rows][d]) as FP32 X (+ the tensor-core images).
+void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX) {
     std::vector<float> xf(static_cast<size_t>(rows) * d);
     for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
     stage(dX, xf);
-    if (tr.use_tc) {
-        std::vector<float> xt(static_cast<size_t>(tr.dp) * rows, 0.0f);
-        for (int r = 0; r < rows; ++r)
-            for (int j = 0; j < d; ++j) xt[static_cast<size_t>(j) * rows + r] = xf[static_cast<size_t>(r) * d + j];
-        stage(dXt, xt);
-        tr.Xt = dXt.as<float>();
-        tr.ld_x = rows;
-    }
+    tr.prepare_x(dX.as<float>(), rows);
 }
 
 }  // namespace
@@ -850,8 +852,8 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         HCVA_CUDA(cudaSetDevice(ctx->device));
         const NetDims n = dims_from(cfg, input_dim);
         Trainer tr(ctx, n, rows);
-        DeviceBuf dX, dXt, dy;
-        stage_features(tr, x, rows, input_dim, dX, dXt);
+        DeviceBuf dX, dy;
+        stage_features(tr, x, rows, input_dim, dX);
         stage(dy, std::vector<double>(y, y + rows));
         tr.set_params(params);
         SplitPartials sp;
@@ -887,8 +889,8 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
         if (cfg->n_batches < 1 || rows % cfg->n_batches != 0)
             throw config_error("make_batches: batch count must divide M*N");
         Trainer tr(ctx, n, rows / cfg->n_batches, rows);
-        DeviceBuf dX, dXt, dy, dl;
-        stage_features(tr, x, rows, input_dim, dX, dXt);
+        DeviceBuf dX, dy, dl;
+        stage_features(tr, x, rows, input_dim, dX);
         stage(dy, std::vector<double>(y, y + rows));
         dl.alloc(sizeof(double) * std::max(cfg->epochs, 1));
         tr.set_params(init);
@@ -931,14 +933,8 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
         if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
         Trainer tr(ctx, n, R / cfg->n_batches, R);
         HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
-        DeviceBuf X, Xt;
+        DeviceBuf X;
         X.alloc(sizeof(float) * R * d);
-        if (tr.use_tc) {
-            Xt.alloc(sizeof(float) * R * tr.dp);
-            HCVA_CUDA(cudaMemsetAsync(Xt.p, 0, sizeof(float) * R * tr.dp, ctx->stream));  // pad rows stay 0
-            tr.Xt = Xt.as<float>();
-            tr.ld_x = R;
-        }
         for (int i = nsteps; i >= 1; --i) {
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
@@ -948,9 +944,9 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
             fa.mean = mean;
             fa.scale = scale;
             fa.X = X.as<float>();
-            fa.Xt = tr.use_tc ? Xt.as<float>() : nullptr;
             k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
             check_launch(ctx);
+            tr.prepare_x(X.as<float>(), R);
             const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
             if (i == nsteps) {
                 const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));
@@ -1022,6 +1018,7 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         fa.X = X.as<float>();
         k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
         check_launch(ctx);
+        tr.prepare_x(X.as<float>(), R);
         tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
         copy_out(ctx, out, pred.p, R * 8);
     });

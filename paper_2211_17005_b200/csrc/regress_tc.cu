@@ -4,21 +4,28 @@
 // network shape: two hidden layers of width U in {16, 32, 64}, input d <= 64.
 // All operands are K-major (canonical no-swizzle core tiles, tc.cuh).
 //
-// k_tile_tc<U>   one 128-row tile per CTA, 128 threads (thread r = row r =
-//                TMEM lane r); thread 0 issues the MMAs, tcgen05.commit
-//                signals an mbarrier, epilogues read TMEM with tcgen05.ld.
-//     F0   D0  = X  W0^T   (M=128, N=U, K=dp)  -> H1 = act(D0 + b0)
+// k_pack_w      parameters -> weight image (W0, W1, W1^T hi/lo planes + biases),
+//               one bulk copy per CTA.
+// k_pack_x      features X [R][d] -> 128-row operand tiles (hi/lo) + Xt [dp][R].
+// k_tile_tc<U, ACT>  persistent: one CTA per SM walks 128-row tiles (thread r
+//               = row r = TMEM lane r); thread 0 issues the MMAs, tcgen05.commit
+//               signals an mbarrier, epilogues read TMEM with tcgen05.ld; the
+//               next tile's features stream in by cp.async.bulk during the
+//               current tile's layer-1 and backward GEMMs.
+//     F0   D0  = X  W0^T   (M=128, N=U, K=dp)  -> H1 = act(D0 + b0); act'(H1) -> D0
 //     F1   D1  = H1 W1^T   (M=128, N=U, K=U)   -> H2, f, loss, G2
 //     B    Dbp = G2 W1     (M=128, N=U, K=U; B operand = W1^T tile)
 //                                              -> G1 = Dbp act'(H1)
 //   SGD mode also writes H1, G2, G1 transposed ([feature][row]) for the
-//   weight-gradient kernel, and per-tile partials of the biases, the output
-//   layer and mu; eval mode produces the loss / min fit / predictions.
+//   weight-gradient kernel; the bias / output-layer / mu gradients are column
+//   sums (butterfly reduce-scatter across the warp, accumulated per CTA).
+//   Eval mode produces the loss / min fit / predictions.
 // k_wgrad_tc<U>  split-K weight gradients over the batch rows: each CTA
 //                accumulates  gW1 = G2^T H1 (M=64, N=U)  and
 //                gW0 = G1^T X (M=64, N=dp) over its rows in TMEM, 64-row
-//                chunks, and writes one partial.
-// Reductions of the partials are fixed-order FP64 (k_adam in regress.cu).
+//                chunks with the next chunk's loads in flight, one partial.
+// Reductions of the per-CTA partials are fixed-order FP64 (k_adam in regress.cu).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -28,29 +35,34 @@
 
 namespace hcva {
 
-__device__ __forceinline__ float tc_act(int a, float z) {
-    switch (a) {
-        case 0: return tanhf(z);
-        case 1: return 1.0f / (1.0f + expf(-z));
-        case 2: return fmaxf(z, 0.0f) + log1pf(expf(-fabsf(z)));
-        default: return fmaxf(z, 0.0f);
-    }
+// Activations (regressor.cpp:35-57), derivative from the activation value.
+template <int ACT>
+__device__ __forceinline__ float act_f(float z) {
+    if constexpr (ACT == 0) return tanhf(z);
+    else if constexpr (ACT == 1) return 1.0f / (1.0f + expf(-z));
+    else if constexpr (ACT == 2) return fmaxf(z, 0.0f) + log1pf(expf(-fabsf(z)));
+    else return fmaxf(z, 0.0f);
 }
-__device__ __forceinline__ float tc_der(int a, float v) {
-    switch (a) {
-        case 0: return 1.0f - v * v;
-        case 1: return v * (1.0f - v);
-        case 2: return -expm1f(-v);
-        default: return v > 0.0f ? 1.0f : 0.0f;
-    }
+template <int ACT>
+__device__ __forceinline__ float act_d(float v) {
+    if constexpr (ACT == 0) return 1.0f - v * v;
+    else if constexpr (ACT == 1) return v * (1.0f - v);
+    else if constexpr (ACT == 2) return -expm1f(-v);
+    else return v > 0.0f ? 1.0f : 0.0f;
 }
 
-constexpr uint32_t kRowTile = 128 * 64 * 4;  // 128 x 64 FP32 core tile
 constexpr int kTcThreads = 128;
 
-__host__ __device__ constexpr size_t tile_tc_smem(int U) {
-    return 4 * static_cast<size_t>(kRowTile) + 6 * static_cast<size_t>(U) * 64 * 4 + 512 * 4 + 64 * 8 + 64;
+__host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
+    return 2u * U * dp * 4 + 4u * U * U * 4 + 1024;
 }
+__host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp * 4; }
+__host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
+    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 64;
+}
+
+size_t tc_weight_image_bytes(int u, int dp) { return w_image_bytes(u, dp); }
+size_t tc_x_tile_bytes(int dp) { return 2ull * x_plane_bytes(dp); }
 
 __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -61,213 +73,340 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Butterfly reduce-scatter of N (16 or 32) per-lane columns over the warp:
+// N-1 shuffles; the result is the warp's sum of column lane % N.
+template <int N>
+__device__ __forceinline__ float bfly_sum(float* v, int lane) {
+#pragma unroll
+    for (int off = N / 2; off >= 1; off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = up ? v[i] : v[i + off];
+            const float keep = up ? v[i + off] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    float s = v[0];
+    if (N < 32) s += __shfl_xor_sync(0xffffffffu, s, 16);
+    return s;
+}
+
+// acc[b] += warp column sum of g[b*32 + lane % NW] (NW = min(U, 32)).
 template <int U>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a) {
+__device__ __forceinline__ void colsum_acc(const float* g, float* acc, int lane) {
+    constexpr int NW = U < 32 ? U : 32;
+#pragma unroll
+    for (int b = 0; b < (U + 31) / 32; ++b) {
+        float t[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) t[i] = g[b * 32 + i];
+        acc[b] += bfly_sum<NW>(t, lane);
+    }
+}
+
+__global__ void k_pack_w(int U, int d, int dp, int off0, int off1, int off2, int P, const float* __restrict__ p,
+                         uint8_t* __restrict__ img) {
+    const uint32_t w0b = U * dp * 4, w1b = U * U * 4;
+    uint8_t* w0 = img;
+    uint8_t* w1 = w0 + 2 * w0b;
+    uint8_t* w1t = w1 + 2 * w1b;
+    float* vec = reinterpret_cast<float*>(w1t + 2 * w1b);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < U * dp) {
+        const int o = i / dp, j = i % dp;
+        tc::put_split(w0, w0b, o, j, U, (j < d) ? p[off0 + o * d + j] : 0.0f);
+    }
+    if (i < U * U) {
+        const int o = i / U, j = i % U;
+        const float wv = p[off1 + o * U + j];
+        tc::put_split(w1, w1b, o, j, U, wv);
+        tc::put_split(w1t, w1b, j, o, U, wv);
+    }
+    if (i < 256) {
+        const int q = i >> 6, k = i & 63;
+        float v = 0.0f;
+        if (q == 0 && k < U) v = p[off0 + U * d + k];
+        else if (q == 1 && k < U) v = p[off1 + U * U + k];
+        else if (q == 2 && k < U) v = p[off2 + k];
+        else if (q == 3 && k == 0) v = p[off2 + U];
+        else if (q == 3 && k == 1) v = p[P - 1];
+        vec[i] = v;
+    }
+}
+
+__global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uint8_t* __restrict__ img,
+                         float* __restrict__ Xt, long ld_x) {
+    const uint32_t xb = x_plane_bytes(dp);
+    uint8_t* tile = img + static_cast<size_t>(blockIdx.x) * 2 * xb;
+    const int r = threadIdx.x;
+    const long row = static_cast<long>(blockIdx.x) * 128 + r;
+    const bool in = row < R;
+    for (int c = 0; c < dp; c += 4) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = (in && c + q < d) ? X[row * d + c + q] : 0.0f;
+        tc::put_split4(tile, xb, r, c, 128, make_float4(v[0], v[1], v[2], v[3]));
+        if (in)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Xt[(c + q) * ld_x + row] = v[q];
+    }
+}
+
+template <int U, int ACT>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_first, long n_tiles) {
     extern __shared__ __align__(128) uint8_t sm[];
-    constexpr uint32_t wbytes = U * 64 * 4;
-    uint8_t* bufX = sm;                // X, then G2 (128 x 64 core tile, lo at +kRowTile)
-    uint8_t* bufH = sm + 2 * kRowTile; // H1
-    uint8_t* w0 = sm + 4 * kRowTile;   // U x 64
-    uint8_t* w1 = w0 + 2 * wbytes;     // U x U (row = out, col = in)
-    uint8_t* w1t = w1 + 2 * wbytes;    // U x U transposed (row = in, col = out)
-    float* vec = reinterpret_cast<float*>(w1t + 2 * wbytes);  // b0 b1 w2 misc [64 each], colsum [4][64]
-    float* colsum = vec + 256;
-    double* red = reinterpret_cast<double*>(vec + 512);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 64);
-    uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
+    const int dp = a.dp;
+    const uint32_t w0b = U * dp * 4, w1b = U * U * 4, hb = 128 * U * 4, xb = x_plane_bytes(dp);
+    const uint32_t wbytes = w_image_bytes(U, dp);
+    uint8_t* w0 = sm;
+    uint8_t* w1 = w0 + 2 * w0b;
+    uint8_t* w1t = w1 + 2 * w1b;
+    const float* vec = reinterpret_cast<const float*>(w1t + 2 * w1b);  // b0 | b1 | w2 | b2, mu
+    uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
+    uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(bufX + 2 * xb);  // [0] MMA, [1] weights, [2] features
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
-    const int d = a.d, dp = a.dp;
     const bool sgd = a.mode == 0;
-    const long base = a.row0 + static_cast<long>(blockIdx.x) * 128;
-    const int rows = static_cast<int>(min(128L, a.row_end - base));
-    const bool live = r < rows;
-    const float* P = a.params;
-
-    if (r == 0) tc::mbar_init(mbar, 1);
-    if (warp == 0) tc::tmem_alloc(tbase, 256);
-    for (int i = r; i < U * dp; i += kTcThreads) {
-        const int o = i / dp, j = i % dp;
-        tc::put_split(w0, wbytes, o, j, U, (j < d) ? P[a.off0 + o * d + j] : 0.0f);
-    }
-    for (int i = r; i < U * U; i += kTcThreads) {
-        const int o = i / U, j = i % U;
-        const float wv = P[a.off1 + o * U + j];
-        tc::put_split(w1, wbytes, o, j, U, wv);
-        if (sgd) tc::put_split(w1t, wbytes, j, o, U, wv);
-    }
-    if (r < 64) {
-        vec[r] = (r < U) ? P[a.off0 + U * d + r] : 0.0f;       // b0
-        vec[64 + r] = (r < U) ? P[a.off1 + U * U + r] : 0.0f;  // b1
-        vec[128 + r] = (r < U) ? P[a.off2 + r] : 0.0f;         // w2
-    }
     if (r == 0) {
-        vec[192] = P[a.off2 + U];  // b2
-        vec[193] = P[a.P - 1];     // mu
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::mbar_init(&bar[2], 1);
+        tc::fence_async_smem();
     }
-    for (int i = r; i < 128 * dp; i += kTcThreads) {
-        const int rr = i / dp, j = i % dp;
-        const float v = (rr < rows && j < d) ? a.X[(base + rr) * d + j] : 0.0f;
-        tc::put_split(bufX, kRowTile, rr, j, 128, v);
-    }
-    tc::fence_async_smem();
+    if (warp == 0) tc::tmem_alloc(tbase, 256);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tm = *tbase;
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    uint32_t phase = 0;
-    auto mma_sync = [&]() {
-        tc::mbar_wait(mbar, phase);
-        phase ^= 1;
+    const uint32_t lb = static_cast<uint32_t>(warp * 32) << 16;
+    const long t_end = t_first + n_tiles;
+    long tile = t_first + blockIdx.x;
+    if (r == 0) {
+        tc::mbar_expect_tx(&bar[1], wbytes);
+        tc::bulk_g2s(w0, a.wimg, wbytes, &bar[1]);
+        tc::mbar_expect_tx(&bar[2], 2 * xb);
+        tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
+    }
+    tc::mbar_wait(&bar[1], 0);
+    uint32_t mph = 0, xph = 0;
+    auto mma_wait = [&]() {
+        tc::mbar_wait(&bar[0], mph);
+        mph ^= 1;
         tc::fence_after_sync();
     };
-    auto smem_sync = [&]() {
+    auto cta_sync = [&]() {
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
     };
-    const long trow = base - a.row0 + r;  // row index in the transposed arrays
+    const float b2 = vec[192], mu = vec[193];
+    constexpr int NB = (U + 31) / 32;
+    double loss = 0.0, dmu = 0.0, mn = INFINITY;
+    float gb2 = 0.0f;
+    float acc_w2[NB], acc_b1[NB], acc_b0[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc_w2[b] = acc_b1[b] = acc_b0[b] = 0.0f;
 
-    // ---- F0: D0 = X W0^T ; H1 = act(D0 + b0)
-    if (r == 0) {
-        tc::gemm3(tm, tc::kmajor(bufX, kRowTile, 128), tc::kmajor(w0, wbytes, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
-        tc::commit(mbar);
-    }
-    mma_sync();
-#pragma unroll
-    for (int c0 = 0; c0 < U; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + c0, v);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const float h = tc_act(a.act, v[q] + vec[c0 + q]);
-            tc::put_split(bufH, kRowTile, r, c0 + q, 128, h);
-            if (sgd && live) a.H1t[(c0 + q) * a.ld_t + trow] = h;
+    for (; tile < t_end; tile += gridDim.x) {
+        const long row = tile * 128 + r;
+        const bool live = row >= a.b0 && row < a.b1;
+        const long trow = row - a.b0;
+        tc::mbar_wait(&bar[2], xph);
+        xph ^= 1;
+        // ---- F0: D0 = X W0^T
+        if (r == 0) {
+            tc::gemm3(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
         }
-    }
-    smem_sync();
-    // ---- F1: D1 = H1 W1^T ; H2, f
-    if (r == 0) {
-        tc::gemm3(tm + 64, tc::kmajor(bufH, kRowTile, 128), tc::kmajor(w1, wbytes, U), U, tc::idesc_tf32(128, U, 0, 0),
-                  0);
-        tc::commit(mbar);
-    }
-    mma_sync();
-    float h2[U];
+        mma_wait();
+        if (r == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
+            tc::mbar_expect_tx(&bar[2], 2 * xb);
+            tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
+        }
+        // H1 = act(D0 + b0) -> bufH (+ H1t); act'(H1) back into D0
 #pragma unroll
-    for (int c0 = 0; c0 < U; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + 64 + c0, v);
+        for (int c0 = 0; c0 < U; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lb + c0, v);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) h2[c0 + q] = tc_act(a.act, v[q] + vec[64 + c0 + q]);
-    }
-    float f = vec[192];
+            for (int q = 0; q < 16; ++q) v[q] = act_f<ACT>(v[q] + vec[c0 + q]);
 #pragma unroll
-    for (int j = 0; j < U; ++j) f = fmaf(h2[j], vec[128 + j], f);
-    const float mu = vec[193];
-
-    if (!sgd) {  // ---------------- evaluation
-        double l = 0.0, mn = INFINITY;
-        if (live) {
-            const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
-            if (a.mode & 1) {
-                const double res = ph - a.y[base + r];
-                l = res * res;
+            for (int q = 0; q < 16; q += 4)
+                tc::put_split4(bufH, hb, r, c0 + q, 128, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+            if (sgd) {
+                if (live)
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = act_d<ACT>(v[q]);
+                tc::tmem_st16(tm + lb + c0, v);
             }
-            if (a.mode & 2) mn = static_cast<double>(f + mu);
-            if (a.mode & 4) a.pred[base + r] = ph;
         }
-        l = warp_sum(l);
-        for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        if (lane == 0) {
-            red[warp] = l;
-            red[4 + warp] = mn;
+        if (sgd) tc::tmem_wait_st();
+        cta_sync();
+        // ---- F1: D1 = H1 W1^T ; H2, f
+        if (r == 0) {
+            tc::gemm3(tm + 64, tc::kmajor(bufH, hb, 128), tc::kmajor(w1, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
+                      0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+        float h2[U];
+#pragma unroll
+        for (int c0 = 0; c0 < U; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lb + 64 + c0, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) h2[c0 + q] = act_f<ACT>(v[q] + vec[64 + c0 + q]);
+        }
+        float f = b2;
+#pragma unroll
+        for (int j = 0; j < U; ++j) f = fmaf(h2[j], vec[128 + j], f);
+
+        if (!sgd) {  // ---------------- evaluation
+            if (live) {
+                const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
+                if (a.mode & 1) {
+                    const double res = ph - a.y[row];
+                    loss += res * res;
+                }
+                if (a.mode & 2) mn = fmin(mn, static_cast<double>(f + mu));
+                if (a.mode & 4) a.pred[row] = ph;
+            }
+            continue;
+        }
+
+        // ---------------- SGD: residual, output layer, mu
+        float dd = 0.0f;
+        if (live) {
+            const float pr = ((a.head && f < 0.0f) ? 0.0f : f) + mu;
+            const double res = static_cast<double>(pr) - a.y[row];
+            loss += res * res;
+            const double dm = 2.0 * res / a.nb;
+            dmu += dm;
+            dd = static_cast<float>(dm);
+            if (a.head && !(f > 0.0f)) dd = 0.0f;
+        }
+        gb2 += dd;
+        {
+            float g[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) g[j] = dd * h2[j];
+            colsum_acc<U>(g, acc_w2, lane);
+        }
+        {  // G2 = dd w2 act'(H2) -> bufH (F1 has consumed H1), G2t
+            float g[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) g[j] = dd * vec[128 + j] * act_d<ACT>(h2[j]);
+#pragma unroll
+            for (int j = 0; j < U; j += 4)
+                tc::put_split4(bufH, hb, r, j, 128, make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]));
+            if (live)
+#pragma unroll
+                for (int j = 0; j < U; ++j) a.G2t[j * a.ld_t + trow] = g[j];
+            colsum_acc<U>(g, acc_b1, lane);
+        }
+        cta_sync();
+        // ---- B: Dbp = G2 W1 (B operand: the W1^T tile, K-major over the outputs of layer 1)
+        if (r == 0) {
+            tc::gemm3(tm + 128, tc::kmajor(bufH, hb, 128), tc::kmajor(w1t, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
+                      0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+        {
+            float g[U];
+#pragma unroll
+            for (int c0 = 0; c0 < U; c0 += 16) {
+                float v[16], dv[16];
+                tc::tmem_ld16(tm + lb + 128 + c0, v);
+                tc::tmem_ld16(tm + lb + c0, dv);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) g[c0 + q] = live ? v[q] * dv[q] : 0.0f;
+            }
+            if (live)
+#pragma unroll
+                for (int j = 0; j < U; ++j) a.G1t[j * a.ld_t + trow] = g[j];
+            colsum_acc<U>(g, acc_b0, lane);
         }
         tc::fence_before_sync();
-        __syncthreads();
-        if (r == 0) {
-            if (a.mode & 1) a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
-            if (a.mode & 2) a.mpart[blockIdx.x] = fmin(fmin(red[4], red[5]), fmin(red[6], red[7]));
-        }
-        if (warp == 0) tc::tmem_dealloc(tm, 256);
-        return;
+        __syncthreads();  // TMEM reads of D0 / Dbp done before the next tile's F0
+        tc::fence_after_sync();
     }
 
-    // ---------------- SGD: residual, output layer, mu
-    double resid2 = 0.0, dmu = 0.0;
-    float dd = 0.0f;
-    if (live) {
-        const float pred = ((a.head && f < 0.0f) ? 0.0f : f) + mu;
-        const double res = static_cast<double>(pred) - a.y[base + r];
-        resid2 = res * res;
-        dmu = 2.0 * res / a.nb;
-        dd = static_cast<float>(dmu);
-        if (a.head && !(f > 0.0f)) dd = 0.0f;
-    }
-    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
-    {
-        const double l = warp_sum(resid2), m = warp_sum(dmu);
-        const float gb = warp_sum(dd);
-        if (lane == 0) {
-            red[warp] = l;
-            red[4 + warp] = m;
-            red[8 + warp] = gb;
-        }
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            const float s = warp_sum(dd * h2[j]);
-            if (lane == 0) colsum[warp * 64 + j] = s;
-        }
-    }
-    __syncthreads();
-    if (r == 0) {
-        a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
-        gout[a.P - 1] = static_cast<float>(red[4] + red[5] + red[6] + red[7]);
-        gout[a.off2 + U] = static_cast<float>(red[8] + red[9] + red[10] + red[11]);
-    }
-    if (r < U) gout[a.off2 + r] = colsum[r] + colsum[64 + r] + colsum[128 + r] + colsum[192 + r];
-    __syncthreads();
-    // G2 = dd w2 act'(H2) -> bufX (K-major), G2t; bias gradient of layer 1.
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-        const float g = dd * vec[128 + j] * tc_der(a.act, h2[j]);
-        tc::put_split(bufX, kRowTile, r, j, 128, g);
-        if (live) a.G2t[j * a.ld_t + trow] = g;
-        const float s = warp_sum(g);
-        if (lane == 0) colsum[warp * 64 + j] = s;
-    }
-    smem_sync();
-    if (r < U) gout[a.off1 + U * U + r] = colsum[r] + colsum[64 + r] + colsum[128 + r] + colsum[192 + r];
-    // ---- B: Dbp = G2 W1 (B operand: the W1^T tile, K-major over the outputs of layer 1)
-    if (r == 0) {
-        tc::gemm3(tm + 128, tc::kmajor(bufX, kRowTile, 128), tc::kmajor(w1t, wbytes, U), U,
-                  tc::idesc_tf32(128, U, 0, 0), 0);
-        tc::commit(mbar);
-    }
-    mma_sync();
-    __syncthreads();  // colsum reads of layer 1 done
-#pragma unroll
-    for (int c0 = 0; c0 < U; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + 128 + c0, v);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const float h1 = tc::get_split(bufH, kRowTile, r, c0 + q, 128);
-            const float g = live ? v[q] * tc_der(a.act, h1) : 0.0f;
-            if (live) a.G1t[(c0 + q) * a.ld_t + trow] = g;
-            const float s = warp_sum(g);
-            if (lane == 0) colsum[warp * 64 + c0 + q] = s;
-        }
-    }
+    // ---- per-CTA partials (fixed order over the 4 warps)
     tc::fence_before_sync();
     __syncthreads();
-    if (r < U) gout[a.off0 + U * d + r] = colsum[r] + colsum[64 + r] + colsum[128 + r] + colsum[192 + r];
+    float* part = reinterpret_cast<float*>(bufH);  // [warp][3][64]
+    double* red = reinterpret_cast<double*>(part + 4 * 3 * 64);
+    constexpr int NW = U < 32 ? U : 32;
+    if (sgd && lane < NW)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            part[(warp * 3 + 0) * 64 + b * 32 + lane] = acc_w2[b];
+            part[(warp * 3 + 1) * 64 + b * 32 + lane] = acc_b1[b];
+            part[(warp * 3 + 2) * 64 + b * 32 + lane] = acc_b0[b];
+        }
+    loss = warp_sum(loss);
+    dmu = warp_sum(dmu);
+    gb2 = warp_sum(gb2);
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) {
+        red[warp] = loss;
+        red[4 + warp] = dmu;
+        red[8 + warp] = gb2;
+        red[12 + warp] = mn;
+    }
+    __syncthreads();
+    const int cta = blockIdx.x;
+    if (sgd) {
+        float* gout = a.gpart + static_cast<size_t>(cta) * a.P;
+        if (r < U) {
+            const auto sum4 = [&](int q) {
+                return part[(0 * 3 + q) * 64 + r] + part[(1 * 3 + q) * 64 + r] + part[(2 * 3 + q) * 64 + r] +
+                       part[(3 * 3 + q) * 64 + r];
+            };
+            gout[a.off2 + r] = sum4(0);
+            gout[a.off1 + U * U + r] = sum4(1);
+            gout[a.off0 + U * a.d + r] = sum4(2);
+        }
+        if (r == 0) {
+            a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
+            gout[a.P - 1] = static_cast<float>(red[4] + red[5] + red[6] + red[7]);
+            gout[a.off2 + U] = static_cast<float>(red[8] + red[9] + red[10] + red[11]);
+        }
+    } else if (r == 0) {
+        if (a.mode & 1) a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
+        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[12], red[13]), fmin(red[14], red[15]));
+    }
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
 constexpr uint32_t kChunkTile = 64 * 64 * 4;  // 64 x 64 FP32 core tile
+
+// Four consecutive floats, zero beyond `valid`; 16-byte load when aligned.
+__device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
+    float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (valid <= 0) return v;
+    if (vec) {
+        v = __ldg(reinterpret_cast<const float4*>(p));
+    } else {
+        v.x = p[0];
+        if (valid > 1) v.y = p[1];
+        if (valid > 2) v.z = p[2];
+        if (valid > 3) v.w = p[3];
+    }
+    if (valid < 4) {
+        if (valid < 2) v.y = 0.0f;
+        if (valid < 3) v.z = 0.0f;
+        v.w = 0.0f;
+    }
+    return v;
+}
 
 template <int U>
 __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
@@ -282,28 +421,53 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
     const int dp = a.dp;
     if (t == 0) tc::mbar_init(mbar, 1);
     if (warp == 0) tc::tmem_alloc(tbase, 128);
-    for (int i = t; i < 8 * kChunkTile / 4; i += kTcThreads) reinterpret_cast<float*>(sm)[i] = 0.0f;
+    for (int i = t; i < 8 * kChunkTile / 16; i += kTcThreads)
+        reinterpret_cast<float4*>(sm)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tm = *tbase;
     const long r_begin = static_cast<long>(blockIdx.x) * a.rows_per_cta;
     const long r_end = min(r_begin + a.rows_per_cta, a.rows);
+    const bool vt = (a.ld_t % 4) == 0;
+    const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
+    constexpr int NF = U * 16 / kTcThreads;  // float4 per thread per activation array
+    float4 rg2[NF], rh1[NF], rg1[NF], rx[8];
+    auto load = [&](long c0) {
+        const int n = static_cast<int>(min(64L, r_end - c0));
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
+            rg2[i] = ld4(a.G2t + o, vt, n - k);
+            rh1[i] = ld4(a.H1t + o, vt, n - k);
+            rg1[i] = ld4(a.G1t + o, vt, n - k);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            if (f < dp) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
+        }
+    };
     uint32_t phase = 0;
     int first = 1;
+    if (r_begin < r_end) load(r_begin);
     for (long c0 = r_begin; c0 < r_end; c0 += 64) {
-        const int n = static_cast<int>(min(64L, r_end - c0));
-        // Coalesced loads: 64 consecutive rows of each feature line.
-        for (int i = t; i < U * 64; i += kTcThreads) {
-            const int f = i / 64, k = i % 64;
-            const bool in = k < n;
-            tc::put_split(tA1, kChunkTile, f, k, 64, in ? a.G2t[f * a.ld_t + c0 + k] : 0.0f);
-            tc::put_split(tB1, kChunkTile, f, k, 64, in ? a.H1t[f * a.ld_t + c0 + k] : 0.0f);
-            tc::put_split(tA0, kChunkTile, f, k, 64, in ? a.G1t[f * a.ld_t + c0 + k] : 0.0f);
+        if (!first) {  // previous chunk's MMAs done reading the tiles
+            tc::mbar_wait(mbar, phase);
+            phase ^= 1;
         }
-        for (int i = t; i < dp * 64; i += kTcThreads) {
-            const int f = i / 64, k = i % 64;
-            tc::put_split(tB0, kChunkTile, f, k, 64, (k < n) ? a.Xt[f * a.ld_x + a.row0 + c0 + k] : 0.0f);
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            tc::put_split4(tA1, kChunkTile, f, k, 64, rg2[i]);
+            tc::put_split4(tB1, kChunkTile, f, k, 64, rh1[i]);
+            tc::put_split4(tA0, kChunkTile, f, k, 64, rg1[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            if (f < dp) tc::put_split4(tB0, kChunkTile, f, k, 64, rx[i]);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -316,11 +480,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
                       tc::idesc_tf32(64, dp, 0, 0), !first);
             tc::commit(mbar);
         }
-        tc::mbar_wait(mbar, phase);
-        phase ^= 1;
-        tc::fence_after_sync();
         first = 0;
-        __syncthreads();  // chunk consumed before the next overwrites it
+        if (c0 + 64 < r_end) load(c0 + 64);  // in flight while the MMAs run
+    }
+    if (!first) {
+        tc::mbar_wait(mbar, phase);
+        tc::fence_after_sync();
     }
     float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
     const int o = warp * 16 + lane;  // M=64 accumulator: row 16w+t in lane 32w+t, t < 16
@@ -405,23 +570,48 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
-    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && d <= 64;
+    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && d <= 64 &&
+           tile_tc_smem(u, ((d + 15) / 16) * 16) <= 227 * 1024;
 }
 
 int tc_dp(int d) { return ((d + 15) / 16) * 16; }
 
-template <int U>
-void launch_tile_u(const TileArgs& a, int tiles, cudaStream_t s) {
-    const size_t smem = tile_tc_smem(U);
-    HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_tc<U><<<tiles, kTcThreads, smem, s>>>(a);
+void launch_pack_w(int u, int d, int dp, int off0, int off1, int off2, int P, const float* params, uint8_t* wimg,
+                   cudaStream_t s) {
+    const int n = std::max(256, std::max(u * dp, u * u));
+    k_pack_w<<<(n + 255) / 256, 256, 0, s>>>(u, d, dp, off0, off1, off2, P, params, wimg);
 }
 
-void launch_tile_tc(int u, const TileArgs& a, cudaStream_t s) {
-    const int tiles = static_cast<int>((a.row_end - a.row0 + 127) / 128);
-    if (u == 16) launch_tile_u<16>(a, tiles, s);
-    else if (u == 32) launch_tile_u<32>(a, tiles, s);
-    else launch_tile_u<64>(a, tiles, s);
+void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, cudaStream_t s) {
+    const long tiles = (R + 127) / 128;
+    if (tiles > 0) k_pack_x<<<static_cast<unsigned>(tiles), 128, 0, s>>>(X, R, d, dp, ximg, Xt, ld_x);
+}
+
+template <int U, int ACT>
+void launch_tile_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = tile_tc_smem(U, a.dp);
+    HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile_tc<U, ACT><<<ctas, kTcThreads, smem, s>>>(a, t_first, n_tiles);
+}
+
+template <int U>
+void launch_tile_u(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    switch (a.act) {
+        case 0: launch_tile_ua<U, 0>(a, t_first, n_tiles, ctas, s); break;
+        case 1: launch_tile_ua<U, 1>(a, t_first, n_tiles, ctas, s); break;
+        case 2: launch_tile_ua<U, 2>(a, t_first, n_tiles, ctas, s); break;
+        default: launch_tile_ua<U, 3>(a, t_first, n_tiles, ctas, s); break;
+    }
+}
+
+int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
+    if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
+    const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
+    const int ctas = static_cast<int>(std::min<long>(n_tiles, sm_count));
+    if (u == 16) launch_tile_u<16>(a, t_first, n_tiles, ctas, s);
+    else if (u == 32) launch_tile_u<32>(a, t_first, n_tiles, ctas, s);
+    else launch_tile_u<64>(a, t_first, n_tiles, ctas, s);
+    return ctas;
 }
 
 template <int U>

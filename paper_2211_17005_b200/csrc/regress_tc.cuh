@@ -6,19 +6,24 @@
 
 namespace hcva {
 
+// Byte sizes of the packed operand images (3xTF32 hi / lo planes in the
+// canonical K-major core layout, tc.cuh).
+size_t tc_weight_image_bytes(int u, int dp);  // W0 | W1 | W1^T planes + bias vector block
+size_t tc_x_tile_bytes(int dp);               // one 128-row feature tile, hi | lo
+
 struct TileArgs {
     int d, dp, act, P, off0, off1, off2;
-    const float* X;  // [R][d]
-    const double* y;
-    long row0, row_end;
-    const float* params;
-    int head, mode;  // mode 0: SGD; else bits 1: loss (head on), 2: min plain fit, 4: predictions
+    const uint8_t* wimg;  // packed weights (k_pack_w)
+    const uint8_t* ximg;  // packed feature tiles [R/128][hi | lo] (k_pack_x)
+    const double* y;      // labels, absolute row index
+    long b0, b1;          // live rows [b0, b1)
+    int head, mode;       // mode 0: SGD; else bits 1: loss (head on), 2: min plain fit, 4: predictions
     double nb;
-    float* gpart;    // SGD: [tile][P] partials of b0, b1, w2, b2, mu
-    double* lpart;   // [tile] sum of squared residuals
-    double* mpart;   // [tile] min of f + mu (plain head)
-    double* pred;    // predictions (head on), indexed by absolute row
-    float *H1t, *G2t, *G1t;  // SGD: [U][ld_t] transposed, row index relative to row0
+    float* gpart;    // SGD: [cta][P] partials of b0, b1, w2, b2, mu
+    double* lpart;   // [cta] sum of squared residuals
+    double* mpart;   // [cta] min of f + mu (plain head)
+    double* pred;    // predictions (head on), absolute row index
+    float *H1t, *G2t, *G1t;  // SGD: [U][ld_t] transposed, row index relative to b0
     long ld_t;
 };
 
@@ -34,7 +39,13 @@ struct WgradArgs {
 
 bool tc_eligible(int d, int h, int u);
 int tc_dp(int d);  // input dimension padded for the tensor-core tiles
-void launch_tile_tc(int u, const TileArgs& a, cudaStream_t s);
+// Pack the FP32 parameters into the weight image.
+void launch_pack_w(int u, int d, int dp, int off0, int off1, int off2, int P, const float* params, uint8_t* wimg,
+                   cudaStream_t s);
+// Pack X [R][d] into 128-row tiles and the transposed copy Xt [dp][ld_x] (pad rows zero).
+void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, cudaStream_t s);
+// Returns the number of per-CTA partials written (gpart / lpart / mpart rows).
+int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s);
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s);
 
 }  // namespace hcva

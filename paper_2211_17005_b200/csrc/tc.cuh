@@ -4,11 +4,11 @@
 // Operand tiles use the canonical no-swizzle "core matrix" layout: a logical
 // R x C FP32 tile (R % 8 == 0, C % 4 == 0) stores element (r, c) at byte
 //   ((c/4) * (R/8) + r/8) * 128 + (r%8) * 16 + (c%4) * 4,
-// i.e. 8x4 core matrices of 128 contiguous bytes, consecutive along r.  The
-// same bytes are a K-major operand (rows = M/N, cols = K: SBO = 128,
-// LBO = R/8*128) and an MN-major operand (rows = K, cols = M/N:
-// SBO = R/8*128, LBO = 128), so activations written once serve the forward
-// GEMM (K-major) and the weight-gradient GEMM (MN-major).
+// i.e. 8x4 core matrices of 128 contiguous bytes, consecutive along r, read
+// as a K-major operand (rows = M/N, cols = K: SBO = 128, LBO = R/8*128).
+// Only K-major operands are used: MN-major reads of these tiles returned
+// zeros on sm_100a in our descriptor tests (tools/debug_gemm.py), so
+// transposed operands are written transposed instead.
 //
 // 3xTF32: every FP32 operand is stored as hi = rna_tf32(a) and lo = a - hi;
 // D += A_hi B_hi + A_lo B_hi + A_hi B_lo gives ~FP32 products with FP32
@@ -39,6 +39,14 @@ __device__ __forceinline__ void put_split(uint8_t* tile, uint32_t lo_bytes, int 
     const uint32_t o = core_off(r, c, R);
     *reinterpret_cast<float*>(tile + o) = hi;
     *reinterpret_cast<float*>(tile + lo_bytes + o) = a - hi;
+}
+
+// Four consecutive columns c..c+3 (c % 4 == 0) of row r: one 16-byte store per plane.
+__device__ __forceinline__ void put_split4(uint8_t* tile, uint32_t lo_bytes, int r, int c, int R, float4 a) {
+    const float4 hi = make_float4(tf32_rna(a.x), tf32_rna(a.y), tf32_rna(a.z), tf32_rna(a.w));
+    const uint32_t o = core_off(r, c, R);
+    *reinterpret_cast<float4*>(tile + o) = hi;
+    *reinterpret_cast<float4*>(tile + lo_bytes + o) = make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
 }
 
 __device__ __forceinline__ float get_split(const uint8_t* tile, uint32_t lo_bytes, int r, int c, int R) {
@@ -87,6 +95,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
         : "memory");
 }
 
+// Arrive on the barrier announcing `bytes` of asynchronous transfer.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+
+// Bulk (non-tensor) global -> shared copy completing on `mbar`; 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -114,6 +137,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// Store 16 consecutive FP32 columns of this thread's TMEM lane (warp-collective).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // D[tmem] (+)= A B^T over K (multiple of 8) in 3xTF32, issued by one thread.
 // A: M x K tile, B: N x K tile, each given by its hi base address, the byte
