@@ -268,12 +268,17 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
         if (!isfinite(s / nb)) atomicExch(nonfinite, 1);
     }
     if (i >= P) return;
-    double g = 0.0;
-    if (sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1))) {
-        for (int c = 0; c < sp.nB; ++c) g += static_cast<double>(sp.gpartB[static_cast<size_t>(c) * P + i]);
-    } else {
-        for (int c = 0; c < nct; ++c) g += static_cast<double>(gpart[static_cast<size_t>(c) * P + i]);
-    }
+    const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
+    const float* src = split ? sp.gpartB : gpart;
+    const int cnt = split ? sp.nB : nct;
+    // Fixed-order sum of the partials: 8 interleaved chains, combined pairwise.
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 8 <= cnt; c += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += static_cast<double>(src[static_cast<size_t>(c + k) * P + i]);
+    for (int k = 0; c < cnt; ++c, ++k) acc[k] += static_cast<double>(src[static_cast<size_t>(c) * P + i]);
+    const double g = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     double w = p64[i];
     if (adam) {
         const double b1 = 0.9, b2 = 0.999, eps = 1e-8;

@@ -58,7 +58,7 @@ __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
 }
 __host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp * 4; }
 __host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
-    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 64;
+    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 2 * 128 * 4 + 64;
 }
 
 size_t tc_weight_image_bytes(int u, int dp) { return w_image_bytes(u, dp); }
@@ -153,8 +153,18 @@ __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uin
     }
 }
 
+// Column split: for U >= 32 two warpgroups share each 128-row tile, warpgroup
+// h owning columns [h*U/2, (h+1)*U/2) of every layer (TMEM lane quarter = warp % 4).
+template <int U>
+struct TileShape {
+    static constexpr int NS = U >= 32 ? 2 : 1;  // warpgroups
+    static constexpr int UH = U / NS;           // columns per thread
+    static constexpr int threads = 128 * NS;
+};
+
 template <int U, int ACT>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_first, long n_tiles) {
+__global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a, long t_first, long n_tiles) {
+    constexpr int NS = TileShape<U>::NS, UH = TileShape<U>::UH;
     extern __shared__ __align__(128) uint8_t sm[];
     const int dp = a.dp;
     const uint32_t w0b = U * dp * 4, w1b = U * U * 4, hb = 128 * U * 4, xb = x_plane_bytes(dp);
@@ -165,12 +175,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
     const float* vec = reinterpret_cast<const float*>(w1t + 2 * w1b);  // b0 | b1 | w2 | b2, mu
     uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
     uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(bufX + 2 * xb);  // [0] MMA, [1] weights, [2] features
+    float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);  // [NS][128] partial output-layer sums
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);  // [0] MMA, [1] weights, [2] features
     uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
 
-    const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid & 127, hf = tid >> 7, cb = hf * UH;
     const bool sgd = a.mode == 0;
-    if (r == 0) {
+    if (tid == 0) {
         tc::mbar_init(&bar[0], 1);
         tc::mbar_init(&bar[1], 1);
         tc::mbar_init(&bar[2], 1);
@@ -181,10 +193,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tm = *tbase;
-    const uint32_t lb = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const long t_end = t_first + n_tiles;
     long tile = t_first + blockIdx.x;
-    if (r == 0) {
+    if (tid == 0) {
         tc::mbar_expect_tx(&bar[1], wbytes);
         tc::bulk_g2s(w0, a.wimg, wbytes, &bar[1]);
         tc::mbar_expect_tx(&bar[2], 2 * xb);
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
         tc::fence_after_sync();
     };
     const float b2 = vec[192], mu = vec[193];
-    constexpr int NB = (U + 31) / 32;
+    constexpr int NB = (UH + 31) / 32;
     double loss = 0.0, dmu = 0.0, mn = INFINITY;
     float gb2 = 0.0f;
     float acc_w2[NB], acc_b1[NB], acc_b0[NB];
@@ -218,18 +230,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
         tc::mbar_wait(&bar[2], xph);
         xph ^= 1;
         // ---- F0: D0 = X W0^T
-        if (r == 0) {
+        if (tid == 0) {
             tc::gemm3(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
             tc::commit(&bar[0]);
         }
         mma_wait();
-        if (r == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
+        if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
             tc::mbar_expect_tx(&bar[2], 2 * xb);
             tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
         }
         // H1 = act(D0 + b0) -> bufH (+ H1t); act'(H1) back into D0
 #pragma unroll
-        for (int c0 = 0; c0 < U; c0 += 16) {
+        for (int c0 = cb; c0 < cb + UH; c0 += 16) {
             float v[16];
             tc::tmem_ld16(tm + lb + c0, v);
 #pragma unroll
@@ -249,26 +261,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
         if (sgd) tc::tmem_wait_st();
         cta_sync();
         // ---- F1: D1 = H1 W1^T ; H2, f
-        if (r == 0) {
+        if (tid == 0) {
             tc::gemm3(tm + 64, tc::kmajor(bufH, hb, 128), tc::kmajor(w1, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
                       0);
             tc::commit(&bar[0]);
         }
         mma_wait();
-        float h2[U];
+        float h2[UH];
 #pragma unroll
-        for (int c0 = 0; c0 < U; c0 += 16) {
+        for (int c0 = 0; c0 < UH; c0 += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lb + 64 + c0, v);
+            tc::tmem_ld16(tm + lb + 64 + cb + c0, v);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) h2[c0 + q] = act_f<ACT>(v[q] + vec[64 + c0 + q]);
+            for (int q = 0; q < 16; ++q) h2[c0 + q] = act_f<ACT>(v[q] + vec[64 + cb + c0 + q]);
         }
-        float f = b2;
+        float f;
+        {
+            float fp = 0.0f;
 #pragma unroll
-        for (int j = 0; j < U; ++j) f = fmaf(h2[j], vec[128 + j], f);
+            for (int j = 0; j < UH; ++j) fp = fmaf(h2[j], vec[128 + cb + j], fp);
+            if (NS > 1) {
+                fsh[hf * 128 + r] = fp;
+                __syncthreads();
+                f = b2 + fsh[r] + fsh[128 + r];
+            } else {
+                f = b2 + fp;
+            }
+        }
 
         if (!sgd) {  // ---------------- evaluation
-            if (live) {
+            if (live && hf == 0) {
                 const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
                 if (a.mode & 1) {
                     const double res = ph - a.y[row];
@@ -285,71 +307,74 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
         if (live) {
             const float pr = ((a.head && f < 0.0f) ? 0.0f : f) + mu;
             const double res = static_cast<double>(pr) - a.y[row];
-            loss += res * res;
             const double dm = 2.0 * res / a.nb;
-            dmu += dm;
+            if (hf == 0) {
+                loss += res * res;
+                dmu += dm;
+            }
             dd = static_cast<float>(dm);
             if (a.head && !(f > 0.0f)) dd = 0.0f;
         }
-        gb2 += dd;
+        if (hf == 0) gb2 += dd;
         {
-            float g[U];
+            float g[UH];
 #pragma unroll
-            for (int j = 0; j < U; ++j) g[j] = dd * h2[j];
-            colsum_acc<U>(g, acc_w2, lane);
+            for (int j = 0; j < UH; ++j) g[j] = dd * h2[j];
+            colsum_acc<UH>(g, acc_w2, lane);
         }
         {  // G2 = dd w2 act'(H2) -> bufH (F1 has consumed H1), G2t
-            float g[U];
+            float g[UH];
 #pragma unroll
-            for (int j = 0; j < U; ++j) g[j] = dd * vec[128 + j] * act_d<ACT>(h2[j]);
+            for (int j = 0; j < UH; ++j) g[j] = dd * vec[128 + cb + j] * act_d<ACT>(h2[j]);
 #pragma unroll
-            for (int j = 0; j < U; j += 4)
-                tc::put_split4(bufH, hb, r, j, 128, make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]));
+            for (int j = 0; j < UH; j += 4)
+                tc::put_split4(bufH, hb, r, cb + j, 128, make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]));
             if (live)
 #pragma unroll
-                for (int j = 0; j < U; ++j) a.G2t[j * a.ld_t + trow] = g[j];
-            colsum_acc<U>(g, acc_b1, lane);
+                for (int j = 0; j < UH; ++j) a.G2t[(cb + j) * a.ld_t + trow] = g[j];
+            colsum_acc<UH>(g, acc_b1, lane);
         }
         cta_sync();
         // ---- B: Dbp = G2 W1 (B operand: the W1^T tile, K-major over the outputs of layer 1)
-        if (r == 0) {
+        if (tid == 0) {
             tc::gemm3(tm + 128, tc::kmajor(bufH, hb, 128), tc::kmajor(w1t, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
                       0);
             tc::commit(&bar[0]);
         }
         mma_wait();
         {
-            float g[U];
+            float g[UH];
 #pragma unroll
-            for (int c0 = 0; c0 < U; c0 += 16) {
+            for (int c0 = 0; c0 < UH; c0 += 16) {
                 float v[16], dv[16];
-                tc::tmem_ld16(tm + lb + 128 + c0, v);
-                tc::tmem_ld16(tm + lb + c0, dv);
+                tc::tmem_ld16(tm + lb + 128 + cb + c0, v);
+                tc::tmem_ld16(tm + lb + cb + c0, dv);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) g[c0 + q] = live ? v[q] * dv[q] : 0.0f;
             }
             if (live)
 #pragma unroll
-                for (int j = 0; j < U; ++j) a.G1t[j * a.ld_t + trow] = g[j];
-            colsum_acc<U>(g, acc_b0, lane);
+                for (int j = 0; j < UH; ++j) a.G1t[(cb + j) * a.ld_t + trow] = g[j];
+            colsum_acc<UH>(g, acc_b0, lane);
         }
         tc::fence_before_sync();
         __syncthreads();  // TMEM reads of D0 / Dbp done before the next tile's F0
         tc::fence_after_sync();
     }
 
-    // ---- per-CTA partials (fixed order over the 4 warps)
+    // ---- per-CTA partials (fixed order over the warps)
     tc::fence_before_sync();
     __syncthreads();
     float* part = reinterpret_cast<float*>(bufH);  // [warp][3][64]
-    double* red = reinterpret_cast<double*>(part + 4 * 3 * 64);
-    constexpr int NW = U < 32 ? U : 32;
+    double* red = reinterpret_cast<double*>(part + 8 * 3 * 64);
+    constexpr int NW = UH < 32 ? UH : 32;
     if (sgd && lane < NW)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-            part[(warp * 3 + 0) * 64 + b * 32 + lane] = acc_w2[b];
-            part[(warp * 3 + 1) * 64 + b * 32 + lane] = acc_b1[b];
-            part[(warp * 3 + 2) * 64 + b * 32 + lane] = acc_b0[b];
+            const int c = cb + b * 32 + lane;
+            part[(warp * 3 + 0) * 64 + c] = acc_w2[b];
+            part[(warp * 3 + 1) * 64 + c] = acc_b1[b];
+            part[(warp * 3 + 2) * 64 + c] = acc_b0[b];
         }
     loss = warp_sum(loss);
     dmu = warp_sum(dmu);
@@ -357,31 +382,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tile_tc(TileArgs a, long t_fi
     for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if (lane == 0) {
         red[warp] = loss;
-        red[4 + warp] = dmu;
-        red[8 + warp] = gb2;
-        red[12 + warp] = mn;
+        red[8 + warp] = dmu;
+        red[16 + warp] = gb2;
+        red[24 + warp] = mn;
     }
     __syncthreads();
     const int cta = blockIdx.x;
     if (sgd) {
         float* gout = a.gpart + static_cast<size_t>(cta) * a.P;
-        if (r < U) {
-            const auto sum4 = [&](int q) {
-                return part[(0 * 3 + q) * 64 + r] + part[(1 * 3 + q) * 64 + r] + part[(2 * 3 + q) * 64 + r] +
-                       part[(3 * 3 + q) * 64 + r];
+        if (tid < U) {
+            const int w0q = (tid / UH) * 4;  // first warp of the owning warpgroup
+            const auto sum4 = [&](int k) {
+                return part[((w0q + 0) * 3 + k) * 64 + tid] + part[((w0q + 1) * 3 + k) * 64 + tid] +
+                       part[((w0q + 2) * 3 + k) * 64 + tid] + part[((w0q + 3) * 3 + k) * 64 + tid];
             };
-            gout[a.off2 + r] = sum4(0);
-            gout[a.off1 + U * U + r] = sum4(1);
-            gout[a.off0 + U * a.d + r] = sum4(2);
+            gout[a.off2 + tid] = sum4(0);
+            gout[a.off1 + U * U + tid] = sum4(1);
+            gout[a.off0 + U * a.d + tid] = sum4(2);
         }
-        if (r == 0) {
+        if (tid == 0) {
             a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
-            gout[a.P - 1] = static_cast<float>(red[4] + red[5] + red[6] + red[7]);
-            gout[a.off2 + U] = static_cast<float>(red[8] + red[9] + red[10] + red[11]);
+            gout[a.P - 1] = static_cast<float>(red[8] + red[9] + red[10] + red[11]);
+            gout[a.off2 + U] = static_cast<float>(red[16] + red[17] + red[18] + red[19]);
         }
-    } else if (r == 0) {
+    } else if (tid == 0) {
         if (a.mode & 1) a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
-        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[12], red[13]), fmin(red[14], red[15]));
+        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[24], red[25]), fmin(red[26], red[27]));
     }
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
@@ -511,10 +537,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
     if (warp == 0) tc::tmem_dealloc(tm, 128);
 }
 
-// Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T, K-major no-swizzle
-// (variant 0) or 128B-swizzled (variant 2) operand tiles; test hook for the
-// descriptor conventions.
-__global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float* B, float* D, int swz) {
+// Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T; test hook for the
+// descriptor conventions.  variant 0: K-major no-swizzle, 1: K-major SW128,
+// 2: A MN-major, 3: B MN-major, 4: both MN-major (no swizzle; an MN-major
+// operand is stored as the K x MN core tile, SBO = K/8*128, LBO = 128).
+__global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float* B, float* D, int variant) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t abytes = M * ((K + 31) / 32) * 32 * 4, bbytes = N * ((K + 31) / 32) * 32 * 4;
@@ -523,16 +550,19 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
     uint64_t* mbar = reinterpret_cast<uint64_t*>(tb + 2 * bbytes);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5;
+    const bool swz = variant == 1, amn = variant == 2 || variant == 4, bmn = variant == 3 || variant == 4;
     if (t == 0) tc::mbar_init(mbar, 1);
     if (warp == 0) tc::tmem_alloc(tbase, 256);
     for (int i = t; i < 2 * (abytes + bbytes) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.0f;
     __syncthreads();
     for (int i = t; i < M * K; i += blockDim.x) {
         if (swz) tc::put_split_sw(ta, abytes, i / K, i % K, M, A[i]);
+        else if (amn) tc::put_split(ta, abytes, i % K, i / K, K, A[i]);
         else tc::put_split(ta, abytes, i / K, i % K, M, A[i]);
     }
     for (int i = t; i < N * K; i += blockDim.x) {
         if (swz) tc::put_split_sw(tb, bbytes, i / K, i % K, N, B[i]);
+        else if (bmn) tc::put_split(tb, bbytes, i % K, i / K, K, B[i]);
         else tc::put_split(tb, bbytes, i / K, i % K, N, B[i]);
     }
     tc::fence_async_smem();
@@ -546,7 +576,9 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
                          tc::OperandSW{tc::smem_u32(tb), bbytes, static_cast<uint32_t>(N), 0}, K,
                          tc::idesc_tf32(M, N, 0, 0), 0);
         } else {
-            tc::gemm3(tm, tc::kmajor(ta, abytes, M), tc::kmajor(tb, bbytes, N), K, tc::idesc_tf32(M, N, 0, 0), 0);
+            tc::gemm3(tm, amn ? tc::mnmajor(ta, abytes, K) : tc::kmajor(ta, abytes, M),
+                      bmn ? tc::mnmajor(tb, bbytes, K) : tc::kmajor(tb, bbytes, N), K,
+                      tc::idesc_tf32(M, N, amn, bmn), 0);
         }
         tc::commit(mbar);
     }
@@ -591,7 +623,7 @@ template <int U, int ACT>
 void launch_tile_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
     const size_t smem = tile_tc_smem(U, a.dp);
     HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_tc<U, ACT><<<ctas, kTcThreads, smem, s>>>(a, t_first, n_tiles);
+    k_tile_tc<U, ACT><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
 }
 
 template <int U>
@@ -637,7 +669,7 @@ int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
 
 using namespace hcva;
 
-extern "C" hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int swizzle, const float* A,
+extern "C" hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int variant, const float* A,
                                          const float* B, float* D) {
     return guarded([&] {
         StreamScope sc__(ctx->stream);
@@ -652,7 +684,7 @@ extern "C" hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int
         const size_t smem = 2 * 4 * kp * (static_cast<size_t>(M) + N) + 2048;
         HCVA_CUDA(cudaFuncSetAttribute(k_tc_gemm_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_tc_gemm_diag<<<1, 128, smem, ctx->stream>>>(M, N, K, dA.as<float>(), dB.as<float>(), dD.as<float>(),
-                                                      swizzle);
+                                                      variant);
         check_launch(ctx);
         copy_out(ctx, D, dD.p, sizeof(float) * M * N);
     });

@@ -1,4 +1,4 @@
-"""Exercise hcva_diag_tc_gemm (K-major operands, no-swizzle and SW128) (debug aid)."""
+"""Exercise hcva_diag_tc_gemm over its operand-layout variants (debug aid)."""
 import ctypes as C
 import os
 import sys
@@ -17,8 +17,8 @@ for M, N, K in ((128, 32, 16), (64, 32, 128), (128, 64, 64), (64, 48, 128)):
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
-    for swz in (0, 1):
+    for var, name in enumerate(("kmajor", "kmajor-sw128", "a-mn", "b-mn", "both-mn")):
         D = np.zeros((M, N), dtype=np.float32)
-        rc = L.hcva_diag_tc_gemm(hcva.context().handle, M, N, K, swz, A.ctypes.data, B.ctypes.data, D.ctypes.data)
+        rc = L.hcva_diag_tc_gemm(hcva.context().handle, M, N, K, var, A.ctypes.data, B.ctypes.data, D.ctypes.data)
         err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
-        print(M, N, K, "sw128", swz, "rc", rc, "relerr %.2e" % err, "D[0,:3]", D[0, :3], "ref", ref[0, :3])
+        print(M, N, K, f"{name:13s}", "rc", rc, "relerr %.2e" % err, "D[0,:3]", D[0, :3], "ref", ref[0, :3])
