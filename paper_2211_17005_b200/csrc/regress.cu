@@ -259,26 +259,30 @@ struct SplitPartials {
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // [lo, hi) index ranges served by gpartB
 };
 
+// Block (32, 8): x = parameter, y = partial group c = y (mod 8); the eight
+// group sums combine pairwise in fixed order.
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
                        double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) {
+    __shared__ double part[8][33];
+    const int x = threadIdx.x, grp = threadIdx.y;
+    const int i = blockIdx.x * 32 + x;
+    if (blockIdx.x == 0 && x == 0 && grp == 0) {
         double s = 0.0;
         for (int c = 0; c < nct; ++c) s += lpart[c];
         if (!isfinite(s / nb)) atomicExch(nonfinite, 1);
     }
-    if (i >= P) return;
-    const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
-    const float* src = split ? sp.gpartB : gpart;
-    const int cnt = split ? sp.nB : nct;
-    // Fixed-order sum of the partials: 8 interleaved chains, combined pairwise.
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int c = 0;
-    for (; c + 8 <= cnt; c += 8)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += static_cast<double>(src[static_cast<size_t>(c + k) * P + i]);
-    for (int k = 0; c < cnt; ++c, ++k) acc[k] += static_cast<double>(src[static_cast<size_t>(c) * P + i]);
-    const double g = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    double s = 0.0;
+    if (i < P) {
+        const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
+        const float* src = split ? sp.gpartB : gpart;
+        const int cnt = split ? sp.nB : nct;
+        for (int c = grp; c < cnt; c += 8) s += static_cast<double>(src[static_cast<size_t>(c) * P + i]);
+    }
+    part[grp][x] = s;
+    __syncthreads();
+    if (grp != 0 || i >= P) return;
+    const double g = ((part[0][x] + part[1][x]) + (part[2][x] + part[3][x])) +
+                     ((part[4][x] + part[5][x]) + (part[6][x] + part[7][x]));
     double w = p64[i];
     if (adam) {
         const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
@@ -531,8 +535,8 @@ struct Trainer {
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
     // Tensor-core path: weight-gradient partials, transposed activations, packed operand images.
-    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt;
-    int max_tiles = 0, last_parts = 0, dp = 0;
+    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2;
+    int max_tiles = 0, last_parts = 0, dp = 0, gram_parts = 0;
     bool use_tc = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
 
@@ -574,7 +578,8 @@ struct Trainer {
         lpart.alloc(static_cast<size_t>(parts) * 8);
         mpart.alloc(static_cast<size_t>(parts) * 8);
         const size_t mm = n.u + 1;
-        gram.alloc(static_cast<size_t>(eval_ctas) * (mm * (mm + 1) / 2 + mm) * 8);
+        gram_parts = std::max(eval_ctas, 4 * ctx->sm_count);
+        gram.alloc(static_cast<size_t>(gram_parts) * (mm * (mm + 1) / 2 + mm) * 8);
         flag.alloc(4);
         best_loss.alloc(8);
         best_epoch.alloc(4);
@@ -607,6 +612,7 @@ struct Trainer {
         ta.wimg = wimg.as<uint8_t>(); ta.ximg = ximg.as<uint8_t>(); ta.y = y; ta.b0 = b0; ta.b1 = b1;
         ta.head = head; ta.mode = mode; ta.nb = nb;
         ta.gpart = gpart.as<float>(); ta.lpart = lpart.as<double>(); ta.mpart = mpart.as<double>(); ta.pred = pred;
+        ta.H2 = h2.as<float>();
         ta.H1t = h1t.as<float>(); ta.G2t = g2t.as<float>(); ta.G1t = g1t.as<float>();
         ta.ld_t = ((b1 - b0 + 63) / 64) * 64;
         const int ctas = launch_tile_tc(n.u, ta, ctx->sm_count, ctx->stream);
@@ -641,7 +647,7 @@ struct Trainer {
     void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
         SplitPartials sp;
         const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
-        k_adam<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
+        k_adam<<<(n.P + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>());
         check_launch(ctx);
@@ -660,12 +666,21 @@ struct Trainer {
     }
 
     void refit(const float* X, const double* y, long R, double ridge) {
-        k_gram<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), gram.as<double>(), TR);
+        int nct = eval_ctas;
+        if (use_tc) {
+            const size_t hbytes = static_cast<size_t>(R) * n.u * 4;
+            if (h2.bytes < hbytes) h2.alloc(hbytes);  // layer-2 activations, first refit only
+            tile_launch(y, 0, R, 1, 8, 1.0, nullptr);
+            nct = launch_gram_h2(n.u, h2.as<float>(), y, R, p32.as<float>(), n.P, gram.as<double>(), gram_parts,
+                                 ctx->sm_count, ctx->stream);
+        } else {
+            k_gram<<<eval_ctas, TR, smem(), ctx->stream>>>(n, X, y, R, p32.as<float>(), gram.as<double>(), TR);
+        }
         check_launch(ctx);
         const int mm = n.u + 1;
         const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
         HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-        k_refit<<<1, 128, sm, ctx->stream>>>(n, gram.as<double>(), eval_ctas, ridge, p64.as<double>(), p32.as<float>());
+        k_refit<<<1, 128, sm, ctx->stream>>>(n, gram.as<double>(), nct, ridge, p64.as<double>(), p32.as<float>());
         check_launch(ctx);
     }
 

@@ -290,6 +290,11 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
 
         if (!sgd) {  // ---------------- evaluation
+            if ((a.mode & 8) && live)
+#pragma unroll
+                for (int j = 0; j < UH; j += 4)
+                    *reinterpret_cast<float4*>(a.H2 + row * U + cb + j) =
+                        make_float4(h2[j], h2[j + 1], h2[j + 2], h2[j + 3]);
             if (live && hf == 0) {
                 const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
                 if (a.mode & 1) {
@@ -412,6 +417,88 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
+// Refit Gram (regressor.cpp:191-213) in FP64 from the FP32 layer-2
+// activations: z = [h2, 1, y - mu] padded to MP = 4 * NBK, one thread per
+// 4x4 block (bi <= bj) of z z^T, 64-row chunks staged in shared memory,
+// chunk c -> CTA c % gridDim.x (fixed), one partial per CTA.
+template <int U>
+struct GramShape {
+    static constexpr int MP = ((U + 2 + 3) / 4) * 4;
+    static constexpr int NBK = MP / 4;
+    static constexpr int pairs = NBK * (NBK + 1) / 2;
+    static constexpr int threads = ((pairs + 31) / 32) * 32;
+    static constexpr int CH = 64;
+    static constexpr int LD = MP + 2;  // padded row (doubles)
+};
+
+template <int U>
+__global__ void __launch_bounds__(GramShape<U>::threads) k_gram_h2(const float* __restrict__ H2,
+                                                                    const double* __restrict__ y, long R,
+                                                                    const float* __restrict__ params, int P,
+                                                                    double* __restrict__ gpart) {
+    using S = GramShape<U>;
+    __shared__ __align__(16) double zs[S::CH * S::LD];
+    const int t = threadIdx.x;
+    int bi = 0, rem = t;  // t -> (bi, bj), bi <= bj
+    while (bi < S::NBK && rem >= S::NBK - bi) {
+        rem -= S::NBK - bi;
+        ++bi;
+    }
+    const bool act = t < S::pairs;
+    const int bj = bi + rem;
+    const double mu = static_cast<double>(params[P - 1]);
+    double acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    const long nch = (R + S::CH - 1) / S::CH;
+    for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const long base = ch * S::CH;
+        const int rows = static_cast<int>(min(static_cast<long>(S::CH), R - base));
+        __syncthreads();
+        for (int i = t; i < S::CH * (U / 4); i += blockDim.x) {
+            const int r = i / (U / 4), c4 = (i % (U / 4)) * 4;
+            float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (r < rows) v = __ldg(reinterpret_cast<const float4*>(H2 + (base + r) * U + c4));
+            double* z = zs + r * S::LD + c4;
+            z[0] = v.x;
+            z[1] = v.y;
+            z[2] = v.z;
+            z[3] = v.w;
+        }
+        for (int r = t; r < S::CH; r += blockDim.x) {
+            double* z = zs + r * S::LD;
+            const bool in = r < rows;
+            z[U] = in ? 1.0 : 0.0;
+            z[U + 1] = in ? y[base + r] - mu : 0.0;
+            for (int c = U + 2; c < S::MP; ++c) z[c] = 0.0;
+        }
+        __syncthreads();
+        if (act)
+            for (int r = 0; r < rows; ++r) {
+                const double2* zi = reinterpret_cast<const double2*>(zs + r * S::LD + 4 * bi);
+                const double2* zj = reinterpret_cast<const double2*>(zs + r * S::LD + 4 * bj);
+                const double2 a0 = zi[0], a1 = zi[1], b0 = zj[0], b1 = zj[1];
+                const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[p * 4 + q] = fma(av[p], bv[q], acc[p * 4 + q]);
+            }
+    }
+    if (!act) return;
+    // Packed output: (a, b) a <= b < m = U+1 -> upper-triangle index; rhs c = (c, U+1).
+    constexpr int m = U + 1, tri = m * (m + 1) / 2;
+    double* out = gpart + static_cast<size_t>(blockIdx.x) * (tri + m);
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ra = 4 * bi + p, cb = 4 * bj + q;
+            if (ra < m && cb < m && ra <= cb) out[ra * m - ra * (ra - 1) / 2 + (cb - ra)] = acc[p * 4 + q];
+            else if (ra < m && cb == m) out[tri + ra] = acc[p * 4 + q];
+        }
+}
+
 constexpr uint32_t kChunkTile = 64 * 64 * 4;  // 64 x 64 FP32 core tile
 
 // Four consecutive floats, zero beyond `valid`; 16-byte load when aligned.
@@ -434,9 +521,12 @@ __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
     return v;
 }
 
+// Chunk tiles are 128B-swizzled K-major (tc.cuh sw_off): the coalesced
+// 16-byte row loads land in distinct bank groups.
 template <int U>
 __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
-    extern __shared__ __align__(128) uint8_t sm[];
+    extern __shared__ __align__(128) uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* tA1 = sm;                   // G2t chunk: 64 (o, zero-padded) x 64 (rows)
     uint8_t* tB1 = sm + 2 * kChunkTile;  // H1t chunk: U x 64
     uint8_t* tA0 = sm + 4 * kChunkTile;  // G1t chunk
@@ -486,24 +576,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
             const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
-            tc::put_split4(tA1, kChunkTile, f, k, 64, rg2[i]);
-            tc::put_split4(tB1, kChunkTile, f, k, 64, rh1[i]);
-            tc::put_split4(tA0, kChunkTile, f, k, 64, rg1[i]);
+            tc::put_split4_sw(tA1, kChunkTile, f, k, 64, rg2[i]);
+            tc::put_split4_sw(tB1, kChunkTile, f, k, 64, rh1[i]);
+            tc::put_split4_sw(tA0, kChunkTile, f, k, 64, rg1[i]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
-            if (f < dp) tc::put_split4(tB0, kChunkTile, f, k, 64, rx[i]);
+            if (f < dp) tc::put_split4_sw(tB0, kChunkTile, f, k, 64, rx[i]);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
         if (t == 0) {
-            tc::gemm3(tm, tc::kmajor(tA1, kChunkTile, 64), tc::kmajor(tB1, kChunkTile, 64), 64,
-                      tc::idesc_tf32(64, U, 0, 0), !first);
-            tc::gemm3(tm + 64, tc::kmajor(tA0, kChunkTile, 64), tc::kmajor(tB0, kChunkTile, 64), 64,
-                      tc::idesc_tf32(64, dp, 0, 0), !first);
+            const uint32_t R64 = 64;
+            tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(tA1), kChunkTile, R64, 0},
+                         tc::OperandSW{tc::smem_u32(tB1), kChunkTile, R64, 0}, 64, tc::idesc_tf32(64, U, 0, 0),
+                         !first);
+            tc::gemm3_sw(tm + 64, tc::OperandSW{tc::smem_u32(tA0), kChunkTile, R64, 0},
+                         tc::OperandSW{tc::smem_u32(tB0), kChunkTile, R64, 0}, 64, tc::idesc_tf32(64, dp, 0, 0),
+                         !first);
             tc::commit(mbar);
         }
         first = 0;
@@ -648,9 +741,25 @@ int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
 
 template <int U>
 void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
-    const size_t smem = 8 * static_cast<size_t>(kChunkTile) + 64;
+    const size_t smem = 8 * static_cast<size_t>(kChunkTile) + 64 + 1024;
     HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_wgrad_tc<U><<<ctas, kTcThreads, smem, s>>>(a);
+}
+
+template <int U>
+int launch_gram_u(const float* H2, const double* y, long R, const float* params, int P, double* gpart, int ctas,
+                  cudaStream_t s) {
+    k_gram_h2<U><<<ctas, GramShape<U>::threads, 0, s>>>(H2, y, R, params, P, gpart);
+    return ctas;
+}
+
+int launch_gram_h2(int u, const float* H2, const double* y, long R, const float* params, int P, double* gpart,
+                   int max_parts, int sm_count, cudaStream_t s) {
+    const long chunks = (R + 63) / 64;
+    const int ctas = static_cast<int>(std::max<long>(1, std::min<long>({chunks, 4L * sm_count, max_parts})));
+    if (u == 16) return launch_gram_u<16>(H2, y, R, params, P, gpart, ctas, s);
+    if (u == 32) return launch_gram_u<32>(H2, y, R, params, P, gpart, ctas, s);
+    return launch_gram_u<64>(H2, y, R, params, P, gpart, ctas, s);
 }
 
 // Returns the number of weight-gradient partials written.

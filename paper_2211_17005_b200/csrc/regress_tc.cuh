@@ -17,12 +17,14 @@ struct TileArgs {
     const uint8_t* ximg;  // packed feature tiles [R/128][hi | lo] (k_pack_x)
     const double* y;      // labels, absolute row index
     long b0, b1;          // live rows [b0, b1)
-    int head, mode;       // mode 0: SGD; else bits 1: loss (head on), 2: min plain fit, 4: predictions
+    int head, mode;       // mode 0: SGD; else bits 1: loss (head on), 2: min plain fit, 4: predictions,
+                          //   8: layer-2 activations -> H2 (refit Gram)
     double nb;
     float* gpart;    // SGD: [cta][P] partials of b0, b1, w2, b2, mu
     double* lpart;   // [cta] sum of squared residuals
     double* mpart;   // [cta] min of f + mu (plain head)
     double* pred;    // predictions (head on), absolute row index
+    float* H2;       // [R][U] layer-2 activations (mode bit 8)
     float *H1t, *G2t, *G1t;  // SGD: [U][ld_t] transposed, row index relative to b0
     long ld_t;
 };
@@ -47,5 +49,9 @@ void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* 
 // Returns the number of per-CTA partials written (gpart / lpart / mpart rows).
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s);
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s);
+// FP64 Gram partials of z = [H2 row, 1] and rhs z (y - mu) in k_refit's packed
+// layout (upper triangle, then rhs); returns the partial count (<= max_parts).
+int launch_gram_h2(int u, const float* H2, const double* y, long R, const float* params, int P, double* gpart,
+                   int max_parts, int sm_count, cudaStream_t s);
 
 }  // namespace hcva

@@ -193,6 +193,14 @@ __device__ __forceinline__ void put_split_sw(uint8_t* tile, uint32_t lo_bytes, i
     *reinterpret_cast<float*>(tile + lo_bytes + o) = a - hi;
 }
 
+// Four consecutive columns c..c+3 (c % 4 == 0): one 16-byte chunk per plane.
+__device__ __forceinline__ void put_split4_sw(uint8_t* tile, uint32_t lo_bytes, int r, int c, int R, float4 a) {
+    const float4 hi = make_float4(tf32_rna(a.x), tf32_rna(a.y), tf32_rna(a.z), tf32_rna(a.w));
+    const uint32_t o = sw_off(r, c, R);
+    *reinterpret_cast<float4*>(tile + o) = hi;
+    *reinterpret_cast<float4*>(tile + lo_bytes + o) = make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
+}
+
 __device__ __forceinline__ float get_split_sw(const uint8_t* tile, uint32_t lo_bytes, int r, int c, int R) {
     const uint32_t o = sw_off(r, c, R);
     return *reinterpret_cast<const float*>(tile + o) + *reinterpret_cast<const float*>(tile + lo_bytes + o);
