@@ -35,7 +35,8 @@ namespace hcva {
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
 }  // namespace hcva
-#include "regress_tc.cuh"  // tensor-core tiles for the paper's network shape
+#include "regress_tc.cuh"
+#include "tc.cuh"  // tensor-core tiles for the paper's network shape
 namespace hcva {
 
 struct NetDims {
@@ -253,6 +254,40 @@ __global__ void k_sgd(NetDims n, const float* X, const double* y, long row0, lon
 // Fixed-order reduction of the tile partials + optimiser step (regressor.cpp:236-261).
 // Parameters whose gradient partials come from the weight-gradient kernel
 // (tensor-core path: W0 and W1) instead of the per-tile kernel.
+// Weight image of the tensor-core tile kernel, refreshed by k_adam (img == nullptr: none).
+struct ImgArgs {
+    uint8_t* img = nullptr;
+    int U = 0, d = 0, dp = 0, off0 = 0, off1 = 0, off2 = 0;
+};
+
+__device__ __forceinline__ void img_store(const ImgArgs& im, int P, int i, float w) {
+    const int U = im.U;
+    const uint32_t w0b = U * im.dp * 4, w1b = U * U * 4;
+    uint8_t* w0 = im.img;
+    uint8_t* w1 = w0 + 2 * w0b;
+    uint8_t* w1t = w1 + 2 * w1b;
+    float* vec = reinterpret_cast<float*>(w1t + 2 * w1b);
+    if (i == P - 1) {
+        vec[193] = w;
+    } else if (i >= im.off2) {
+        const int k = i - im.off2;
+        if (k < U) vec[128 + k] = w;
+        else vec[192] = w;
+    } else if (i >= im.off1) {
+        const int k = i - im.off1;
+        if (k < U * U) {
+            tc::put_split(w1, w1b, k / U, k % U, U, w);
+            tc::put_split(w1t, w1b, k % U, k / U, U, w);
+        } else {
+            vec[64 + k - U * U] = w;
+        }
+    } else {
+        const int k = i - im.off0;
+        if (k < U * im.d) tc::put_split(w0, w0b, k / im.d, k % im.d, U, w);
+        else vec[k - U * im.d] = w;
+    }
+}
+
 struct SplitPartials {
     const float* gpartB = nullptr;
     int nB = 0;
@@ -262,7 +297,8 @@ struct SplitPartials {
 // Block (32, 8): x = parameter, y = partial group c = y (mod 8); the eight
 // group sums combine pairwise in fixed order.
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
-                       double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite) {
+                       double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite,
+                       ImgArgs im) {
     __shared__ double part[8][33];
     const int x = threadIdx.x, grp = threadIdx.y;
     const int i = blockIdx.x * 32 + x;
@@ -297,6 +333,7 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
     }
     p64[i] = w;
     p32[i] = static_cast<float>(w);
+    if (im.img) img_store(im, P, i, static_cast<float>(w));
 }
 
 // Full-sample forward over tiles (grid-stride, fixed tile->CTA map).
@@ -539,6 +576,7 @@ struct Trainer {
     int max_tiles = 0, last_parts = 0, dp = 0, gram_parts = 0;
     bool use_tc = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
+    bool wimg_valid = false;  // weight image matches p32
 
     Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0) : ctx(c), n(dims) {
         use_tc = tc_eligible(n.d, n.h, n.u);
@@ -591,6 +629,7 @@ struct Trainer {
         HCVA_CUDA(cudaMemcpyAsync(p64.p, host_or_dev, n.P * 8, cudaMemcpyDefault, ctx->stream));
         k_to_f32<<<grid1(n.P, 256), 256, 0, ctx->stream>>>(p64.as<double>(), p32.as<float>(), n.P);
         check_launch(ctx);
+        wimg_valid = false;
     }
 
     // Features of the sample (X [R][d], device) -> the tensor-core operand images.
@@ -603,9 +642,12 @@ struct Trainer {
 
     // Launch the persistent tile kernel over rows [b0, b1); returns the partial count.
     int tile_launch(const double* y, long b0, long b1, int head, int mode, double nb, double* pred) {
-        launch_pack_w(n.u, n.d, dp, n.off[0], n.off[1], n.off[2], n.P, p32.as<float>(), wimg.as<uint8_t>(),
-                      ctx->stream);
-        check_launch(ctx);
+        if (!wimg_valid) {
+            launch_pack_w(n.u, n.d, dp, n.off[0], n.off[1], n.off[2], n.P, p32.as<float>(), wimg.as<uint8_t>(),
+                          ctx->stream);
+            check_launch(ctx);
+            wimg_valid = true;
+        }
         TileArgs ta{};
         ta.d = n.d; ta.dp = dp; ta.act = n.act; ta.P = n.P;
         ta.off0 = n.off[0]; ta.off1 = n.off[1]; ta.off2 = n.off[2];
@@ -649,8 +691,15 @@ struct Trainer {
         const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
         k_adam<<<(n.P + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
-                                                         m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>());
+                                                         m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>(),
+                                                         img_args());
         check_launch(ctx);
+    }
+
+    ImgArgs img_args() {
+        ImgArgs im;
+        if (use_tc && wimg_valid) im = ImgArgs{wimg.as<uint8_t>(), n.u, n.d, dp, n.off[0], n.off[1], n.off[2]};
+        return im;
     }
 
     // Full-sample forward; sets last_parts = number of loss / min partials written.
@@ -681,6 +730,7 @@ struct Trainer {
         const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
         HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         k_refit<<<1, 128, sm, ctx->stream>>>(n, gram.as<double>(), nct, ridge, p64.as<double>(), p32.as<float>());
+        wimg_valid = false;
         check_launch(ctx);
     }
 
@@ -706,6 +756,7 @@ struct Trainer {
             if (e == sw) {
                 refit(X, y, R, ridge);
                 eval(X, y, R, 2, nullptr);
+                wimg_valid = false;
                 k_switch<<<1, 256, 0, ctx->stream>>>(n, mpart.as<double>(), last_parts, p64.as<double>(),
                                                       p32.as<float>(), m.as<double>(), v.as<double>());
                 check_launch(ctx);
@@ -973,6 +1024,7 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
                 tr.set_params(p.data());
                 HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
                 k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
+                tr.wimg_valid = false;
                 check_launch(ctx);
             } else {
                 tr.set_params(tr.best.as<double>());  // warm start from step i+1's best

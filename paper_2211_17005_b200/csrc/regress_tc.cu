@@ -58,7 +58,7 @@ __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
 }
 __host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp * 4; }
 __host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
-    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 2 * 128 * 4 + 64;
+    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 4 * 128 * 4 + 64;
 }
 
 size_t tc_weight_image_bytes(int u, int dp) { return w_image_bytes(u, dp); }
@@ -153,12 +153,12 @@ __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uin
     }
 }
 
-// Column split: for U >= 32 two warpgroups share each 128-row tile, warpgroup
-// h owning columns [h*U/2, (h+1)*U/2) of every layer (TMEM lane quarter = warp % 4).
+// Column split: U/16 warpgroups share each 128-row tile, warpgroup h owning
+// columns [16h, 16h + 16) of every layer (TMEM lane quarter = warp % 4).
 template <int U>
 struct TileShape {
-    static constexpr int NS = U >= 32 ? 2 : 1;  // warpgroups
-    static constexpr int UH = U / NS;           // columns per thread
+    static constexpr int NS = U / 16;  // warpgroups
+    static constexpr int UH = 16;      // columns per thread
     static constexpr int threads = 128 * NS;
 };
 
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
     uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
     float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);  // [NS][128] partial output-layer sums
-    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);  // [0] MMA, [1] weights, [2] features
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 4 * 128);  // [0] MMA, [1] weights, [2] features
     uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -283,7 +283,10 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             if (NS > 1) {
                 fsh[hf * 128 + r] = fp;
                 __syncthreads();
-                f = b2 + fsh[r] + fsh[128 + r];
+                float fs = fsh[r];
+#pragma unroll
+                for (int h = 1; h < NS; ++h) fs += fsh[h * 128 + r];
+                f = b2 + fs;
             } else {
                 f = b2 + fp;
             }
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     tc::fence_before_sync();
     __syncthreads();
     float* part = reinterpret_cast<float*>(bufH);  // [warp][3][64]
-    double* red = reinterpret_cast<double*>(part + 8 * 3 * 64);
+    double* red = reinterpret_cast<double*>(part + 16 * 3 * 64);  // [4][16 warps]
     constexpr int NW = UH < 32 ? UH : 32;
     if (sgd && lane < NW)
 #pragma unroll
@@ -387,9 +390,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if (lane == 0) {
         red[warp] = loss;
-        red[8 + warp] = dmu;
-        red[16 + warp] = gb2;
-        red[24 + warp] = mn;
+        red[16 + warp] = dmu;
+        red[32 + warp] = gb2;
+        red[48 + warp] = mn;
     }
     __syncthreads();
     const int cta = blockIdx.x;
@@ -406,13 +409,13 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             gout[a.off0 + U * a.d + tid] = sum4(2);
         }
         if (tid == 0) {
-            a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
-            gout[a.P - 1] = static_cast<float>(red[8] + red[9] + red[10] + red[11]);
-            gout[a.off2 + U] = static_cast<float>(red[16] + red[17] + red[18] + red[19]);
+            a.lpart[cta] = red[0] + red[1] + red[2] + red[3];  // warpgroup 0 holds the per-row terms
+            gout[a.P - 1] = static_cast<float>(red[16] + red[17] + red[18] + red[19]);
+            gout[a.off2 + U] = static_cast<float>(red[32] + red[33] + red[34] + red[35]);
         }
     } else if (tid == 0) {
         if (a.mode & 1) a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
-        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[24], red[25]), fmin(red[26], red[27]));
+        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[48], red[49]), fmin(red[50], red[51]));
     }
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
@@ -633,7 +636,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
 // Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T; test hook for the
 // descriptor conventions.  variant 0: K-major no-swizzle, 1: K-major SW128,
 // 2: A MN-major, 3: B MN-major, 4: both MN-major (no swizzle; an MN-major
-// operand is stored as the K x MN core tile, SBO = K/8*128, LBO = 128).
+// operand is stored as the K x MN core tile, SBO = K/8*128, LBO = 128),
+// 5 / 6 / 7: A / B / both MN-major with 128B swizzle (K x MN atoms).
 __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float* B, float* D, int variant) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -643,18 +647,22 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
     uint64_t* mbar = reinterpret_cast<uint64_t*>(tb + 2 * bbytes);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5;
-    const bool swz = variant == 1, amn = variant == 2 || variant == 4, bmn = variant == 3 || variant == 4;
+    const bool swz = variant == 1 || variant >= 5;
+    const bool amn = variant == 2 || variant == 4 || variant == 5 || variant == 7;
+    const bool bmn = variant == 3 || variant == 4 || variant == 6 || variant == 7;
     if (t == 0) tc::mbar_init(mbar, 1);
     if (warp == 0) tc::tmem_alloc(tbase, 256);
     for (int i = t; i < 2 * (abytes + bbytes) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.0f;
     __syncthreads();
     for (int i = t; i < M * K; i += blockDim.x) {
-        if (swz) tc::put_split_sw(ta, abytes, i / K, i % K, M, A[i]);
+        if (swz && amn) tc::put_split_sw(ta, abytes, i % K, i / K, K, A[i]);
+        else if (swz) tc::put_split_sw(ta, abytes, i / K, i % K, M, A[i]);
         else if (amn) tc::put_split(ta, abytes, i % K, i / K, K, A[i]);
         else tc::put_split(ta, abytes, i / K, i % K, M, A[i]);
     }
     for (int i = t; i < N * K; i += blockDim.x) {
-        if (swz) tc::put_split_sw(tb, bbytes, i / K, i % K, N, B[i]);
+        if (swz && bmn) tc::put_split_sw(tb, bbytes, i % K, i / K, K, B[i]);
+        else if (swz) tc::put_split_sw(tb, bbytes, i / K, i % K, N, B[i]);
         else if (bmn) tc::put_split(tb, bbytes, i % K, i / K, K, B[i]);
         else tc::put_split(tb, bbytes, i / K, i % K, N, B[i]);
     }
@@ -665,9 +673,10 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
     const uint32_t tm = *tbase;
     if (t == 0) {
         if (swz) {
-            tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(ta), abytes, static_cast<uint32_t>(M), 0},
-                         tc::OperandSW{tc::smem_u32(tb), bbytes, static_cast<uint32_t>(N), 0}, K,
-                         tc::idesc_tf32(M, N, 0, 0), 0);
+            // MN-major SW128 tiles hold K rows x MN columns (R = K).
+            tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(ta), abytes, static_cast<uint32_t>(amn ? K : M), amn},
+                         tc::OperandSW{tc::smem_u32(tb), bbytes, static_cast<uint32_t>(bmn ? K : N), bmn}, K,
+                         tc::idesc_tf32(M, N, amn, bmn), 0);
         } else {
             tc::gemm3(tm, amn ? tc::mnmajor(ta, abytes, K) : tc::kmajor(ta, abytes, M),
                       bmn ? tc::mnmajor(tb, bbytes, K) : tc::kmajor(tb, bbytes, N), K,

@@ -17,7 +17,7 @@ for M, N, K in ((128, 32, 16), (64, 32, 128), (128, 64, 64), (64, 48, 128)):
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
-    for var, name in enumerate(("kmajor", "kmajor-sw128", "a-mn", "b-mn", "both-mn")):
+    for var, name in enumerate(("kmajor", "kmajor-sw128", "a-mn", "b-mn", "both-mn", "a-mn-sw", "b-mn-sw", "both-mn-sw")):
         D = np.zeros((M, N), dtype=np.float32)
         rc = L.hcva_diag_tc_gemm(hcva.context().handle, M, N, K, var, A.ctypes.data, B.ctypes.data, D.ctypes.data)
         err = np.max(np.abs(D - ref)) / np.max(np.abs(ref))
