@@ -35,10 +35,20 @@
 
 namespace hcva {
 
+// tanh from one exp2 and one reciprocal: (1 - e^{-2|z|}) / (1 + e^{-2|z|}),
+// absolute error ~1e-7 (FP32 rounding level of the O(1) activations that
+// feed the next layer), a third of tanhf's instruction count.
+__device__ __forceinline__ float tanh_fast(float z) {
+    float t;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(-2.8853900817779268f * fabsf(z)));
+    const float y = __fdividef(1.0f - t, 1.0f + t);
+    return copysignf(y, z);
+}
+
 // Activations (regressor.cpp:35-57), derivative from the activation value.
 template <int ACT>
 __device__ __forceinline__ float act_f(float z) {
-    if constexpr (ACT == 0) return tanhf(z);
+    if constexpr (ACT == 0) return tanh_fast(z);
     else if constexpr (ACT == 1) return 1.0f / (1.0f + expf(-z));
     else if constexpr (ACT == 2) return fmaxf(z, 0.0f) + log1pf(expf(-fabsf(z)));
     else return fmaxf(z, 0.0f);
@@ -204,9 +214,10 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     }
     tc::mbar_wait(&bar[1], 0);
     uint32_t mph = 0, xph = 0;
-    auto mma_wait = [&]() {
-        tc::mbar_wait(&bar[0], mph);
+    auto mma_wait = [&]() {  // one waiting warp, the rest parked at the barrier
+        if (warp == 0) tc::mbar_wait(&bar[0], mph);
         mph ^= 1;
+        __syncthreads();
         tc::fence_after_sync();
     };
     auto cta_sync = [&]() {
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         const long row = tile * 128 + r;
         const bool live = row >= a.b0 && row < a.b1;
         const long trow = row - a.b0;
-        tc::mbar_wait(&bar[2], xph);
+        if (tid == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing thread reads the feature tile
         xph ^= 1;
         // ---- F0: D0 = X W0^T
         if (tid == 0) {
@@ -526,8 +537,10 @@ __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
 
 // Chunk tiles are 128B-swizzled K-major (tc.cuh sw_off): the coalesced
 // 16-byte row loads land in distinct bank groups.
+constexpr int kWgThreads = 256;
+
 template <int U>
-__global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
+__global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* tA1 = sm;                   // G2t chunk: 64 (o, zero-padded) x 64 (rows)
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
     const int dp = a.dp;
     if (t == 0) tc::mbar_init(mbar, 1);
     if (warp == 0) tc::tmem_alloc(tbase, 128);
-    for (int i = t; i < 8 * kChunkTile / 16; i += kTcThreads)
+    for (int i = t; i < 8 * kChunkTile / 16; i += kWgThreads)
         reinterpret_cast<float4*>(sm)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     tc::fence_before_sync();
     __syncthreads();
@@ -550,21 +563,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
     const long r_end = min(r_begin + a.rows_per_cta, a.rows);
     const bool vt = (a.ld_t % 4) == 0;
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
-    constexpr int NF = U * 16 / kTcThreads;  // float4 per thread per activation array
-    float4 rg2[NF], rh1[NF], rg1[NF], rx[8];
+    constexpr int NF = U * 16 / kWgThreads;  // float4 per thread per activation array
+    constexpr int NX = 64 * 16 / kWgThreads;  // float4 per thread of a 64-feature Xt chunk (dp <= 64)
+    float4 rg2[NF], rh1[NF], rg1[NF], rx[NX];
     auto load = [&](long c0) {
         const int n = static_cast<int>(min(64L, r_end - c0));
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
-            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
             const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
             rg2[i] = ld4(a.G2t + o, vt, n - k);
             rh1[i] = ld4(a.H1t + o, vt, n - k);
             rg1[i] = ld4(a.G1t + o, vt, n - k);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+        for (int i = 0; i < NX; ++i) {
+            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
             if (f < dp) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
         }
     };
@@ -578,14 +592,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
         }
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
-            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
             tc::put_split4_sw(tA1, kChunkTile, f, k, 64, rg2[i]);
             tc::put_split4_sw(tB1, kChunkTile, f, k, 64, rh1[i]);
             tc::put_split4_sw(tA0, kChunkTile, f, k, 64, rg1[i]);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int idx = t + i * kTcThreads, f = idx >> 4, k = (idx & 15) * 4;
+        for (int i = 0; i < NX; ++i) {
+            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
             if (f < dp) tc::put_split4_sw(tB0, kChunkTile, f, k, 64, rx[i]);
         }
         tc::fence_async_smem();
@@ -610,6 +624,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
         tc::fence_after_sync();
     }
     float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
+    if (warp < 4) {
     const int o = warp * 16 + lane;  // M=64 accumulator: row 16w+t in lane 32w+t, t < 16
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
 #pragma unroll
@@ -627,6 +642,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_wgrad_tc(WgradArgs a) {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
                 if (c + q < a.d) gout[a.off0 + o * a.d + c + q] = first ? 0.0f : v[q];
+    }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -752,7 +768,7 @@ template <int U>
 void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
     const size_t smem = 8 * static_cast<size_t>(kChunkTile) + 64 + 1024;
     HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_wgrad_tc<U><<<ctas, kTcThreads, smem, s>>>(a);
+    k_wgrad_tc<U><<<ctas, kWgThreads, smem, s>>>(a);
 }
 
 template <int U>
