@@ -294,31 +294,38 @@ struct SplitPartials {
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // [lo, hi) index ranges served by gpartB
 };
 
-// Block (32, 8): x = parameter, y = partial group c = y (mod 8); the eight
-// group sums combine pairwise in fixed order.
+// Block (32, 16): x = parameter, y = partial group c = y (mod 16); the group
+// sums combine in a fixed pairwise tree.  Warp 0 of CTA 0 also checks the loss.
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
                        double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite,
                        ImgArgs im) {
-    __shared__ double part[8][33];
+    constexpr int G = 16;
+    __shared__ double part[G][33];
     const int x = threadIdx.x, grp = threadIdx.y;
     const int i = blockIdx.x * 32 + x;
-    if (blockIdx.x == 0 && x == 0 && grp == 0) {
+    if (blockIdx.x == 0 && grp == 0) {
         double s = 0.0;
-        for (int c = 0; c < nct; ++c) s += lpart[c];
-        if (!isfinite(s / nb)) atomicExch(nonfinite, 1);
+        for (int c = x; c < nct; c += 32) s += lpart[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (x == 0 && !isfinite(s / nb)) atomicExch(nonfinite, 1);
     }
     double s = 0.0;
     if (i < P) {
         const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
         const float* src = split ? sp.gpartB : gpart;
         const int cnt = split ? sp.nB : nct;
-        for (int c = grp; c < cnt; c += 8) s += static_cast<double>(src[static_cast<size_t>(c) * P + i]);
+#pragma unroll 4
+        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * P + i));
     }
     part[grp][x] = s;
     __syncthreads();
+#pragma unroll
+    for (int h = G / 2; h >= 1; h >>= 1) {
+        if (grp < h) part[grp][x] += part[grp + h][x];
+        __syncthreads();
+    }
     if (grp != 0 || i >= P) return;
-    const double g = ((part[0][x] + part[1][x]) + (part[2][x] + part[3][x])) +
-                     ((part[4][x] + part[5][x]) + (part[6][x] + part[7][x]));
+    const double g = part[0][x];
     double w = p64[i];
     if (adam) {
         const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
@@ -438,6 +445,22 @@ __global__ void k_gram(NetDims n, const float* X, const double* y, long R, const
             out[idx] += s;
         }
     }
+}
+
+// out[idx] = sum over c of parts[c * stride + idx], four interleaved chains
+// combined pairwise (fixed order).
+__global__ void k_sum_parts(const double* parts, int n, int stride, double* out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= stride) return;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;
+    for (; c + 4 <= n; c += 4)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] += parts[static_cast<size_t>(c + k) * stride + idx];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (c + k < n) a[k] += parts[static_cast<size_t>(c + k) * stride + idx];
+    out[idx] = (a[0] + a[1]) + (a[2] + a[3]);
 }
 
 // One CTA: reduce the Gram partials (fixed order), ridge lam = max(ridge tr/(u+1), 1e-300),
@@ -572,7 +595,7 @@ struct Trainer {
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
     // Tensor-core path: weight-gradient partials, transposed activations, packed operand images.
-    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2;
+    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2, gram_sum;
     int max_tiles = 0, last_parts = 0, dp = 0, gram_parts = 0;
     bool use_tc = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
@@ -689,7 +712,7 @@ struct Trainer {
     void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
         SplitPartials sp;
         const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
-        k_adam<<<(n.P + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
+        k_adam<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>(),
                                                          img_args());
@@ -729,7 +752,17 @@ struct Trainer {
         const int mm = n.u + 1;
         const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
         HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-        k_refit<<<1, 128, sm, ctx->stream>>>(n, gram.as<double>(), nct, ridge, p64.as<double>(), p32.as<float>());
+        const double* gsrc = gram.as<double>();
+        if (nct > 8) {  // pre-reduce the partials across the GPU, k_refit then reads one
+            const int stride = mm * (mm + 1) / 2 + mm;
+            if (gram_sum.bytes < static_cast<size_t>(stride) * 8) gram_sum.alloc(static_cast<size_t>(stride) * 8);
+            k_sum_parts<<<(stride + 127) / 128, 128, 0, ctx->stream>>>(gram.as<double>(), nct, stride,
+                                                                         gram_sum.as<double>());
+            check_launch(ctx);
+            gsrc = gram_sum.as<double>();
+            nct = 1;
+        }
+        k_refit<<<1, 128, sm, ctx->stream>>>(n, gsrc, nct, ridge, p64.as<double>(), p32.as<float>());
         wimg_valid = false;
         check_launch(ctx);
     }
@@ -786,7 +819,11 @@ struct FeatArgs {
     const uint16_t* steps;
     const double* mean;
     const double* scale;
-    float* X;
+    float* X;          // [R][d] row-major (SIMT path), or
+    uint8_t* ximg;     // tensor-core path: 128-row operand tiles (hi | lo) ...
+    float* Xt;         // ... and the transposed copy [dp][ld_x]
+    long ld_x;
+    int dp;
 };
 
 __device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
@@ -803,9 +840,32 @@ __device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
 __global__ void k_build_x(FeatArgs a) {
     const size_t R = static_cast<size_t>(a.M) * a.N;
     const size_t row = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const int Cc = a.Cn - 1, q = 3 * a.E - 1 + Cc, d = Cc + q;
+    if (a.ximg) {  // grid covers the padded last tile: rows >= R are zero
+        const size_t tiles = (R + 127) / 128;
+        if (row >= tiles * 128) return;
+        const bool in = row < R;
+        const int k = in ? static_cast<int>(row / a.N) : 0;
+        const uint32_t xb = 128u * a.dp * 4;
+        uint8_t* tb = a.ximg + (row / 128) * 2 * xb;
+        for (int c = 0; c < a.dp; c += 4) {
+            float v[4];
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int col = c + qq;
+                float x = 0.0f;
+                if (in && col < Cc) x = (a.steps[(col + 1) * R + row] <= a.step) ? 1.0f : 0.0f;
+                else if (in && col < d)
+                    x = static_cast<float>((state_col(a, k, col - Cc) - a.mean[col]) / a.scale[col]);
+                v[qq] = x;
+                if (in) a.Xt[col * a.ld_x + row] = x;
+            }
+            tc::put_split4(tb, xb, static_cast<int>(row % 128), c, 128, make_float4(v[0], v[1], v[2], v[3]));
+        }
+        return;
+    }
     if (row >= R) return;
     const int k = static_cast<int>(row / a.N);
-    const int Cc = a.Cn - 1, q = 3 * a.E - 1 + Cc, d = Cc + q;
     float* o = a.X + row * d;
     for (int c = 1; c <= Cc; ++c) o[c - 1] = (a.steps[c * R + row] <= a.step) ? 1.0f : 0.0f;
     for (int j = 0; j < q; ++j)
@@ -899,6 +959,24 @@ void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX
     for (size_t i = 0; i < xf.size(); ++i) xf[i] = static_cast<float>(x[i]);
     stage(dX, xf);
     tr.prepare_x(dX.as<float>(), rows);
+}
+
+// Standardised features of one step (fa with mean / scale set): straight into
+// the tensor-core operand images, or into X [R][d] for the SIMT path.
+void build_features(Trainer& tr, FeatArgs fa, DeviceBuf& X, long R) {
+    hcva_ctx* ctx = tr.ctx;
+    if (tr.use_tc) {
+        if (R > tr.x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
+        fa.ximg = tr.ximg.as<uint8_t>();
+        fa.Xt = tr.xt.as<float>();
+        fa.ld_x = tr.ld_x;
+        fa.dp = tr.dp;
+        k_build_x<<<grid1(((R + 127) / 128) * 128, 256), 256, 0, ctx->stream>>>(fa);
+    } else {
+        fa.X = X.as<float>();
+        k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
+    }
+    check_launch(ctx);
 }
 
 }  // namespace
@@ -1005,7 +1083,7 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
         Trainer tr(ctx, n, R / cfg->n_batches, R);
         HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
         DeviceBuf X;
-        X.alloc(sizeof(float) * R * d);
+        if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
         for (int i = nsteps; i >= 1; --i) {
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
@@ -1014,10 +1092,7 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
             check_launch(ctx);
             fa.mean = mean;
             fa.scale = scale;
-            fa.X = X.as<float>();
-            k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
-            check_launch(ctx);
-            tr.prepare_x(X.as<float>(), R);
+            build_features(tr, fa, X, R);
             const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
             if (i == nsteps) {
                 const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));
@@ -1085,12 +1160,9 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         fa.mean = m->mean.as<double>() + static_cast<size_t>(step - 1) * d;
         fa.scale = m->scale.as<double>() + static_cast<size_t>(step - 1) * d;
         DeviceBuf X, pred;
-        X.alloc(sizeof(float) * R * d);
+        if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
         pred.alloc(sizeof(double) * R);
-        fa.X = X.as<float>();
-        k_build_x<<<grid1(R, 256), 256, 0, ctx->stream>>>(fa);
-        check_launch(ctx);
-        tr.prepare_x(X.as<float>(), R);
+        build_features(tr, fa, X, R);
         tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
         copy_out(ctx, out, pred.p, R * 8);
     });
