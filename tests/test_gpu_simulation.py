@@ -228,9 +228,10 @@ def test_nested_cva_vs_golden(name):
     val, se = hcva.nested_cva(cfg, book, st, surv, step, inner, parent)
     close(val, z["nested"][:, 0], 1e-9, 1e-12, "nested value")
     # The reference's variance (sum_sq - L m^2)/(L-1) cancels badly when the
-    # inner payoffs are close, so the standard error is compared against the
-    # value's scale rather than its own.
-    assert np.all(np.abs(se - z["nested"][:, 1]) <= 1e-6 * np.abs(z["nested"][:, 1]) + 1e-9 * np.abs(val))
+    # inner payoffs are close: its rounding noise is O(eps m^2), i.e. the
+    # standard error carries noise O(sqrt(eps) |m|), so it is compared against
+    # the value's scale at sqrt(eps) ~ 1.5e-8 rather than against its own.
+    assert np.all(np.abs(se - z["nested"][:, 1]) <= 1e-6 * np.abs(z["nested"][:, 1]) + 2e-8 * np.abs(val))
 
 
 def test_nested_batching_is_per_state_pure():
