@@ -119,6 +119,16 @@ hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva
                               const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
                               int n_replicas, uint64_t key_market, uint64_t key_defaults,
                               hcva_sim** out);
+/* Interleaved shard of the global path space: local path k is global path
+ * path_offset + (k / shard_blk) * shard_stride + k % shard_blk (shard_blk == 0:
+ * path_offset + k).  Rank g of G owning slice g of every regression batch of
+ * P_B paths: shard_blk = P_B / G, shard_stride = P_B, path_offset = g * P_B / G,
+ * n_paths = M / G -- its local batches are then the rank's slices of the
+ * global batches (regressor.cpp:160-170), SURVEY §8(e). */
+hcva_status hcva_simulate_set_sharded(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                      const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
+                                      int shard_blk, int shard_stride, int n_replicas, uint64_t key_market,
+                                      uint64_t key_defaults, hcva_sim** out);
 /* simulate_conditional_market (market.cpp:236-310) for ONE outer state:
  * state = rates[E], log_fx[E-1], intensities[Cc+1], lagged_rates[E]. */
 hcva_status hcva_simulate_conditional(hcva_ctx* ctx, const hcva_model* model,
@@ -209,6 +219,28 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
  * make_label_source (pipeline.cpp:72-111) on a simulated set; label_kind 0 =
  * defaults, 1 = intensity.  Everything stays on the GPU. */
 hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out);
+
+/* --- multi-GPU regression -------------------------------------
+ * Y-paths shard by hcva_simulate_set_sharded (rank g owns slice g of every
+ * batch); each rank trains on its rows and every cross-rank sum (gradient +
+ * loss per SGD step, epoch loss, head-switch minimum, refit Gram, scaler
+ * moments, label mean) is an allgather of FP64 partials combined in rank
+ * order on the device, so all ranks hold identical networks.  Transports:
+ * NCCL (one process per GPU; id from rank 0, broadcast by the caller) or an
+ * in-process group (one host thread + context per rank). */
+typedef struct hcva_comm hcva_comm;
+typedef struct hcva_group hcva_group;
+hcva_status hcva_comm_nccl_id(uint8_t* id /* [128] */);
+hcva_status hcva_comm_create_nccl(hcva_ctx* ctx, int world, int rank, const uint8_t* id /* [128] */,
+                                  hcva_comm** out);
+hcva_status hcva_group_create(int world, hcva_group** out);
+hcva_status hcva_group_destroy(hcva_group* group);
+hcva_status hcva_comm_create_local(hcva_ctx* ctx, hcva_group* group, int rank, hcva_comm** out);
+hcva_status hcva_comm_info(const hcva_comm* comm, int* rank, int* world);
+hcva_status hcva_comm_destroy(hcva_comm* comm);
+/* backward_learn over this rank's shard; comm == NULL is hcva_backward_learn. */
+hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_comm* comm,
+                                     hcva_models** out);
 /* info: [0] n_steps [1] input_dim [2] n_params [3] epochs */
 hcva_status hcva_models_info(const hcva_models* m, int* info /* [4] */);
 /* Per-step model (steps[i-1]): params, scaler mean/scale, report.  NULL skips. */

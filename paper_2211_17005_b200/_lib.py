@@ -114,6 +114,8 @@ def lib():
                                u64, C.POINTER(Swap)],
         "hcva_simulate_set": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int,
                               C.c_int, C.c_int, C.c_int, u64, u64, C.POINTER(vp)],
+        "hcva_simulate_set_sharded": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, u64, u64, C.POINTER(vp)],
         "hcva_simulate_conditional": [vp, C.POINTER(Model), C.POINTER(Grid), dptr, dptr, dptr, dptr,
                                       C.c_int, C.c_int, C.c_int, u64, C.POINTER(vp)],
         "hcva_sample_defaults": [vp, C.c_int, u64],
@@ -140,6 +142,14 @@ def lib():
         "hcva_train_base": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr, dptr, dptr, dptr,
                             C.POINTER(C.c_int)],
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
+        "hcva_backward_learn_dist": [vp, C.POINTER(TrainCfg), C.c_int, vp, C.POINTER(vp)],
+        "hcva_comm_nccl_id": [C.c_char_p],
+        "hcva_comm_create_nccl": [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)],
+        "hcva_group_create": [C.c_int, C.POINTER(vp)],
+        "hcva_group_destroy": [vp],
+        "hcva_comm_create_local": [vp, vp, C.c_int, C.POINTER(vp)],
+        "hcva_comm_info": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "hcva_comm_destroy": [vp],
         "hcva_models_info": [vp, C.POINTER(C.c_int)],
         "hcva_models_get": [vp, C.c_int, dptr, dptr, dptr, dptr, dptr, C.POINTER(C.c_int)],
         "hcva_predict": [vp, vp, C.c_int, dptr],
@@ -164,11 +174,13 @@ EXPORTED = [
     "hcva_last_error", "hcva_version", "hcva_ctx_create", "hcva_ctx_destroy", "hcva_ctx_stream",
     "hcva_ctx_synchronize", "hcva_ctx_launch_count", "hcva_rng_root_key", "hcva_rng_split_key",
     "hcva_rng_draw", "hcva_cholesky", "hcva_par_rate", "hcva_zc_price", "hcva_generate_book",
-    "hcva_simulate_set", "hcva_simulate_conditional", "hcva_sample_defaults", "hcva_build_cube",
+    "hcva_simulate_set", "hcva_simulate_set_sharded", "hcva_simulate_conditional", "hcva_sample_defaults", "hcva_build_cube",
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
     "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch", "hcva_net_size",
     "hcva_init_network", "hcva_quadratic_loss", "hcva_train_base", "hcva_backward_learn", "hcva_models_info",
-    "hcva_models_get", "hcva_predict", "hcva_models_destroy",
+    "hcva_models_get", "hcva_predict", "hcva_models_destroy", "hcva_comm_nccl_id", "hcva_comm_create_nccl",
+    "hcva_group_create", "hcva_group_destroy", "hcva_comm_create_local", "hcva_comm_info", "hcva_comm_destroy",
+    "hcva_backward_learn_dist",
 ]

@@ -130,6 +130,7 @@ struct hcva_sim {
     hcva_ctx* ctx = nullptr;
     hcva::Model model;
     int M = 0, n = 0, N = 0, start_step = 0, path_offset = 0;
+    int shard_blk = 0, shard_stride = 0;  // interleaved shard map (simulate.cu shard_path)
     int n_groups = 1;  // conditional blocks: states, each with M / n_groups inner paths
     hcva::DeviceBuf rates, fx, intens, hazard, disc, lag0, cube, steps, labels, ties, scratch, profile;
     bool has_cube = false, has_defaults = false;

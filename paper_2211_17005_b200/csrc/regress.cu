@@ -35,6 +35,7 @@ namespace hcva {
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
 }  // namespace hcva
+#include "comm.cuh"
 #include "regress_tc.cuh"
 #include "tc.cuh"  // tensor-core tiles for the paper's network shape
 namespace hcva {
@@ -288,6 +289,26 @@ __device__ __forceinline__ void img_store(const ImgArgs& im, int P, int i, float
     }
 }
 
+// Adam / SGD update of parameter i (regressor.cpp:236-261).
+__device__ __forceinline__ void optimizer_step(int i, double g, int P, double* p64, float* p32, double* m, double* v,
+                                               long t, double lr, int adam, const ImgArgs& im) {
+    double w = p64[i];
+    if (adam) {
+        const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+        const double c1 = 1.0 - pow(b1, static_cast<double>(t)), c2 = 1.0 - pow(b2, static_cast<double>(t));
+        const double mi = b1 * m[i] + (1.0 - b1) * g;
+        const double vi = b2 * v[i] + (1.0 - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        w -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+    } else {
+        w -= lr * g;
+    }
+    p64[i] = w;
+    p32[i] = static_cast<float>(w);
+    if (im.img) img_store(im, P, i, static_cast<float>(w));
+}
+
 struct SplitPartials {
     const float* gpartB = nullptr;
     int nB = 0;
@@ -325,22 +346,65 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
         __syncthreads();
     }
     if (grp != 0 || i >= P) return;
-    const double g = part[0][x];
-    double w = p64[i];
-    if (adam) {
-        const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-        const double c1 = 1.0 - pow(b1, static_cast<double>(t)), c2 = 1.0 - pow(b2, static_cast<double>(t));
-        const double mi = b1 * m[i] + (1.0 - b1) * g;
-        const double vi = b2 * v[i] + (1.0 - b2) * g * g;
-        m[i] = mi;
-        v[i] = vi;
-        w -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
-    } else {
-        w -= lr * g;
+    optimizer_step(i, part[0][x], P, p64, p32, m, v, t, lr, adam, im);
+}
+
+// Multi-GPU: this rank's gradient (FP64, fixed-order sum of its partials) and
+// loss sum -> red[0..P], red[P]; gathered across ranks before k_adam_dist.
+__global__ void k_rank_sum(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double* red) {
+    constexpr int G = 16;
+    __shared__ double part[G][33];
+    const int x = threadIdx.x, grp = threadIdx.y;
+    const int i = blockIdx.x * 32 + x;
+    if (blockIdx.x == 0 && grp == 0) {
+        double s = 0.0;
+        for (int c = x; c < nct; c += 32) s += lpart[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (x == 0) red[P] = s;
     }
-    p64[i] = w;
-    p32[i] = static_cast<float>(w);
-    if (im.img) img_store(im, P, i, static_cast<float>(w));
+    double s = 0.0;
+    if (i < P) {
+        const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
+        const float* src = split ? sp.gpartB : gpart;
+        const int cnt = split ? sp.nB : nct;
+#pragma unroll 4
+        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * P + i));
+    }
+    part[grp][x] = s;
+    __syncthreads();
+#pragma unroll
+    for (int h = G / 2; h >= 1; h >>= 1) {
+        if (grp < h) part[grp][x] += part[grp + h][x];
+        __syncthreads();
+    }
+    if (grp == 0 && i < P) red[i] = part[0][x];
+}
+
+// Update from the gathered per-rank vectors all[G][stride], summed in rank order.
+__global__ void k_adam_dist(int P, const double* all, int G, int stride, double nb, double* p64, float* p32, double* m,
+                            double* v, long t, double lr, int adam, int* nonfinite, ImgArgs im) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        double s = 0.0;
+        for (int r = 0; r < G; ++r) s += all[static_cast<size_t>(r) * stride + P];
+        if (!isfinite(s / nb)) atomicExch(nonfinite, 1);
+    }
+    if (i >= P) return;
+    double g = 0.0;
+    for (int r = 0; r < G; ++r) g += all[static_cast<size_t>(r) * stride + i];
+    optimizer_step(i, g, P, p64, p32, m, v, t, lr, adam, im);
+}
+
+// out[0] = sum (op 0) or min (op 1) of parts[0..n), fixed order (one warp).
+__global__ void k_reduce_scalar(const double* parts, int n, int op, double* out) {
+    const int x = threadIdx.x;
+    double s = op ? INFINITY : 0.0;
+    for (int c = x; c < n; c += 32) s = op ? fmin(s, parts[c]) : s + parts[c];
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, s, o);
+        s = op ? fmin(s, w) : s + w;
+    }
+    if (x == 0) out[0] = s;
 }
 
 // Full-sample forward over tiles (grid-stride, fixed tile->CTA map).
@@ -587,6 +651,22 @@ __global__ void k_set_mu_mean(const double* y, long R, double* p64, float* p32, 
     }
 }
 
+// Label mean over all ranks' rows: mu = sum_r all[r] / R_total.
+__global__ void k_set_mu_from(const double* all, int G, double R_total, double* p64, float* p32, int P) {
+    double s = 0.0;
+    for (int r = 0; r < G; ++r) s += all[r];
+    p64[P - 1] = s / R_total;
+    p32[P - 1] = static_cast<float>(s / R_total);
+}
+
+__global__ void k_local_sum(const double* y, long R, double* out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long r = threadIdx.x; r < R; r += blockDim.x) s += y[r];
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) out[0] = t;
+}
+
 // ---------------------------------------------------------------- trainer
 
 struct Trainer {
@@ -600,6 +680,22 @@ struct Trainer {
     bool use_tc = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
     bool wimg_valid = false;  // weight image matches p32
+    hcva_comm* comm = nullptr;  // multi-GPU: rank-ordered allgather of the FP64 partials
+    int world = 1;
+    DeviceBuf red, gath;
+
+    void set_comm(hcva_comm* c, size_t max_len) {
+        comm = (c && c->world > 1) ? c : nullptr;
+        world = comm ? comm->world : 1;
+        if (!comm) return;
+        red.alloc(max_len * 8);
+        gath.alloc(max_len * 8 * world);
+    }
+    // Gather this rank's vector local[0..len) from every rank: [world][len] in rank order.
+    const double* gather(const double* local, size_t len) {
+        comm->allgather(local, gath.p, len * 8, ctx->stream);
+        return gath.as<double>();
+    }
 
     Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0) : ctx(c), n(dims) {
         use_tc = tc_eligible(n.d, n.h, n.u);
@@ -711,7 +807,19 @@ struct Trainer {
 
     void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
         SplitPartials sp;
-        const int tiles = grad_tiles(X, y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
+        const double nb = static_cast<double>(b1 - b0) * world;  // the global batch
+        const int tiles = grad_tiles(X, y, b0, b1, head, nb, &sp);
+        if (comm) {
+            k_rank_sum<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp,
+                                                                           lpart.as<double>(), red.as<double>());
+            check_launch(ctx);
+            const double* all = gather(red.as<double>(), n.P + 1);
+            k_adam_dist<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, all, world, n.P + 1, nb, p64.as<double>(),
+                                                                  p32.as<float>(), m.as<double>(), v.as<double>(), t,
+                                                                  lr, adam, flag.as<int>(), img_args());
+            check_launch(ctx);
+            return;
+        }
         k_adam<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>(),
@@ -753,7 +861,7 @@ struct Trainer {
         const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
         HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         const double* gsrc = gram.as<double>();
-        if (nct > 8) {  // pre-reduce the partials across the GPU, k_refit then reads one
+        if (nct > 8 || comm) {  // pre-reduce the partials across the GPU, k_refit then reads one
             const int stride = mm * (mm + 1) / 2 + mm;
             if (gram_sum.bytes < static_cast<size_t>(stride) * 8) gram_sum.alloc(static_cast<size_t>(stride) * 8);
             k_sum_parts<<<(stride + 127) / 128, 128, 0, ctx->stream>>>(gram.as<double>(), nct, stride,
@@ -761,10 +869,23 @@ struct Trainer {
             check_launch(ctx);
             gsrc = gram_sum.as<double>();
             nct = 1;
+            if (comm) {  // every rank's Gram + rhs, summed in rank order by k_refit
+                gsrc = gather(gsrc, stride);
+                nct = world;
+            }
         }
         k_refit<<<1, 128, sm, ctx->stream>>>(n, gsrc, nct, ridge, p64.as<double>(), p32.as<float>());
         wimg_valid = false;
         check_launch(ctx);
+    }
+
+    // This rank's sum (op 0) / min (op 1) of n partials, gathered from every rank
+    // ([world] in rank order); without a comm the partials themselves.
+    const double* rank_scalar(const double* parts, int cnt, int op) {
+        if (!comm) return parts;
+        k_reduce_scalar<<<1, 32, 0, ctx->stream>>>(parts, cnt, op, red.as<double>());
+        check_launch(ctx);
+        return gather(red.as<double>(), 1);
     }
 
     // train_base (regressor.cpp:265-347) on device-resident X [R][d] (FP32), y [R] (FP64).
@@ -790,14 +911,16 @@ struct Trainer {
                 refit(X, y, R, ridge);
                 eval(X, y, R, 2, nullptr);
                 wimg_valid = false;
-                k_switch<<<1, 256, 0, ctx->stream>>>(n, mpart.as<double>(), last_parts, p64.as<double>(),
+                const double* mp = rank_scalar(mpart.as<double>(), last_parts, 1);
+                k_switch<<<1, 256, 0, ctx->stream>>>(n, mp, comm ? world : last_parts, p64.as<double>(),
                                                       p32.as<float>(), m.as<double>(), v.as<double>());
                 check_launch(ctx);
                 head = 1;
                 t = 0;
             }
             eval(X, y, R, 1, nullptr);
-            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lpart.as<double>(), last_parts, static_cast<double>(R), e,
+            const double* lp = rank_scalar(lpart.as<double>(), last_parts, 0);
+            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lp, comm ? world : last_parts, static_cast<double>(R) * world, e,
                                                  p64.as<double>(), best.as<double>(), losses_dev,
                                                  best_loss.as<double>(), best_epoch.as<int>(), flag.as<int>());
             check_launch(ctx);
@@ -903,6 +1026,44 @@ __global__ void k_scaler(FeatArgs a, double* mean, double* scale) {
         const double sd = sqrt(vt / a.M);
         mean[j] = mu;
         scale[j] = (sd > 1e-12) ? sd : 1.0;
+    }
+}
+
+// Multi-GPU scaler: this rank's column sums (pass 0) or centred squared sums
+// about the global mean (pass 1) over its paths; indicator columns give 0.
+__global__ void k_scaler_moment(FeatArgs a, int pass, const double* mean, double* out) {
+    __shared__ double red[32];
+    const int Cc = a.Cn - 1, j = blockIdx.x;
+    if (j < Cc) {
+        if (threadIdx.x == 0) out[j] = 0.0;
+        return;
+    }
+    const int js = j - Cc;
+    const double mu = pass ? mean[j] : 0.0;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < a.M; k += blockDim.x) {
+        const double x = state_col(a, k, js) - mu;
+        s += pass ? x * x : x;
+    }
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) out[j] = t;
+}
+
+// Gathered moments all[G][d] (rank order) -> mean (pass 0) / scale (pass 1) over Mt paths.
+__global__ void k_scaler_fin(const double* all, int G, int d, int Cc, double Mt, int pass, double* mean,
+                             double* scale) {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < G; ++r) s += all[static_cast<size_t>(r) * d + j];
+        if (j < Cc) {
+            mean[j] = 0.0;
+            scale[j] = 1.0;
+        } else if (pass == 0) {
+            mean[j] = s / Mt;
+        } else {
+            const double sd = sqrt(s / Mt);
+            scale[j] = (sd > 1e-12) ? sd : 1.0;
+        }
     }
 }
 
@@ -1056,6 +1217,11 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
 // backward_learn (regressor.cpp:354-395) over a simulated set with the label
 // source of pipeline.cpp:72-111 (features_at + defaults_/intensity_label).
 hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out) {
+    return hcva_backward_learn_dist(sim, cfg, label_kind, nullptr, out);
+}
+
+hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_comm* comm,
+                                     hcva_models** out) {
     return guarded([&] {
         hcva_ctx* ctx = sim->ctx;
         StreamScope sc__(ctx->stream);
@@ -1081,6 +1247,10 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
         models->best_epoch.alloc(static_cast<size_t>(nsteps) * 4);
         if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
         Trainer tr(ctx, n, R / cfg->n_batches, R);
+        const int mm = n.u + 1;
+        tr.set_comm(comm, std::max<size_t>({static_cast<size_t>(n.P) + 1, static_cast<size_t>(mm * (mm + 1) / 2 + mm),
+                                            static_cast<size_t>(d)}));
+        const int world = tr.world;
         HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
         DeviceBuf X;
         if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
@@ -1088,7 +1258,17 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
             double* scale = models->scale.as<double>() + static_cast<size_t>(i - 1) * d;
-            k_scaler<<<d, 256, 0, ctx->stream>>>(fa, mean, scale);
+            if (world == 1) {
+                k_scaler<<<d, 256, 0, ctx->stream>>>(fa, mean, scale);
+            } else {  // moments over every rank's paths: sums, gathered, then centred sums
+                const double Mt = static_cast<double>(sim->M) * world;
+                k_scaler_moment<<<d, 256, 0, ctx->stream>>>(fa, 0, mean, tr.red.as<double>());
+                k_scaler_fin<<<1, 64, 0, ctx->stream>>>(tr.gather(tr.red.as<double>(), d), world, d, Cc, Mt, 0, mean,
+                                                        scale);
+                k_scaler_moment<<<d, 256, 0, ctx->stream>>>(fa, 1, mean, tr.red.as<double>());
+                k_scaler_fin<<<1, 64, 0, ctx->stream>>>(tr.gather(tr.red.as<double>(), d), world, d, Cc, Mt, 1, mean,
+                                                        scale);
+            }
             check_launch(ctx);
             fa.mean = mean;
             fa.scale = scale;
@@ -1098,7 +1278,14 @@ hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int la
                 const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));
                 tr.set_params(p.data());
                 HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
-                k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
+                if (world == 1) {
+                    k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
+                } else {
+                    k_local_sum<<<1, 1024, 0, ctx->stream>>>(y, R, tr.red.as<double>());
+                    k_set_mu_from<<<1, 1, 0, ctx->stream>>>(tr.gather(tr.red.as<double>(), 1), world,
+                                                            static_cast<double>(R) * world, tr.p64.as<double>(),
+                                                            tr.p32.as<float>(), n.P);
+                }
                 tr.wimg_valid = false;
                 check_launch(ctx);
             } else {

@@ -43,12 +43,22 @@ __global__ void k_draws(uint64_t key, uint64_t start, size_t count, int kind, vo
     static_cast<double*>(out)[t] = v;
 }
 
+// Global path index of local path k in an interleaved shard: blocks of `blk`
+// consecutive global paths every `stride` (blk == 0: identity).  Rank g of G
+// owning slice g of every regression batch of P_B paths uses blk = P_B / G,
+// stride = P_B and path_offset = g * P_B / G.
+__host__ __device__ __forceinline__ uint64_t shard_path(int k, int blk, int stride) {
+    return blk ? static_cast<uint64_t>(k / blk) * static_cast<uint64_t>(stride) + static_cast<uint64_t>(k % blk)
+               : static_cast<uint64_t>(k);
+}
+
 // ------------------------------------------------------------------ K1
 struct MarketArgs {
     int E, Cn, D, substeps, n_store, M, T, nnz;
     int mode;    // profiling probe: bit 0 skips normal generation, bit 1 skips the recursion
     int W_econ;  // economy-thread slots per path (E rounded up to whole warps)
     int paths_per_group;
+    int shard_blk, shard_stride;  // interleaved shard map (0: identity), see shard_path
     uint64_t local_offset;
     double h, sqh;
     uint64_t key0;               // key of group 0 when group_keys == nullptr
@@ -117,7 +127,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     const bool valid = kloc < M;
     const int kk = valid ? kloc : M - 1;
     const int grp = kk / a.paths_per_group;
-    const uint64_t within = static_cast<uint64_t>(kk - grp * a.paths_per_group) + a.local_offset;
+    const uint64_t within = shard_path(kk - grp * a.paths_per_group, a.shard_blk, a.shard_stride) + a.local_offset;
     const uint64_t pkey = split_key(a.group_keys ? a.group_keys[grp] : a.key0, within);
 
     // Roles.  Economy threads w < We (We = E rounded up so warps are role-uniform);
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(128) k_mtm_direct(DirectArgs a) {
 
 // ------------------------------------------------------------------ K3
 struct DefaultArgs {
-    int M, N, n, Cn, path_offset;
+    int M, N, n, Cn, path_offset, shard_blk, shard_stride;
     uint64_t key;
     const double* hazard;  // SoA [(i*Cn+c)*M + k]
     uint16_t* steps;       // [c][k*N+l]
@@ -445,7 +455,7 @@ __global__ void __launch_bounds__(128) k_defaults(DefaultArgs a) {
         hz[t] = a.hazard[(static_cast<size_t>(i) * Cn + c) * a.M + k];
     }
     __syncthreads();
-    const uint64_t pkey = split_key(a.key, static_cast<uint64_t>(a.path_offset) + k);
+    const uint64_t pkey = split_key(a.key, static_cast<uint64_t>(a.path_offset) + shard_path(k, a.shard_blk, a.shard_stride));
     unsigned long long tie_ulp = 0, tie_rel = 0;
     const size_t R = static_cast<size_t>(a.M) * a.N;
     for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
@@ -780,6 +790,7 @@ void launch_market(hcva_sim* sim, uint64_t key0) {
     MarketArgs a{};
     a.E = m.E; a.Cn = m.Cn; a.D = m.D; a.substeps = m.substeps; a.n_store = sim->n; a.M = sim->M;
     a.T = sim->m_T; a.nnz = sim->m_nnz; a.paths_per_group = sim->m_ppg; a.local_offset = sim->m_local_offset;
+    a.shard_blk = sim->shard_blk; a.shard_stride = sim->shard_stride;
     a.h = m.dt / m.substeps; a.sqh = std::sqrt(a.h);
     a.key0 = key0;
     a.W_econ = sim->m_We;
@@ -914,6 +925,7 @@ void launch_defaults(hcva_sim* sim, uint64_t key) {
     HCVA_CUDA(cudaMemsetAsync(sim->ties.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     DefaultArgs a{};
     a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = sim->model.Cn; a.path_offset = sim->path_offset; a.key = key;
+    a.shard_blk = sim->shard_blk; a.shard_stride = sim->shard_stride;
     a.hazard = sim->hazard.as<double>(); a.steps = sim->steps.as<uint16_t>();
     a.ties = sim->ties.as<unsigned long long>();
     const size_t smem = sizeof(double) * (sim->n + 1) * sim->model.Cn;
@@ -1054,16 +1066,28 @@ hcva_status hcva_rng_draw(hcva_ctx* ctx, uint64_t key, uint64_t start, size_t co
 hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
                               const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
                               int n_replicas, uint64_t key_market, uint64_t key_defaults, hcva_sim** out) {
+    return hcva_simulate_set_sharded(ctx, model, grid, book, n_swaps, n_paths, path_offset, 0, 0, n_replicas,
+                                     key_market, key_defaults, out);
+}
+
+hcva_status hcva_simulate_set_sharded(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                      const hcva_swap* book, int n_swaps, int n_paths, int path_offset,
+                                      int shard_blk, int shard_stride, int n_replicas, uint64_t key_market,
+                                      uint64_t key_defaults, hcva_sim** out) {
     return guarded([&] {
         StreamScope sc__(ctx->stream);
         if (!grid) throw contract_error("simulate_set: null grid");
         if (n_paths < 1) throw contract_error("simulate_market: n_paths must be >= 1");
         if (path_offset < 0) throw contract_error("simulate_set: negative path offset");
+        if (shard_blk < 0 || (shard_blk > 0 && (shard_stride < shard_blk || n_paths % shard_blk != 0)))
+            throw contract_error("simulate_set: shard map needs 0 < blk <= stride and blk | n_paths");
         std::unique_ptr<hcva_sim> sim(new_sim(ctx, model, grid));
         const Model& m = sim->model;
         sim->M = n_paths;
         sim->n = m.n_steps;
         sim->path_offset = path_offset;
+        sim->shard_blk = shard_blk;
+        sim->shard_stride = shard_stride;
         std::vector<double> init(m.D);
         for (int e = 0; e < m.E; ++e) init[e] = m.rates[e].r0;
         for (int e = 1; e < m.E; ++e) init[m.E + e - 1] = std::log(m.fx[e - 1].chi0);
@@ -1071,7 +1095,7 @@ hcva_status hcva_simulate_set(hcva_ctx* ctx, const hcva_model* model, const hcva
         std::vector<double> lag0(m.E);
         for (int e = 0; e < m.E; ++e) lag0[e] = m.rates[e].r0;
         stage(sim->lag0, lag0);
-        prepare_market(sim.get(), {key_market}, init, n_paths + path_offset, static_cast<uint64_t>(path_offset));
+        prepare_market(sim.get(), {key_market}, init, n_paths, static_cast<uint64_t>(path_offset));
         if (n_replicas > 0) prepare_defaults(sim.get(), n_replicas);
         if (book) prepare_cube(sim.get(), book, n_swaps);
         launch_market(sim.get(), key_market);

@@ -318,9 +318,13 @@ def _kind(kind: str) -> int:
 
 
 def simulate_set(cfg: PipelineConfig, book: Optional[np.ndarray], n_paths: int, n_replicas: int,
-                 stream: RandomStream, path_offset: int = 0, ctx: Optional[Context] = None
-                 ) -> SimulationSet:
-    """simulate_set (pipeline.cpp:63-70): market from stream.split(0), defaults from stream.split(1)."""
+                 stream: RandomStream, path_offset: int = 0, ctx: Optional[Context] = None,
+                 shard: Optional[Tuple[int, int]] = None) -> SimulationSet:
+    """simulate_set (pipeline.cpp:63-70): market from stream.split(0), defaults from stream.split(1).
+
+    Local path k is global path ``path_offset + k``, or with ``shard = (blk, stride)``
+    ``path_offset + (k // blk) * stride + k % blk`` (an interleaved multi-GPU shard,
+    see ``dist.shard_spec``)."""
     ctx = ctx or context()
     m, g = cfg.to_model()
     h = C.c_void_p()
@@ -329,9 +333,10 @@ def simulate_set(cfg: PipelineConfig, book: Optional[np.ndarray], n_paths: int, 
         nsw = len(bk)
     else:
         bp, nsw = None, 0
-    _lib.check(_lib.lib().hcva_simulate_set(ctx.handle, C.byref(m), C.byref(g), bp, nsw, n_paths,
-                                            path_offset, n_replicas, stream.split(0).key,
-                                            stream.split(1).key, C.byref(h)))
+    blk, stride = shard if shard else (0, 0)
+    _lib.check(_lib.lib().hcva_simulate_set_sharded(ctx.handle, C.byref(m), C.byref(g), bp, nsw, n_paths,
+                                                    path_offset, blk, stride, n_replicas, stream.split(0).key,
+                                                    stream.split(1).key, C.byref(h)))
     return SimulationSet(h, ctx)
 
 

@@ -102,13 +102,18 @@ class Models:
         return out
 
 
-def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults") -> Models:
-    """backward_learn (regressor.cpp:354-395) over the label source of make_label_source."""
+def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults", comm=None) -> Models:
+    """backward_learn (regressor.cpp:354-395) over the label source of make_label_source.
+
+    With ``comm`` (a ``dist.Comm`` of world G) ``sim`` is this rank's interleaved
+    shard (``dist.shard_spec``) and every cross-rank sum is a rank-ordered
+    allgather of FP64 partials: all ranks end with the same networks."""
     kind = {"defaults": 0, "intensity": 1}.get(label_kind)
     if kind is None:
         raise _lib.ConfigError("config: label_kind must be 'defaults' or 'intensity'")
     h = C.c_void_p()
-    _lib.check(_lib.lib().hcva_backward_learn(sim.handle, C.byref(train_cfg(t)), kind, C.byref(h)))
+    _lib.check(_lib.lib().hcva_backward_learn_dist(sim.handle, C.byref(train_cfg(t)), kind,
+                                                   comm.handle if comm is not None else None, C.byref(h)))
     return Models(h, sim.ctx)
 
 
