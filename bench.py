@@ -285,8 +285,8 @@ def ours_arm(args):
     if not args.no_e2e:
         e2e = e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args)
     learning = None
-    if not args.no_learning and world == 1:
-        learning = learning_leg(hcva, cfg, book, ctx, args)
+    if not args.no_learning:
+        learning = learning_leg(hcva, cfg, book, ctx, args, rank, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
@@ -359,13 +359,19 @@ def e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args):
             "cva0": float(prof[0])}
 
 
-def learning_leg(hcva, cfg, book, ctx, args):
+def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
     """BASELINE metric 2: end-to-end CVA learning time on the same workload --
     host config -> simulate_set -> labels -> backward_learn over every pricing
     step (Alg. 2, E epochs x |B| batches, refit, best tracking) -> the time-0
     CVA estimate back on the host.  One run, wall clock around a synchronised
     device pipeline (the regression is a dependent chain of ~100*(E|B|+E)
-    phases, so there is no batch of independent steps to average)."""
+    phases, so there is no batch of independent steps to average).  With N
+    GPUs (C3) the same global problem is sharded by Y-path (dist.shard_spec,
+    strong scaling) and the trainer allgathers FP64 partials over NCCL; the
+    time is the max over ranks."""
+    import torch
+
+    from paper_2211_17005_b200 import dist
     from paper_2211_17005_b200 import regression as rg
 
     t = cfg.training
@@ -380,17 +386,29 @@ def learning_leg(hcva, cfg, book, ctx, args):
         cfg = hcva.parse_config(_json.dumps(j))
         book = hcva.generate_book(cfg)
     root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    spec = dist.shard_spec(cfg.paths, t.n_batches, world, rank)
+    comm = None
+    if world > 1:
+        comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
+        torch.distributed.barrier()
     ctx.synchronize()
     t0 = time.perf_counter()
-    sim = hcva.simulate_set(cfg, book, cfg.paths, cfg.replicas, root, ctx=ctx)
+    sim = hcva.simulate_set(cfg, book, spec["n_paths"], cfg.replicas, root, path_offset=spec["path_offset"],
+                            ctx=ctx, shard=spec["shard"])
     sim.labels_all(cfg.label_kind, to_host=False)
     ctx.synchronize()
     t1 = time.perf_counter()
-    models = rg.backward_learn(sim, t, cfg.label_kind)
+    models = rg.backward_learn(sim, t, cfg.label_kind, comm=comm)
     p, mean, scale, rep = models.get(1)
     t2 = time.perf_counter()
+    total, sim_s, train_s = t2 - t0, t1 - t0, t2 - t1
+    if world > 1:  # max over ranks
+        tt = torch.tensor([total, sim_s, train_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total, sim_s, train_s = (float(v) for v in tt)
+        comm.close()
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         # CPU reference of the regression: the FP64 restatement of regressor.cpp
         # (the reference's own regressor needs Eigen, absent) timed on a bounded
         # sample -- one train_base of step n on the first rows of its data --
@@ -412,9 +430,10 @@ def learning_leg(hcva, cfg, book, ctx, args):
         cpu = {"value": full, "unit": "s (extrapolated)", "cores": 1, "kind": "port",
                "sample": f"train_base of step {cfg.n_steps} on {rows} rows: {sec:.2f} s, x{cfg.paths * cfg.replicas // rows}"
                          f" rows x {steps} steps (FP64 restatement of regressor.cpp; simulation not included)"}
-    return {"value": t2 - t0, "unit": "s", "higher_is_better": False, "pricing_steps": steps, "cpu_baseline": cpu,
-            "simulate_and_labels_s": t1 - t0, "backward_learn_s": t2 - t1,
-            "sgd_steps": steps * t.epochs * t.n_batches, "rows": cfg.paths * cfg.replicas,
+    return {"value": total, "unit": "s", "higher_is_better": False, "pricing_steps": steps, "cpu_baseline": cpu,
+            "simulate_and_labels_s": sim_s, "backward_learn_s": train_s,
+            "sgd_steps": steps * t.epochs * t.n_batches, "rows": cfg.paths * cfg.replicas, "n_gpus": world,
+            "scaling": "strong (global C2 problem sharded by Y-path)" if world > 1 else None,
             "net": f"{t.hidden_layers}x{t.width} {t.activation}", "best_loss_step1": rep["best_loss"],
             "path": "hcva_simulate_set + hcva_labels_all + hcva_backward_learn (K1-K5, device resident)"}
 
