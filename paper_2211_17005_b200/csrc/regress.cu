@@ -685,7 +685,7 @@ struct Trainer {
     DeviceBuf red, gath;
 
     void set_comm(hcva_comm* c, size_t max_len) {
-        comm = (c && c->world > 1) ? c : nullptr;
+        comm = c;  // an explicit comm always takes the gather path (world 1 included)
         world = comm ? comm->world : 1;
         if (!comm) return;
         red.alloc(max_len * 8);
@@ -1258,7 +1258,7 @@ hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, i
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
             double* scale = models->scale.as<double>() + static_cast<size_t>(i - 1) * d;
-            if (world == 1) {
+            if (!comm) {
                 k_scaler<<<d, 256, 0, ctx->stream>>>(fa, mean, scale);
             } else {  // moments over every rank's paths: sums, gathered, then centred sums
                 const double Mt = static_cast<double>(sim->M) * world;
@@ -1278,7 +1278,7 @@ hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, i
                 const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));
                 tr.set_params(p.data());
                 HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
-                if (world == 1) {
+                if (!comm) {
                     k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
                 } else {
                     k_local_sum<<<1, 1024, 0, ctx->stream>>>(y, R, tr.red.as<double>());

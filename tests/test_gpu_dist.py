@@ -84,3 +84,25 @@ def test_comm_reports_rank_and_world():
     assert c.rank_world == (2, 3)
     with pytest.raises(hcva.ContractError):
         group.comm(ctx, 3)
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL transport (dlopen'ed libnccl, ncclCommInitRank, ncclAllGather on
+    the context stream) driving the gather path of the trainer with one rank:
+    same networks as the plain single-GPU run within the regression tolerance
+    (the gather path reduces losses / scaler moments in a different order)."""
+    cfg, book, M, N = _case()
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    ctx = hcva.Context(0)
+    sim = hcva.simulate_set(cfg, book, M, N, root, ctx=ctx)
+    plain = rg.backward_learn(sim, cfg.training, "defaults")
+    comm = dist.nccl_comm(ctx, 1, 0, dist.nccl_unique_id())
+    assert comm.rank_world == (0, 1)
+    viacomm = rg.backward_learn(sim, cfg.training, "defaults", comm=comm)
+    for i in range(1, cfg.n_steps + 1):
+        pp, mp, sp, rp = plain.get(i)
+        pc, mc, sc, rc = viacomm.get(i)
+        assert np.allclose(mc, mp, rtol=1e-12, atol=1e-15) and np.allclose(sc, sp, rtol=1e-12), i
+        assert rc["best_loss"] == pytest.approx(rp["best_loss"], rel=1e-3, abs=1e-12), i
+        assert np.max(np.abs(pc - pp)) <= 1e-3 * max(np.max(np.abs(pp)), 1e-12), i
+    comm.close()
