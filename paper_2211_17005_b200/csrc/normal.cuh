@@ -120,6 +120,124 @@ __device__ __forceinline__ double halley_refine(double x, double p) {
     return x - u * (1.0 - v * (1.0 - v));
 }
 
+// ---- two independent central-region draws at once (K1's Philox block yields
+// a pair): every coefficient is fetched once for both chains and the two
+// dependency chains interleave.  Same arithmetic as acklam_central +
+// halley_refine on each element (bit-identical results).
+__constant__ double kAcklamA[6] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                                   1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
+__constant__ double kAcklamB[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                                   6.680131188771972e+01,  -1.328068155288572e+01};
+
+__device__ __forceinline__ void rcp_nr2(const double (&d)[2], double (&r)[2]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        double x = rcp_approx(d[i]);
+        double e = fma(-d[i], x, 1.0);
+        x = fma(x, e, x);
+        e = fma(-d[i], x, 1.0);
+        r[i] = fma(x, e, x);
+    }
+}
+
+__device__ __forceinline__ void exp_neg2(const double (&z)[2], double (&out)[2]) {
+    const double magic = 6755399441055744.0;
+    double r[2], q[2];
+    int k[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double t = fma(z[i], 1.4426950408889634, magic);
+        const double kf = t - magic;
+        k[i] = __double2loint(t);
+        r[i] = fma(-kf, 6.93147180559945286e-01, z[i]);
+        r[i] = fma(-kf, 2.31904681384629956e-17, r[i]);
+        q[i] = kExpQ[11];
+    }
+#pragma unroll
+    for (int j = 10; j >= 0; --j) {
+        const double c = kExpQ[j];
+        q[0] = fma(q[0], r[0], c);
+        q[1] = fma(q[1], r[1], c);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) out[i] = __hiloint2double(__double2hiint(q[i]) + (k[i] << 20), __double2loint(q[i]));
+}
+
+__device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (&x)[2]) {
+    // Acklam seed (rng.cpp:103-107)
+    double q[2], r[2], num[2], den[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        q[i] = p[i] - 0.5;
+        r[i] = q[i] * q[i];
+        num[i] = kAcklamA[0];
+        den[i] = kAcklamB[0];
+    }
+#pragma unroll
+    for (int j = 1; j < 6; ++j) {
+        const double a = kAcklamA[j];
+        num[0] = num[0] * r[0] + a;
+        num[1] = num[1] * r[1] + a;
+    }
+#pragma unroll
+    for (int j = 1; j < 5; ++j) {
+        const double b = kAcklamB[j];
+        den[0] = den[0] * r[0] + b;
+        den[1] = den[1] * r[1] + b;
+    }
+    double rd[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        num[i] = num[i] * q[i];
+        den[i] = den[i] * r[i] + 1.0;
+    }
+    rcp_nr2(den, rd);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double qq = num[i] * rd[i];
+        x[i] = fma(fma(-qq, den[i], num[i]), rd[i], qq);
+    }
+    // Halley step against erfc (rng.cpp:120-127)
+    double y[2], a[2], t[2], ap2[2], rap2[2], P[2], nz[2], lo[2], E[2], den2[2], rden2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double y0 = -x[i] * kInvSqrt2;
+        y[i] = fma(fma(-y0, kSqrt2, -x[i]), kInvSqrt2, y0);
+        a[i] = fabs(y[i]);
+        ap2[i] = a[i] + 2.0;
+        den2[i] = fma(2.0, a[i], 1.0);
+    }
+    rcp_nr2(ap2, rap2);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        t[i] = (a[i] - 2.0) * rap2[i];
+        P[i] = kErfcP[21];
+        const double hi = a[i] * a[i];
+        lo[i] = fma(a[i], a[i], -hi);
+        nz[i] = -hi;
+    }
+#pragma unroll
+    for (int j = 20; j >= 0; --j) {
+        const double c = kErfcP[j];
+        P[0] = fma(P[0], t[0], c);
+        P[1] = fma(P[1], t[1], c);
+    }
+    exp_neg2(nz, E);
+    rcp_nr2(den2, rden2);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        E[i] = E[i] * (1.0 - lo[i]);
+        const double qv = E[i] * P[i] * rden2[i];
+        const double erfc = (y[i] < 0.0) ? 2.0 - qv : qv;
+        const double e = 0.5 * erfc - p[i];
+        double ri = rcp_approx(E[i]);
+        ri = fma(ri, fma(-E[i], ri, 1.0), ri);
+        const double u = e * kSqrt2Pi * ri;
+        const double v = x[i] * u * 0.5;
+        x[i] = x[i] - u * (1.0 - v * (1.0 - v));
+    }
+}
+
 __device__ __forceinline__ double normal_from_uniform(double p) {
     return halley_refine(acklam_tail(p) ? acklam_tail_seed(p) : acklam_central(p), p);
 }

@@ -190,21 +190,29 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const bool vb = b < nb;
         uint64_t w0 = 0, w1 = 0;
         if (vb) philox2x64(blk0 + b, pkey, w0, w1);
+        const double uu[2] = {u64_to_uniform(w0), u64_to_uniform(w1)};
+        bool keep[2];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
             const int j = 2 * b + hf;
             const bool v = vb && j < nn;
-            const double u = u64_to_uniform(hf ? w1 : w0);
-            const bool tail = v && acklam_tail(u);
+            const bool tail = v && acklam_tail(uu[hf]);
             const unsigned m = __ballot_sync(0xffffffffu, tail);
             if (tail) {
                 const int pos = qn + __popc(m & lanemask_lt);
                 qs[pos] = j * P + p;
-                qp[pos] = u;
+                qp[pos] = uu[hf];
             }
             qn += __popc(m);
-            if (v && !tail) zb[j * P + p] = halley_refine(acklam_central(u), u);
+            keep[hf] = v && !tail;
         }
+        // Both draws through the central transform, branch-free (a tail or
+        // invalid lane's value is simply not stored).
+        double xx[2];
+        normal_central_x2(uu, xx);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+            if (keep[hf]) zb[(2 * b + hf) * P + p] = xx[hf];
         if (qn > kQueueCap - 64 || it == iters - 1) {
             __syncwarp();
             for (int base = 0; base < qn; base += 32) {
