@@ -68,7 +68,7 @@ __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
 }
 __host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp * 4; }
 __host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
-    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 4 * 128 * 4 + 64;
+    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 8 * 128 * 4 + 64;
 }
 
 size_t tc_weight_image_bytes(int u, int dp) { return w_image_bytes(u, dp); }
@@ -83,8 +83,9 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Butterfly reduce-scatter of N (16 or 32) per-lane columns over the warp:
-// N-1 shuffles; the result is the warp's sum of column lane % N.
+// Butterfly reduce-scatter of N (8, 16 or 32) per-lane columns over the warp:
+// N-1 shuffles, then log2(32/N) more to add the lane groups; the result is
+// the warp's sum of column lane % N.
 template <int N>
 __device__ __forceinline__ float bfly_sum(float* v, int lane) {
 #pragma unroll
@@ -98,7 +99,8 @@ __device__ __forceinline__ float bfly_sum(float* v, int lane) {
         }
     }
     float s = v[0];
-    if (N < 32) s += __shfl_xor_sync(0xffffffffu, s, 16);
+#pragma unroll
+    for (int off = N; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     return s;
 }
 
@@ -163,13 +165,17 @@ __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uin
     }
 }
 
-// Column split: U/16 warpgroups share each 128-row tile, warpgroup h owning
-// columns [16h, 16h + 16) of every layer (TMEM lane quarter = warp % 4).
+// Column split: U/UH warpgroups share each 128-row tile, warpgroup h owning
+// columns [UH h, UH (h+1)) of every layer (TMEM lane quarter = warp % 4).
+#ifndef HCVA_TILE_UH
+#define HCVA_TILE_UH 8
+#endif
 template <int U>
 struct TileShape {
-    static constexpr int NS = U / 16;  // warpgroups
-    static constexpr int UH = 16;      // columns per thread
+    static constexpr int UH = HCVA_TILE_UH < U ? HCVA_TILE_UH : U;  // columns per thread
+    static constexpr int NS = U / UH;                               // warpgroups
     static constexpr int threads = 128 * NS;
+    static constexpr int warps = 4 * NS;
 };
 
 template <int U, int ACT>
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
     uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
     float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);  // [NS][128] partial output-layer sums
-    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 4 * 128);  // [0] MMA, [1] weights, [2] features
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 8 * 128);  // [0] MMA, [1] weights, [2] features
     uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -252,21 +258,22 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
         // H1 = act(D0 + b0) -> bufH (+ H1t); act'(H1) back into D0
 #pragma unroll
-        for (int c0 = cb; c0 < cb + UH; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lb + c0, v);
+        {
+            const int c0 = cb;
+            float v[UH];
+            tc::tmem_ldw<UH>(tm + lb + c0, v);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = act_f<ACT>(v[q] + vec[c0 + q]);
+            for (int q = 0; q < UH; ++q) v[q] = act_f<ACT>(v[q] + vec[c0 + q]);
 #pragma unroll
-            for (int q = 0; q < 16; q += 4)
+            for (int q = 0; q < UH; q += 4)
                 tc::put_split4(bufH, hb, r, c0 + q, 128, make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
             if (sgd) {
                 if (live)
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
+                    for (int q = 0; q < UH; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = act_d<ACT>(v[q]);
-                tc::tmem_st16(tm + lb + c0, v);
+                for (int q = 0; q < UH; ++q) v[q] = act_d<ACT>(v[q]);
+                tc::tmem_stw<UH>(tm + lb + c0, v);
             }
         }
         if (sgd) tc::tmem_wait_st();
@@ -279,13 +286,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
         mma_wait();
         float h2[UH];
+        tc::tmem_ldw<UH>(tm + lb + 64 + cb, h2);
 #pragma unroll
-        for (int c0 = 0; c0 < UH; c0 += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lb + 64 + cb + c0, v);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) h2[c0 + q] = act_f<ACT>(v[q] + vec[64 + cb + c0 + q]);
-        }
+        for (int q = 0; q < UH; ++q) h2[q] = act_f<ACT>(h2[q] + vec[64 + cb + q]);
         float f;
         {
             float fp = 0.0f;
@@ -362,15 +365,11 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
         mma_wait();
         {
-            float g[UH];
+            float g[UH], dv[UH];
+            tc::tmem_ldw<UH>(tm + lb + 128 + cb, g);
+            tc::tmem_ldw<UH>(tm + lb + cb, dv);
 #pragma unroll
-            for (int c0 = 0; c0 < UH; c0 += 16) {
-                float v[16], dv[16];
-                tc::tmem_ld16(tm + lb + 128 + cb + c0, v);
-                tc::tmem_ld16(tm + lb + cb + c0, dv);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) g[c0 + q] = live ? v[q] * dv[q] : 0.0f;
-            }
+            for (int q = 0; q < UH; ++q) g[q] = live ? g[q] * dv[q] : 0.0f;
             if (live)
 #pragma unroll
                 for (int j = 0; j < UH; ++j) a.G1t[(cb + j) * a.ld_t + trow] = g[j];
@@ -384,8 +383,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     // ---- per-CTA partials (fixed order over the warps)
     tc::fence_before_sync();
     __syncthreads();
+    constexpr int NWP = TileShape<U>::warps;
     float* part = reinterpret_cast<float*>(bufH);  // [warp][3][64]
-    double* red = reinterpret_cast<double*>(part + 16 * 3 * 64);  // [4][16 warps]
+    double* red = reinterpret_cast<double*>(part + NWP * 3 * 64);  // [4][warps]
     constexpr int NW = UH < 32 ? UH : 32;
     if (sgd && lane < NW)
 #pragma unroll
@@ -401,9 +401,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if (lane == 0) {
         red[warp] = loss;
-        red[16 + warp] = dmu;
-        red[32 + warp] = gb2;
-        red[48 + warp] = mn;
+        red[NWP + warp] = dmu;
+        red[2 * NWP + warp] = gb2;
+        red[3 * NWP + warp] = mn;
     }
     __syncthreads();
     const int cta = blockIdx.x;
@@ -421,12 +421,14 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
         if (tid == 0) {
             a.lpart[cta] = red[0] + red[1] + red[2] + red[3];  // warpgroup 0 holds the per-row terms
-            gout[a.P - 1] = static_cast<float>(red[16] + red[17] + red[18] + red[19]);
-            gout[a.off2 + U] = static_cast<float>(red[32] + red[33] + red[34] + red[35]);
+            gout[a.P - 1] = static_cast<float>(red[NWP] + red[NWP + 1] + red[NWP + 2] + red[NWP + 3]);
+            gout[a.off2 + U] =
+                static_cast<float>(red[2 * NWP] + red[2 * NWP + 1] + red[2 * NWP + 2] + red[2 * NWP + 3]);
         }
     } else if (tid == 0) {
         if (a.mode & 1) a.lpart[cta] = red[0] + red[1] + red[2] + red[3];
-        if (a.mode & 2) a.mpart[cta] = fmin(fmin(red[48], red[49]), fmin(red[50], red[51]));
+        if (a.mode & 2)
+            a.mpart[cta] = fmin(fmin(red[3 * NWP], red[3 * NWP + 1]), fmin(red[3 * NWP + 2], red[3 * NWP + 3]));
     }
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
