@@ -168,7 +168,7 @@ __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uin
 // Column split: U/UH warpgroups share each 128-row tile, warpgroup h owning
 // columns [UH h, UH (h+1)) of every layer (TMEM lane quarter = warp % 4).
 #ifndef HCVA_TILE_UH
-#define HCVA_TILE_UH 8
+#define HCVA_TILE_UH 16
 #endif
 template <int U>
 struct TileShape {
