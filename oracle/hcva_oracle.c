@@ -621,6 +621,179 @@ int or_nested_cva(const or_model* m, const or_swap* book, int n_swaps, const dou
     return rc;
 }
 
+/* --------------------------------------------- twin MC validator (f1) */
+
+/* twin_labels (labels.cpp:90-140): per outer path k two fresh market
+ * continuations from state_at(k, step) (market.cpp:100-113, log of the stored
+ * FX) with inner paths 0 / 1 from split(k).split(0); per replica l and twin t
+ * the surviving clients (default_step > step) redraw their default on the
+ * continuation with resample_continuation (defaults.cpp:47-57): one
+ * exponential per survivor from split(k).split(1).split(l).split(t), first
+ * continuation step whose hazard increment reaches it; the label sums the
+ * continuation discount times the positive exposure at that step. */
+int or_twin_labels(const or_model* m, const or_swap* book, int n_swaps, int step, int M, int N,
+                   const double* rates, const double* fx, const double* intens, const double* lagged,
+                   const uint16_t* steps, uint64_t key, double* t1, double* t2) {
+    const int n = m->n_steps, E = m->n_economies, C = m->n_clients, Cn = C + 1;
+    if (step < 0 || step > n) return fail(2, "labels: step outside the simulated grid");
+    const int h = n - step;
+    for (size_t r = 0; r < (size_t)M * N; ++r) t1[r] = t2[r] = 0.0;
+    if (h == 0) return 0;
+    const size_t rows = (size_t)2 * (h + 1);
+    double* cr = malloc(sizeof(double) * rows * E);
+    double* cf = malloc(sizeof(double) * rows * (E > 1 ? E - 1 : 1));
+    double* ci = malloc(sizeof(double) * rows * Cn);
+    double* cl = malloc(sizeof(double) * rows * E);
+    double* cd = malloc(sizeof(double) * rows);
+    double* ch = malloc(sizeof(double) * rows * Cn);
+    double* cq = malloc(sizeof(double) * rows * (C > 0 ? C : 1));
+    double* st_r = malloc(sizeof(double) * E);
+    double* st_f = malloc(sizeof(double) * (E > 1 ? E - 1 : 1));
+    double* st_i = malloc(sizeof(double) * Cn);
+    double* st_l = malloc(sizeof(double) * E);
+    int rc = 0;
+    for (int k = 0; k < M && !rc; ++k) {
+        const size_t row = (size_t)k * (n + 1) + step;
+        for (int e = 0; e < E; ++e) {
+            st_r[e] = rates[row * E + e];
+            st_l[e] = lagged[row * E + e];
+        }
+        for (int e = 1; e < E; ++e) st_f[e - 1] = log(fx[row * (E - 1) + e - 1]);
+        for (int c = 0; c < Cn; ++c) st_i[c] = intens[row * Cn + c];
+        const uint64_t pkey = or_split_key(key, (uint64_t)k);
+        rc = or_simulate_conditional(m, st_r, st_f, st_i, st_l, step, h, 2, or_split_key(pkey, 0), cr, cf, ci, cl,
+                                     cd, ch);
+        if (!rc) rc = or_build_cube(m, 2, h, step, cr, cf, cl, book, n_swaps, cq);
+        if (rc) break;
+        const uint64_t dkey = or_split_key(pkey, 1);
+        for (int l = 0; l < N; ++l) {
+            const uint64_t rkey = or_split_key(dkey, (uint64_t)l);
+            for (int t = 0; t < 2; ++t) {
+                const uint64_t tkey = or_split_key(rkey, (uint64_t)t);
+                uint64_t draw = 0;
+                double sum = 0.0;
+                for (int c = 1; c < Cn; ++c) {
+                    if (steps[((size_t)k * N + l) * Cn + c] <= step) continue; /* stays defaulted */
+                    double eps;
+                    or_exponentials(tkey, draw++, 1, &eps);
+                    const double base = ch[((size_t)t * (h + 1)) * Cn + c];
+                    int hit = -1;
+                    for (int j = 1; j <= h; ++j)
+                        if (ch[((size_t)t * (h + 1) + j) * Cn + c] - base >= eps) {
+                            hit = j;
+                            break;
+                        }
+                    if (hit >= 0) {
+                        const double mtm = cq[((size_t)t * (h + 1) + hit) * C + c - 1];
+                        const double exposure = (mtm < 0.0) ? 0.0 : mtm;
+                        sum += cd[(size_t)t * (h + 1) + hit] * exposure;
+                    }
+                }
+                (t == 0 ? t1 : t2)[(size_t)k * N + l] = sum;
+            }
+        }
+    }
+    free(cr), free(cf), free(ci), free(cl), free(cd), free(ch), free(cq);
+    free(st_r), free(st_f), free(st_i), free(st_l);
+    return rc;
+}
+
+/* clustered_std_error (validation.cpp:19-38): blocks of `block` entries. */
+static double clustered_se(const double* v, size_t n, int block) {
+    if (block <= 1 || n % (size_t)block != 0) block = 1;
+    const size_t nb = n / block;
+    if (nb < 2) return 0.0;
+    double grand = 0.0;
+    for (size_t j = 0; j < n; ++j) grand += v[j];
+    grand /= (double)n;
+    double s = 0.0;
+    for (size_t b = 0; b < nb; ++b) {
+        double bm = 0.0;
+        for (int j = 0; j < block; ++j) bm += v[b * block + j];
+        bm /= (double)block;
+        s += (bm - grand) * (bm - grand);
+    }
+    s /= (double)(nb - 1);
+    return sqrt(s / (double)nb);
+}
+
+/* twin_l2_error (validation.cpp:41-56). */
+int or_twin_l2_error(const double* pred, const double* t1, const double* t2, size_t n, int block,
+                     double* value, double* std_error) {
+    if (n == 0) return fail(2, "twin estimator: size mismatch or empty input");
+    double* terms = malloc(sizeof(double) * n);
+    double sum = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+        const double phi = pred[j];
+        terms[j] = phi * phi - (t1[j] + t2[j]) * phi + t1[j] * t2[j];
+        sum += terms[j];
+    }
+    *value = sum / (double)n;
+    *std_error = clustered_se(terms, n, block);
+    free(terms);
+    return 0;
+}
+
+/* twin_relative_rmse (validation.cpp:58-69). */
+int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2, size_t n, double* out) {
+    if (n == 0) return fail(2, "twin estimator: size mismatch or empty input");
+    double denom = 0.0;
+    for (size_t j = 0; j < n; ++j) denom += t1[j] * t2[j];
+    denom /= (double)n;
+    if (denom <= 0.0) return fail(3, "twin_relative_rmse: E[xi1 xi2] <= 0 (degenerate portfolio)");
+    double l2, se;
+    or_twin_l2_error(pred, t1, t2, n, 1, &l2, &se);
+    *out = sqrt((l2 > 0.0 ? l2 : 0.0) / denom);
+    return 0;
+}
+
+/* twin_relative_rmse_std_error (validation.cpp:71-117): delta method, clustered. */
+int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, size_t n, int block,
+                             double* out) {
+    if (n == 0) return fail(2, "twin estimator: size mismatch or empty input");
+    double* at = malloc(sizeof(double) * n);
+    double* bt = malloc(sizeof(double) * n);
+    for (size_t j = 0; j < n; ++j) {
+        const double phi = pred[j];
+        at[j] = phi * phi - (t1[j] + t2[j]) * phi + t1[j] * t2[j];
+        bt[j] = t1[j] * t2[j];
+    }
+    double ma = 0.0, mb = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+        ma += at[j];
+        mb += bt[j];
+    }
+    ma /= (double)n;
+    mb /= (double)n;
+    *out = 0.0;
+    if (block <= 1 || n % (size_t)block != 0) block = 1;
+    const size_t nb = n / block;
+    if (ma > 0.0 && mb > 0.0 && nb >= 2) {
+        double va = 0.0, vb = 0.0, cab = 0.0;
+        for (size_t b = 0; b < nb; ++b) {
+            double bma = 0.0, bmb = 0.0;
+            for (int j = 0; j < block; ++j) {
+                bma += at[b * block + j];
+                bmb += bt[b * block + j];
+            }
+            bma /= (double)block;
+            bmb /= (double)block;
+            va += (bma - ma) * (bma - ma);
+            vb += (bmb - mb) * (bmb - mb);
+            cab += (bma - ma) * (bmb - mb);
+        }
+        const double nbm1 = (double)(nb - 1) * (double)nb;
+        va /= nbm1;
+        vb /= nbm1;
+        cab /= nbm1;
+        const double rho = sqrt(ma / mb);
+        const double rel = va / (ma * ma) + vb / (mb * mb) - 2.0 * cab / (ma * mb);
+        *out = 0.5 * rho * sqrt(rel > 0.0 ? rel : 0.0);
+    }
+    free(at), free(bt);
+    return 0;
+}
+
 /* ------------------------------------------------------ timed baseline */
 #include <time.h>
 

@@ -108,6 +108,17 @@ int or_nested_cva(const or_model* m, const or_swap* book, int n_swaps, const dou
                   const int* survived, int step, int inner, uint64_t key, double* value,
                   double* std_error);
 
+/* --- twin MC validator (labels.cpp:90-140, defaults.cpp:47-57, validation.cpp:41-117) ---
+ * market / steps: the outer AoS blocks above; t1, t2 [M*N]. */
+int or_twin_labels(const or_model* m, const or_swap* book, int n_swaps, int step, int M, int N,
+                   const double* rates, const double* fx, const double* intens, const double* lagged,
+                   const uint16_t* steps, uint64_t key, double* t1, double* t2);
+int or_twin_l2_error(const double* pred, const double* t1, const double* t2, size_t n, int block,
+                     double* value, double* std_error);
+int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2, size_t n, double* out);
+int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, size_t n, int block,
+                             double* out);
+
 /* --- regression (regressor.cpp, restated in regress_oracle.c) ---
  * activation: 0 tanh, 1 sigmoid, 2 softplus, 3 relu.  Flat parameters: for
  * l = 0..hidden, W_l [fan_out][fan_in] then b_l [fan_out]; then mu. */

@@ -341,6 +341,44 @@ int or_nested_cva(const or_model* m, const or_swap* book, int n_swaps, const dou
     });
 }
 
+int or_twin_labels(const or_model* m, const or_swap* book, int n_swaps, int step, int M, int N,
+                   const double* rates, const double* fx, const double* intens, const double* lagged,
+                   const std::uint16_t* steps, std::uint64_t key, double* t1, double* t2) {
+    return guarded([&] {
+        const int n = m->n_steps, E = m->n_economies, Cn = m->n_clients + 1;
+        MarketBlock b = import_market(M, n, E, Cn, m->dt, 0, rates, fx, intens, lagged, nullptr, nullptr);
+        auto tw = twin_labels(step, to_params(m), to_grid(m), to_book(book, n_swaps), b,
+                              import_defaults(M, N, n, Cn, steps), stream_for(key));
+        std::memcpy(t1, tw.first.values.data(), sizeof(double) * tw.first.values.size());
+        std::memcpy(t2, tw.second.values.data(), sizeof(double) * tw.second.values.size());
+    });
+}
+
+int or_twin_l2_error(const double* pred, const double* t1, const double* t2, std::size_t n, int block,
+                     double* value, double* std_error) {
+    return guarded([&] {
+        EstimateWithError e = twin_l2_error(std::vector<double>(pred, pred + n), std::vector<double>(t1, t1 + n),
+                                            std::vector<double>(t2, t2 + n), block);
+        *value = e.value;
+        *std_error = e.std_error;
+    });
+}
+
+int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2, std::size_t n, double* out) {
+    return guarded([&] {
+        *out = twin_relative_rmse(std::vector<double>(pred, pred + n), std::vector<double>(t1, t1 + n),
+                                  std::vector<double>(t2, t2 + n));
+    });
+}
+
+int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, std::size_t n, int block,
+                             double* out) {
+    return guarded([&] {
+        *out = twin_relative_rmse_std_error(std::vector<double>(pred, pred + n), std::vector<double>(t1, t1 + n),
+                                            std::vector<double>(t2, t2 + n), block);
+    });
+}
+
 }  // extern "C"
 
 // Timed CPU baseline through the reference's own functions, exactly the work

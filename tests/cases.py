@@ -80,3 +80,25 @@ def oracle_model(cfg):
     return dict(rates=cfg.rates, fx=cfg.fx, credit=cfg.credit,
                 corr=None if cfg.correlation is None else cfg.correlation,
                 n_steps=cfg.n_steps, substeps=cfg.substeps, dt=cfg.dt)
+
+
+def twin_block(O, cfg, m, book, mk, st, step):
+    """twin_labels at `step` (key seed/2/4/step) and the twin estimators on a
+    fixed synthetic prediction; NaN where the reference raises numeric_error."""
+    t1, t2 = O.twin_labels(m, book, step, mk, st, O.key(cfg.seed, 2, 4, step))
+    pred = twin_prediction(t1, t2)
+    N = st.shape[1]
+    stats = []
+    for block in (1, N):
+        stats += list(O.twin_l2_error(pred, t1, t2, block))
+    try:
+        stats.append(O.twin_relative_rmse(pred, t1, t2))
+    except Exception:  # OracleError: numeric_error (degenerate E[xi1 xi2])
+        stats.append(float("nan"))
+    stats += [O.twin_relative_rmse_std_error(pred, t1, t2, b) for b in (1, N)]
+    return t1, t2, np.array(stats)
+
+
+def twin_prediction(t1, t2):
+    wiggle = 1.0 + 0.1 * np.sin(np.arange(t1.size).reshape(t1.shape))
+    return np.mean(t1) * wiggle  # a path-blind prediction: the twin L2 is then positive

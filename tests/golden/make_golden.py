@@ -19,16 +19,16 @@ import cases  # noqa: E402
 import oracle_api  # noqa: E402
 from paper_2211_17005_b200.config import parse_config  # noqa: E402
 
-# (case, M, N, label steps, feature step, nested (step, states, inner))
+# (case, M, N, label steps, feature step, nested (step, states, inner), twin step)
 SPECS = [
-    ("minimal", 64, 2, [0, 2, 4], 1, (2, 3, 16)),
-    ("c1", 48, 16, [0, 10, 25, 49, 50], 25, (5, 2, 32)),
-    ("desk_corr", 40, 8, [0, 3, 6, 12], 6, (6, 3, 24)),
-    ("c2", 12, 8, [0, 20, 50, 99, 100], 50, (50, 2, 8)),
+    ("minimal", 64, 2, [0, 2, 4], 1, (2, 3, 16), 1),
+    ("c1", 48, 16, [0, 10, 25, 49, 50], 25, (5, 2, 32), 10),
+    ("desk_corr", 40, 8, [0, 3, 6, 12], 6, (6, 3, 24), 3),
+    ("c2", 12, 8, [0, 20, 50, 99, 100], 50, (50, 2, 8), 20),
 ]
 
 
-def make(ref, name, M, N, steps, fstep, nested):
+def make(ref, name, M, N, steps, fstep, nested, tstep):
     cfg = parse_config(cases.text(name))
     m = cases.oracle_model(cfg)
     root = ref.key(cfg.seed)
@@ -53,6 +53,8 @@ def make(ref, name, M, N, steps, fstep, nested):
         vals.append(ref.nested_cva(m, book, state, surv, step, inner, ref.key(cfg.seed, 2, 3, step, s)))
     out["nested"] = np.array(vals)
     out["nested_spec"] = np.array(nested)
+    out["twin1"], out["twin2"], out["twin_stats"] = cases.twin_block(ref, cfg, m, book, mk, st, tstep)
+    out["twin_step"] = tstep
     del out["chol"]
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print(name, {k: getattr(v, "shape", None) for k, v in out.items()})

@@ -256,6 +256,46 @@ class Oracle:
         return v.value, se.value
 
 
+    # -- twin MC validator (labels.cpp:90-140, validation.cpp:41-117) -------
+    def twin_labels(self, m, book, step, market, steps, key):
+        rates = np.ascontiguousarray(market["rates"])
+        M, n1, E = rates.shape
+        fx = np.ascontiguousarray(market["fx"]) if E > 1 else np.zeros(M * n1)
+        intens = np.ascontiguousarray(market["intens"])
+        lagged = np.ascontiguousarray(market["lagged"])
+        st = np.ascontiguousarray(steps, dtype=np.uint16)
+        N = st.shape[1]
+        t1, t2 = np.zeros((M, N)), np.zeros((M, N))
+        book = np.ascontiguousarray(book, dtype=SWAP_DTYPE)
+        mm = self.model(m)
+        self._check(self.lib.or_twin_labels(C.byref(mm), book.ctypes.data_as(C.c_void_p), len(book), int(step), M, N,
+                                            _ptr(rates), _ptr(fx), _ptr(intens), _ptr(lagged),
+                                            _ptr(st, C.c_uint16), _u64(key), _ptr(t1), _ptr(t2)))
+        return t1, t2
+
+    def _triplet(self, pred, t1, t2):
+        return [np.ascontiguousarray(np.ravel(a), dtype=np.float64) for a in (pred, t1, t2)]
+
+    def twin_l2_error(self, pred, t1, t2, block=1):
+        p, a, b = self._triplet(pred, t1, t2)
+        v, se = C.c_double(), C.c_double()
+        self._check(self.lib.or_twin_l2_error(_ptr(p), _ptr(a), _ptr(b), C.c_size_t(p.size), int(block),
+                                              C.byref(v), C.byref(se)))
+        return v.value, se.value
+
+    def twin_relative_rmse(self, pred, t1, t2):
+        p, a, b = self._triplet(pred, t1, t2)
+        v = C.c_double()
+        self._check(self.lib.or_twin_relative_rmse(_ptr(p), _ptr(a), _ptr(b), C.c_size_t(p.size), C.byref(v)))
+        return v.value
+
+    def twin_relative_rmse_std_error(self, pred, t1, t2, block=1):
+        p, a, b = self._triplet(pred, t1, t2)
+        v = C.c_double()
+        self._check(self.lib.or_twin_relative_rmse_se(_ptr(p), _ptr(a), _ptr(b), C.c_size_t(p.size), int(block),
+                                                      C.byref(v)))
+        return v.value
+
     # -- regression (regressor.cpp restated) -------------------------------
     def _shape(self, d, hidden, width, activation=0):
         class S(C.Structure):

@@ -51,7 +51,7 @@ def test_rng_golden(R):
     assert np.array_equal(R.normals(R.key(7, 1, 0, 3), 0, 256), z["normal_7_1_0_3"])
 
 
-def run_case(O, name, M, N, steps, fstep, nested):
+def run_case(O, name, M, N, steps, fstep, nested, tstep=None):
     cfg = parse_config(cases.text(name))
     m = cases.oracle_model(cfg)
     root = O.key(cfg.seed)
@@ -74,6 +74,8 @@ def run_case(O, name, M, N, steps, fstep, nested):
         surv = (st[s, 0, 1:] > step).astype(np.int32)
         vals.append(O.nested_cva(m, book, state, surv, step, inner, O.key(cfg.seed, 2, 3, step, s)))
     out["nested"] = np.array(vals)
+    if tstep is not None:
+        out["twin1"], out["twin2"], out["twin_stats"] = cases.twin_block(O, cfg, m, book, mk, st, tstep)
     return out
 
 
@@ -81,9 +83,9 @@ def run_case(O, name, M, N, steps, fstep, nested):
 def test_restatement_matches_golden_bit_exact(R, name):
     z = np.load(f"{oracle_api.ROOT}/tests/golden/{name}.npz")
     got = run_case(R, name, int(z["M"]), int(z["N"]), list(z["label_steps"]), int(z["feature_step"]),
-                   tuple(int(x) for x in z["nested_spec"]))
+                   tuple(int(x) for x in z["nested_spec"]), int(z["twin_step"]))
     for key, v in got.items():
-        assert np.array_equal(v, z[key]), key
+        assert np.array_equal(v, z[key], equal_nan=key == "twin_stats"), key
 
 
 def test_restatement_matches_compiled_reference_live(R):
@@ -111,7 +113,8 @@ def test_restatement_matches_compiled_reference_live(R):
         state = dict(rates=mk["rates"][3, 2], log_fx=np.log(mk["fx"][3, 2]), intens=mk["intens"][3, 2],
                      lagged=mk["lagged"][3, 2])
         cond = O.simulate_conditional(m, state, 2, 4, 9, O.key(5, 1))
-        outs.append([book, mk, st, cube, lab, il, cond])
+        twin = cases.twin_block(O, cfg, m, book, mk, st, 3)
+        outs.append([book, mk, st, cube, lab, il, cond, twin])
     a, b = outs
     assert np.array_equal(a[0], b[0])
     for k in a[1]:
@@ -121,6 +124,7 @@ def test_restatement_matches_compiled_reference_live(R):
     assert all(np.array_equal(x, y) for x, y in zip(a[5], b[5]))
     for k in a[6]:
         assert np.array_equal(a[6][k], b[6][k]), k
+    assert all(np.array_equal(x, y, equal_nan=True) for x, y in zip(a[7], b[7]))
 
 
 def small_model(**kw):
