@@ -188,6 +188,25 @@ hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const 
                                   const int* survived, int n_states, int step, int inner,
                                   uint64_t parent_key, double* value, double* std_error);
 
+/* --- twin Monte Carlo validator ------------------------- */
+/* twin_labels (labels.cpp:90-140) at pricing step `step` of an outer set: per
+ * outer path k two market continuations from state_at(k, step) (inner paths
+ * 0/1 of split(k).split(0)), per replica l and twin t the surviving clients
+ * re-sample their default on the continuation (resample_continuation,
+ * defaults.cpp:47-57, draws from split(k).split(1).split(l).split(t)); twin1/2
+ * [M*N] row k*N+l.  `key` is the key of the reference's twin stream. */
+hcva_status hcva_twin_labels(hcva_sim* sim, const hcva_swap* book, int n_swaps, int step, uint64_t key,
+                             double* twin1, double* twin2);
+/* twin_l2_error / twin_relative_rmse / twin_relative_rmse_std_error
+ * (validation.cpp:41-117); block = paths_per_block of the clustered s.e.
+ * twin_relative_rmse fails with HCVA_ERR_NUMERIC when E[xi1 xi2] <= 0. */
+hcva_status hcva_twin_l2_error(const double* pred, const double* twin1, const double* twin2, size_t n, int block,
+                               double* value, double* std_error);
+hcva_status hcva_twin_relative_rmse(const double* pred, const double* twin1, const double* twin2, size_t n,
+                                    double* out);
+hcva_status hcva_twin_relative_rmse_se(const double* pred, const double* twin1, const double* twin2, size_t n,
+                                       int block, double* out);
+
 /* --- regression (regressor.hpp:33-139) ----------------------------------- */
 typedef struct {              /* TrainConfig, regressor.hpp:33-44 */
     int epochs;               /* >= 2, head switch at floor(epochs/2)  */

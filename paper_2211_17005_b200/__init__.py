@@ -10,11 +10,13 @@ from .config import PipelineConfig, TrainConfig, load_config, parse_config  # no
 from .engine import (  # noqa: F401
     K_BOOK, K_TRAIN_SIM, K_VALIDATION_SIM, SWAP_DTYPE, Context, RandomStream, SimulationSet,
     build_mtm_cube, cholesky, context, defaults_label, features, generate_book, intensity_label,
-    load_book_csv, nested_cva, nested_relative_rmse, par_rate, resolve_book, sample_default_block, simulate, simulate_conditional_market,
+    load_book_csv, nested_cva, nested_relative_rmse, twin_l2_error, twin_labels, twin_relative_rmse,
+    twin_relative_rmse_std_error, par_rate, resolve_book, sample_default_block, simulate, simulate_conditional_market,
     simulate_market, simulate_set, zc_price,
 )
 
 __all__ = [
+    "twin_labels", "twin_l2_error", "twin_relative_rmse", "twin_relative_rmse_std_error",
     "ConfigError", "NumericError", "ContractError", "CudaError", "PipelineConfig", "RandomStream",
     "SimulationSet", "defaults_label", "features", "intensity_label", "load_config", "parse_config",
     "simulate", "simulate_set", "simulate_market", "simulate_conditional_market",

@@ -143,6 +143,10 @@ def lib():
                             C.POINTER(C.c_int)],
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
         "hcva_backward_learn_dist": [vp, C.POINTER(TrainCfg), C.c_int, vp, C.POINTER(vp)],
+        "hcva_twin_labels": [vp, C.POINTER(Swap), C.c_int, C.c_int, u64, dptr, dptr],
+        "hcva_twin_l2_error": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr, dptr],
+        "hcva_twin_relative_rmse": [dptr, dptr, dptr, C.c_size_t, dptr],
+        "hcva_twin_relative_rmse_se": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr],
         "hcva_comm_nccl_id": [C.c_char_p],
         "hcva_comm_create_nccl": [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)],
         "hcva_group_create": [C.c_int, C.POINTER(vp)],
@@ -182,5 +186,6 @@ EXPORTED = [
     "hcva_init_network", "hcva_quadratic_loss", "hcva_train_base", "hcva_backward_learn", "hcva_models_info",
     "hcva_models_get", "hcva_predict", "hcva_models_destroy", "hcva_comm_nccl_id", "hcva_comm_create_nccl",
     "hcva_group_create", "hcva_group_destroy", "hcva_comm_create_local", "hcva_comm_info", "hcva_comm_destroy",
-    "hcva_backward_learn_dist",
+    "hcva_backward_learn_dist", "hcva_twin_labels", "hcva_twin_l2_error", "hcva_twin_relative_rmse",
+    "hcva_twin_relative_rmse_se",
 ]

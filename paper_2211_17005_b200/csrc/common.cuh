@@ -169,6 +169,7 @@ void stage(DeviceBuf& buf, const std::vector<T>& v) {
 // Launch helpers shared by the C-ABI translation units (simulate.cu).
 void check_launch(hcva_ctx* ctx);
 hcva_sim* new_sim(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid);
+hcva_sim* new_sim(hcva_ctx* ctx, const Model& model);
 void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys, const std::vector<double>& init_state,
                     int paths_per_group, uint64_t local_offset);
 void launch_market(hcva_sim* sim, uint64_t key0);

@@ -10,6 +10,7 @@
 // cube, and K6 computes the payoff per inner path and the per-state mean and
 // standard error in the reference's summation order.  States are processed in
 // batches sized to a memory budget.
+#include <algorithm>
 #include <cmath>
 #include <memory>
 
@@ -74,6 +75,59 @@ __global__ void k_nested_reduce(const double* payoff, int S, int L, const int* a
         e = sqrt((var > 0.0 ? var : 0.0) / L);
     }
     se[s] = e;
+}
+
+// ------------------------------------------------------------------ twin MC
+// twin_labels (labels.cpp:90-140): outer path k (batch-local s) has two
+// continuation paths 2s, 2s+1 in the conditional block (group s, key
+// split(k).split(0)).  Thread per (s, l): for twin t the surviving clients
+// redraw their default on continuation t with resample_continuation
+// (defaults.cpp:47-57) -- one Exp(1) per survivor, in client order, from
+// split(k).split(1).split(l).split(t) -- found by binary search over the
+// nondecreasing continuation hazard (the reference's linear scan), and the
+// label sums discount x positive exposure at the hit step in client order.
+struct TwinArgs {
+    int S, N, h, Cn, step, k0, Mc;
+    size_t R;               // outer rows M*N
+    uint64_t key;
+    const uint16_t* steps;  // outer default steps [c][k*N + l]
+    const double* hazard;   // continuation [(j*Cn + c)*Mc + kk]
+    const double* disc;     // [j*Mc + kk]
+    const double* cube;     // [(j*Cc + c-1)*Mc + kk]
+    double* t1;             // [s*N + l] (batch rows)
+    double* t2;
+};
+
+__global__ void k_twin(TwinArgs a) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= a.S * a.N) return;
+    const int s = idx / a.N, l = idx % a.N, k = a.k0 + s;
+    const int Cc = a.Cn - 1, Mc = a.Mc, h = a.h;
+    const uint64_t rkey = split_key(split_key(split_key(a.key, static_cast<uint64_t>(k)), 1), static_cast<uint64_t>(l));
+    const size_t orow = static_cast<size_t>(k) * a.N + l;
+    for (int t = 0; t < 2; ++t) {
+        const uint64_t tkey = split_key(rkey, static_cast<uint64_t>(t));
+        const int kk = 2 * s + t;
+        uint64_t draw = 0;
+        double sum = 0.0;
+        for (int c = 1; c <= Cc; ++c) {
+            if (a.steps[c * a.R + orow] <= a.step) continue;  // stays defaulted
+            const double eps = -log(u64_to_uniform(draw_u64(tkey, draw++)));
+            const double base = a.hazard[static_cast<size_t>(c) * Mc + kk];
+            int lo = 1, hi = h + 1;  // first j in [1, h] with H_j - base >= eps, h+1 if none
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (a.hazard[(static_cast<size_t>(mid) * a.Cn + c) * Mc + kk] - base >= eps) hi = mid;
+                else lo = mid + 1;
+            }
+            if (lo <= h) {
+                const double mtm = a.cube[(static_cast<size_t>(lo) * Cc + c - 1) * Mc + kk];
+                const double expo = (mtm < 0.0) ? 0.0 : mtm;
+                sum = __dadd_rn(sum, __dmul_rn(a.disc[static_cast<size_t>(lo) * Mc + kk], expo));
+            }
+        }
+        (t == 0 ? a.t1 : a.t2)[static_cast<size_t>(s) * a.N + l] = sum;
+    }
 }
 
 }  // namespace hcva
@@ -155,5 +209,88 @@ extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* mo
         }
         std::copy(val.begin(), val.end(), value);
         std::copy(err.begin(), err.end(), std_error);
+    });
+}
+
+extern "C" hcva_status hcva_twin_labels(hcva_sim* outer, const hcva_swap* book, int n_swaps, int step, uint64_t key,
+                                        double* twin1, double* twin2) {
+    return guarded([&] {
+        hcva_ctx* ctx = outer->ctx;
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (!outer->has_defaults) throw contract_error("twin_labels: simulate a default block first");
+        if (outer->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+        const Model& m = outer->model;
+        const int E = m.E, Cn = m.Cn, Cc = m.Cc, D = m.D, M = outer->M, N = outer->N, n = outer->n;
+        if (step < 0 || step > n) throw contract_error("labels: step outside the simulated grid");
+        const size_t R = static_cast<size_t>(M) * N;
+        const int h = n - step;
+        if (h == 0) {
+            std::fill(twin1, twin1 + R, 0.0);
+            std::fill(twin2, twin2 + R, 0.0);
+            return;
+        }
+        // state_at(k, step) (market.cpp:100-113) on the host: log of the stored FX
+        // with the host libm, as the reference does.
+        std::vector<double> r(static_cast<size_t>(E) * M), f(static_cast<size_t>(std::max(E - 1, 1)) * M),
+            g(static_cast<size_t>(Cn) * M), lag(static_cast<size_t>(E) * M);
+        copy_out(ctx, r.data(), outer->rates.as<double>() + static_cast<size_t>(step) * E * M, sizeof(double) * E * M);
+        if (E > 1)
+            copy_out(ctx, f.data(), outer->fx.as<double>() + static_cast<size_t>(step) * (E - 1) * M,
+                     sizeof(double) * (E - 1) * M);
+        copy_out(ctx, g.data(), outer->intens.as<double>() + static_cast<size_t>(step) * Cn * M,
+                 sizeof(double) * Cn * M);
+        if (step > 0) {
+            copy_out(ctx, lag.data(), outer->rates.as<double>() + static_cast<size_t>(step - 1) * E * M,
+                     sizeof(double) * E * M);
+        } else {
+            std::vector<double> l0(E);
+            copy_out(ctx, l0.data(), outer->lag0.as<double>(), sizeof(double) * E);
+            for (int e = 0; e < E; ++e)
+                for (int k = 0; k < M; ++k) lag[static_cast<size_t>(e) * M + k] = l0[e];
+        }
+        // Batches of outer paths by memory: 2 continuations x (h+1) steps x (3E + 2Cn + Cc) doubles.
+        const double per_path = 2.0 * (h + 1) * (3 * E + 2 * Cn + Cc) * 8.0;
+        const int batch = std::max(1, std::min(M, static_cast<int>(12e9 / per_path)));
+        for (int k0 = 0; k0 < M; k0 += batch) {
+            const int S = std::min(batch, M - k0);
+            std::unique_ptr<hcva_sim> sim(new_sim(ctx, m));
+            sim->M = 2 * S;
+            sim->n = h;
+            sim->start_step = step;
+            sim->n_groups = S;
+            std::vector<uint64_t> keys(S);
+            std::vector<double> init(static_cast<size_t>(S) * D), lg(static_cast<size_t>(S) * E);
+            for (int s = 0; s < S; ++s) {
+                const int k = k0 + s;
+                keys[s] = split_key(split_key(key, static_cast<uint64_t>(k)), 0);
+                for (int e = 0; e < E; ++e) init[s * D + e] = r[static_cast<size_t>(e) * M + k];
+                for (int e = 1; e < E; ++e) init[s * D + E + e - 1] = std::log(f[static_cast<size_t>(e - 1) * M + k]);
+                for (int c = 0; c < Cn; ++c) init[s * D + 2 * E - 1 + c] = g[static_cast<size_t>(c) * M + k];
+                for (int e = 0; e < E; ++e) lg[s * E + e] = lag[static_cast<size_t>(e) * M + k];
+            }
+            stage(sim->lag0, lg);
+            if (S == 1) {
+                prepare_market(sim.get(), {}, init, 2, 0);
+                launch_market(sim.get(), keys[0]);
+            } else {
+                prepare_market(sim.get(), keys, init, 2, 0);
+                launch_market(sim.get(), 0);
+            }
+            prepare_cube(sim.get(), book, n_swaps);
+            launch_cube(sim.get());
+            DeviceBuf d1, d2;
+            d1.alloc(sizeof(double) * S * N);
+            d2.alloc(sizeof(double) * S * N);
+            TwinArgs a{};
+            a.S = S; a.N = N; a.h = h; a.Cn = Cn; a.step = step; a.k0 = k0; a.Mc = 2 * S; a.R = R; a.key = key;
+            a.steps = outer->steps.as<uint16_t>(); a.hazard = sim->hazard.as<double>();
+            a.disc = sim->disc.as<double>(); a.cube = sim->cube.as<double>();
+            a.t1 = d1.as<double>(); a.t2 = d2.as<double>();
+            k_twin<<<grid1(static_cast<size_t>(S) * N, 128), 128, 0, ctx->stream>>>(a);
+            check_launch(ctx);
+            copy_out(ctx, twin1 + static_cast<size_t>(k0) * N, d1.p, sizeof(double) * S * N);
+            copy_out(ctx, twin2 + static_cast<size_t>(k0) * N, d2.p, sizeof(double) * S * N);
+        }
     });
 }

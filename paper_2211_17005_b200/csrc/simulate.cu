@@ -984,11 +984,15 @@ void copy_out(hcva_ctx* ctx, void* dst, const void* src, size_t bytes) {
 }
 
 hcva_sim* new_sim(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid) {
+    return new_sim(ctx, make_model(model, grid));
+}
+
+hcva_sim* new_sim(hcva_ctx* ctx, const Model& model) {
     if (!ctx) throw contract_error("null context");
     HCVA_CUDA(cudaSetDevice(ctx->device));
     auto sim = std::make_unique<hcva_sim>();
     sim->ctx = ctx;
-    sim->model = make_model(model, grid);
+    sim->model = model;
     return sim.release();
 }
 

@@ -405,6 +405,54 @@ def nested_cva(cfg: PipelineConfig, book: np.ndarray, states: Dict[str, np.ndarr
     return val, se
 
 
+def twin_labels(sim: SimulationSet, book: np.ndarray, step: int, stream: RandomStream):
+    """twin_labels (labels.cpp:90-140) of an outer set at `step`: (twin1, twin2), each (M, N).
+
+    ``stream`` is the reference's twin stream (outer path k uses stream.split(k))."""
+    bk, bp = _swaps(book)
+    t1 = np.zeros((sim.n_paths, sim.n_replicas))
+    t2 = np.zeros_like(t1)
+    _lib.check(_lib.lib().hcva_twin_labels(sim.handle, bp, len(bk), int(step), stream.key,
+                                           t1.ctypes.data_as(_lib.dptr), t2.ctypes.data_as(_lib.dptr)))
+    return t1, t2
+
+
+def _triplet(pred, t1, t2):
+    out = [np.ascontiguousarray(np.ravel(a), dtype=np.float64) for a in (pred, t1, t2)]
+    if not (out[0].size == out[1].size == out[2].size):
+        raise _lib.ContractError("twin estimator: size mismatch or empty input")
+    return out
+
+
+def twin_l2_error(predictions, twin1, twin2, paths_per_block: int = 1):
+    """twin_l2_error (validation.cpp:41-56): (value, clustered std error)."""
+    p, a, b = _triplet(predictions, twin1, twin2)
+    v, se = C.c_double(), C.c_double()
+    _lib.check(_lib.lib().hcva_twin_l2_error(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+                                             b.ctypes.data_as(_lib.dptr), p.size, int(paths_per_block),
+                                             C.byref(v), C.byref(se)))
+    return v.value, se.value
+
+
+def twin_relative_rmse(predictions, twin1, twin2) -> float:
+    """twin_relative_rmse (validation.cpp:58-69); NumericError when E[xi1 xi2] <= 0."""
+    p, a, b = _triplet(predictions, twin1, twin2)
+    v = C.c_double()
+    _lib.check(_lib.lib().hcva_twin_relative_rmse(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+                                                  b.ctypes.data_as(_lib.dptr), p.size, C.byref(v)))
+    return v.value
+
+
+def twin_relative_rmse_std_error(predictions, twin1, twin2, paths_per_block: int = 1) -> float:
+    """twin_relative_rmse_std_error (validation.cpp:71-117)."""
+    p, a, b = _triplet(predictions, twin1, twin2)
+    v = C.c_double()
+    _lib.check(_lib.lib().hcva_twin_relative_rmse_se(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+                                                     b.ctypes.data_as(_lib.dptr), p.size, int(paths_per_block),
+                                                     C.byref(v)))
+    return v.value
+
+
 def nested_relative_rmse(predictions: np.ndarray, nested: np.ndarray):
     """nested_relative_rmse (validation.cpp:181-210): (value, std_error, excluded_zero, used)."""
     pred = np.asarray(predictions, dtype=np.float64)
