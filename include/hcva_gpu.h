@@ -239,6 +239,22 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
  * defaults, 1 = intensity.  Everything stays on the GPU. */
 hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out);
 
+/* backward_learn with the Q/R probe (pipeline.cpp:79-108, regressor.cpp:328-338,
+ * collect_qr_trace): two extra replicas per path from probe_key (the
+ * reference's root.split(kTrainSim).split(2)); after every epoch of every
+ * step the current network predicts them and estimate_qr (planner.cpp:11-70)
+ * gives (Q, R).  trace [n_steps*epochs][4] = step, epoch, Q, R in training
+ * order (steps n..1, epochs 1..E).  Single GPU. */
+hcva_status hcva_backward_learn_qr(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, uint64_t probe_key,
+                                   double* trace, hcva_models** out);
+/* The probe's default block and labels alone (make_label_source's aux block):
+ * steps_out [M][2][Cn] (AoS, DefaultBlock layout), labels_out [n+1][M*2];
+ * NULL skips either. */
+hcva_status hcva_probe_block(hcva_sim* sim, uint64_t probe_key, int label_kind, uint16_t* steps_out,
+                             double* labels_out);
+/* estimate_qr (planner.cpp:11-70): out = Q, R, total, n_pairs, Q s.e., R s.e. */
+hcva_status hcva_estimate_qr(const double* g1, const double* g2, size_t n, double* out /* [6] */);
+
 /* --- multi-GPU regression -------------------------------------
  * Y-paths shard by hcva_simulate_set_sharded (rank g owns slice g of every
  * batch); each rank trains on its rows and every cross-rank sum (gradient +

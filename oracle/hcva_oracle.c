@@ -794,6 +794,61 @@ int or_twin_relative_rmse_se(const double* pred, const double* t1, const double*
     return 0;
 }
 
+/* estimate_qr (planner.cpp:11-70): R = Cov(g1, g2), total = pooled variance,
+ * Q = total - R; batch-means standard errors over min(20, n/2) batches. */
+static double qr_se(const double* v, size_t nb) {
+    double mm = 0.0;
+    for (size_t b = 0; b < nb; ++b) mm += v[b];
+    mm /= (double)nb;
+    double s = 0.0;
+    for (size_t b = 0; b < nb; ++b) s += (v[b] - mm) * (v[b] - mm);
+    s /= (double)(nb - 1);
+    return sqrt(s / (double)nb);
+}
+
+int or_estimate_qr(const double* g1, const double* g2, size_t n, double* out) {
+    if (n < 2) return fail(3, "estimate_qr: need at least two outer paths");
+    double grand = 0.0;
+    for (size_t k = 0; k < n; ++k) grand += g1[k] + g2[k];
+    grand /= (double)(2 * n);
+    double total = 0.0, r = 0.0;
+    for (size_t k = 0; k < n; ++k) {
+        const double d1 = g1[k] - grand, d2 = g2[k] - grand;
+        total += d1 * d1 + d2 * d2;
+        r += d1 * d2;
+    }
+    total /= (double)(2 * n);
+    r /= (double)n;
+    out[0] = total - r;
+    out[1] = r;
+    out[2] = total;
+    out[3] = (double)n;
+    out[4] = out[5] = 0.0;
+    const size_t nb = (n / 2 < 20) ? n / 2 : 20;
+    if (nb >= 2) {
+        double qb[20], rb[20];
+        const size_t bs = n / nb;
+        for (size_t b = 0; b < nb; ++b) {
+            double bg = 0.0;
+            for (size_t k = b * bs; k < (b + 1) * bs; ++k) bg += g1[k] + g2[k];
+            bg /= (double)(2 * bs);
+            double bt = 0.0, br = 0.0;
+            for (size_t k = b * bs; k < (b + 1) * bs; ++k) {
+                const double d1 = g1[k] - bg, d2 = g2[k] - bg;
+                bt += d1 * d1 + d2 * d2;
+                br += d1 * d2;
+            }
+            bt /= (double)(2 * bs);
+            br /= (double)bs;
+            qb[b] = bt - br;
+            rb[b] = br;
+        }
+        out[4] = qr_se(qb, nb);
+        out[5] = qr_se(rb, nb);
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------ timed baseline */
 #include <time.h>
 

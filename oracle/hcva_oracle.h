@@ -119,6 +119,9 @@ int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2
 int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, size_t n, int block,
                              double* out);
 
+/* --- Q/R probe (planner.cpp:11-70): out = q, r, total, n_pairs, q_se, r_se --- */
+int or_estimate_qr(const double* g1, const double* g2, size_t n, double* out);
+
 /* --- regression (regressor.cpp, restated in regress_oracle.c) ---
  * activation: 0 tanh, 1 sigmoid, 2 softplus, 3 relu.  Flat parameters: for
  * l = 0..hidden, W_l [fan_out][fan_in] then b_l [fan_out]; then mu. */

@@ -17,6 +17,7 @@
 #include "hiercva/market.hpp"
 #include "hiercva/portfolio.hpp"
 #include "hiercva/rng.hpp"
+#include "hiercva/planner.hpp"
 #include "hiercva/validation.hpp"
 #include "hcva_oracle.h"
 
@@ -376,6 +377,18 @@ int or_twin_relative_rmse_se(const double* pred, const double* t1, const double*
     return guarded([&] {
         *out = twin_relative_rmse_std_error(std::vector<double>(pred, pred + n), std::vector<double>(t1, t1 + n),
                                             std::vector<double>(t2, t2 + n), block);
+    });
+}
+
+int or_estimate_qr(const double* g1, const double* g2, std::size_t n, double* out) {
+    return guarded([&] {
+        QRDecomposition qr = estimate_qr(std::vector<double>(g1, g1 + n), std::vector<double>(g2, g2 + n));
+        out[0] = qr.q;
+        out[1] = qr.r;
+        out[2] = qr.total;
+        out[3] = static_cast<double>(qr.n_pairs);
+        out[4] = qr.q_std_error;
+        out[5] = qr.r_std_error;
     });
 }
 

@@ -144,6 +144,9 @@ def lib():
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
         "hcva_backward_learn_dist": [vp, C.POINTER(TrainCfg), C.c_int, vp, C.POINTER(vp)],
         "hcva_twin_labels": [vp, C.POINTER(Swap), C.c_int, C.c_int, u64, dptr, dptr],
+        "hcva_backward_learn_qr": [vp, C.POINTER(TrainCfg), C.c_int, u64, dptr, C.POINTER(vp)],
+        "hcva_probe_block": [vp, u64, C.c_int, C.POINTER(C.c_uint16), dptr],
+        "hcva_estimate_qr": [dptr, dptr, C.c_size_t, dptr],
         "hcva_twin_l2_error": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr, dptr],
         "hcva_twin_relative_rmse": [dptr, dptr, dptr, C.c_size_t, dptr],
         "hcva_twin_relative_rmse_se": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr],
@@ -187,5 +190,5 @@ EXPORTED = [
     "hcva_models_get", "hcva_predict", "hcva_models_destroy", "hcva_comm_nccl_id", "hcva_comm_create_nccl",
     "hcva_group_create", "hcva_group_destroy", "hcva_comm_create_local", "hcva_comm_info", "hcva_comm_destroy",
     "hcva_backward_learn_dist", "hcva_twin_labels", "hcva_twin_l2_error", "hcva_twin_relative_rmse",
-    "hcva_twin_relative_rmse_se",
+    "hcva_twin_relative_rmse_se", "hcva_backward_learn_qr", "hcva_probe_block", "hcva_estimate_qr",
 ]

@@ -35,6 +35,8 @@ namespace hcva {
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
 }  // namespace hcva
+#include <functional>
+
 #include "comm.cuh"
 #include "regress_tc.cuh"
 #include "tc.cuh"  // tensor-core tiles for the paper's network shape
@@ -680,6 +682,8 @@ struct Trainer {
     bool use_tc = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
     bool wimg_valid = false;  // weight image matches p32
+    const uint8_t* ximg_over = nullptr;    // evaluation on another feature image (Q/R probe)
+    std::function<void(int)> on_epoch;     // after each epoch's bookkeeping (Q/R probe)
     hcva_comm* comm = nullptr;  // multi-GPU: rank-ordered allgather of the FP64 partials
     int world = 1;
     DeviceBuf red, gath;
@@ -770,7 +774,8 @@ struct Trainer {
         TileArgs ta{};
         ta.d = n.d; ta.dp = dp; ta.act = n.act; ta.P = n.P;
         ta.off0 = n.off[0]; ta.off1 = n.off[1]; ta.off2 = n.off[2];
-        ta.wimg = wimg.as<uint8_t>(); ta.ximg = ximg.as<uint8_t>(); ta.y = y; ta.b0 = b0; ta.b1 = b1;
+        ta.wimg = wimg.as<uint8_t>(); ta.ximg = ximg_over ? ximg_over : ximg.as<uint8_t>(); ta.y = y; ta.b0 = b0;
+        ta.b1 = b1;
         ta.head = head; ta.mode = mode; ta.nb = nb;
         ta.gpart = gpart.as<float>(); ta.lpart = lpart.as<double>(); ta.mpart = mpart.as<double>(); ta.pred = pred;
         ta.H2 = h2.as<float>();
@@ -924,6 +929,7 @@ struct Trainer {
                                                  p64.as<double>(), best.as<double>(), losses_dev,
                                                  best_loss.as<double>(), best_epoch.as<int>(), flag.as<int>());
             check_launch(ctx);
+            if (on_epoch) on_epoch(e);
         }
     }
 
@@ -981,7 +987,7 @@ __global__ void k_build_x(FeatArgs a) {
                 else if (in && col < d)
                     x = static_cast<float>((state_col(a, k, col - Cc) - a.mean[col]) / a.scale[col]);
                 v[qq] = x;
-                if (in) a.Xt[col * a.ld_x + row] = x;
+                if (in && a.Xt) a.Xt[col * a.ld_x + row] = x;
             }
             tc::put_split4(tb, xb, static_cast<int>(row % 128), c, 128, make_float4(v[0], v[1], v[2], v[3]));
         }
@@ -1124,12 +1130,14 @@ void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX
 
 // Standardised features of one step (fa with mean / scale set): straight into
 // the tensor-core operand images, or into X [R][d] for the SIMT path.
-void build_features(Trainer& tr, FeatArgs fa, DeviceBuf& X, long R) {
+// With `img` (tensor-core path) the features go to that operand image only
+// (evaluation rows, e.g. the Q/R probe), not to the trainer's own.
+void build_features(Trainer& tr, FeatArgs fa, DeviceBuf& X, long R, DeviceBuf* img = nullptr) {
     hcva_ctx* ctx = tr.ctx;
     if (tr.use_tc) {
-        if (R > tr.x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
-        fa.ximg = tr.ximg.as<uint8_t>();
-        fa.Xt = tr.xt.as<float>();
+        if (!img && R > tr.x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
+        fa.ximg = img ? img->as<uint8_t>() : tr.ximg.as<uint8_t>();
+        fa.Xt = img ? nullptr : tr.xt.as<float>();
         fa.ld_x = tr.ld_x;
         fa.dp = tr.dp;
         k_build_x<<<grid1(((R + 127) / 128) * 128, 256), 256, 0, ctx->stream>>>(fa);
@@ -1216,12 +1224,26 @@ hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_
 
 // backward_learn (regressor.cpp:354-395) over a simulated set with the label
 // source of pipeline.cpp:72-111 (features_at + defaults_/intensity_label).
+static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_comm* comm,
+                                          uint64_t probe_key, double* qr_trace, hcva_models** out);
+
 hcva_status hcva_backward_learn(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_models** out) {
     return hcva_backward_learn_dist(sim, cfg, label_kind, nullptr, out);
 }
 
 hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_comm* comm,
                                      hcva_models** out) {
+    return hcva_backward_learn_ex(sim, cfg, label_kind, comm, 0, nullptr, out);
+}
+
+hcva_status hcva_backward_learn_qr(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, uint64_t probe_key,
+                                   double* trace, hcva_models** out) {
+    if (!trace) return hcva_backward_learn_ex(sim, cfg, label_kind, nullptr, 0, nullptr, out);
+    return hcva_backward_learn_ex(sim, cfg, label_kind, nullptr, probe_key, trace, out);
+}
+
+static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* cfg, int label_kind, hcva_comm* comm,
+                                          uint64_t probe_key, double* qr_trace, hcva_models** out) {
     return guarded([&] {
         hcva_ctx* ctx = sim->ctx;
         StreamScope sc__(ctx->stream);
@@ -1254,6 +1276,40 @@ hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, i
         HCVA_CUDA(cudaMemsetAsync(tr.flag.p, 0, 4, ctx->stream));
         DeviceBuf X;
         if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
+        // Q/R probe (pipeline.cpp:79-108, regressor.cpp:328-338): two extra
+        // replicas per path; after every epoch the current network (positive
+        // head) predicts both, g_t = squared errors, estimate_qr on the host.
+        const bool probe = qr_trace != nullptr;
+        if (probe && comm) throw contract_error("Q/R probe: single-GPU runs only");
+        DeviceBuf p_steps, p_labels, p_img, p_X, p_pred;
+        const long R2 = 2L * sim->M;
+        std::vector<double> p_y(R2), p_p(R2), g1(sim->M), g2(sim->M);
+        size_t trace_row = 0;
+        int cur_step = 0;
+        if (probe) {
+            probe_block(sim, probe_key, label_kind, p_steps, p_labels);
+            if (tr.use_tc) p_img.alloc(static_cast<size_t>((R2 + 127) / 128) * tc_x_tile_bytes(tr.dp));
+            else p_X.alloc(sizeof(float) * R2 * d);
+            p_pred.alloc(sizeof(double) * R2);
+            tr.on_epoch = [&](int epoch) {
+                tr.ximg_over = tr.use_tc ? p_img.as<uint8_t>() : nullptr;
+                tr.eval(p_X.as<float>(), nullptr, R2, 4, p_pred.as<double>());
+                tr.ximg_over = nullptr;
+                copy_out(ctx, p_p.data(), p_pred.p, sizeof(double) * R2);
+                for (int k = 0; k < sim->M; ++k) {
+                    const double e1 = p_p[2 * k] - p_y[2 * k], e2 = p_p[2 * k + 1] - p_y[2 * k + 1];
+                    g1[k] = e1 * e1;
+                    g2[k] = e2 * e2;
+                }
+                double qr[6];
+                estimate_qr_host(g1.data(), g2.data(), sim->M, qr);
+                double* row = qr_trace + 4 * trace_row++;
+                row[0] = cur_step;
+                row[1] = epoch;
+                row[2] = qr[0];
+                row[3] = qr[1];
+            };
+        }
         for (int i = nsteps; i >= 1; --i) {
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
@@ -1273,6 +1329,14 @@ hcva_status hcva_backward_learn_dist(hcva_sim* sim, const hcva_train_cfg* cfg, i
             fa.mean = mean;
             fa.scale = scale;
             build_features(tr, fa, X, R);
+            if (probe) {  // the probe rows, standardised with this step's scaler
+                FeatArgs fp = fa;
+                fp.N = 2;
+                fp.steps = p_steps.as<uint16_t>();
+                build_features(tr, fp, p_X, R2, &p_img);
+                copy_out(ctx, p_y.data(), p_labels.as<double>() + static_cast<size_t>(i) * R2, sizeof(double) * R2);
+                cur_step = i;
+            }
             const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
             if (i == nsteps) {
                 const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), i));

@@ -928,35 +928,45 @@ void prepare_defaults(hcva_sim* sim, int N) {
         HCVA_CUDA(cudaFuncSetAttribute(k_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
 }
 
-void launch_defaults(hcva_sim* sim, uint64_t key) {
+// K3 for N replicas of every path of sim's market into `steps` ([c][k*N+l]).
+void launch_defaults_into(hcva_sim* sim, uint64_t key, int N, uint16_t* steps, unsigned long long* ties) {
     hcva_ctx* ctx = sim->ctx;
-    HCVA_CUDA(cudaMemsetAsync(sim->ties.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    HCVA_CUDA(cudaMemsetAsync(ties, 0, 2 * sizeof(unsigned long long), ctx->stream));
     DefaultArgs a{};
-    a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = sim->model.Cn; a.path_offset = sim->path_offset; a.key = key;
+    a.M = sim->M; a.N = N; a.n = sim->n; a.Cn = sim->model.Cn; a.path_offset = sim->path_offset; a.key = key;
     a.shard_blk = sim->shard_blk; a.shard_stride = sim->shard_stride;
-    a.hazard = sim->hazard.as<double>(); a.steps = sim->steps.as<uint16_t>();
-    a.ties = sim->ties.as<unsigned long long>();
+    a.hazard = sim->hazard.as<double>(); a.steps = steps;
+    a.ties = ties;
     const size_t smem = sizeof(double) * (sim->n + 1) * sim->model.Cn;
-    const int threads = std::min(128, ((sim->N + 31) / 32) * 32);
+    const int threads = std::min(128, ((N + 31) / 32) * 32);
     k_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
     check_launch(ctx);
+}
+
+void launch_defaults(hcva_sim* sim, uint64_t key) {
+    launch_defaults_into(sim, key, sim->N, sim->steps.as<uint16_t>(), sim->ties.as<unsigned long long>());
     sim->has_defaults = true;
     sim->labels_kind = -1;
 }
 
 void launch_labels(hcva_sim* sim, int kind, int i0, int i1, double* dev_out) {
-    hcva_ctx* ctx = sim->ctx;
     if (!sim->has_defaults) throw contract_error("labels: no default block");
+    launch_labels_from(sim, kind, i0, i1, sim->steps.as<uint16_t>(), sim->N, dev_out);
+}
+
+// K4 over an arbitrary default block of sim's market (steps [c][k*N+l], N replicas).
+void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t* steps, int N, double* dev_out) {
+    hcva_ctx* ctx = sim->ctx;
     if (!sim->has_cube) throw contract_error("labels: no MtM cube");
     if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
     if (i0 < 0 || i1 > sim->n || i0 > i1) throw contract_error("label step out of range");
     const Model& m = sim->model;
     LabelArgs a{};
-    a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = m.Cn; a.E = m.E; a.dt = m.dt;
+    a.M = sim->M; a.N = N; a.n = sim->n; a.Cn = m.Cn; a.E = m.E; a.dt = m.dt;
     a.disc = sim->disc.as<double>(); a.intens = sim->intens.as<double>(); a.cube = sim->cube.as<double>();
-    a.steps = sim->steps.as<uint16_t>(); a.out = dev_out; a.i0 = i0; a.i1 = i1;
+    a.steps = steps; a.out = dev_out; a.i0 = i0; a.i1 = i1;
     const int n1 = sim->n + 1, Cc = m.Cc;
-    const int threads = std::min(128, ((sim->N + 31) / 32) * 32);
+    const int threads = std::min(128, ((N + 31) / 32) * 32);
     if (kind == 0) {
         const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc);
         if (smem > 48 * 1024)
@@ -969,6 +979,20 @@ void launch_labels(hcva_sim* sim, int kind, int i0, int i1, double* dev_out) {
         k_labels_intensity<<<sim->M, 128, smem, ctx->stream>>>(a);
     }
     check_launch(ctx);
+}
+
+// Q/R probe block (pipeline.cpp:79-81): two extra replicas per path from
+// `key` and their labels at every step, beside the set's own default block.
+void probe_block(hcva_sim* sim, uint64_t key, int kind, DeviceBuf& steps, DeviceBuf& labels) {
+    if (!sim->has_cube) throw contract_error("labels: no MtM cube");
+    if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+    const size_t R2 = static_cast<size_t>(sim->M) * 2;
+    steps.alloc(R2 * sim->model.Cn * sizeof(uint16_t));
+    labels.alloc(R2 * (sim->n + 1) * sizeof(double));
+    DeviceBuf ties;
+    ties.alloc(2 * sizeof(unsigned long long));
+    launch_defaults_into(sim, key, 2, steps.as<uint16_t>(), ties.as<unsigned long long>());
+    launch_labels_from(sim, kind, 0, sim->n, steps.as<uint16_t>(), 2, labels.as<double>());
 }
 
 void launch_labels_all(hcva_sim* sim, int kind) {
@@ -1180,6 +1204,24 @@ hcva_status hcva_sample_defaults(hcva_sim* sim, int n_replicas, uint64_t key) {
         prepare_defaults(sim, n_replicas);
         launch_defaults(sim, key);
         HCVA_CUDA(cudaStreamSynchronize(sim->ctx->stream));
+    });
+}
+
+hcva_status hcva_probe_block(hcva_sim* sim, uint64_t key, int label_kind, uint16_t* steps_out, double* labels_out) {
+    return guarded([&] {
+        StreamScope sc__(sim->ctx->stream);
+        HCVA_CUDA(cudaSetDevice(sim->ctx->device));
+        if (label_kind != 0 && label_kind != 1) throw config_error("config: label_kind must be 'defaults' or 'intensity'");
+        DeviceBuf st, lab;
+        probe_block(sim, key, label_kind, st, lab);
+        const size_t R2 = static_cast<size_t>(sim->M) * 2, Cn = sim->model.Cn;
+        if (steps_out) {
+            std::vector<uint16_t> soa(R2 * Cn);
+            copy_out(sim->ctx, soa.data(), st.p, soa.size() * 2);
+            for (size_t r = 0; r < R2; ++r)
+                for (size_t c = 0; c < Cn; ++c) steps_out[r * Cn + c] = soa[c * R2 + r];
+        }
+        if (labels_out) copy_out(sim->ctx, labels_out, lab.p, R2 * (sim->n + 1) * 8);
     });
 }
 

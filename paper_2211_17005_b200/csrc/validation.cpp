@@ -125,4 +125,69 @@ hcva_status hcva_twin_relative_rmse_se(const double* pred, const double* twin1, 
     });
 }
 
+// estimate_qr (planner.cpp:11-70): per outer path two conditionally
+// independent losses; R = Cov(g1, g2), total = pooled variance, Q = total - R,
+// batch-means standard errors over min(20, n/2) batches.
+hcva_status hcva_estimate_qr(const double* g1, const double* g2, size_t n, double* out) {
+    return guarded([&] {
+        if (!g1 || !g2) throw contract_error("estimate_qr: pair length mismatch");
+        estimate_qr_host(g1, g2, n, out);
+    });
+}
+
 }  // extern "C"
+
+void hcva::estimate_qr_host(const double* g1, const double* g2, size_t n, double* out) {
+    {
+        if (n < 2) throw numeric_error("estimate_qr: need at least two outer paths");
+        double grand = 0.0;
+        for (size_t k = 0; k < n; ++k) grand += g1[k] + g2[k];
+        grand /= static_cast<double>(2 * n);
+        double total = 0.0, r = 0.0;
+        for (size_t k = 0; k < n; ++k) {
+            const double d1 = g1[k] - grand;
+            const double d2 = g2[k] - grand;
+            total += d1 * d1 + d2 * d2;
+            r += d1 * d2;
+        }
+        total /= static_cast<double>(2 * n);
+        r /= static_cast<double>(n);
+        out[0] = total - r;
+        out[1] = r;
+        out[2] = total;
+        out[3] = static_cast<double>(n);
+        out[4] = out[5] = 0.0;
+        const size_t nb = std::min<size_t>(20, n / 2);
+        if (nb >= 2) {
+            std::vector<double> qb(nb), rb(nb);
+            const size_t bs = n / nb;
+            for (size_t b = 0; b < nb; ++b) {
+                double bgrand = 0.0;
+                for (size_t k = b * bs; k < (b + 1) * bs; ++k) bgrand += g1[k] + g2[k];
+                bgrand /= static_cast<double>(2 * bs);
+                double bt = 0.0, br = 0.0;
+                for (size_t k = b * bs; k < (b + 1) * bs; ++k) {
+                    const double d1 = g1[k] - bgrand;
+                    const double d2 = g2[k] - bgrand;
+                    bt += d1 * d1 + d2 * d2;
+                    br += d1 * d2;
+                }
+                bt /= static_cast<double>(2 * bs);
+                br /= static_cast<double>(bs);
+                qb[b] = bt - br;
+                rb[b] = br;
+            }
+            auto se = [](const std::vector<double>& v) {
+                double m = 0.0;
+                for (double x : v) m += x;
+                m /= static_cast<double>(v.size());
+                double s = 0.0;
+                for (double x : v) s += (x - m) * (x - m);
+                s /= static_cast<double>(v.size() - 1);
+                return std::sqrt(s / static_cast<double>(v.size()));
+            };
+            out[4] = se(qb);
+            out[5] = se(rb);
+        }
+    }
+}

@@ -102,19 +102,56 @@ class Models:
         return out
 
 
-def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults", comm=None) -> Models:
+def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults", comm=None,
+                   qr_probe=None) -> Models:
     """backward_learn (regressor.cpp:354-395) over the label source of make_label_source.
 
     With ``comm`` (a ``dist.Comm`` of world G) ``sim`` is this rank's interleaved
     shard (``dist.shard_spec``) and every cross-rank sum is a rank-ordered
-    allgather of FP64 partials: all ranks end with the same networks."""
+    allgather of FP64 partials: all ranks end with the same networks.
+
+    With ``qr_probe`` (the reference's probe stream, root.split(kTrainSim).split(2))
+    the Q/R trace of collect_qr_trace is recorded: ``models.qr_trace`` is an
+    array of rows (step, epoch, Q, R) in training order."""
     kind = {"defaults": 0, "intensity": 1}.get(label_kind)
     if kind is None:
         raise _lib.ConfigError("config: label_kind must be 'defaults' or 'intensity'")
     h = C.c_void_p()
+    if qr_probe is not None:
+        if comm is not None:
+            raise _lib.ContractError("Q/R probe: single-GPU runs only")
+        trace = np.zeros((sim.n_steps * t.epochs, 4))
+        _lib.check(_lib.lib().hcva_backward_learn_qr(sim.handle, C.byref(train_cfg(t)), kind, qr_probe.key,
+                                                     trace.ctypes.data_as(_lib.dptr), C.byref(h)))
+        models = Models(h, sim.ctx)
+        models.qr_trace = trace
+        return models
     _lib.check(_lib.lib().hcva_backward_learn_dist(sim.handle, C.byref(train_cfg(t)), kind,
                                                    comm.handle if comm is not None else None, C.byref(h)))
     return Models(h, sim.ctx)
+
+
+def probe_block(sim: SimulationSet, stream, label_kind: str = "defaults"):
+    """The Q/R probe's two extra replicas per path (pipeline.cpp:79-81) and their labels:
+    (steps (M, 2, Cn) uint16, labels (n+1, M, 2))."""
+    kind = {"defaults": 0, "intensity": 1}[label_kind]
+    st = np.zeros((sim.n_paths, 2, sim.n_credit), dtype=np.uint16)
+    lab = np.zeros((sim.n_steps + 1, sim.n_paths, 2))
+    _lib.check(_lib.lib().hcva_probe_block(sim.handle, stream.key, kind, st.ctypes.data_as(C.POINTER(C.c_uint16)),
+                                           lab.ctypes.data_as(_lib.dptr)))
+    return st, lab
+
+
+def estimate_qr(g1, g2) -> Dict[str, float]:
+    """estimate_qr (planner.cpp:11-70)."""
+    a = np.ascontiguousarray(g1, dtype=np.float64)
+    b = np.ascontiguousarray(g2, dtype=np.float64)
+    if a.size != b.size:
+        raise _lib.ContractError("estimate_qr: pair length mismatch")
+    out = np.zeros(6)
+    _lib.check(_lib.lib().hcva_estimate_qr(a.ctypes.data_as(_lib.dptr), b.ctypes.data_as(_lib.dptr), a.size,
+                                           out.ctypes.data_as(_lib.dptr)))
+    return dict(q=out[0], r=out[1], total=out[2], n_pairs=int(out[3]), q_std_error=out[4], r_std_error=out[5])
 
 
 def percentile_table(models: Models, validation: SimulationSet) -> Dict[int, Dict[str, float]]:

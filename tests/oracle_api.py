@@ -296,6 +296,14 @@ class Oracle:
                                                       C.byref(v)))
         return v.value
 
+    def estimate_qr(self, g1, g2):
+        """planner.cpp:11-70 -> dict(q, r, total, n_pairs, q_std_error, r_std_error)."""
+        a = np.ascontiguousarray(g1, dtype=np.float64)
+        b = np.ascontiguousarray(g2, dtype=np.float64)
+        out = np.zeros(6)
+        self._check(self.lib.or_estimate_qr(_ptr(a), _ptr(b), C.c_size_t(a.size), _ptr(out)))
+        return dict(q=out[0], r=out[1], total=out[2], n_pairs=int(out[3]), q_std_error=out[4], r_std_error=out[5])
+
     # -- regression (regressor.cpp restated) -------------------------------
     def _shape(self, d, hidden, width, activation=0):
         class S(C.Structure):
