@@ -188,6 +188,13 @@ hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const 
                                   const int* survived, int n_states, int step, int inner,
                                   uint64_t parent_key, double* value, double* std_error);
 
+/* save_market / load_market (pipeline.cpp:371-442): the HCVAMKT1 dump of a
+ * set's market block; a loaded outer block becomes a set on which defaults,
+ * cube, labels and training run (model / grid must match the dump). */
+hcva_status hcva_sim_save_market(const hcva_sim* sim, const char* path, uint64_t seed);
+hcva_status hcva_market_load(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid, const char* path,
+                             uint64_t* seed, hcva_sim** out);
+
 /* --- twin Monte Carlo validator ------------------------- */
 /* twin_labels (labels.cpp:90-140) at pricing step `step` of an outer set: per
  * outer path k two market continuations from state_at(k, step) (inner paths
@@ -284,6 +291,13 @@ hcva_status hcva_models_get(const hcva_models* m, int step, double* params, doub
 /* TrainedModelSequence::predict (regressor.cpp:349-352) on sim's features at step. */
 hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* out /* [M*N] */);
 hcva_status hcva_models_destroy(hcva_models* m);
+/* TrainedModelSequence::save / load (regressor.cpp:397-481), the HCVAMDL1
+ * format byte for byte (weights column-major as Eigen writes them).  Loaded
+ * models carry no training reports; config_hash is NUL-terminated into
+ * config_hash[hash_capacity] (NULL skips). */
+hcva_status hcva_models_save(const hcva_models* m, const char* path, uint64_t seed, const char* config_hash);
+hcva_status hcva_models_load(hcva_ctx* ctx, const char* path, uint64_t* seed, char* config_hash, int hash_capacity,
+                             hcva_models** out);
 
 /* features_at: row-major (M*N) x (p+q) FP64. */
 hcva_status hcva_features(hcva_sim* sim, int step, double* out);

@@ -119,6 +119,9 @@ int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2
 int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, size_t n, int block,
                              double* out);
 
+/* --- book CSV (portfolio.cpp:216-226); compiled reference only --- */
+int or_save_book_csv(const char* path, const or_swap* book, int n_swaps);
+
 /* --- Q/R probe (planner.cpp:11-70): out = q, r, total, n_pairs, q_se, r_se --- */
 int or_estimate_qr(const double* g1, const double* g2, size_t n, double* out);
 

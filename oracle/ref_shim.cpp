@@ -380,6 +380,10 @@ int or_twin_relative_rmse_se(const double* pred, const double* t1, const double*
     });
 }
 
+int or_save_book_csv(const char* path, const or_swap* book, int n_swaps) {
+    return guarded([&] { save_book_csv(path, to_book(book, n_swaps)); });
+}
+
 int or_estimate_qr(const double* g1, const double* g2, std::size_t n, double* out) {
     return guarded([&] {
         QRDecomposition qr = estimate_qr(std::vector<double>(g1, g1 + n), std::vector<double>(g2, g2 + n));

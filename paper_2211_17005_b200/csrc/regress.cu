@@ -35,6 +35,7 @@ namespace hcva {
 constexpr int kMaxLayers = 5;  // hidden layers <= 4
 
 }  // namespace hcva
+#include <fstream>
 #include <functional>
 
 #include "comm.cuh"
@@ -1416,6 +1417,159 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         build_features(tr, fa, X, R);
         tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
         copy_out(ctx, out, pred.p, R * 8);
+    });
+}
+
+// ---- HCVAMDL1 model files (TrainedModelSequence::save/load, regressor.cpp:397-481):
+// magic, u32 version 1, u64 seed, i32 n_steps, u32 + bytes config hash; per
+// step i32 layers (h+1), i32 activation, f64 mu, then every weight, every
+// bias, scaler mean and scale as (i64 rows, i64 cols, column-major f64).
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+void put(std::ofstream& o, T v) {
+    o.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <typename T>
+T get(std::ifstream& in) {
+    T v;
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) throw numeric_error("model file truncated");
+    return v;
+}
+constexpr char kModelMagic[8] = {'H', 'C', 'V', 'A', 'M', 'D', 'L', '1'};
+
+}  // namespace
+
+extern "C" {
+
+hcva_status hcva_models_save(const hcva_models* m, const char* path, uint64_t seed, const char* config_hash) {
+    return guarded([&] {
+        StreamScope sc__(m->ctx->stream);
+        const NetDims& n = m->n;
+        const int S = m->n_steps, d = n.d;
+        std::vector<double> p(static_cast<size_t>(S) * n.P), mean(static_cast<size_t>(S) * d), scale(mean.size());
+        copy_out(m->ctx, p.data(), m->params.p, p.size() * 8);
+        copy_out(m->ctx, mean.data(), m->mean.p, mean.size() * 8);
+        copy_out(m->ctx, scale.data(), m->scale.p, scale.size() * 8);
+        std::ofstream o(path, std::ios::binary);
+        if (!o) throw config_error(std::string("cannot write model file ") + path);
+        const std::string hash = config_hash ? config_hash : "";
+        o.write(kModelMagic, 8);
+        put<uint32_t>(o, 1u);
+        put<uint64_t>(o, seed);
+        put<int32_t>(o, S);
+        put<uint32_t>(o, static_cast<uint32_t>(hash.size()));
+        o.write(hash.data(), static_cast<std::streamsize>(hash.size()));
+        for (int s = 0; s < S; ++s) {
+            const double* q = p.data() + static_cast<size_t>(s) * n.P;
+            put<int32_t>(o, n.h + 1);
+            put<int32_t>(o, n.act);
+            put<double>(o, q[n.P - 1]);
+            for (int l = 0; l <= n.h; ++l) {
+                put<int64_t>(o, n.fout[l]);
+                put<int64_t>(o, n.fin[l]);
+                for (int c = 0; c < n.fin[l]; ++c)
+                    for (int r = 0; r < n.fout[l]; ++r) put<double>(o, q[n.off[l] + r * n.fin[l] + c]);
+            }
+            for (int l = 0; l <= n.h; ++l) {
+                put<int64_t>(o, n.fout[l]);
+                put<int64_t>(o, 1);
+                for (int r = 0; r < n.fout[l]; ++r) put<double>(o, q[n.off[l] + n.fout[l] * n.fin[l] + r]);
+            }
+            for (const std::vector<double>* v : {&mean, &scale}) {
+                put<int64_t>(o, d);
+                put<int64_t>(o, 1);
+                for (int j = 0; j < d; ++j) put<double>(o, (*v)[static_cast<size_t>(s) * d + j]);
+            }
+        }
+        if (!o) throw config_error(std::string("cannot write model file ") + path);
+    });
+}
+
+hcva_status hcva_models_load(hcva_ctx* ctx, const char* path, uint64_t* seed, char* config_hash, int hash_capacity,
+                             hcva_models** out) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw config_error(std::string("cannot open model file ") + path);
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, kModelMagic, 8) != 0) throw config_error(std::string("not a model file: ") + path);
+        if (get<uint32_t>(in) != 1u) throw config_error("unsupported model file version");
+        const uint64_t sd = get<uint64_t>(in);
+        const int S = get<int32_t>(in);
+        const uint32_t hl = get<uint32_t>(in);
+        std::string hash(hl, '\0');
+        in.read(hash.data(), hl);
+        if (!in) throw numeric_error("model file truncated");
+        if (S < 1) throw contract_error("model file: no steps");
+        auto matrix = [&](int64_t want_r, int64_t want_c, std::vector<double>& v) {
+            const int64_t r = get<int64_t>(in), c = get<int64_t>(in);
+            if ((want_r >= 0 && r != want_r) || (want_c >= 0 && c != want_c) || r < 0 || c < 0)
+                throw contract_error("model file: inconsistent network shapes");
+            v.resize(static_cast<size_t>(r * c));
+            in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(sizeof(double) * v.size()));
+            if (!in) throw numeric_error("model file truncated");
+            return std::pair<int64_t, int64_t>(r, c);
+        };
+        NetDims n{};
+        std::vector<double> params, means, scales;
+        for (int s = 0; s < S; ++s) {
+            const int layers = get<int32_t>(in), act = get<int32_t>(in);
+            const double mu = get<double>(in);
+            std::vector<std::vector<double>> W(layers), B(layers);
+            std::vector<std::pair<int64_t, int64_t>> shape(layers);
+            for (int l = 0; l < layers; ++l) shape[l] = matrix(-1, -1, W[l]);
+            if (s == 0) {
+                if (layers < 2) throw contract_error("model file: inconsistent network shapes");
+                n = make_dims(static_cast<int>(shape[0].second), layers - 1, static_cast<int>(shape[0].first), act);
+                params.assign(static_cast<size_t>(S) * n.P, 0.0);
+                means.assign(static_cast<size_t>(S) * n.d, 0.0);
+                scales.assign(means.size(), 0.0);
+            }
+            if (layers != n.h + 1 || act != n.act) throw contract_error("model file: inconsistent network shapes");
+            double* q = params.data() + static_cast<size_t>(s) * n.P;
+            for (int l = 0; l < layers; ++l) {
+                if (shape[l].first != n.fout[l] || shape[l].second != n.fin[l])
+                    throw contract_error("model file: inconsistent network shapes");
+                for (int c = 0; c < n.fin[l]; ++c)
+                    for (int r = 0; r < n.fout[l]; ++r)
+                        q[n.off[l] + r * n.fin[l] + c] = W[l][static_cast<size_t>(c) * n.fout[l] + r];
+            }
+            for (int l = 0; l < layers; ++l) {
+                matrix(n.fout[l], 1, B[l]);
+                for (int r = 0; r < n.fout[l]; ++r) q[n.off[l] + n.fout[l] * n.fin[l] + r] = B[l][r];
+            }
+            q[n.P - 1] = mu;
+            std::vector<double> v;
+            matrix(n.d, 1, v);
+            std::copy(v.begin(), v.end(), means.begin() + static_cast<size_t>(s) * n.d);
+            matrix(n.d, 1, v);
+            std::copy(v.begin(), v.end(), scales.begin() + static_cast<size_t>(s) * n.d);
+        }
+        auto models = std::make_unique<hcva_models>();
+        models->ctx = ctx;
+        models->n = n;
+        models->n_steps = S;
+        models->epochs = 0;  // reports are not part of the file
+        stage(models->params, params);
+        stage(models->mean, means);
+        stage(models->scale, scales);
+        models->losses.alloc(8);
+        stage(models->best_loss, std::vector<double>(S, 0.0));
+        stage(models->best_epoch, std::vector<int>(S, 0));
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (seed) *seed = sd;
+        if (config_hash && hash_capacity > 0) {
+            const size_t k = std::min<size_t>(hash.size(), static_cast<size_t>(hash_capacity - 1));
+            std::memcpy(config_hash, hash.data(), k);
+            config_hash[k] = '\0';
+        }
+        *out = models.release();
     });
 }
 

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <memory>
 
 #include "common.cuh"
@@ -1147,6 +1148,7 @@ hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defa
     return guarded([&] {
         StreamScope sc__(sim->ctx->stream);
         if (sim->start_step != 0 || sim->n_groups != 1) throw contract_error("rerun: outer blocks only");
+        if (!sim->m_coef.p) throw contract_error("rerun: the set was loaded, not simulated");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
         record(sim, event_slot, 0);
         launch_market(sim, key_market);
@@ -1382,6 +1384,121 @@ hcva_status hcva_features(hcva_sim* sim, int step, double* out) {
         k_features<<<grid1(R, 128), 128, 0, ctx->stream>>>(a);
         check_launch(ctx);
         copy_out(ctx, out, tmp.p, R * cols * sizeof(double));
+    });
+}
+
+// ---- HCVAMKT1 market dumps (save_market / load_market, pipeline.cpp:371-442):
+// magic, u32 version 1, u64 seed, i32 paths, steps, economies, credit names,
+// start step, f64 dt, i32 substeps, then per (k, i): rates[E], fx[E-1],
+// intensities[Cn], lagged[E], discount, hazards[Cn] (f64).
+}  // extern "C"
+
+namespace {
+constexpr char kMarketMagic[8] = {'H', 'C', 'V', 'A', 'M', 'K', 'T', '1'};
+template <typename T>
+void mput(std::ofstream& o, T v) {
+    o.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <typename T>
+T mget(std::ifstream& in) {
+    T v;
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) throw numeric_error("market dump truncated");
+    return v;
+}
+}  // namespace
+
+extern "C" {
+
+hcva_status hcva_sim_save_market(const hcva_sim* sim, const char* path, uint64_t seed) {
+    return guarded([&] {
+        const Model& m = sim->model;
+        const int M = sim->M, n1 = sim->n + 1, E = m.E, Cn = m.Cn;
+        const size_t rows = static_cast<size_t>(M) * n1;
+        std::vector<double> r(rows * E), f(rows * std::max(E - 1, 1)), g(rows * Cn), lg(rows * E), d(rows),
+            hz(rows * Cn);
+        const hcva_status st = hcva_sim_export_market(sim, r.data(), E > 1 ? f.data() : nullptr, g.data(), lg.data(),
+                                                      d.data(), hz.data());
+        if (st != HCVA_OK) throw contract_error(hcva_last_error());
+        std::ofstream o(path, std::ios::binary);
+        if (!o) throw config_error(std::string("cannot write ") + path);
+        o.write(kMarketMagic, 8);
+        mput<uint32_t>(o, 1u);
+        mput<uint64_t>(o, seed);
+        mput<int32_t>(o, M);
+        mput<int32_t>(o, sim->n);
+        mput<int32_t>(o, E);
+        mput<int32_t>(o, Cn);
+        mput<int32_t>(o, sim->start_step);
+        mput<double>(o, m.dt);
+        mput<int32_t>(o, m.substeps);
+        for (size_t row = 0; row < rows; ++row) {
+            for (int e = 0; e < E; ++e) mput(o, r[row * E + e]);
+            for (int e = 1; e < E; ++e) mput(o, f[row * (E - 1) + e - 1]);
+            for (int c = 0; c < Cn; ++c) mput(o, g[row * Cn + c]);
+            for (int e = 0; e < E; ++e) mput(o, lg[row * E + e]);
+            mput(o, d[row]);
+            for (int c = 0; c < Cn; ++c) mput(o, hz[row * Cn + c]);
+        }
+        if (!o) throw config_error(std::string("cannot write ") + path);
+    });
+}
+
+hcva_status hcva_market_load(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid, const char* path,
+                             uint64_t* seed, hcva_sim** out) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        std::unique_ptr<hcva_sim> sim(new_sim(ctx, model, grid));
+        const Model& m = sim->model;
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw config_error(std::string("cannot open ") + path);
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, kMarketMagic, 8) != 0) throw config_error(std::string("not a market dump: ") + path);
+        if (mget<uint32_t>(in) != 1u) throw config_error("unsupported market dump version");
+        const uint64_t sd = mget<uint64_t>(in);
+        const int M = mget<int32_t>(in), n = mget<int32_t>(in), E = mget<int32_t>(in), Cn = mget<int32_t>(in);
+        const int start = mget<int32_t>(in);
+        const double dt = mget<double>(in);
+        const int substeps = mget<int32_t>(in);
+        if (E != m.E || Cn != m.Cn) throw contract_error("market dump: economies / credit names differ from the model");
+        if (n != m.n_steps || dt != m.dt || substeps != m.substeps)
+            throw contract_error("market dump: time grid differs from the model's");
+        if (start != 0) throw contract_error("market dump: only outer (start step 0) blocks load into a set");
+        if (M < 1) throw contract_error("market dump: no paths");
+        const int n1 = n + 1;
+        const size_t Ms = M;
+        std::vector<double> r(static_cast<size_t>(n1) * E * Ms), f(static_cast<size_t>(n1) * std::max(E - 1, 1) * Ms),
+            g(static_cast<size_t>(n1) * Cn * Ms), hz(g.size()), d(static_cast<size_t>(n1) * Ms), lag0(E);
+        std::vector<double> lg(E);
+        for (int k = 0; k < M; ++k)
+            for (int i = 0; i < n1; ++i) {
+                for (int e = 0; e < E; ++e) r[(static_cast<size_t>(i) * E + e) * Ms + k] = mget<double>(in);
+                for (int e = 1; e < E; ++e) f[(static_cast<size_t>(i) * (E - 1) + e - 1) * Ms + k] = mget<double>(in);
+                for (int c = 0; c < Cn; ++c) g[(static_cast<size_t>(i) * Cn + c) * Ms + k] = mget<double>(in);
+                for (int e = 0; e < E; ++e) lg[e] = mget<double>(in);
+                d[static_cast<size_t>(i) * Ms + k] = mget<double>(in);
+                for (int c = 0; c < Cn; ++c) hz[(static_cast<size_t>(i) * Cn + c) * Ms + k] = mget<double>(in);
+                // Lagged rates are derived here (market.cpp:186-195): the dump's must agree.
+                for (int e = 0; e < E; ++e) {
+                    const double want = (i == 0) ? ((k == 0) ? (lag0[e] = lg[e]) : lag0[e])
+                                                 : r[(static_cast<size_t>(i - 1) * E + e) * Ms + k];
+                    if (lg[e] != want)
+                        throw contract_error("market dump: lagged rates do not follow the simulated layout");
+                }
+            }
+        sim->M = M;
+        sim->n = n;
+        sim->start_step = 0;
+        stage(sim->rates, r);
+        stage(sim->fx, f);
+        stage(sim->intens, g);
+        stage(sim->hazard, hz);
+        stage(sim->disc, d);
+        stage(sim->lag0, lag0);
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (seed) *seed = sd;
+        *out = sim.release();
     });
 }
 

@@ -151,6 +151,28 @@ def load_book_csv(path: str, cfg: PipelineConfig) -> np.ndarray:
     return np.array(rows, dtype=SWAP_DTYPE)
 
 
+def save_book_csv(path: str, book: np.ndarray) -> None:
+    """save_book_csv (portfolio.cpp:216-226): header + %d,%d,%.17g x4 rows."""
+    with open(path, "w") as f:
+        f.write("economy,client,notional,tenor,maturity,rate\n")
+        for sw in np.asarray(book, dtype=SWAP_DTYPE):
+            f.write("%d,%d,%.17g,%.17g,%.17g,%.17g\n" % (sw["economy"], sw["client"], sw["notional"], sw["tenor"],
+                                                        sw["maturity"], sw["fixed_rate"]))
+
+
+def load_market(cfg: PipelineConfig, path: str, ctx: Optional[Context] = None) -> "SimulationSet":
+    """load_market (pipeline.cpp:408-442) into a set on the GPU (HCVAMKT1); ``.seed`` set."""
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    h = C.c_void_p()
+    seed = C.c_uint64()
+    _lib.check(_lib.lib().hcva_market_load(ctx.handle, C.byref(m), C.byref(g), path.encode(), C.byref(seed),
+                                           C.byref(h)))
+    sim = SimulationSet(h, ctx)
+    sim.seed = seed.value
+    return sim
+
+
 def resolve_book(cfg: PipelineConfig) -> np.ndarray:  # pipeline.cpp:57-61
     return load_book_csv(cfg.book_file, cfg) if cfg.book_file else generate_book(cfg)
 
@@ -229,6 +251,10 @@ class SimulationSet:
         out = np.zeros((self.n_paths, self.n_steps + 1, self.n_clients))
         _lib.check(_lib.lib().hcva_sim_export_cube(self.handle, out.ctypes.data_as(C.c_void_p)))
         return out
+
+    def save_market(self, path: str, seed: int = 0) -> None:
+        """save_market (pipeline.cpp:371-406): the HCVAMKT1 dump of this set's market block."""
+        _lib.check(_lib.lib().hcva_sim_save_market(self.handle, path.encode(), seed))
 
     def tie_counts(self) -> Tuple[int, int]:
         out = (C.c_uint64 * 2)()

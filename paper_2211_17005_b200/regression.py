@@ -101,6 +101,22 @@ class Models:
         _lib.check(_lib.lib().hcva_predict(self.handle, sim.handle, step, out.ctypes.data_as(_lib.dptr)))
         return out
 
+    def save(self, path: str, seed: int = 0, config_hash: str = "") -> None:
+        """TrainedModelSequence::save (regressor.cpp:435-452): the HCVAMDL1 file."""
+        _lib.check(_lib.lib().hcva_models_save(self.handle, path.encode(), seed, config_hash.encode()))
+
+
+def load_models(path: str, ctx: Optional[Context] = None) -> Models:
+    """TrainedModelSequence::load (regressor.cpp:454-481); ``.seed`` / ``.config_hash`` set."""
+    ctx = ctx or context()
+    h = C.c_void_p()
+    seed = C.c_uint64()
+    buf = C.create_string_buffer(4096)
+    _lib.check(_lib.lib().hcva_models_load(ctx.handle, path.encode(), C.byref(seed), buf, len(buf), C.byref(h)))
+    m = Models(h, ctx)
+    m.seed, m.config_hash = seed.value, buf.value.decode()
+    return m
+
 
 def backward_learn(sim: SimulationSet, t: TrainConfig, label_kind: str = "defaults", comm=None,
                    qr_probe=None) -> Models:
