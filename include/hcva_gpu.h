@@ -195,6 +195,16 @@ hcva_status hcva_sim_save_market(const hcva_sim* sim, const char* path, uint64_t
 hcva_status hcva_market_load(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid, const char* path,
                              uint64_t* seed, hcva_sim** out);
 
+/* --- ARD variance sampling (ard.cpp:56-125) -------------- */
+/* prior[6] = vol_lo, vol_hi, level_lo, level_hi, speed_lo, speed_hi (ArdPrior);
+ * n_dgp parameter draws from key.split(0) (rejected draws redrawn, count in
+ * *rejected), draw d simulated from key.split(1).split(d) with one replica;
+ * v_x [n_dgp][Cc], v_y [n_dgp][2E-1+Cc], v_xi [n_dgp] (VarianceSample). */
+hcva_status hcva_ard_sample_variances(hcva_ctx* ctx, const hcva_model* base, const hcva_grid* grid,
+                                      const hcva_swap* book, int n_swaps, const double* prior, int n_dgp,
+                                      int paths_per_dgp, uint64_t key, double* v_x, double* v_y, double* v_xi,
+                                      int* rejected);
+
 /* --- twin Monte Carlo validator ------------------------- */
 /* twin_labels (labels.cpp:90-140) at pricing step `step` of an outer set: per
  * outer path k two market continuations from state_at(k, step) (inner paths

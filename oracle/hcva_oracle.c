@@ -849,6 +849,125 @@ int or_estimate_qr(const double* g1, const double* g2, size_t n, double* out) {
     return 0;
 }
 
+/* -------------------------------------------- ARD sampling (f4) */
+
+/* time_averaged_variance (ard.cpp:37-52): values[k*(n+1)+i]. */
+static double ta_var(const double* v, int M, int n) {
+    double acc = 0.0;
+    for (int i = 0; i <= n; ++i) {
+        double mm = 0.0;
+        for (int k = 0; k < M; ++k) mm += v[(size_t)k * (n + 1) + i];
+        mm /= M;
+        double var = 0.0;
+        for (int k = 0; k < M; ++k) {
+            const double d = v[(size_t)k * (n + 1) + i] - mm;
+            var += d * d;
+        }
+        acc += var / M;
+    }
+    return acc / (n + 1);
+}
+
+/* sample_variances (ard.cpp:56-125): prior = vol_lo, vol_hi, level_lo,
+ * level_hi, speed_lo, speed_hi (ArdPrior); draws from key.split(0) with
+ * rejection; draw d simulates from key.split(1).split(d) with one replica;
+ * v_x [n_dgp][Cc], v_y [n_dgp][2E-1+Cc], v_xi [n_dgp]. */
+int or_ard_sample_variances(const or_model* base, const or_swap* book, int n_swaps, const double* prior, int n_dgp,
+                            int paths, uint64_t key, double* v_x, double* v_y, double* v_xi, int* rejected) {
+    int rc = validate_model(base);
+    if (rc) return rc;
+    if (n_dgp < 1 || paths < 2) return fail(1, "ard: need n_dgp >= 1 and paths >= 2");
+    const int E = base->n_economies, C = base->n_clients, Cn = C + 1, n = base->n_steps, M = paths;
+    const int nf = 2 * E - 1 + C;
+    const uint64_t pkey = or_split_key(key, 0);
+    uint64_t draw = 0;
+#define UNIF(lo, hi) ((lo) + ((hi) - (lo)) * u64_to_uniform(draw_u64(pkey, draw++)))
+    double* pr = malloc(sizeof(double) * (size_t)n_dgp * 4 * E);
+    double* pf = malloc(sizeof(double) * (size_t)n_dgp * 3 * (E > 1 ? E - 1 : 1));
+    double* pc = malloc(sizeof(double) * (size_t)n_dgp * 4 * Cn);
+    int have = 0, rej = 0;
+    while (have < n_dgp) {
+        double* r = pr + (size_t)have * 4 * E;
+        double* f = pf + (size_t)have * 3 * (E > 1 ? E - 1 : 1);
+        double* c = pc + (size_t)have * 4 * Cn;
+        memcpy(r, base->rates, sizeof(double) * 4 * E);
+        if (E > 1) memcpy(f, base->fx, sizeof(double) * 3 * (E - 1));
+        memcpy(c, base->credit, sizeof(double) * 4 * Cn);
+        for (int e = 0; e < E; ++e) {
+            r[4 * e + 0] *= UNIF(prior[4], prior[5]);
+            r[4 * e + 1] *= UNIF(prior[2], prior[3]);
+            r[4 * e + 2] *= UNIF(prior[0], prior[1]);
+        }
+        for (int e = 0; e + 1 < E; ++e) f[3 * e] *= UNIF(prior[0], prior[1]);
+        for (int k = 0; k < Cn; ++k) {
+            c[4 * k + 0] *= UNIF(prior[4], prior[5]);
+            c[4 * k + 1] *= UNIF(prior[2], prior[3]);
+            c[4 * k + 2] *= UNIF(prior[0], prior[1]);
+            c[4 * k + 3] *= UNIF(prior[2], prior[3]);
+        }
+        or_model nu = *base;
+        nu.rates = r;
+        nu.fx = f;
+        nu.credit = c;
+        if (validate_model(&nu)) {
+            ++rej;
+            continue;
+        }
+        ++have;
+    }
+#undef UNIF
+    if (rejected) *rejected = rej;
+    const size_t rows = (size_t)M * (n + 1);
+    double* rates = malloc(sizeof(double) * rows * E);
+    double* fx = malloc(sizeof(double) * rows * (E > 1 ? E - 1 : 1));
+    double* intens = malloc(sizeof(double) * rows * Cn);
+    double* lagged = malloc(sizeof(double) * rows * E);
+    double* disc = malloc(sizeof(double) * rows);
+    double* hazard = malloc(sizeof(double) * rows * Cn);
+    double* cube = malloc(sizeof(double) * rows * (C > 0 ? C : 1));
+    uint16_t* steps = malloc(sizeof(uint16_t) * (size_t)M * Cn);
+    double* buf = malloc(sizeof(double) * rows);
+    double* lab = malloc(sizeof(double) * M);
+    for (int d = 0; d < n_dgp && !rc; ++d) {
+        or_model nu = *base;
+        nu.rates = pr + (size_t)d * 4 * E;
+        nu.fx = pf + (size_t)d * 3 * (E > 1 ? E - 1 : 1);
+        nu.credit = pc + (size_t)d * 4 * Cn;
+        const uint64_t skey = or_split_key(or_split_key(key, 1), (uint64_t)d);
+        rc = or_simulate_market(&nu, M, or_split_key(skey, 0), rates, fx, intens, lagged, disc, hazard);
+        if (!rc) rc = or_sample_defaults(M, n, Cn, hazard, 1, or_split_key(skey, 1), steps);
+        if (!rc) rc = or_build_cube(&nu, M, n, 0, rates, fx, lagged, book, n_swaps, cube);
+        if (rc) break;
+        for (int c = 1; c <= C; ++c) {
+            for (int k = 0; k < M; ++k)
+                for (int i = 0; i <= n; ++i) buf[(size_t)k * (n + 1) + i] = steps[(size_t)k * Cn + c] <= i ? 1.0 : 0.0;
+            v_x[(size_t)d * C + c - 1] = ta_var(buf, M, n);
+        }
+        double* vy = v_y + (size_t)d * nf;
+        int col = 0;
+        for (int e = 0; e < E; ++e) {
+            for (size_t r = 0; r < rows; ++r) buf[r] = rates[r * E + e];
+            vy[col++] = ta_var(buf, M, n);
+        }
+        for (int e = 1; e < E; ++e) {
+            for (size_t r = 0; r < rows; ++r) buf[r] = fx[r * (E - 1) + e - 1];
+            vy[col++] = ta_var(buf, M, n);
+        }
+        for (int c = 1; c <= C; ++c) {
+            for (size_t r = 0; r < rows; ++r) buf[r] = intens[r * Cn + c];
+            vy[col++] = ta_var(buf, M, n);
+        }
+        for (int i = 0; i <= n && !rc; ++i) {
+            rc = or_defaults_label(i, M, n, E, Cn, 1, base->dt, disc, intens, steps, cube, lab);
+            for (int k = 0; k < M; ++k) buf[(size_t)k * (n + 1) + i] = lab[k];
+        }
+        v_xi[d] = ta_var(buf, M, n);
+    }
+    free(pr), free(pf), free(pc), free(rates), free(fx), free(intens), free(lagged), free(disc), free(hazard);
+    free(cube), free(steps), free(buf), free(lab);
+    return rc;
+}
+
 /* ------------------------------------------------------ timed baseline */
 #include <time.h>
 

@@ -119,6 +119,12 @@ int or_twin_relative_rmse(const double* pred, const double* t1, const double* t2
 int or_twin_relative_rmse_se(const double* pred, const double* t1, const double* t2, size_t n, int block,
                              double* out);
 
+/* --- ARD sampling (ard.cpp:56-125; the reference's ard.cpp needs Eigen, so
+ * this restatement is pinned through its parts: simulate / defaults / cube /
+ * labels above, time_averaged_variance and perturb restated) --- */
+int or_ard_sample_variances(const or_model* base, const or_swap* book, int n_swaps, const double* prior, int n_dgp,
+                            int paths, uint64_t key, double* v_x, double* v_y, double* v_xi, int* rejected);
+
 /* --- book CSV (portfolio.cpp:216-226); compiled reference only --- */
 int or_save_book_csv(const char* path, const or_swap* book, int n_swaps);
 

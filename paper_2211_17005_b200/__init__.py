@@ -11,7 +11,7 @@ from .engine import (  # noqa: F401
     K_BOOK, K_TRAIN_SIM, K_VALIDATION_SIM, SWAP_DTYPE, Context, RandomStream, SimulationSet,
     build_mtm_cube, cholesky, context, defaults_label, features, generate_book, intensity_label,
     load_book_csv, nested_cva, nested_relative_rmse, twin_l2_error, twin_labels, twin_relative_rmse,
-    twin_relative_rmse_std_error, load_market, save_book_csv, par_rate, resolve_book, sample_default_block, simulate, simulate_conditional_market,
+    twin_relative_rmse_std_error, load_market, save_book_csv, ard_sample_variances, par_rate, resolve_book, sample_default_block, simulate, simulate_conditional_market,
     simulate_market, simulate_set, zc_price,
 )
 

@@ -479,6 +479,28 @@ def twin_relative_rmse_std_error(predictions, twin1, twin2, paths_per_block: int
     return v.value
 
 
+ARD_PRIOR = dict(vol_lo=0.5, vol_hi=1.5, level_lo=0.5, level_hi=2.0, speed_lo=0.5, speed_hi=1.5)  # ard.hpp:23-27
+
+
+def ard_sample_variances(cfg: PipelineConfig, book: np.ndarray, n_dgp: int, paths_per_dgp: int,
+                         stream: RandomStream, prior: Optional[Dict[str, float]] = None,
+                         ctx: Optional[Context] = None) -> Dict[str, object]:
+    """sample_variances (ard.cpp:56-125): per prior draw the time-averaged variances of the
+    default indicators (v_x), market factors (v_y) and defaults labels (v_xi)."""
+    ctx = ctx or context()
+    m, g = cfg.to_model()
+    pr = dict(ARD_PRIOR, **(prior or {}))
+    pv = np.array([pr[k] for k in ("vol_lo", "vol_hi", "level_lo", "level_hi", "speed_lo", "speed_hi")])
+    bk, bp = _swaps(book)
+    C_, E = cfg.n_clients, cfg.n_economies
+    vx, vy, vxi = np.zeros((n_dgp, C_)), np.zeros((n_dgp, 2 * E - 1 + C_)), np.zeros(n_dgp)
+    rej = C.c_int()
+    d = lambda a: a.ctypes.data_as(_lib.dptr)  # noqa: E731
+    _lib.check(_lib.lib().hcva_ard_sample_variances(ctx.handle, C.byref(m), C.byref(g), bp, len(bk), d(pv), n_dgp,
+                                                    paths_per_dgp, stream.key, d(vx), d(vy), d(vxi), C.byref(rej)))
+    return dict(v_x=vx, v_y=vy, v_xi=vxi, rejected=rej.value)
+
+
 def nested_relative_rmse(predictions: np.ndarray, nested: np.ndarray):
     """nested_relative_rmse (validation.cpp:181-210): (value, std_error, excluded_zero, used)."""
     pred = np.asarray(predictions, dtype=np.float64)

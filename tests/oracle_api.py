@@ -296,6 +296,19 @@ class Oracle:
                                                       C.byref(v)))
         return v.value
 
+    def ard_sample_variances(self, m, book, prior, n_dgp, paths, key):
+        C_ = len(m["credit"]) - 1
+        E = len(m["rates"])
+        vx, vy, vxi = np.zeros((n_dgp, C_)), np.zeros((n_dgp, 2 * E - 1 + C_)), np.zeros(n_dgp)
+        rej = C.c_int()
+        pv = np.ascontiguousarray(prior, dtype=np.float64)
+        book = np.ascontiguousarray(book, dtype=SWAP_DTYPE)
+        mm = self.model(m)
+        self._check(self.lib.or_ard_sample_variances(C.byref(mm), book.ctypes.data_as(C.c_void_p), len(book),
+                                                     _ptr(pv), n_dgp, paths, _u64(key), _ptr(vx), _ptr(vy),
+                                                     _ptr(vxi), C.byref(rej)))
+        return dict(v_x=vx, v_y=vy, v_xi=vxi, rejected=rej.value)
+
     def estimate_qr(self, g1, g2):
         """planner.cpp:11-70 -> dict(q, r, total, n_pairs, q_std_error, r_std_error)."""
         a = np.ascontiguousarray(g1, dtype=np.float64)
