@@ -232,20 +232,32 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         return (nb + TPP - 1) / TPP;
     };
 
-    // Recursion: substep t of chunk c for the factors this thread owns.
+    // Recursion: substep t of chunk c for the factors this thread owns.  The
+    // Cholesky rows of the owned factors live in registers (<= 2 nonzeros:
+    // two coefficients and tile offsets; dense rows read the CSR in smem).
+    struct ZRow {
+        double v0, v1;
+        int o0, o1, d;
+        bool dense;
+    };
+    auto zrow = [&](int d) {
+        const FactorCoef& k = coef[d];
+        return ZRow{k.v0, k.v1, k.col0 * P, k.col1 * P, d, k.dense != 0};
+    };
+    const ZRow zr_a = zrow(econ ? fr : fg0), zr_b = zrow(econ ? 0 : fg1), zr_c = zrow(econ ? fx : fg1);
+    int sub_ctr = a.substeps, next_store = 1;  // countdown to the next pricing step
     auto rec_step = [&](int cc, int t) {
         const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
-        auto zcorr = [&](int d) {
-            const FactorCoef& k = coef[d];
-            if (!k.dense) return dadd(dmul(k.v0, zt[k.col0 * P]), dmul(k.v1, zt[k.col1 * P]));
+        auto zcorr = [&](const ZRow& k) {
+            if (!k.dense) return dadd(dmul(k.v0, zt[k.o0]), dmul(k.v1, zt[k.o1]));
             double acc = 0.0;
-            for (int q = chol_row[d]; q < chol_row[d + 1]; ++q)
+            for (int q = chol_row[k.d]; q < chol_row[k.d + 1]; ++q)
                 acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
             return acc;
         };
         if (econ) {
             const double r0 = s1, re = s0;
-            const double zr = zcorr(fr), z0 = zcorr(0), zx = zcorr(fx);
+            const double zr = zcorr(zr_a), z0 = zcorr(zr_b), zx = zcorr(zr_c);
             s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
             // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
             const FactorCoef& kx = coef[fx];
@@ -254,7 +266,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             s1 = vasicek_step(r0, coef[0], h, z0);
         } else {
             // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
-            const double z0 = zcorr(fg0), z1 = zcorr(fg1);
+            const double z0 = zcorr(zr_a), z1 = zcorr(zr_b);
             const FactorCoef& k0 = coef[fg0];
             const FactorCoef& k1 = coef[fg1];
             s2 = dadd(s2, dmul(s0, h));
@@ -267,8 +279,10 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             s0 = (nx0 < 0.0) ? 0.0 : nx0;
             s1 = (nx1 < 0.0) ? 0.0 : nx1;
         }
-        const int s_done = cc * T + t + 1;
-        if (s_done % a.substeps == 0) store(s_done / a.substeps);
+        if (--sub_ctr == 0) {
+            store(next_store++);
+            sub_ctr = a.substeps;
+        }
     };
 
     // Software pipeline: generation of chunk c+1 (into the other buffer) is
