@@ -183,14 +183,29 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     // are queued per warp (ballot + popc) and refined by full warps at the end
     // of the chunk, so the log/sqrt branch does not serialise ~80% of warps.
     // it, iters and qn are warp-uniform.
-    auto gen_iter = [&](int cc, int it, int iters, int& qn) {
-        double* zb = zs + (cc & 1) * (T * D * P);
-        const int nn = min(T, total_sub - cc * T) * D, nb = (nn + 1) >> 1;
-        const uint64_t blk0 = (static_cast<uint64_t>(cc) * T * D) >> 1;
+    // Per-chunk constants of the generator (hoisted out of the iterations).
+    struct GenChunk {
+        double* zb;         // the chunk's tile
+        uint32_t zb_s;      // its shared-space address
+        int nn, nb;         // draws and Philox blocks of the chunk
+        uint64_t blk0;      // first block
+    };
+    auto gen_chunk = [&](int cc) {
+        GenChunk g;
+        g.zb = zs + (cc & 1) * (T * D * P);
+        g.zb_s = static_cast<uint32_t>(__cvta_generic_to_shared(g.zb));
+        g.nn = min(T, total_sub - cc * T) * D;
+        g.nb = (g.nn + 1) >> 1;
+        g.blk0 = (static_cast<uint64_t>(cc) * T * D) >> 1;
+        return g;
+    };
+    auto gen_iter = [&](const GenChunk& g, int it, int iters, int& qn) {
+        double* zb = g.zb;
+        const int nn = g.nn;
         const int b = w + it * TPP;
-        const bool vb = b < nb;
-        uint64_t w0 = 0, w1 = 0;
-        if (vb) philox2x64(blk0 + b, pkey, w0, w1);
+        const bool vb = b < g.nb;
+        uint64_t w0, w1;
+        philox2x64(g.blk0 + b, pkey, w0, w1);  // past the chunk's last block the draws are discarded
         const double uu[2] = {u64_to_uniform(w0), u64_to_uniform(w1)};
         bool keep[2];
 #pragma unroll
@@ -211,9 +226,15 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         // invalid lane's value is simply not stored).
         double xx[2];
         normal_central_x2(uu, xx);
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf)
-            if (keep[hf]) zb[(2 * b + hf) * P + p] = xx[hf];
+        const uint32_t sa = g.zb_s + static_cast<uint32_t>((2 * b * P + p) * 8);
+        asm volatile(
+            "{\n\t.reg .pred q0, q1;\n\t"
+            "setp.ne.b32 q0, %2, 0;\n\t"
+            "setp.ne.b32 q1, %4, 0;\n\t"
+            "@q0 st.shared.f64 [%0], %1;\n\t"
+            "@q1 st.shared.f64 [%0+%5], %3;\n\t}" ::"r"(sa),
+            "d"(xx[0]), "r"(static_cast<int>(keep[0])), "d"(xx[1]), "r"(static_cast<int>(keep[1])), "n"(P * 8)
+            : "memory");
         if (qn > kQueueCap - 64 || it == iters - 1) {
             __syncwarp();
             for (int base = 0; base < qn; base += 32) {
@@ -292,7 +313,8 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     if (do_gen) {
         int qn = 0;
         const int iters = gen_iters(0);
-        for (int it = 0; it < iters; ++it) gen_iter(0, it, iters, qn);
+        const GenChunk g0 = gen_chunk(0);
+        for (int it = 0; it < iters; ++it) gen_iter(g0, it, iters, qn);
     }
     __syncthreads();
     for (int c = 0; c < n_chunks; ++c) {
@@ -300,8 +322,9 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const int tc = min(T, total_sub - c * T);
         const int steps = max(iters, tc);
         int qn = 0;
+        const GenChunk gn = gen_chunk(c + 1);
         for (int s = 0; s < steps; ++s) {
-            if (s < iters) gen_iter(c + 1, s, iters, qn);
+            if (s < iters) gen_iter(gn, s, iters, qn);
             if (s < tc && do_rec) rec_step(c, s);
         }
         __syncthreads();
