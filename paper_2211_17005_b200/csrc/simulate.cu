@@ -579,6 +579,57 @@ __global__ void __launch_bounds__(128) k_labels_defaults(LabelArgs a) {
     }
 }
 
+// Register form for Cc <= CMAX: each replica's default steps, the discount at
+// its default step and the exposure there are loop invariants over the label
+// step i, so per (i, c) only (inv_i * beta_s) * exposure remains -- the same
+// rounded products, summed in client order.
+template <int CMAX>
+__global__ void __launch_bounds__(128) k_labels_defaults_reg(LabelArgs a) {
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cc = a.Cn - 1;
+    double* disc = sm;             // [n1]
+    double* inv = sm + n1;         // [n1]
+    double* expo = sm + 2 * n1;    // [n1][Cc]
+    for (int t = threadIdx.x; t < n1; t += blockDim.x) {
+        disc[t] = a.disc[static_cast<size_t>(t) * a.M + k];
+        inv[t] = 1.0 / disc[t];
+    }
+    for (int t = threadIdx.x; t < n1 * Cc; t += blockDim.x) {
+        const int i = t / Cc, c = t % Cc;
+        const double v = a.cube[(static_cast<size_t>(i) * Cc + c) * a.M + k];
+        expo[t] = (v < 0.0) ? 0.0 : v;
+    }
+    __syncthreads();
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
+        const size_t row = static_cast<size_t>(k) * a.N + l;
+        int st[CMAX];
+        double ds[CMAX], ex[CMAX];
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) {
+            st[c] = -1;
+            ds[c] = ex[c] = 0.0;
+            if (c < Cc) {
+                const int s = a.steps[(c + 1) * R + row];
+                if (s <= a.n) {
+                    st[c] = s;
+                    ds[c] = disc[s];
+                    ex[c] = expo[s * Cc + c];
+                }
+            }
+        }
+        for (int i = a.i0; i <= a.i1; ++i) {
+            const double vi = inv[i];
+            double sum = 0.0;
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+                if (st[c] > i) sum = __dadd_rn(sum, __dmul_rn(__dmul_rn(vi, ds[c]), ex[c]));
+            a.out[static_cast<size_t>(i - a.i0) * R + row] = sum;
+        }
+    }
+}
+
 // Intensity labels (labels.cpp:50-88).  Phase 1: survivor values per
 // (step, client) in the reference's loop order; phase 2: per replica sum over
 // surviving clients.
@@ -1009,7 +1060,19 @@ void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t*
         const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc);
         if (smem > 48 * 1024)
             HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        k_labels_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
+        if (Cc <= 8) {
+            if (smem > 48 * 1024)
+                HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_reg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem)));
+            k_labels_defaults_reg<8><<<sim->M, threads, smem, ctx->stream>>>(a);
+        } else if (Cc <= 16) {
+            if (smem > 48 * 1024)
+                HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_reg<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem)));
+            k_labels_defaults_reg<16><<<sim->M, threads, smem, ctx->stream>>>(a);
+        } else {
+            k_labels_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
+        }
     } else {
         const size_t smem = sizeof(double) * (n1 + 3 * static_cast<size_t>(n1) * Cc);
         if (smem > 48 * 1024)
