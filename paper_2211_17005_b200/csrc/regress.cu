@@ -743,6 +743,7 @@ struct Trainer {
         gram_parts = std::max(eval_ctas, 4 * ctx->sm_count);
         gram.alloc(static_cast<size_t>(gram_parts) * (mm * (mm + 1) / 2 + mm) * 8);
         flag.alloc(4);
+        HCVA_CUDA(cudaMemsetAsync(flag.p, 0, 4, ctx->stream));  // pool memory is not zeroed
         best_loss.alloc(8);
         best_epoch.alloc(4);
     }
