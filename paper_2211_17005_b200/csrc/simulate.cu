@@ -386,12 +386,27 @@ __global__ void __launch_bounds__(128) k_mtm_linear(MtmArgs a) {
                     v[c] = 0.0;
                 }
             }
-            for (int m = 1; g + m <= a.n_total; ++m) {
-                const double z = exp(lnA[m] - B[m] * r);
-                const double* h = a.H + (static_cast<size_t>(e) * n1 + g + m) * Cc + c0;
+            if (CB % 2 == 0 && Cc % 2 == 0) {  // 16-byte loads of the (warp-uniform) H rows
+                for (int m = 1; g + m <= a.n_total; ++m) {
+                    const double z = exp_neg(lnA[m] - B[m] * r);  // Cody-Waite exp, |arg| << 708
+                    const double2* h =
+                        reinterpret_cast<const double2*>(a.H + (static_cast<size_t>(e) * n1 + g + m) * Cc + c0);
 #pragma unroll
-                for (int c = 0; c < CB; ++c)
-                    if (c0 + c < Cc) v[c] -= z * __ldg(h + c);
+                    for (int c = 0; c < CB; c += 2)
+                        if (c0 + c < Cc) {
+                            const double2 hv = __ldg(h + c / 2);
+                            v[c] -= z * hv.x;
+                            v[c + 1] -= z * hv.y;
+                        }
+                }
+            } else {
+                for (int m = 1; g + m <= a.n_total; ++m) {
+                    const double z = exp_neg(lnA[m] - B[m] * r);
+                    const double* h = a.H + (static_cast<size_t>(e) * n1 + g + m) * Cc + c0;
+#pragma unroll
+                    for (int c = 0; c < CB; ++c)
+                        if (c0 + c < Cc) v[c] -= z * __ldg(h + c);
+                }
             }
 #pragma unroll
             for (int c = 0; c < CB; ++c) acc[c] += chi * v[c];
