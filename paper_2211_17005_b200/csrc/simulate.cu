@@ -97,7 +97,7 @@ constexpr int kQueueCap = 128;  // per-warp queue of tail draws
 
 template <int P>
 #ifndef HCVA_K1_MAXNREG
-#define HCVA_K1_MAXNREG 128  // <= 128 keeps 512-thread CTAs launchable
+#define HCVA_K1_MAXNREG 128  // <= 128 keeps 512-thread CTAs launchable (80: 3 CTAs/SM measured slower)
 #endif
 __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     extern __shared__ double smem[];
