@@ -123,7 +123,7 @@ __device__ __forceinline__ double halley_refine(double x, double p) {
 // ---- two independent central-region draws at once (K1's Philox block yields
 // a pair): every coefficient is fetched once for both chains and the two
 // dependency chains interleave.  Same arithmetic as acklam_central +
-// halley_refine on each element (bit-identical results).
+// halley_refine on each element except the seed quotient (see below).
 __constant__ double kAcklamA[6] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
                                    1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
 __constant__ double kAcklamB[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
@@ -185,17 +185,16 @@ __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (
         den[0] = den[0] * r[0] + b;
         den[1] = den[1] * r[1] + b;
     }
-    double rd[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         num[i] = num[i] * q[i];
         den[i] = den[i] * r[i] + 1.0;
-    }
-    rcp_nr2(den, rd);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double qq = num[i] * rd[i];
-        x[i] = fma(fma(-qq, den[i], num[i]), rd[i], qq);
+        // The seed only needs ~1e-12: Halley's step below is insensitive to the
+        // seed's low bits (its error enters squared), so one Newton step on the
+        // hardware reciprocal replaces the correctly rounded quotient.
+        double rd = rcp_approx(den[i]);
+        rd = fma(rd, fma(-den[i], rd, 1.0), rd);
+        x[i] = num[i] * rd;
     }
     // Halley step against erfc (rng.cpp:120-127)
     double y[2], a[2], t[2], ap2[2], rap2[2], P[2], nz[2], lo[2], E[2], den2[2], rden2[2];

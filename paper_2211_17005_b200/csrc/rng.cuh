@@ -69,7 +69,13 @@ HCVA_HD uint64_t draw_u64(uint64_t key, uint64_t j) {
 }
 
 HCVA_HD double u64_to_uniform(uint64_t x) {
+#ifdef __CUDA_ARCH__
+    // fl(v + 0.5) * 2^-53 == fl(v * 2^-53 + 2^-54): scaling by 2^-53 commutes
+    // with rounding (results >= 2^-54 are normal), so one FMA is bit-identical.
+    return fma(static_cast<double>(x >> 11), 0x1.0p-53, 0x1.0p-54);
+#else
     return (static_cast<double>(x >> 11) + 0.5) * 0x1.0p-53;
+#endif
 }
 
 // Acklam's rational approximation + one Halley refinement against erfc
