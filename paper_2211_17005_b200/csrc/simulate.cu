@@ -266,6 +266,9 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         return ZRow{k.v0, k.v1, k.col0 * P, k.col1 * P, d, k.dense != 0};
     };
     const ZRow zr_a = zrow(econ ? fr : fg0), zr_b = zrow(econ ? 0 : fg1), zr_c = zrow(econ ? fx : fg1);
+    // Drift / vol coefficients of the owned factors, also register resident.
+    const FactorCoef kc_a = coef[econ ? fr : fg0], kc_b = coef[econ ? 0 : fg1];
+    const double kx_c0 = coef[fx].c0, kx_c1 = coef[fx].c1;
     int sub_ctr = a.substeps, next_store = 1;  // countdown to the next pricing step
     auto rec_step = [&](int cc, int t) {
         const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
@@ -281,15 +284,14 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             const double zr = zcorr(zr_a), z0 = zcorr(zr_b), zx = zcorr(zr_c);
             s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
             // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
-            const FactorCoef& kx = coef[fx];
-            s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx.c0), h)), dmul(kx.c1, zx));
-            s0 = vasicek_step(re, coef[fr], h, zr);
-            s1 = vasicek_step(r0, coef[0], h, z0);
+            s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx_c0), h)), dmul(kx_c1, zx));
+            s0 = vasicek_step(re, kc_a, h, zr);
+            s1 = vasicek_step(r0, kc_b, h, z0);
         } else {
             // Hazards first (left endpoint, market.cpp:209), then full-truncation CIR (:130-134).
             const double z0 = zcorr(zr_a), z1 = zcorr(zr_b);
-            const FactorCoef& k0 = coef[fg0];
-            const FactorCoef& k1 = coef[fg1];
+            const FactorCoef& k0 = kc_a;
+            const FactorCoef& k1 = kc_b;
             s2 = dadd(s2, dmul(s0, h));
             s3 = dadd(s3, dmul(s1, h));
             const double gp0 = (s0 < 0.0) ? 0.0 : s0, gp1 = (s1 < 0.0) ? 0.0 : s1;
