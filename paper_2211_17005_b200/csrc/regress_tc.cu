@@ -515,8 +515,6 @@ __global__ void __launch_bounds__(GramShape<U>::threads) k_gram_h2(const float* 
         }
 }
 
-constexpr uint32_t kChunkTile = 64 * 64 * 4;  // 64 x 64 FP32 core tile
-
 // Four consecutive floats, zero beyond `valid`; 16-byte load when aligned.
 __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
     float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -537,25 +535,30 @@ __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
     return v;
 }
 
-// Chunk tiles are 128B-swizzled K-major (tc.cuh sw_off): the coalesced
-// 16-byte row loads land in distinct bank groups.
+// Chunk tiles are 128B-swizzled K-major (tc.cuh sw_off): 64 feature rows x
+// kWgK batch rows (one 128-byte atom column), so the coalesced 16-byte row
+// loads land in distinct bank groups.  64 KB of tiles and <= 85 registers keep
+// three CTAs per SM, whose load / split / MMA phases interleave.
 constexpr int kWgThreads = 256;
+constexpr int kWgK = 32;                     // batch rows per chunk (the MMAs' K)
+constexpr uint32_t kWgTile = 64 * kWgK * 4;  // one plane of a chunk tile
+constexpr size_t kWgSmem = 8 * static_cast<size_t>(kWgTile) + 64 + 1024;
 
 template <int U>
-__global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
+__global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* tA1 = sm;                   // G2t chunk: 64 (o, zero-padded) x 64 (rows)
-    uint8_t* tB1 = sm + 2 * kChunkTile;  // H1t chunk: U x 64
-    uint8_t* tA0 = sm + 4 * kChunkTile;  // G1t chunk
-    uint8_t* tB0 = sm + 6 * kChunkTile;  // Xt chunk: dp x 64
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 8 * kChunkTile);
+    uint8_t* tA1 = sm;                // G2t chunk: 64 (o, zero-padded) x kWgK (rows)
+    uint8_t* tB1 = sm + 2 * kWgTile;  // H1t chunk: U x kWgK
+    uint8_t* tA0 = sm + 4 * kWgTile;  // G1t chunk
+    uint8_t* tB0 = sm + 6 * kWgTile;  // Xt chunk: dp x kWgK
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 8 * kWgTile);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int dp = a.dp;
     if (t == 0) tc::mbar_init(mbar, 1);
     if (warp == 0) tc::tmem_alloc(tbase, 128);
-    for (int i = t; i < 8 * kChunkTile / 16; i += kWgThreads)
+    for (int i = t; i < 8 * kWgTile / 16; i += kWgThreads)
         reinterpret_cast<float4*>(sm)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     tc::fence_before_sync();
     __syncthreads();
@@ -565,44 +568,49 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
     const long r_end = min(r_begin + a.rows_per_cta, a.rows);
     const bool vt = (a.ld_t % 4) == 0;
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
-    constexpr int NF = U * 16 / kWgThreads;  // float4 per thread per activation array
-    constexpr int NX = 64 * 16 / kWgThreads;  // float4 per thread of a 64-feature Xt chunk (dp <= 64)
+    constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
+    constexpr int NF = (U * Q + kWgThreads - 1) / kWgThreads;   // per thread per activation array
+    constexpr int NX = (64 * Q + kWgThreads - 1) / kWgThreads;  // per thread of the Xt chunk (dp <= 64)
     float4 rg2[NF], rh1[NF], rg1[NF], rx[NX];
     auto load = [&](long c0) {
-        const int n = static_cast<int>(min(64L, r_end - c0));
+        const int n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
-            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
-            const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
-            rg2[i] = ld4(a.G2t + o, vt, n - k);
-            rh1[i] = ld4(a.H1t + o, vt, n - k);
-            rg1[i] = ld4(a.G1t + o, vt, n - k);
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < U) {
+                const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
+                rg2[i] = ld4(a.G2t + o, vt, n - k);
+                rh1[i] = ld4(a.H1t + o, vt, n - k);
+                rg1[i] = ld4(a.G1t + o, vt, n - k);
+            }
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
             if (f < dp) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
         }
     };
     uint32_t phase = 0;
     int first = 1;
     if (r_begin < r_end) load(r_begin);
-    for (long c0 = r_begin; c0 < r_end; c0 += 64) {
+    for (long c0 = r_begin; c0 < r_end; c0 += kWgK) {
         if (!first) {  // previous chunk's MMAs done reading the tiles
             tc::mbar_wait(mbar, phase);
             phase ^= 1;
         }
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
-            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
-            tc::put_split4_sw(tA1, kChunkTile, f, k, 64, rg2[i]);
-            tc::put_split4_sw(tB1, kChunkTile, f, k, 64, rh1[i]);
-            tc::put_split4_sw(tA0, kChunkTile, f, k, 64, rg1[i]);
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < U) {
+                tc::put_split4_sw(tA1, kWgTile, f, k, 64, rg2[i]);
+                tc::put_split4_sw(tB1, kWgTile, f, k, 64, rh1[i]);
+                tc::put_split4_sw(tA0, kWgTile, f, k, 64, rg1[i]);
+            }
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-            const int idx = t + i * kWgThreads, f = idx >> 4, k = (idx & 15) * 4;
-            if (f < dp) tc::put_split4_sw(tB0, kChunkTile, f, k, 64, rx[i]);
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < dp) tc::put_split4_sw(tB0, kWgTile, f, k, 64, rx[i]);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -610,16 +618,16 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
         tc::fence_after_sync();
         if (t == 0) {
             const uint32_t R64 = 64;
-            tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(tA1), kChunkTile, R64, 0},
-                         tc::OperandSW{tc::smem_u32(tB1), kChunkTile, R64, 0}, 64, tc::idesc_tf32(64, U, 0, 0),
+            tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(tA1), kWgTile, R64, 0},
+                         tc::OperandSW{tc::smem_u32(tB1), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, U, 0, 0),
                          !first);
-            tc::gemm3_sw(tm + 64, tc::OperandSW{tc::smem_u32(tA0), kChunkTile, R64, 0},
-                         tc::OperandSW{tc::smem_u32(tB0), kChunkTile, R64, 0}, 64, tc::idesc_tf32(64, dp, 0, 0),
+            tc::gemm3_sw(tm + 64, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
+                         tc::OperandSW{tc::smem_u32(tB0), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, dp, 0, 0),
                          !first);
             tc::commit(mbar);
         }
         first = 0;
-        if (c0 + 64 < r_end) load(c0 + 64);  // in flight while the MMAs run
+        if (c0 + kWgK < r_end) load(c0 + kWgK);  // in flight while the MMAs run
     }
     if (!first) {
         tc::mbar_wait(mbar, phase);
@@ -768,9 +776,8 @@ int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
 
 template <int U>
 void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
-    const size_t smem = 8 * static_cast<size_t>(kChunkTile) + 64 + 1024;
-    HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_wgrad_tc<U><<<ctas, kWgThreads, smem, s>>>(a);
+    HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWgSmem));
+    k_wgrad_tc<U><<<ctas, kWgThreads, kWgSmem, s>>>(a);
 }
 
 template <int U>
@@ -791,9 +798,10 @@ int launch_gram_h2(int u, const float* H2, const double* y, long R, const float*
 
 // Returns the number of weight-gradient partials written.
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
-    const long chunks = (a.rows + 63) / 64;
-    const long per = std::max(1L, (chunks + sm_count - 1) / sm_count);
-    a.rows_per_cta = static_cast<int>(per * 64);
+    const long chunks = (a.rows + kWgK - 1) / kWgK;
+    const long slots = 3L * sm_count;  // resident CTAs
+    const long per = std::max(1L, (chunks + slots - 1) / slots);
+    a.rows_per_cta = static_cast<int>(per * kWgK);
     const int ctas = static_cast<int>((a.rows + a.rows_per_cta - 1) / a.rows_per_cta);
     if (u == 16) launch_wgrad_u<16>(a, ctas, s);
     else if (u == 32) launch_wgrad_u<32>(a, ctas, s);
