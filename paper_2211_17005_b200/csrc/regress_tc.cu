@@ -63,15 +63,6 @@ __device__ __forceinline__ float act_d(float v) {
 
 constexpr int kTcThreads = 128;
 
-// Transposed activations for the weight gradients, chunk-blocked: the 32
-// consecutive batch rows of chunk q and feature f sit at [(q * U + f) * 32 +
-// row % 32], so a weight-gradient chunk is one contiguous U x 32 block in HBM.
-constexpr int kTChunk = 32;
-template <int U>
-__device__ __forceinline__ size_t tix(int f, long trow) {
-    return (static_cast<size_t>(trow / kTChunk) * U + f) * kTChunk + (trow % kTChunk);
-}
-
 __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
     return 2u * U * dp * 4 + 4u * U * U * 4 + 1024;
 }
@@ -279,7 +270,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             if (sgd) {
                 if (live)
 #pragma unroll
-                    for (int q = 0; q < UH; ++q) a.H1t[tix<U>(c0 + q, trow)] = v[q];
+                    for (int q = 0; q < UH; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
 #pragma unroll
                 for (int q = 0; q < UH; ++q) v[q] = act_d<ACT>(v[q]);
                 tc::tmem_stw<UH>(tm + lb + c0, v);
@@ -362,7 +353,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
                 tc::put_split4(bufH, hb, r, cb + j, 128, make_float4(g[j], g[j + 1], g[j + 2], g[j + 3]));
             if (live)
 #pragma unroll
-                for (int j = 0; j < UH; ++j) a.G2t[tix<U>(cb + j, trow)] = g[j];
+                for (int j = 0; j < UH; ++j) a.G2t[(cb + j) * a.ld_t + trow] = g[j];
             colsum_acc<UH>(g, acc_b1, lane);
         }
         cta_sync();
@@ -381,7 +372,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             for (int q = 0; q < UH; ++q) g[q] = live ? g[q] * dv[q] : 0.0f;
             if (live)
 #pragma unroll
-                for (int j = 0; j < UH; ++j) a.G1t[tix<U>(cb + j, trow)] = g[j];
+                for (int j = 0; j < UH; ++j) a.G1t[(cb + j) * a.ld_t + trow] = g[j];
             colsum_acc<UH>(g, acc_b0, lane);
         }
         tc::fence_before_sync();
@@ -575,6 +566,7 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     const uint32_t tm = *tbase;
     const long r_begin = static_cast<long>(blockIdx.x) * a.rows_per_cta;
     const long r_end = min(r_begin + a.rows_per_cta, a.rows);
+    const bool vt = (a.ld_t % 4) == 0;
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
     constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
     constexpr int NF = (U * Q + kWgThreads - 1) / kWgThreads;   // per thread per activation array
@@ -586,10 +578,10 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
         for (int i = 0; i < NF; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
             if (f < U) {
-                const size_t o = tix<U>(f, c0) + k;  // c0 is chunk-aligned: one contiguous block
-                rg2[i] = ld4(a.G2t + o, true, n - k);
-                rh1[i] = ld4(a.H1t + o, true, n - k);
-                rg1[i] = ld4(a.G1t + o, true, n - k);
+                const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
+                rg2[i] = ld4(a.G2t + o, vt, n - k);
+                rh1[i] = ld4(a.H1t + o, vt, n - k);
+                rg1[i] = ld4(a.G1t + o, vt, n - k);
             }
         }
 #pragma unroll

@@ -25,13 +25,13 @@ struct TileArgs {
     double* mpart;   // [cta] min of f + mu (plain head)
     double* pred;    // predictions (head on), absolute row index
     float* H2;       // [R][U] layer-2 activations (mode bit 8)
-    float *H1t, *G2t, *G1t;  // SGD: transposed, chunk-blocked (regress_tc.cu tix), row relative to b0
-    long ld_t;               // unused by the chunked layout (capacity >= U * roundup(rows, 32))
+    float *H1t, *G2t, *G1t;  // SGD: [U][ld_t] transposed, row index relative to b0
+    long ld_t;
 };
 
 struct WgradArgs {
     int d, dp, P, off0, off1;
-    const float *G2t, *H1t, *G1t;  // chunk-blocked (tix)
+    const float *G2t, *H1t, *G1t;  // [U][ld_t]
     long ld_t;
     const float* Xt;               // [dp][ld_x] transposed features, column = absolute row
     long ld_x, row0, rows;         // rows of the batch (relative index 0..rows-1)
