@@ -247,10 +247,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         if (tid == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing thread reads the feature tile
         xph ^= 1;
         // ---- F0: D0 = X W0^T
-        if (tid == 0) {
-            tc::gemm3(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
-            tc::commit(&bar[0]);
-        }
+        if (warp == 0)
+            tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0),
+                           0, &bar[0]);
         mma_wait();
         if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
             tc::mbar_expect_tx(&bar[2], 2 * xb);
@@ -279,11 +278,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         if (sgd) tc::tmem_wait_st();
         cta_sync();
         // ---- F1: D1 = H1 W1^T ; H2, f
-        if (tid == 0) {
-            tc::gemm3(tm + 64, tc::kmajor(bufH, hb, 128), tc::kmajor(w1, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
-                      0);
-            tc::commit(&bar[0]);
-        }
+        if (warp == 0)
+            tc::gemm3_warp(tm + 64, tc::kmajor(bufH, hb, 128), tc::kmajor(w1, w1b, U), U,
+                           tc::idesc_tf32(128, U, 0, 0), 0, &bar[0]);
         mma_wait();
         float h2[UH];
         tc::tmem_ldw<UH>(tm + lb + 64 + cb, h2);
@@ -358,11 +355,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         }
         cta_sync();
         // ---- B: Dbp = G2 W1 (B operand: the W1^T tile, K-major over the outputs of layer 1)
-        if (tid == 0) {
-            tc::gemm3(tm + 128, tc::kmajor(bufH, hb, 128), tc::kmajor(w1t, w1b, U), U, tc::idesc_tf32(128, U, 0, 0),
-                      0);
-            tc::commit(&bar[0]);
-        }
+        if (warp == 0)
+            tc::gemm3_warp(tm + 128, tc::kmajor(bufH, hb, 128), tc::kmajor(w1t, w1b, U), U,
+                           tc::idesc_tf32(128, U, 0, 0), 0, &bar[0]);
         mma_wait();
         {
             float g[UH], dv[UH];
@@ -536,35 +531,23 @@ __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
 }
 
 // Chunk tiles are 128B-swizzled K-major (tc.cuh sw_off): 64 feature rows x
-// kWgK batch rows (one 128-byte atom column).  The chunks' raw FP32 rows
-// stream in with cp.async through a kWgStages-deep ring (kWgStages - 1 chunks
-// in flight while one is split into hi/lo tiles and fed to the MMAs).
+// kWgK batch rows (one 128-byte atom column), so the coalesced 16-byte row
+// loads land in distinct bank groups.  64 KB of tiles and <= 85 registers keep
+// three CTAs per SM, whose load / split / MMA phases interleave.
 constexpr int kWgThreads = 256;
-constexpr int kWgK = 32;                          // batch rows per chunk (the MMAs' K)
-constexpr int kWgStages = 4;
-constexpr uint32_t kWgTile = 64 * kWgK * 4;       // one plane of a chunk tile
-constexpr uint32_t kWgRaw = 4 * 64 * kWgK * 4;    // raw chunk: G2t | H1t | G1t | Xt rows
-constexpr size_t kWgSmem = 8 * static_cast<size_t>(kWgTile) + kWgStages * static_cast<size_t>(kWgRaw) + 64 + 1024;
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+constexpr int kWgK = 32;                     // batch rows per chunk (the MMAs' K)
+constexpr uint32_t kWgTile = 64 * kWgK * 4;  // one plane of a chunk tile
+constexpr size_t kWgSmem = 8 * static_cast<size_t>(kWgTile) + 64 + 1024;
 
 template <int U>
-__global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
+__global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    // tiles: G2t | H1t | G1t | Xt at sm + arr * 2 * kWgTile (hi, then lo)
-    uint8_t* ring = sm + 8 * kWgTile;
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + kWgStages * kWgRaw);
+    uint8_t* tA1 = sm;                // G2t chunk: 64 (o, zero-padded) x kWgK (rows)
+    uint8_t* tB1 = sm + 2 * kWgTile;  // H1t chunk: U x kWgK
+    uint8_t* tA0 = sm + 4 * kWgTile;  // G1t chunk
+    uint8_t* tB0 = sm + 6 * kWgTile;  // Xt chunk: dp x kWgK
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 8 * kWgTile);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int dp = a.dp;
@@ -578,78 +561,68 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_wgrad_tc(WgradArgs a) {
     const uint32_t tm = *tbase;
     const long r_begin = static_cast<long>(blockIdx.x) * a.rows_per_cta;
     const long r_end = min(r_begin + a.rows_per_cta, a.rows);
-    const int nch = static_cast<int>((max(r_end - r_begin, 0L) + kWgK - 1) / kWgK);
+    const bool vt = (a.ld_t % 4) == 0;
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
-    constexpr int Q = kWgK / 4;                    // float4 per feature row of a chunk
-    const int slots = (3 * U + dp) * Q;            // float4 slots of a chunk
-    const uint32_t ring_s = tc::smem_u32(ring);
-    // Slot s -> (array, feature, row offset): arrays 0..2 have U features, array 3 has dp.
-    auto slot = [&](int s, int& arr, int& f, int& k) {
-        const int fr = s / Q;
-        k = (s % Q) * 4;
-        arr = fr < 3 * U ? fr / U : 3;
-        f = fr < 3 * U ? fr % U : fr - 3 * U;
-    };
-    auto issue = [&](int j) {  // chunk j -> ring stage j % kWgStages
-        if (j < nch) {
-            const long c0 = r_begin + static_cast<long>(j) * kWgK;
-            const int n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
-            const uint32_t stage = ring_s + (j % kWgStages) * kWgRaw;
-            for (int s = t; s < slots; s += kWgThreads) {
-                int arr, f, k;
-                slot(s, arr, f, k);
-                const uint32_t dst = stage + ((arr * 64 + f) * kWgK + k) * 4;
-                const int valid = n - k;
-                if (arr < 3) {
-                    const float* base = arr == 0 ? a.G2t : (arr == 1 ? a.H1t : a.G1t);
-                    const float* p = base + static_cast<size_t>(f) * a.ld_t + c0 + k;
-                    cp_async16(dst, valid > 0 ? p : base, valid >= 4 ? 16 : (valid > 0 ? valid * 4 : 0));
-                } else {
-                    const float* p = a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k;
-                    if (vx) {
-                        cp_async16(dst, valid > 0 ? p : a.Xt, valid >= 4 ? 16 : (valid > 0 ? valid * 4 : 0));
-                    } else {
+    constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
+    constexpr int NF = (U * Q + kWgThreads - 1) / kWgThreads;   // per thread per activation array
+    constexpr int NX = (64 * Q + kWgThreads - 1) / kWgThreads;  // per thread of the Xt chunk (dp <= 64)
+    float4 rg2[NF], rh1[NF], rg1[NF], rx[NX];
+    auto load = [&](long c0) {
+        const int n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) cp_async4(dst + 4 * q, q < valid ? p + q : a.Xt, q < valid ? 4 : 0);
-                    }
-                }
+        for (int i = 0; i < NF; ++i) {
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < U) {
+                const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
+                rg2[i] = ld4(a.G2t + o, vt, n - k);
+                rh1[i] = ld4(a.H1t + o, vt, n - k);
+                rg1[i] = ld4(a.G1t + o, vt, n - k);
             }
         }
-        cp_async_commit();  // an empty group past the end keeps the wait counts uniform
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < dp) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
+        }
     };
-    for (int j = 0; j < kWgStages - 1; ++j) issue(j);
     uint32_t phase = 0;
-    for (int j = 0; j < nch; ++j) {
-        issue(j + kWgStages - 1);
-        cp_async_wait<kWgStages - 1>();  // this thread's copies of chunk j landed
-        __syncthreads();                 // ... and everyone's
-        if (j > 0) {                     // chunk j-1's MMAs done reading the tiles
+    int first = 1;
+    if (r_begin < r_end) load(r_begin);
+    for (long c0 = r_begin; c0 < r_end; c0 += kWgK) {
+        if (!first) {  // previous chunk's MMAs done reading the tiles
             tc::mbar_wait(mbar, phase);
             phase ^= 1;
         }
-        const uint8_t* stage = ring + (j % kWgStages) * kWgRaw;
-        for (int s = t; s < slots; s += kWgThreads) {
-            int arr, f, k;
-            slot(s, arr, f, k);
-            const float4 v = *reinterpret_cast<const float4*>(stage + ((arr * 64 + f) * kWgK + k) * 4);
-            tc::put_split4_sw(sm + arr * 2 * kWgTile, kWgTile, f, k, 64, v);
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < U) {
+                tc::put_split4_sw(tA1, kWgTile, f, k, 64, rg2[i]);
+                tc::put_split4_sw(tB1, kWgTile, f, k, 64, rh1[i]);
+                tc::put_split4_sw(tA0, kWgTile, f, k, 64, rg1[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
+            if (f < dp) tc::put_split4_sw(tB0, kWgTile, f, k, 64, rx[i]);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
         tc::fence_after_sync();
-        if (t == 0) {
+        if (warp == 0) {
             const uint32_t R64 = 64;
-            const uint32_t t0 = tc::smem_u32(sm);
-            tc::gemm3_sw(tm, tc::OperandSW{t0, kWgTile, R64, 0}, tc::OperandSW{t0 + 2 * kWgTile, kWgTile, R64, 0},
-                         kWgK, tc::idesc_tf32(64, U, 0, 0), j > 0);
-            tc::gemm3_sw(tm + 64, tc::OperandSW{t0 + 4 * kWgTile, kWgTile, R64, 0},
-                         tc::OperandSW{t0 + 6 * kWgTile, kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, dp, 0, 0), j > 0);
-            tc::commit(mbar);
+            tc::gemm3_sw_warp(tm, tc::OperandSW{tc::smem_u32(tA1), kWgTile, R64, 0},
+                              tc::OperandSW{tc::smem_u32(tB1), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, U, 0, 0),
+                              !first, nullptr);
+            tc::gemm3_sw_warp(tm + 64, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
+                              tc::OperandSW{tc::smem_u32(tB0), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, dp, 0, 0),
+                              !first, mbar);
         }
+        first = 0;
+        if (c0 + kWgK < r_end) load(c0 + kWgK);  // in flight while the MMAs run
     }
-    cp_async_wait<0>();
-    const int first = nch == 0;
     if (!first) {
         tc::mbar_wait(mbar, phase);
         tc::fence_after_sync();
@@ -820,7 +793,8 @@ int launch_gram_h2(int u, const float* H2, const double* y, long R, const float*
 // Returns the number of weight-gradient partials written.
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
     const long chunks = (a.rows + kWgK - 1) / kWgK;
-    const long per = std::max(1L, (chunks + sm_count - 1) / sm_count);  // one CTA per SM
+    const long slots = 3L * sm_count;  // resident CTAs
+    const long per = std::max(1L, (chunks + slots - 1) / slots);
     a.rows_per_cta = static_cast<int>(per * kWgK);
     const int ctas = static_cast<int>((a.rows + a.rows_per_cta - 1) / a.rows_per_cta);
     if (u == 16) launch_wgrad_u<16>(a, ctas, s);

@@ -75,6 +75,39 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
 
+// Warp-collective issue: the whole warp evaluates the (warp-uniform)
+// descriptors, one elected lane issues.  Keeps descriptor arithmetic in the
+// uniform datapath instead of a divergent single-thread branch.
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(e));
+    return e;
+}
+
+__device__ __forceinline__ void mma_tf32_if(uint32_t issue, uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                            int accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(issue));
+}
+
+__device__ __forceinline__ void commit_if(uint32_t issue, uint64_t* mbar) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.b32 q, %1, 0;\n\t"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(mbar)),
+        "r"(issue)
+        : "memory");
+}
+
 __device__ __forceinline__ void commit(uint64_t* mbar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
                  : "memory");
@@ -193,6 +226,24 @@ struct Operand {
     }
 };
 
+// Warp-collective gemm3 (call from a whole warp): descriptors from one base
+// plus address-field offsets, one elected lane issues every MMA and commits.
+__device__ __forceinline__ void gemm3_warp(uint32_t d_tmem, const Operand& A, const Operand& B, int K,
+                                           uint32_t idesc, int accumulate, uint64_t* mbar) {
+    const uint32_t issue = elect_one();
+    const uint64_t a0 = sdesc(A.hi, A.lbo, A.sbo), b0 = sdesc(B.hi, B.lbo, B.sbo);
+    const uint64_t al = static_cast<uint64_t>(A.lo_off >> 4), bl = static_cast<uint64_t>(B.lo_off >> 4);
+    const uint64_t as = static_cast<uint64_t>(A.mn_major ? 8u : (2u * A.lbo) >> 4);
+    const uint64_t bs = static_cast<uint64_t>(B.mn_major ? 8u : (2u * B.lbo) >> 4);
+    for (int ks = 0; ks < K / 8; ++ks) {
+        const uint64_t da = a0 + as * ks, db = b0 + bs * ks;
+        mma_tf32_if(issue, d_tmem, da, db, idesc, (ks > 0 || accumulate) ? 1 : 0);
+        mma_tf32_if(issue, d_tmem, da + al, db, idesc, 1);
+        mma_tf32_if(issue, d_tmem, da, db + bl, idesc, 1);
+    }
+    if (mbar) commit_if(issue, mbar);
+}
+
 __device__ __forceinline__ void gemm3(uint32_t d_tmem, const Operand& A, const Operand& B, int K, uint32_t idesc,
                                       int accumulate) {
     for (int ks = 0; ks < K / 8; ++ks) {
@@ -249,6 +300,23 @@ struct OperandSW {
         return sdesc_sw128(base + (col >> 5) * (R / 8) * 1024u + (col & 31) * 4u, 16u, 1024u);
     }
 };
+
+// Warp-collective gemm3_sw (K-major SW128 operands).
+__device__ __forceinline__ void gemm3_sw_warp(uint32_t d_tmem, const OperandSW& A, const OperandSW& B, int K,
+                                              uint32_t idesc, int accumulate, uint64_t* mbar) {
+    const uint32_t issue = elect_one();
+    const uint64_t a0 = A.desc(0, 0), b0 = B.desc(0, 0);
+    const uint64_t al = static_cast<uint64_t>(A.lo_off >> 4), bl = static_cast<uint64_t>(B.lo_off >> 4);
+    for (int ks = 0; ks < K / 8; ++ks) {
+        const uint32_t col = 8 * ks;  // first K column of this step
+        const uint64_t da = a0 + ((((col >> 5) * (A.R / 8) * 1024u) + (col & 31) * 4u) >> 4);
+        const uint64_t db = b0 + ((((col >> 5) * (B.R / 8) * 1024u) + (col & 31) * 4u) >> 4);
+        mma_tf32_if(issue, d_tmem, da, db, idesc, (ks > 0 || accumulate) ? 1 : 0);
+        mma_tf32_if(issue, d_tmem, da + al, db, idesc, 1);
+        mma_tf32_if(issue, d_tmem, da, db + bl, idesc, 1);
+    }
+    if (mbar) commit_if(issue, mbar);
+}
 
 __device__ __forceinline__ void gemm3_sw(uint32_t d_tmem, const OperandSW& A, const OperandSW& B, int K,
                                          uint32_t idesc, int accumulate) {
