@@ -24,6 +24,7 @@
 // Reductions are over fixed CTA partitions in fixed order: results are
 // deterministic and independent of scheduling.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -312,14 +313,24 @@ __device__ __forceinline__ void optimizer_step(int i, double g, int P, double* p
     if (im.img) img_store(im, P, i, static_cast<float>(w));
 }
 
+struct SplitPartials;
+__host__ __device__ inline size_t split_index(const SplitPartials& sp, int i);
+
 struct SplitPartials {
     const float* gpartB = nullptr;
     int nB = 0;
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // [lo, hi) index ranges served by gpartB
+    int stride = 0, U = 0, d = 0, dp = 0;    // gpartB rows: W1 [U][U] then W0 [U][dp] (regress_tc.cuh)
 };
 
 // Block (32, 16): x = parameter, y = partial group c = y (mod 16); the group
 // sums combine in a fixed pairwise tree.  Warp 0 of CTA 0 also checks the loss.
+__host__ __device__ inline size_t split_index(const SplitPartials& sp, int i) {
+    if (i >= sp.lo1 && i < sp.hi1) return static_cast<size_t>(i - sp.lo1);
+    const int k = i - sp.lo0;
+    return static_cast<size_t>(sp.U) * sp.U + static_cast<size_t>(k / sp.d) * sp.dp + (k % sp.d);
+}
+
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
                        double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite,
                        ImgArgs im) {
@@ -336,10 +347,11 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
     double s = 0.0;
     if (i < P) {
         const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
-        const float* src = split ? sp.gpartB : gpart;
+        const float* src = split ? sp.gpartB + split_index(sp, i) : gpart + i;
+        const size_t stride = split ? sp.stride : P;
         const int cnt = split ? sp.nB : nct;
 #pragma unroll 4
-        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * P + i));
+        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * stride));
     }
     part[grp][x] = s;
     __syncthreads();
@@ -368,10 +380,11 @@ __global__ void k_rank_sum(int P, const float* gpart, int nct, SplitPartials sp,
     double s = 0.0;
     if (i < P) {
         const bool split = sp.nB && ((i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1));
-        const float* src = split ? sp.gpartB : gpart;
+        const float* src = split ? sp.gpartB + split_index(sp, i) : gpart + i;
+        const size_t stride = split ? sp.stride : P;
         const int cnt = split ? sp.nB : nct;
 #pragma unroll 4
-        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * P + i));
+        for (int c = grp; c < cnt; c += G) s += static_cast<double>(__ldg(src + static_cast<size_t>(c) * stride));
     }
     part[grp][x] = s;
     __syncthreads();
@@ -724,7 +737,7 @@ struct Trainer {
             h1t.alloc(tsz);
             g2t.alloc(tsz);
             g1t.alloc(tsz);
-            gpartB.alloc(static_cast<size_t>(ctx->sm_count) * P * 4);
+            gpartB.alloc(static_cast<size_t>(tc_wgrad_max_ctas(ctx->sm_count)) * (n.u * n.u + n.u * dp) * 4);
             wimg.alloc(tc_weight_image_bytes(n.u, dp));
             x_rows = std::max(max_rows, max_batch);
             ld_x = ((x_rows + 64 + 3) / 4) * 4;  // slack for the 64-row chunk loads
@@ -798,10 +811,16 @@ struct Trainer {
             wa.G2t = g2t.as<float>(); wa.H1t = h1t.as<float>(); wa.G1t = g1t.as<float>();
             wa.ld_t = ((b1 - b0 + 63) / 64) * 64;
             wa.Xt = xt.as<float>(); wa.ld_x = ld_x; wa.row0 = b0; wa.rows = b1 - b0; wa.gpart = gpartB.as<float>();
+            static const bool twice = std::getenv("HCVA_WGRAD_TWICE") != nullptr;  // profiling probe
+            if (twice) {  // an extra launch with the row loop skipped: the kernel's fixed costs
+                WgradArgs wp = wa;
+                wp.probe = 1;
+                launch_wgrad_tc(n.u, wp, ctx->sm_count, ctx->stream);
+            }
             const int nB = launch_wgrad_tc(n.u, wa, ctx->sm_count, ctx->stream);
             check_launch(ctx);
             if (sp) *sp = SplitPartials{gpartB.as<float>(), nB, n.off[0], n.off[0] + n.u * n.d, n.off[1],
-                                        n.off[1] + n.u * n.u};
+                                        n.off[1] + n.u * n.u, n.u * n.u + n.u * dp, n.u, n.d, dp};
             return ctas;
         }
         const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);
@@ -1179,7 +1198,7 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         SplitPartials sp;
         const int tiles =
             tr.grad_tiles(dX.as<float>(), dy.as<double>(), 0, rows, head, static_cast<double>(rows), &sp);
-        std::vector<float> gp(static_cast<size_t>(tiles) * n.P), gb(static_cast<size_t>(sp.nB) * n.P);
+        std::vector<float> gp(static_cast<size_t>(tiles) * n.P), gb(static_cast<size_t>(sp.nB) * sp.stride);
         std::vector<double> lp(tiles);
         copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);
         if (sp.nB) copy_out(ctx, gb.data(), sp.gpartB, gb.size() * 4);
@@ -1190,10 +1209,12 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         if (grads)
             for (int i = 0; i < n.P; ++i) {
                 const bool split = (i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1);
-                const std::vector<float>& src = (split && sp.nB) ? gb : gp;
-                const int cnt = (split && sp.nB) ? sp.nB : tiles;
+                const bool fromB = split && sp.nB;
+                const float* src = fromB ? gb.data() + split_index(sp, i) : gp.data() + i;
+                const size_t stride = fromB ? sp.stride : n.P;
+                const int cnt = fromB ? sp.nB : tiles;
                 double g = 0.0;
-                for (int c = 0; c < cnt; ++c) g += src[static_cast<size_t>(c) * n.P + i];
+                for (int c = 0; c < cnt; ++c) g += src[static_cast<size_t>(c) * stride];
                 grads[i] = g;
             }
     });

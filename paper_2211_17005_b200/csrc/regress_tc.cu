@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     tc::fence_after_sync();
     const uint32_t tm = *tbase;
     const long r_begin = static_cast<long>(blockIdx.x) * a.rows_per_cta;
-    const long r_end = min(r_begin + a.rows_per_cta, a.rows);
+    const long r_end = a.probe ? r_begin : min(r_begin + a.rows_per_cta, a.rows);  // probe: fixed costs only
     const bool vt = (a.ld_t % 4) == 0;
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
     constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
@@ -627,26 +627,31 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
         tc::mbar_wait(mbar, phase);
         tc::fence_after_sync();
     }
-    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
+    // Partial row of this CTA: W1 [U][U] then W0 [U][dp] (16-byte stores).
+    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * (U * U + U * dp);
     if (warp < 4) {
-    const int o = warp * 16 + lane;  // M=64 accumulator: row 16w+t in lane 32w+t, t < 16
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        const int o = warp * 16 + lane;  // M=64 accumulator: row 16w+t in lane 32w+t, t < 16
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        const bool own = lane < 16 && o < U;
 #pragma unroll
-    for (int c = 0; c < U; c += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + c, v);
-        if (lane < 16 && o < U)
+        for (int c = 0; c < U; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_base + c, v);
+            if (own)
 #pragma unroll
-            for (int q = 0; q < 16; ++q) gout[a.off1 + o * U + c + q] = first ? 0.0f : v[q];
-    }
-    for (int c = 0; c < dp; c += 16) {
-        float v[16];
-        tc::tmem_ld16(tm + lane_base + 64 + c, v);
-        if (lane < 16 && o < U)
+                for (int q = 0; q < 16; q += 4)
+                    *reinterpret_cast<float4*>(gout + o * U + c + q) =
+                        first ? make_float4(0.0f, 0.0f, 0.0f, 0.0f) : make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+        for (int c = 0; c < dp; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lane_base + 64 + c, v);
+            if (own)
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (c + q < a.d) gout[a.off0 + o * a.d + c + q] = first ? 0.0f : v[q];
-    }
+                for (int q = 0; q < 16; q += 4)
+                    *reinterpret_cast<float4*>(gout + U * U + o * dp + c + q) =
+                        first ? make_float4(0.0f, 0.0f, 0.0f, 0.0f) : make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -713,6 +718,42 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
         const int row = (M == 128) ? t : ((lane < 16) ? warp * 16 + lane : -1);
         if (row >= 0)
             for (int q = 0; q < 16 && c0 + q < N; ++q) D[row * N + c0 + q] = v[q];
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
+// Tensor-core rate probe: every CTA (one per SM) issues `iters` kind::tf32
+// MMAs of M x N x 8 back to back on the same K-major tiles into one TMEM
+// accumulator (warp-collective issue, one commit at the end).
+__global__ void k_tc_rate(int M, int N, int iters, float* sink) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 2 * 128 * 8 * 4 * 2);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
+    const int t = threadIdx.x, warp = t >> 5;
+    for (int i = t; i < 2 * 128 * 8 * 2; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.001f * (i % 7);
+    if (t == 0) tc::mbar_init(mbar, 1);
+    if (warp == 0) tc::tmem_alloc(tbase, 256);
+    tc::fence_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = *tbase;
+    if (warp == 0) {
+        const uint32_t issue = tc::elect_one();
+        const uint64_t da = tc::sdesc(tc::smem_u32(sm), 128u * 16, 128u);
+        const uint64_t db = tc::sdesc(tc::smem_u32(sm + 128 * 8 * 4), 256u / 8 * 128, 128u);
+        const uint32_t id = tc::idesc_tf32(M, N, 0, 0);
+        for (int i = 0; i < iters; ++i) tc::mma_tf32_if(issue, tm, da, db, id, i > 0);
+        tc::commit_if(issue, mbar);
+    }
+    tc::mbar_wait(mbar, 0);
+    tc::fence_after_sync();
+    if (warp == 0) {
+        float v[16];
+        tc::tmem_ld16(tm, v);
+        if (t == 0) sink[blockIdx.x] = v[0];
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -790,10 +831,12 @@ int launch_gram_h2(int u, const float* H2, const double* y, long R, const float*
     return launch_gram_u<64>(H2, y, R, params, P, gpart, ctas, s);
 }
 
+int tc_wgrad_max_ctas(int sm_count) { return 3 * sm_count; }
+
 // Returns the number of weight-gradient partials written.
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
     const long chunks = (a.rows + kWgK - 1) / kWgK;
-    const long slots = 3L * sm_count;  // resident CTAs
+    const long slots = tc_wgrad_max_ctas(sm_count);  // resident CTAs
     const long per = std::max(1L, (chunks + slots - 1) / slots);
     a.rows_per_cta = static_cast<int>(per * kWgK);
     const int ctas = static_cast<int>((a.rows + a.rows_per_cta - 1) / a.rows_per_cta);
@@ -825,5 +868,33 @@ extern "C" hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int
                                                       variant);
         check_launch(ctx);
         copy_out(ctx, D, dD.p, sizeof(float) * M * N);
+    });
+}
+
+extern "C" hcva_status hcva_diag_tc_rate(hcva_ctx* ctx, int M, int N, int iters, double* tflops) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if ((M != 64 && M != 128) || N % 16 || N < 16 || N > 256) throw contract_error("tc rate: bad shape");
+        DeviceBuf sink;
+        sink.alloc(sizeof(float) * ctx->sm_count);
+        const size_t smem = 2 * 128 * 8 * 4 * 2 + 64;
+        cudaEvent_t e0, e1;
+        HCVA_CUDA(cudaEventCreate(&e0));
+        HCVA_CUDA(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+            HCVA_CUDA(cudaEventRecord(e0, ctx->stream));
+            k_tc_rate<<<ctx->sm_count, 128, smem, ctx->stream>>>(M, N, iters, sink.as<float>());
+            HCVA_CUDA(cudaEventRecord(e1, ctx->stream));
+            HCVA_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            HCVA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0) best = std::min(best, ms);
+        }
+        check_launch(ctx);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *tflops = 2.0 * M * N * 8.0 * iters * ctx->sm_count / (best * 1e-3) / 1e12;
     });
 }

@@ -35,8 +35,9 @@ struct WgradArgs {
     long ld_t;
     const float* Xt;               // [dp][ld_x] transposed features, column = absolute row
     long ld_x, row0, rows;         // rows of the batch (relative index 0..rows-1)
-    int rows_per_cta;              // multiple of 64 (set by the launcher)
-    float* gpart;                  // [cta][P]: W0, W1 entries
+    int rows_per_cta;              // multiple of the chunk (set by the launcher)
+    int probe;                     // profiling: skip the row loop
+    float* gpart;                  // [cta][U*U + U*dp]: W1 rows, then W0 rows padded to dp
 };
 
 bool tc_eligible(int d, int h, int u);
@@ -49,6 +50,7 @@ void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* 
 // Returns the number of per-CTA partials written (gpart / lpart / mpart rows).
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s);
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s);
+int tc_wgrad_max_ctas(int sm_count);  // rows of WgradArgs::gpart the launcher may write
 // FP64 Gram partials of z = [H2 row, 1] and rhs z (y - mu) in k_refit's packed
 // layout (upper triangle, then rhs); returns the partial count (<= max_parts).
 int launch_gram_h2(int u, const float* H2, const double* y, long R, const float* params, int P, double* gpart,
