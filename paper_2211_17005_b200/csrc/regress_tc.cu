@@ -836,7 +836,12 @@ int tc_wgrad_max_ctas(int sm_count) { return 3 * sm_count; }
 // Returns the number of weight-gradient partials written.
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
     const long chunks = (a.rows + kWgK - 1) / kWgK;
-    const long slots = tc_wgrad_max_ctas(sm_count);  // resident CTAs
+    static const int per_sm = [] {  // CTAs per SM (profiling override HCVA_WGRAD_SLOTS)
+        const char* e = std::getenv("HCVA_WGRAD_SLOTS");
+        const int v = e ? std::atoi(e) : 2;  // 2 measured best (partials vs overlap)
+        return v < 1 ? 1 : (v > 3 ? 3 : v);
+    }();
+    const long slots = static_cast<long>(per_sm) * sm_count;  // resident CTAs
     const long per = std::max(1L, (chunks + slots - 1) / slots);
     a.rows_per_cta = static_cast<int>(per * kWgK);
     const int ctas = static_cast<int>((a.rows + a.rows_per_cta - 1) / a.rows_per_cta);
