@@ -320,15 +320,21 @@ struct SplitPartials {
     const float* gpartB = nullptr;
     int nB = 0;
     int lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // [lo, hi) index ranges served by gpartB
-    int stride = 0, U = 0, d = 0, dp = 0;    // gpartB rows: W1 [U][U] then W0 [U][dp] (regress_tc.cuh)
+    int stride = 0, U = 0, d = 0, dp = 0;    // gpartB rows: W1 | b1 as [U][U+8], then W0 | b0 as [U][dp]
 };
 
 // Block (32, 16): x = parameter, y = partial group c = y (mod 16); the group
 // sums combine in a fixed pairwise tree.  Warp 0 of CTA 0 also checks the loss.
 __host__ __device__ inline size_t split_index(const SplitPartials& sp, int i) {
-    if (i >= sp.lo1 && i < sp.hi1) return static_cast<size_t>(i - sp.lo1);
-    const int k = i - sp.lo0;
-    return static_cast<size_t>(sp.U) * sp.U + static_cast<size_t>(k / sp.d) * sp.dp + (k % sp.d);
+    const int U = sp.U;
+    if (i >= sp.lo1 && i < sp.hi1) {  // W1 row-major, then b1
+        const int k = i - sp.lo1;
+        return k < U * U ? static_cast<size_t>(k / U) * (U + 8) + k % U : static_cast<size_t>(k - U * U) * (U + 8) + U;
+    }
+    const int k = i - sp.lo0;  // W0 row-major, then b0 (pad column d of the feature tile)
+    const size_t base = static_cast<size_t>(U) * (U + 8);
+    return k < U * sp.d ? base + static_cast<size_t>(k / sp.d) * sp.dp + k % sp.d
+                        : base + static_cast<size_t>(k - U * sp.d) * sp.dp + sp.d;
 }
 
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
@@ -737,7 +743,7 @@ struct Trainer {
             h1t.alloc(tsz);
             g2t.alloc(tsz);
             g1t.alloc(tsz);
-            gpartB.alloc(static_cast<size_t>(tc_wgrad_max_ctas(ctx->sm_count)) * (n.u * n.u + n.u * dp) * 4);
+            gpartB.alloc(static_cast<size_t>(tc_wgrad_max_ctas(ctx->sm_count)) * (n.u * (n.u + 8) + n.u * dp) * 4);
             wimg.alloc(tc_weight_image_bytes(n.u, dp));
             x_rows = std::max(max_rows, max_batch);
             ld_x = ((x_rows + 64 + 3) / 4) * 4;  // slack for the 64-row chunk loads
@@ -819,8 +825,8 @@ struct Trainer {
             }
             const int nB = launch_wgrad_tc(n.u, wa, ctx->sm_count, ctx->stream);
             check_launch(ctx);
-            if (sp) *sp = SplitPartials{gpartB.as<float>(), nB, n.off[0], n.off[0] + n.u * n.d, n.off[1],
-                                        n.off[1] + n.u * n.u, n.u * n.u + n.u * dp, n.u, n.d, dp};
+            if (sp) *sp = SplitPartials{gpartB.as<float>(), nB, n.off[0], n.off[0] + n.u * n.d + n.u, n.off[1],
+                                        n.off[1] + n.u * n.u + n.u, n.u * (n.u + 8) + n.u * dp, n.u, n.d, dp};
             return ctas;
         }
         const int tiles = static_cast<int>((b1 - b0 + TR - 1) / TR);

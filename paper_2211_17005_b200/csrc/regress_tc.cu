@@ -236,9 +236,9 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     constexpr int NB = (UH + 31) / 32;
     double loss = 0.0, dmu = 0.0, mn = INFINITY;
     float gb2 = 0.0f;
-    float acc_w2[NB], acc_b1[NB], acc_b0[NB];
+    float acc_w2[NB];  // output-layer gradient; the hidden biases come from the weight-gradient GEMMs
 #pragma unroll
-    for (int b = 0; b < NB; ++b) acc_w2[b] = acc_b1[b] = acc_b0[b] = 0.0f;
+    for (int b = 0; b < NB; ++b) acc_w2[b] = 0.0f;
 
     for (; tile < t_end; tile += gridDim.x) {
         const long row = tile * 128 + r;
@@ -351,7 +351,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             if (live)
 #pragma unroll
                 for (int j = 0; j < UH; ++j) a.G2t[(cb + j) * a.ld_t + trow] = g[j];
-            colsum_acc<UH>(g, acc_b1, lane);
         }
         cta_sync();
         // ---- B: Dbp = G2 W1 (B operand: the W1^T tile, K-major over the outputs of layer 1)
@@ -368,7 +367,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             if (live)
 #pragma unroll
                 for (int j = 0; j < UH; ++j) a.G1t[(cb + j) * a.ld_t + trow] = g[j];
-            colsum_acc<UH>(g, acc_b0, lane);
         }
         tc::fence_before_sync();
         __syncthreads();  // TMEM reads of D0 / Dbp done before the next tile's F0
@@ -387,8 +385,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         for (int b = 0; b < NB; ++b) {
             const int c = cb + b * 32 + lane;
             part[(warp * 3 + 0) * 64 + c] = acc_w2[b];
-            part[(warp * 3 + 1) * 64 + c] = acc_b1[b];
-            part[(warp * 3 + 2) * 64 + c] = acc_b0[b];
         }
     loss = warp_sum(loss);
     dmu = warp_sum(dmu);
@@ -411,8 +407,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
                        part[((w0q + 2) * 3 + k) * 64 + tid] + part[((w0q + 3) * 3 + k) * 64 + tid];
             };
             gout[a.off2 + tid] = sum4(0);
-            gout[a.off1 + U * U + tid] = sum4(1);
-            gout[a.off0 + U * a.d + tid] = sum4(2);
         }
         if (tid == 0) {
             a.lpart[cta] = red[0] + red[1] + red[2] + red[3];  // warpgroup 0 holds the per-row terms
@@ -536,24 +530,28 @@ __device__ __forceinline__ float4 ld4(const float* p, bool vec, int valid) {
 // three CTAs per SM, whose load / split / MMA phases interleave.
 constexpr int kWgThreads = 256;
 constexpr int kWgK = 32;                     // batch rows per chunk (the MMAs' K)
-constexpr uint32_t kWgTile = 64 * kWgK * 4;  // one plane of a chunk tile
-constexpr size_t kWgSmem = 8 * static_cast<size_t>(kWgTile) + 64 + 1024;
+constexpr uint32_t kWgTile = 64 * kWgK * 4;   // one plane of a 64-row chunk tile
+constexpr uint32_t kWgTileB1 = 72 * kWgK * 4; // H1t tile: U rows + a row of ones (+ zero rows to 8)
+constexpr size_t kWgSmem = 6 * static_cast<size_t>(kWgTile) + 2 * static_cast<size_t>(kWgTileB1) + 64 + 1024;
 
 template <int U>
 __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* tA1 = sm;                // G2t chunk: 64 (o, zero-padded) x kWgK (rows)
-    uint8_t* tB1 = sm + 2 * kWgTile;  // H1t chunk: U x kWgK
-    uint8_t* tA0 = sm + 4 * kWgTile;  // G1t chunk
-    uint8_t* tB0 = sm + 6 * kWgTile;  // Xt chunk: dp x kWgK
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 8 * kWgTile);
+    // The row of ones in tB1 (row U) and tB0 (row d, a pad column of the
+    // features) turns the last output columns into the bias gradients
+    // sum_r G2[r][o] (gb1) and sum_r G1[r][o] (gb0).
+    uint8_t* tA1 = sm;                                // G2t chunk: 64 (o, zero-padded) x kWgK (rows)
+    uint8_t* tA0 = sm + 2 * kWgTile;                  // G1t chunk
+    uint8_t* tB0 = sm + 4 * kWgTile;                  // Xt chunk: dp x kWgK, row d = 1
+    uint8_t* tB1 = sm + 6 * kWgTile;                  // H1t chunk: U x kWgK, row U = 1
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(tB1 + 2 * kWgTileB1);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int dp = a.dp;
     if (t == 0) tc::mbar_init(mbar, 1);
-    if (warp == 0) tc::tmem_alloc(tbase, 128);
-    for (int i = t; i < 8 * kWgTile / 16; i += kWgThreads)
+    if (warp == 0) tc::tmem_alloc(tbase, 256);
+    for (int i = t; i < (6 * kWgTile + 2 * kWgTileB1) / 16; i += kWgThreads)
         reinterpret_cast<float4*>(sm)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     tc::fence_before_sync();
     __syncthreads();
@@ -582,7 +580,7 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
-            if (f < dp) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
+            if (f < dp && f != a.d) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
         }
     };
     uint32_t phase = 0;
@@ -598,14 +596,21 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
             if (f < U) {
                 tc::put_split4_sw(tA1, kWgTile, f, k, 64, rg2[i]);
-                tc::put_split4_sw(tB1, kWgTile, f, k, 64, rh1[i]);
+                tc::put_split4_sw(tB1, kWgTileB1, f, k, 72, rh1[i]);
                 tc::put_split4_sw(tA0, kWgTile, f, k, 64, rg1[i]);
             }
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
-            if (f < dp) tc::put_split4_sw(tB0, kWgTile, f, k, 64, rx[i]);
+            if (f < dp && f != a.d) tc::put_split4_sw(tB0, kWgTile, f, k, 64, rx[i]);
+        }
+        if (t < 2 * Q) {  // the rows of ones (1 for the chunk's live rows, 0 past the batch end)
+            const int k = (t % Q) * 4, n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
+            const float4 one = make_float4(k < n ? 1.0f : 0.0f, k + 1 < n ? 1.0f : 0.0f, k + 2 < n ? 1.0f : 0.0f,
+                                           k + 3 < n ? 1.0f : 0.0f);
+            if (t < Q) tc::put_split4_sw(tB1, kWgTileB1, U, k, 72, one);
+            else tc::put_split4_sw(tB0, kWgTile, a.d, k, 64, one);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -614,9 +619,9 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
         if (warp == 0) {
             const uint32_t R64 = 64;
             tc::gemm3_sw_warp(tm, tc::OperandSW{tc::smem_u32(tA1), kWgTile, R64, 0},
-                              tc::OperandSW{tc::smem_u32(tB1), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, U, 0, 0),
-                              !first, nullptr);
-            tc::gemm3_sw_warp(tm + 64, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
+                              tc::OperandSW{tc::smem_u32(tB1), kWgTileB1, 72u, 0}, kWgK,
+                              tc::idesc_tf32(64, U + 8, 0, 0), !first, nullptr);
+            tc::gemm3_sw_warp(tm + 128, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
                               tc::OperandSW{tc::smem_u32(tB0), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, dp, 0, 0),
                               !first, mbar);
         }
@@ -627,35 +632,36 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
         tc::mbar_wait(mbar, phase);
         tc::fence_after_sync();
     }
-    // Partial row of this CTA: W1 [U][U] then W0 [U][dp] (16-byte stores).
-    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * (U * U + U * dp);
+    // Partial row of this CTA: W1 [U][U+8] (column U = gb1) then W0 [U][dp]
+    // (column d = gb0), 16-byte stores.
+    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * (U * (U + 8) + U * dp);
     if (warp < 4) {
         const int o = warp * 16 + lane;  // M=64 accumulator: row 16w+t in lane 32w+t, t < 16
         const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
         const bool own = lane < 16 && o < U;
 #pragma unroll
-        for (int c = 0; c < U; c += 16) {
-            float v[16];
-            tc::tmem_ld16(tm + lane_base + c, v);
+        for (int c = 0; c < U + 8; c += 8) {
+            float v[8];
+            tc::tmem_ld8(tm + lane_base + c, v);
             if (own)
 #pragma unroll
-                for (int q = 0; q < 16; q += 4)
-                    *reinterpret_cast<float4*>(gout + o * U + c + q) =
+                for (int q = 0; q < 8; q += 4)
+                    *reinterpret_cast<float4*>(gout + o * (U + 8) + c + q) =
                         first ? make_float4(0.0f, 0.0f, 0.0f, 0.0f) : make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
         }
         for (int c = 0; c < dp; c += 16) {
             float v[16];
-            tc::tmem_ld16(tm + lane_base + 64 + c, v);
+            tc::tmem_ld16(tm + lane_base + 128 + c, v);
             if (own)
 #pragma unroll
                 for (int q = 0; q < 16; q += 4)
-                    *reinterpret_cast<float4*>(gout + U * U + o * dp + c + q) =
+                    *reinterpret_cast<float4*>(gout + U * (U + 8) + o * dp + c + q) =
                         first ? make_float4(0.0f, 0.0f, 0.0f, 0.0f) : make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
         }
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tm, 128);
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
 // Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T; test hook for the
@@ -765,11 +771,13 @@ __global__ void k_tc_rate(int M, int N, int iters, float* sink) {
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
-    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && d <= 64 &&
-           tile_tc_smem(u, ((d + 15) / 16) * 16) <= 227 * 1024;
+    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && d <= 63 &&  // dp = tc_dp(d) <= 64
+           tile_tc_smem(u, ((d + 16) / 16) * 16) <= 227 * 1024;
 }
 
-int tc_dp(int d) { return ((d + 15) / 16) * 16; }
+// Input width padded for the tensor-core tiles, with at least one pad column:
+// the weight-gradient kernel puts a row of ones there (bias gradient of layer 0).
+int tc_dp(int d) { return ((d + 16) / 16) * 16; }
 
 void launch_pack_w(int u, int d, int dp, int off0, int off1, int off2, int P, const float* params, uint8_t* wimg,
                    cudaStream_t s) {
@@ -831,7 +839,7 @@ int launch_gram_h2(int u, const float* H2, const double* y, long R, const float*
     return launch_gram_u<64>(H2, y, R, params, P, gpart, ctas, s);
 }
 
-int tc_wgrad_max_ctas(int sm_count) { return 3 * sm_count; }
+int tc_wgrad_max_ctas(int sm_count) { return 2 * sm_count; }  // 256 TMEM columns each
 
 // Returns the number of weight-gradient partials written.
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
@@ -839,7 +847,7 @@ int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
     static const int per_sm = [] {  // CTAs per SM (profiling override HCVA_WGRAD_SLOTS)
         const char* e = std::getenv("HCVA_WGRAD_SLOTS");
         const int v = e ? std::atoi(e) : 2;  // 2 measured best (partials vs overlap)
-        return v < 1 ? 1 : (v > 3 ? 3 : v);
+        return v < 1 ? 1 : (v > 2 ? 2 : v);
     }();
     const long slots = static_cast<long>(per_sm) * sm_count;  // resident CTAs
     const long per = std::max(1L, (chunks + slots - 1) / slots);
