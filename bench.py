@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-learning", action="store_true", help="skip metric 2 (CVA learning time)")
     ap.add_argument("--learning-steps", type=int, default=0, help="pricing steps for metric 2 (default: all)")
+    ap.add_argument("--learning-timeout", type=float, default=600.0,
+                    help="N > 1: abort (exit 3) if the sharded learning leg exceeds this many seconds")
     return ap.parse_args()
 
 
@@ -398,9 +400,21 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
     sim.labels_all(cfg.label_kind, to_host=False)
     ctx.synchronize()
     t1 = time.perf_counter()
+    watchdog = None
+    if world > 1:  # a stuck collective must not hang the scaling run: fail loudly instead
+        def _abort():
+            sys.stderr.write(f"bench: rank {rank}: multi-GPU learning leg exceeded {args.learning_timeout} s\n")
+            sys.stderr.flush()
+            os._exit(3)
+
+        watchdog = threading.Timer(args.learning_timeout, _abort)
+        watchdog.daemon = True
+        watchdog.start()
     models = rg.backward_learn(sim, t, cfg.label_kind, comm=comm)
     p, mean, scale, rep = models.get(1)
     t2 = time.perf_counter()
+    if watchdog is not None:
+        watchdog.cancel()
     total, sim_s, train_s = t2 - t0, t1 - t0, t2 - t1
     if world > 1:  # max over ranks
         tt = torch.tensor([total, sim_s, train_s], device="cuda", dtype=torch.float64)
