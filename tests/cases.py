@@ -35,6 +35,14 @@ def _desk_corr():
     return c.tolist()
 
 
+def _c5_uniforms():
+    """256 uniforms of RandomStream(7).split(99) (rng.cpp:69-72), restated."""
+    import oracle_api  # test infrastructure: the restated RNG
+
+    R = oracle_api.restatement()
+    return [float(x) for x in R.uniforms(R.key(7, 99), 0, 256)]
+
+
 def case(name):
     if name == "minimal":
         j = _load("minimal.json")
@@ -60,6 +68,18 @@ def case(name):
         j = _load("paper_shape.json")
         j["grid"] = {"pricing_steps": 100, "substeps": 25, "dt_years": 0.25}
         j["simulation"] = {"paths": 16384, "replicas": 128}
+        return j
+    if name == "c5":
+        # paper_shape economies, 64 clients with CIR parameters drawn
+        # uniformly (alpha [0.3,0.7], delta [0.02,0.08], nu [0.05,0.15], gamma0
+        # [0.01,0.06]) from RandomStream(7).split(99), 500 swaps, M=2^17, N=2^8.
+        j = _load("paper_shape.json")
+        u = _c5_uniforms()
+        j["model"]["clients"] = [
+            {"alpha": 0.3 + 0.4 * u[4 * c], "delta": 0.02 + 0.06 * u[4 * c + 1],
+             "nu": 0.05 + 0.10 * u[4 * c + 2], "gamma0": 0.01 + 0.05 * u[4 * c + 3]} for c in range(64)]
+        j["grid"] = {"pricing_steps": 100, "substeps": 25, "dt_years": 0.25}
+        j["simulation"] = {"paths": 131072, "replicas": 256}
         return j
     if name == "c2_annual":
         j = case("c2")

@@ -25,6 +25,7 @@ SPECS = [
     ("c1", 48, 16, [0, 10, 25, 49, 50], 25, (5, 2, 32), 10),
     ("desk_corr", 40, 8, [0, 3, 6, 12], 6, (6, 3, 24), 3),
     ("c2", 12, 8, [0, 20, 50, 99, 100], 50, (50, 2, 8), 20),
+    ("c5", 8, 4, [0, 50, 100], 50, (50, 2, 4), 20),
 ]
 
 
@@ -80,5 +81,7 @@ if __name__ == "__main__":
     if ref is None:
         raise SystemExit("compiled reference unavailable (needs /root/reference)")
     kats(ref)
+    only = set(sys.argv[1:])
     for spec in SPECS:
-        make(ref, *spec)
+        if not only or spec[0] in only:
+            make(ref, *spec)

@@ -149,3 +149,32 @@ def test_batch_divisibility_is_config_error():
     cfg.training.n_batches = 7
     with pytest.raises(hcva.ConfigError):
         rg.backward_learn(sim, cfg.training)
+
+
+def test_backward_learn_c5_shape_simt_path():
+    """C5's feature width (64 clients: d = 64 + 29 + 64 = 157 > the tensor-core
+    tile's 63) runs the SIMT trainer; per step it must match the FP64 oracle."""
+    import json
+
+    j = cases.case("c5")
+    j["grid"] = {"pricing_steps": 4, "substeps": 4, "dt_years": 0.25}
+    cfg = hcva.parse_config(json.dumps(j))
+    t = cfg.training
+    t.width, t.n_batches, t.epochs = 16, 4, 4
+    book = hcva.generate_book(cfg)
+    sim = hcva.simulate_set(cfg, book, 16, 4, hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM))
+    models = rg.backward_learn(sim, t, "defaults")
+    assert models.input_dim == 157
+    R = oracle_api.restatement()
+    mk, st, cube = sim.market_arrays(), sim.default_steps(), sim.cube_values()
+    for i in range(cfg.n_steps, 0, -1):
+        p, mean, scale, rep = models.get(i)
+        x = (R.features(i, mk, st) - mean) / scale
+        y = R.defaults_label(i, mk, st, cube, cfg.dt).reshape(-1)
+        start = models.get(i + 1)[0] if i < cfg.n_steps else R.init_network(
+            x.shape[1], t.hidden_layers, t.width, R.key(cfg.seed, 0xBEEF, i))
+        if i == cfg.n_steps:
+            start[-1] = float(np.mean(y))
+        bo, ro = R.train_base(x, y, start, t.hidden_layers, t.width, t.n_batches, t.epochs, t.learning_rate)
+        assert rep["best_loss"] == pytest.approx(ro["best_loss"], rel=1e-3, abs=1e-12), i
+

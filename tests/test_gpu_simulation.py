@@ -19,7 +19,7 @@ import paper_2211_17005_b200 as hcva
 
 pytestmark = pytest.mark.gpu
 
-GOLDEN = ["minimal", "c1", "desk_corr", "c2"]
+GOLDEN = ["minimal", "c1", "desk_corr", "c2", "c5"]
 MARKET_RTOL = 1e-11
 
 

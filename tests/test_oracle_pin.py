@@ -18,7 +18,7 @@ import cases
 import oracle_api
 from paper_2211_17005_b200.config import parse_config
 
-GOLDEN = ["minimal", "c1", "desk_corr", "c2"]
+GOLDEN = ["minimal", "c1", "desk_corr", "c2", "c5"]
 
 
 @pytest.fixture(scope="module")

@@ -9,7 +9,7 @@ import cases
 import oracle_api
 import paper_2211_17005_b200 as hcva
 
-GOLDEN = ["minimal", "c1", "desk_corr", "c2"]
+GOLDEN = ["minimal", "c1", "desk_corr", "c2", "c5"]
 
 
 def golden(name):
