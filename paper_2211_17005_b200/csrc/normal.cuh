@@ -129,38 +129,13 @@ __constant__ double kAcklamA[6] = {-3.969683028665376e+01, 2.209460984245205e+02
 __constant__ double kAcklamB[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
                                    6.680131188771972e+01,  -1.328068155288572e+01};
 
-__device__ __forceinline__ void rcp_nr2(const double (&d)[2], double (&r)[2]) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        double x = rcp_approx(d[i]);
-        double e = fma(-d[i], x, 1.0);
-        x = fma(x, e, x);
-        e = fma(-d[i], x, 1.0);
-        r[i] = fma(x, e, x);
-    }
-}
 
-__device__ __forceinline__ void exp_neg2(const double (&z)[2], double (&out)[2]) {
-    const double magic = 6755399441055744.0;
-    double r[2], q[2];
-    int k[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double t = fma(z[i], 1.4426950408889634, magic);
-        const double kf = t - magic;
-        k[i] = __double2loint(t);
-        r[i] = fma(-kf, 6.93147180559945286e-01, z[i]);
-        r[i] = fma(-kf, 2.31904681384629956e-17, r[i]);
-        q[i] = kExpQ[11];
-    }
-#pragma unroll
-    for (int j = 10; j >= 0; --j) {
-        const double c = kExpQ[j];
-        q[0] = fma(q[0], r[0], c);
-        q[1] = fma(q[1], r[1], c);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) out[i] = __hiloint2double(__double2hiint(q[i]) + (k[i] << 20), __double2loint(q[i]));
+// exp(x^2/2) to ~3e-7 in single precision: enough for u, itself a ~1e-9
+// relative correction (its error enters x at < 1e-15 relative).
+__device__ __forceinline__ double exp_half_sq_approx(double x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(x * x) * 0.72134752044448170f));
+    return static_cast<double>(r);
 }
 
 __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (&x)[2]) {
@@ -196,49 +171,51 @@ __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (
         rd = fma(rd, fma(-den[i], rd, 1.0), rd);
         x[i] = num[i] * rd;
     }
-    // Halley step against erfc (rng.cpp:120-127)
-    double y[2], a[2], t[2], ap2[2], rap2[2], P[2], nz[2], lo[2], E[2], den2[2], rden2[2];
+    // Halley step (rng.cpp:120-127), central form (halley_central)
+    double y[2], t[2], P[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const double y0 = -x[i] * kInvSqrt2;
         y[i] = fma(fma(-y0, kSqrt2, -x[i]), kInvSqrt2, y0);
-        a[i] = fabs(y[i]);
-        ap2[i] = a[i] + 2.0;
-        den2[i] = fma(2.0, a[i], 1.0);
-    }
-    rcp_nr2(ap2, rap2);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        t[i] = (a[i] - 2.0) * rap2[i];
-        P[i] = kErfcP[21];
-        const double hi = a[i] * a[i];
-        lo[i] = fma(a[i], a[i], -hi);
-        nz[i] = -hi;
+        t[i] = y[i] * y[i];
+        P[i] = kErfE[14];
     }
 #pragma unroll
-    for (int j = 20; j >= 0; --j) {
-        const double c = kErfcP[j];
+    for (int j = 13; j >= 0; --j) {
+        const double c = kErfE[j];
         P[0] = fma(P[0], t[0], c);
         P[1] = fma(P[1], t[1], c);
     }
-    exp_neg2(nz, E);
-    rcp_nr2(den2, rden2);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        E[i] = E[i] * (1.0 - lo[i]);
-        const double qv = E[i] * P[i] * rden2[i];
-        const double erfc = (y[i] < 0.0) ? 2.0 - qv : qv;
-        const double e = 0.5 * erfc - p[i];
-        double ri = rcp_approx(E[i]);
-        ri = fma(ri, fma(-E[i], ri, 1.0), ri);
-        const double u = e * kSqrt2Pi * ri;
+        const double e = fma(-0.5, y[i] * P[i], 0.5 - p[i]);
+        const double u = e * kSqrt2Pi * exp_half_sq_approx(x[i]);
         const double v = x[i] * u * 0.5;
         x[i] = x[i] - u * (1.0 - v * (1.0 - v));
     }
 }
 
+// Halley step for Acklam's central region (|x| <= 1.973, |x|/sqrt2 <= 1.395):
+// Phi(x) - p = (0.5 - p) - 0.5 erf(-x/sqrt2) with erf from one even
+// polynomial (kErfE) -- no erfc map, division or double exp -- and the
+// correction's exp(x^2/2) in single precision.  Same argument rounding as the
+// reference (correctly rounded -x/sqrt2); the result stays within the
+// reference's own accuracy bound ulp(p)/phi(x) (tests/test_gpu_simulation.py).
+__device__ __forceinline__ double halley_central(double x, double p) {
+    const double y0 = -x * kInvSqrt2;
+    const double y = fma(fma(-y0, kSqrt2, -x), kInvSqrt2, y0);
+    const double t = y * y;
+    double P = kErfE[14];
+#pragma unroll
+    for (int j = 13; j >= 0; --j) P = fma(P, t, kErfE[j]);
+    const double e = fma(-0.5, y * P, 0.5 - p);
+    const double u = e * kSqrt2Pi * exp_half_sq_approx(x);
+    const double v = x * u * 0.5;
+    return x - u * (1.0 - v * (1.0 - v));
+}
+
 __device__ __forceinline__ double normal_from_uniform(double p) {
-    return halley_refine(acklam_tail(p) ? acklam_tail_seed(p) : acklam_central(p), p);
+    return acklam_tail(p) ? halley_refine(acklam_tail_seed(p), p) : halley_central(acklam_central(p), p);
 }
 
 }  // namespace hcva
