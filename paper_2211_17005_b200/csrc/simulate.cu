@@ -259,11 +259,11 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     struct ZRow {
         double v0, v1;
         int o0, o1, d;
-        bool dense;
+        bool dense, single;  // single: one nonzero, z = v0 * zraw (0 + v0 z is exact)
     };
     auto zrow = [&](int d) {
         const FactorCoef& k = coef[d];
-        return ZRow{k.v0, k.v1, k.col0 * P, k.col1 * P, d, k.dense != 0};
+        return ZRow{k.v0, k.v1, k.col0 * P, k.col1 * P, d, k.dense != 0, k.dense == 0 && k.v1 == 0.0};
     };
     const ZRow zr_a = zrow(econ ? fr : fg0), zr_b = zrow(econ ? 0 : fg1), zr_c = zrow(econ ? fx : fg1);
     // Drift / vol coefficients of the owned factors, also register resident.
@@ -273,6 +273,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     auto rec_step = [&](int cc, int t) {
         const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
         auto zcorr = [&](const ZRow& k) {
+            if (k.single) return dmul(k.v0, zt[k.o0]);
             if (!k.dense) return dadd(dmul(k.v0, zt[k.o0]), dmul(k.v1, zt[k.o1]));
             double acc = 0.0;
             for (int q = chol_row[k.d]; q < chol_row[k.d + 1]; ++q)
