@@ -142,7 +142,7 @@ struct hcva_sim {
     uint64_t m_local_offset = 0;
     size_t m_smem = 0;
     // MtM: coefficient tables (linear form) or the book (direct form)
-    hcva::DeviceBuf c_lnA, c_B, c_Nsuf, c_N, c_NSsuf, c_H, c_book, c_vas;
+    hcva::DeviceBuf c_lnA, c_B, c_dAB, c_Nsuf, c_N, c_NSsuf, c_H, c_book, c_vas;
     bool c_linear = true;
     int c_nswaps = 0;
     // per-phase CUDA events of re-runs: [slot][market, defaults, cube, labels, end]
