@@ -192,10 +192,8 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
     uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
     float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);  // [NS][128] partial output-layer sums
-    // [0] F1 / B MMAs, [1] weights, [2] features, [3] F0 MMAs (each barrier has
-    // at most one outstanding phase, as parity waits require)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 8 * 128);
-    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 4);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 8 * 128);  // [0] MMA, [1] weights, [2] features
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r = tid & 127, hf = tid >> 7, cb = hf * UH;
@@ -204,7 +202,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         tc::mbar_init(&bar[0], 1);
         tc::mbar_init(&bar[1], 1);
         tc::mbar_init(&bar[2], 1);
-        tc::mbar_init(&bar[3], 1);
         tc::fence_async_smem();
     }
     if (warp == 0) tc::tmem_alloc(tbase, 256);
@@ -222,16 +219,10 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
     }
     tc::mbar_wait(&bar[1], 0);
-    uint32_t mph = 0, xph = 0, fph = 0;
+    uint32_t mph = 0, xph = 0;
     auto mma_wait = [&]() {  // one waiting warp, the rest parked at the barrier
         if (warp == 0) tc::mbar_wait(&bar[0], mph);
         mph ^= 1;
-        __syncthreads();
-        tc::fence_after_sync();
-    };
-    auto f0_wait = [&]() {
-        if (warp == 0) tc::mbar_wait(&bar[3], fph);
-        fph ^= 1;
         __syncthreads();
         tc::fence_after_sync();
     };
@@ -249,28 +240,18 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
 #pragma unroll
     for (int b = 0; b < NB; ++b) acc_w2[b] = 0.0f;
 
-    // F0 of tile i+1 is issued right behind tile i's last GEMM, into the other
-    // of two D0 slots (TMEM columns 0 / 192), so it runs under tile i's last
-    // epilogue.  Issued by warp 0 once the feature tile has landed.
-    auto issue_f0 = [&](uint32_t slot) {
-        if (warp == 0) {
-            if (lane == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing lane reads the feature tile
-            __syncwarp();
-            tc::gemm3_warp(tm + slot, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp,
-                           tc::idesc_tf32(128, U, 0, 0), 0, &bar[3]);
-        }
-        xph ^= 1;
-    };
-    issue_f0(0);
-    for (int it = 0; tile < t_end; tile += gridDim.x, ++it) {
+    for (; tile < t_end; tile += gridDim.x) {
         const long row = tile * 128 + r;
         const bool live = row >= a.b0 && row < a.b1;
         const long trow = row - a.b0;
-        const uint32_t d0 = (it & 1) ? 192u : 0u;  // this tile's D0 slot
-        const bool more = tile + gridDim.x < t_end;
-        // ---- F0 (issued earlier): D0 = X W0^T
-        f0_wait();
-        if (tid == 0 && more) {  // feature tile consumed: stream in the next one
+        if (tid == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing thread reads the feature tile
+        xph ^= 1;
+        // ---- F0: D0 = X W0^T
+        if (warp == 0)
+            tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0),
+                           0, &bar[0]);
+        mma_wait();
+        if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
             tc::mbar_expect_tx(&bar[2], 2 * xb);
             tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
         }
@@ -279,7 +260,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         {
             const int c0 = cb;
             float v[UH];
-            tc::tmem_ldw<UH>(tm + lb + d0 + c0, v);
+            tc::tmem_ldw<UH>(tm + lb + c0, v);
 #pragma unroll
             for (int q = 0; q < UH; ++q) v[q] = act_f<ACT>(v[q] + vec[c0 + q]);
 #pragma unroll
@@ -291,7 +272,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
                     for (int q = 0; q < UH; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
 #pragma unroll
                 for (int q = 0; q < UH; ++q) v[q] = act_d<ACT>(v[q]);
-                tc::tmem_stw<UH>(tm + lb + d0 + c0, v);
+                tc::tmem_stw<UH>(tm + lb + c0, v);
             }
         }
         if (sgd) tc::tmem_wait_st();
@@ -300,7 +281,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         if (warp == 0)
             tc::gemm3_warp(tm + 64, tc::kmajor(bufH, hb, 128), tc::kmajor(w1, w1b, U), U,
                            tc::idesc_tf32(128, U, 0, 0), 0, &bar[0]);
-        if (!sgd && more) issue_f0(d0 ^ 192u);  // evaluation: F1 is this tile's last GEMM
         mma_wait();
         float h2[UH];
         tc::tmem_ldw<UH>(tm + lb + 64 + cb, h2);
@@ -377,12 +357,11 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         if (warp == 0)
             tc::gemm3_warp(tm + 128, tc::kmajor(bufH, hb, 128), tc::kmajor(w1t, w1b, U), U,
                            tc::idesc_tf32(128, U, 0, 0), 0, &bar[0]);
-        if (more) issue_f0(d0 ^ 192u);
         mma_wait();
         {
             float g[UH], dv[UH];
             tc::tmem_ldw<UH>(tm + lb + 128 + cb, g);
-            tc::tmem_ldw<UH>(tm + lb + d0 + cb, dv);
+            tc::tmem_ldw<UH>(tm + lb + cb, dv);
 #pragma unroll
             for (int q = 0; q < UH; ++q) g[q] = live ? g[q] * dv[q] : 0.0f;
             if (live)
@@ -390,7 +369,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
                 for (int j = 0; j < UH; ++j) a.G1t[(cb + j) * a.ld_t + trow] = g[j];
         }
         tc::fence_before_sync();
-        __syncthreads();  // TMEM reads of this D0 slot / Dbp done before they are written again
+        __syncthreads();  // TMEM reads of D0 / Dbp done before the next tile's F0
         tc::fence_after_sync();
     }
 
