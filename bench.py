@@ -51,6 +51,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-learning", action="store_true", help="skip metric 2 (CVA learning time)")
     ap.add_argument("--learning-steps", type=int, default=0, help="pricing steps for metric 2 (default: all)")
+    ap.add_argument("--no-nested", action="store_true", help="skip the nested MC benchmark (C4)")
+    ap.add_argument("--nested-step", type=int, default=5)
+    ap.add_argument("--nested-inner", type=int, default=128)
+    ap.add_argument("--nested-states", type=int, default=0, help="outer states (default: all validation paths)")
     ap.add_argument("--learning-timeout", type=float, default=600.0,
                     help="N > 1: abort (exit 3) if the sharded learning leg exceeds this many seconds")
     return ap.parse_args()
@@ -286,9 +290,14 @@ def ours_arm(args):
     e2e = None
     if not args.no_e2e:
         e2e = e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args)
-    learning = None
+    learning, models = None, None
     if not args.no_learning:
-        learning = learning_leg(hcva, cfg, book, ctx, args, rank, world)
+        learning, models = learning_leg(hcva, cfg, book, ctx, args, rank, world)
+    nested = None
+    if not args.no_nested:
+        del sim
+        nested = nested_leg(hcva, cfg, book, ctx, args, models, rank, world)
+    del models
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
@@ -313,6 +322,7 @@ def ours_arm(args):
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
             "cva_learning": learning,
+            "nested_mc": nested,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -444,12 +454,92 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
         cpu = {"value": full, "unit": "s (extrapolated)", "cores": 1, "kind": "port",
                "sample": f"train_base of step {cfg.n_steps} on {rows} rows: {sec:.2f} s, x{cfg.paths * cfg.replicas // rows}"
                          f" rows x {steps} steps (FP64 restatement of regressor.cpp; simulation not included)"}
-    return {"value": total, "unit": "s", "higher_is_better": False, "pricing_steps": steps, "cpu_baseline": cpu,
+    out = {"value": total, "unit": "s", "higher_is_better": False, "pricing_steps": steps, "cpu_baseline": cpu,
             "simulate_and_labels_s": sim_s, "backward_learn_s": train_s,
             "sgd_steps": steps * t.epochs * t.n_batches, "rows": cfg.paths * cfg.replicas, "n_gpus": world,
             "scaling": "strong (global C2 problem sharded by Y-path)" if world > 1 else None,
             "net": f"{t.hidden_layers}x{t.width} {t.activation}", "best_loss_step1": rep["best_loss"],
             "path": "hcva_simulate_set + hcva_labels_all + hcva_backward_learn (K1-K5, device resident)"}
+    return out, (models if steps == cfg.n_steps and world == 1 else None)
+
+
+def nested_leg(hcva, cfg, book, ctx, args, models=None, rank=0, world=1):
+    """BASELINE config 4: the nested Monte Carlo CVA benchmark (the accuracy
+    oracle, validation.cpp:123-179 as driven by pipeline.cpp:269-292) on the
+    paper case -- outer states = the validation set's paths at `step`
+    (root.split(2), N=1), `inner` conditional re-simulations per state from
+    root.split(2).split(3).split(step).split(s).  The paper quotes >= 32 min on
+    a V100 for 16384 states x 128 inner.  Timed: host states -> device ->
+    grouped conditional K1 + K2 + payoff/reduction -> values on the host (wall
+    clock around the synchronous call; max over ranks).  With N GPUs each rank
+    takes a contiguous block of states (no collective; the estimates are
+    per-state pure).  When the learning leg trained on one GPU, the nested
+    relative RMSE of its predictions (validation.cpp:181-210) is reported."""
+    import torch
+
+    step, inner = args.nested_step, args.nested_inner
+    vroot = hcva.RandomStream(cfg.seed).split(hcva.K_VALIDATION_SIM)
+    n_val = cfg.paths
+    val = hcva.simulate_set(cfg, book, n_val, 1, vroot, ctx=ctx)
+    states = min(args.nested_states or n_val, n_val)
+    lo, hi = rank * states // world, (rank + 1) * states // world
+    st, surv = val.states_at(step)
+    st = {k: np.ascontiguousarray(v[lo:hi]) for k, v in st.items()}
+    surv = np.ascontiguousarray(surv[lo:hi])
+    parent = vroot.split(3).split(step)
+    if world > 1:
+        torch.distributed.barrier()
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    value, se = hcva.nested_cva(cfg, book, st, surv, step, inner, parent, ctx=ctx, first_state=lo)
+    sec = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        sec = float(tt.item())
+    h = cfg.n_steps - step
+    normals = float(states) * inner * h * cfg.substeps * cfg.n_factors
+    out = {"value": sec, "unit": "s", "higher_is_better": False, "states": states, "inner": inner, "step": step,
+           "states_per_s": states / sec, "normals_per_s": normals / sec, "n_gpus": world,
+           "scaling": "strong (states split across ranks)" if world > 1 else None,
+           "mean_nested_cva": float(np.mean(value)), "mean_std_error": float(np.mean(se)),
+           "path": "hcva_nested_cva_range (grouped conditional K1 + K2 + k_nested_payoff/k_nested_reduce)",
+           "paper_v100": ">= 32 min for 16384 states x 128 inner (PAPER.md:871)"}
+    if models is not None and world == 1:
+        pred = models.predict(step, val)[:states]
+        rm, rse, zero, used = hcva.nested_relative_rmse(pred, value)
+        out["relative_rmse"] = {"value": rm, "std_error": rse, "excluded_zero": zero, "used": used,
+                                "training": f"M={cfg.paths}, N={cfg.replicas}"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = nested_reference_sample(cfg, book, st, surv, step, inner, sec, states)
+    return out
+
+
+def nested_reference_sample(cfg, book, st, surv, step, inner, gpu_sec, states, seconds_target=10.0):
+    """The reference's own nested_cva (oracle/_ref, HIERCVA_THREADS = host
+    cores, inner paths in its parallel_for) on the first few states of the
+    same set, extrapolated linearly to all states."""
+    import cases
+    import oracle_api
+
+    ref = oracle_api.reference()
+    kind = "reference"
+    if ref is None:
+        ref, kind = oracle_api.restatement(), "port"
+    threads = cpu_threads()
+    os.environ["HIERCVA_THREADS"] = str(threads)
+    m = cases.oracle_model(cfg)
+    bk = np.ascontiguousarray(book, dtype=oracle_api.SWAP_DTYPE)
+    done, c0 = 0, time.perf_counter()
+    while done < states and (time.perf_counter() - c0 < seconds_target or done == 0):
+        one = {k: v[done] for k, v in st.items()}
+        ref.nested_cva(m, bk, one, surv[done], step, inner, ref.key(cfg.seed, 2, 3, step, done))
+        done += 1
+    sec = time.perf_counter() - c0
+    full = sec * states / done
+    return {"value": full, "unit": "s (extrapolated)", "cores": threads if kind == "reference" else 1, "kind": kind,
+            "sample": f"nested_cva on {done} of {states} states ({sec:.1f} s), x{states / done:.0f}",
+            "ratio_vs_gpu": full / gpu_sec}
 
 
 def main():

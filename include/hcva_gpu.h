@@ -187,6 +187,13 @@ hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const 
                                   const hcva_swap* book, int n_swaps, const double* states,
                                   const int* survived, int n_states, int step, int inner,
                                   uint64_t parent_key, double* value, double* std_error);
+/* The same for states first_state .. first_state+n_states-1 of a larger set
+ * (state s draws from split(parent_key, first_state + s)): one rank's
+ * contiguous block of outer states in the multi-GPU nested benchmark. */
+hcva_status hcva_nested_cva_range(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                  const hcva_swap* book, int n_swaps, const double* states,
+                                  const int* survived, int n_states, int first_state, int step, int inner,
+                                  uint64_t parent_key, double* value, double* std_error);
 
 /* save_market / load_market (pipeline.cpp:371-442): the HCVAMKT1 dump of a
  * set's market block; a loaded outer block becomes a set on which defaults,

@@ -136,6 +136,8 @@ def lib():
         "hcva_diag_special": [vp, C.c_int, vp, C.c_size_t, vp],
         "hcva_nested_cva_batch": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
                                   C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, u64, dptr, dptr],
+        "hcva_nested_cva_range": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
+                                  C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, u64, dptr, dptr],
         "hcva_net_size": [C.POINTER(TrainCfg), C.c_int, C.POINTER(C.c_int)],
         "hcva_init_network": [C.POINTER(TrainCfg), C.c_int, u64, dptr],
         "hcva_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, dptr, dptr],
@@ -191,7 +193,7 @@ EXPORTED = [
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
-    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch", "hcva_net_size",
+    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch", "hcva_nested_cva_range", "hcva_net_size",
     "hcva_init_network", "hcva_quadratic_loss", "hcva_train_base", "hcva_backward_learn", "hcva_models_info",
     "hcva_models_get", "hcva_predict", "hcva_models_destroy", "hcva_comm_nccl_id", "hcva_comm_create_nccl",
     "hcva_group_create", "hcva_group_destroy", "hcva_comm_create_local", "hcva_comm_info", "hcva_comm_destroy",

@@ -134,14 +134,15 @@ __global__ void k_twin(TwinArgs a) {
 
 using namespace hcva;
 
-extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+extern "C" hcva_status hcva_nested_cva_range(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
                                              const hcva_swap* book, int n_swaps, const double* states,
-                                             const int* survived, int n_states, int step, int inner,
-                                             uint64_t parent_key, double* value, double* std_error) {
+                                             const int* survived, int n_states, int first_state, int step,
+                                             int inner, uint64_t parent_key, double* value, double* std_error) {
     return guarded([&] {
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
         if (inner < 1) throw contract_error("nested_cva: inner_count must be >= 1");
+        if (first_state < 0) throw contract_error("nested_cva: negative first state");
         if (!grid) throw contract_error("nested_cva: null grid");
         const Model probe = make_model(model, grid);
         const int E = probe.E, Cn = probe.Cn, Cc = probe.Cc, D = probe.D;
@@ -169,7 +170,7 @@ extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* mo
             std::vector<int> surv(static_cast<size_t>(S) * Cc), any(S, 0);
             for (int s = 0; s < S; ++s) {
                 const double* st = states + static_cast<size_t>(s0 + s) * stride;
-                keys[s] = split_key(parent_key, static_cast<uint64_t>(s0 + s));
+                keys[s] = split_key(parent_key, static_cast<uint64_t>(first_state + s0 + s));
                 for (int e = 0; e < E; ++e) init[s * D + e] = st[e];
                 for (int e = 1; e < E; ++e) init[s * D + E + e - 1] = st[E + e - 1];
                 for (int c = 0; c < Cn; ++c) init[s * D + 2 * E - 1 + c] = st[2 * E - 1 + c];
@@ -210,6 +211,14 @@ extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* mo
         std::copy(val.begin(), val.end(), value);
         std::copy(err.begin(), err.end(), std_error);
     });
+}
+
+extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid,
+                                             const hcva_swap* book, int n_swaps, const double* states,
+                                             const int* survived, int n_states, int step, int inner,
+                                             uint64_t parent_key, double* value, double* std_error) {
+    return hcva_nested_cva_range(ctx, model, grid, book, n_swaps, states, survived, n_states, 0, step, inner,
+                                 parent_key, value, std_error);
 }
 
 extern "C" hcva_status hcva_twin_labels(hcva_sim* outer, const hcva_swap* book, int n_swaps, int step, uint64_t key,

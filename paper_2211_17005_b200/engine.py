@@ -295,6 +295,16 @@ class SimulationSet:
         return dict(rates=mk["rates"][k, i].copy(), log_fx=np.log(mk["fx"][k, i]),
                     intens=mk["intens"][k, i].copy(), lagged=mk["lagged"][k, i].copy())
 
+    def states_at(self, i: int, replica: int = 0) -> Tuple[Dict[str, np.ndarray], np.ndarray]:
+        """MarketState of every path at step i and the clients' survival to i on
+        `replica` -- the outer states of nested_cva (pipeline.cpp:276-288,
+        validation.cpp:129-131): (states dict of (M, .) arrays, survived (M, Cc))."""
+        mk = self.market_arrays()
+        st = dict(rates=np.ascontiguousarray(mk["rates"][:, i]), log_fx=np.log(mk["fx"][:, i]),
+                  intens=np.ascontiguousarray(mk["intens"][:, i]), lagged=np.ascontiguousarray(mk["lagged"][:, i]))
+        surv = self.default_steps()[:, replica, 1:] > i
+        return st, surv
+
     # -- labels and features -------------------------------------------
     def labels(self, step: int, kind: str = "defaults") -> np.ndarray:
         out = np.zeros((self.n_paths, self.n_replicas))
@@ -408,11 +418,12 @@ def build_mtm_cube(sim: SimulationSet, book: np.ndarray) -> SimulationSet:
 
 
 def nested_cva(cfg: PipelineConfig, book: np.ndarray, states: Dict[str, np.ndarray], survived: np.ndarray,
-               step: int, inner: int, parent: RandomStream, ctx: Optional[Context] = None):
+               step: int, inner: int, parent: RandomStream, ctx: Optional[Context] = None, first_state: int = 0):
     """nested_cva (validation.cpp:123-179) for a batch of outer states.
 
     states: dict of arrays rates (S,E), log_fx (S,E-1), intens (S,Cn), lagged (S,E);
-    survived: (S, Cc) bool; state s uses parent.split(s) (pipeline.cpp:284-288).
+    survived: (S, Cc) bool; state s uses parent.split(first_state + s) (pipeline.cpp:284-288),
+    so a rank holding states first_state.. of a larger set reproduces their estimates.
     Returns (value[S], std_error[S]).
     """
     ctx = ctx or context()
@@ -424,9 +435,10 @@ def nested_cva(cfg: PipelineConfig, book: np.ndarray, states: Dict[str, np.ndarr
     surv = np.ascontiguousarray(survived, dtype=np.int32)
     bk, bp = _swaps(book)
     val, se = np.zeros(S), np.zeros(S)
-    _lib.check(_lib.lib().hcva_nested_cva_batch(
+    _lib.check(_lib.lib().hcva_nested_cva_range(
         ctx.handle, C.byref(m), C.byref(g), bp, len(bk), packed.ctypes.data_as(_lib.dptr),
-        surv.ctypes.data_as(C.POINTER(C.c_int)), S, step, inner, parent.key, val.ctypes.data_as(_lib.dptr),
+        surv.ctypes.data_as(C.POINTER(C.c_int)), S, int(first_state), step, inner, parent.key,
+        val.ctypes.data_as(_lib.dptr),
         se.ctypes.data_as(_lib.dptr)))
     return val, se
 

@@ -248,3 +248,7 @@ def test_nested_batching_is_per_state_pure():
     # only the first states reproduces their estimates bit for bit
     v3, _ = hcva.nested_cva(cfg, z["book"], {k: v[0:3] for k, v in st.items()}, surv[0:3], step, 16, parent)
     assert np.array_equal(v3, all_v[:3])
+    # a rank's block of states (first_state > 0) reproduces the same states of the full set
+    v4, _ = hcva.nested_cva(cfg, z["book"], {k: v[3:7] for k, v in st.items()}, surv[3:7], step, 16, parent,
+                            first_state=3)
+    assert np.array_equal(v4, all_v[3:7])
