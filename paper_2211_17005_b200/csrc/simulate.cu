@@ -438,6 +438,108 @@ __global__ void __launch_bounds__(128) k_mtm_linear(MtmArgs a) {
     }
 }
 
+// NP paths per thread (k + 128 j of the CTA's 128 NP-path slab): the
+// warp-uniform coefficient loads (dA/dB, H rows), address arithmetic and loop
+// control are shared by the paths, and their independent ZC recurrences
+// interleave.  chi_e is folded into the running ZC (z' = chi z), so the client
+// accumulators take the maturity sum directly: acc_c += chi (lead Nsuf - N -
+// NSsuf) - sum_m z'_m H_{g+m} (same terms as k_mtm_linear, re-associated at
+// rounding level).  Requires Cc even (16-byte H loads).
+template <int CB, int NP>
+__global__ void __launch_bounds__(128) k_mtm_multi(MtmArgs a) {
+    const int M = a.M;
+    const int kb = blockIdx.x * (128 * NP) + threadIdx.x;
+    if (kb >= M) return;
+    int kp[NP];
+    bool own[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        own[j] = kb + 128 * j < M;
+        kp[j] = own[j] ? kb + 128 * j : kb;
+    }
+    const int i = blockIdx.y;
+    const int g = a.start + i;
+    const int E = a.E, Cc = a.Cc, n1 = a.n_total + 1;
+    for (int c0 = 0; c0 < Cc; c0 += CB) {
+        double acc[NP][CB];
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[j][c] = 0.0;
+        for (int e = 0; e < E; ++e) {
+            const size_t ri = (static_cast<size_t>(i) * E + e) * M;
+            const double* lnA = a.lnA + e * n1;
+            const double* B = a.B + e * n1;
+            double r[NP], z[NP], lead[NP], chi[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                r[j] = a.rates[ri + kp[j]];
+                chi[j] = (e > 0) ? a.fx[(static_cast<size_t>(i) * (E - 1) + e - 1) * M + kp[j]] : 1.0;
+                lead[j] = 1.0;
+                if (g > 0) {
+                    const double rl = (i > 0) ? a.rates[(static_cast<size_t>(i - 1) * E + e) * M + kp[j]]
+                                              : a.lag0[(kp[j] / a.paths_per_group) * E + e];
+                    lead[j] = 1.0 / exp(lnA[1] - B[1] * rl);
+                }
+            }
+            const size_t base = (static_cast<size_t>(e) * n1 + g) * Cc + c0;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (c0 + c < Cc) {
+                    const double ns = a.Nsuf[base + c], nn = a.N[base + c];
+                    const double nss = (g > 0) ? a.NSsuf[base + c] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) acc[j][c] += chi[j] * (lead[j] * ns - nn - nss);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NP; ++j) z[j] = chi[j] * exp_neg(lnA[1] - B[1] * r[j]);
+            const double2* dab = a.dAB + e * n1;
+            const double2* hrow = reinterpret_cast<const double2*>(a.H + (static_cast<size_t>(e) * n1 + g + 1) * Cc + c0);
+            const int hstep = Cc / 2;
+            for (int m = 1; g + m <= a.n_total; ++m, hrow += hstep) {
+                if (m > 1) {  // Z_m = Z_{m-1} exp(dA - dB r), degree-9 Taylor (|dA - dB r| <~ dt r)
+                    const double2 d = __ldg(dab + m - 1);
+                    double x[NP], q[NP];
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        x[j] = fma(-d.y, r[j], d.x);
+                        q[j] = 2.7557319223985893e-6;  // 1/9!
+                    }
+#define HCVA_TAYLOR_STEP(cf) _Pragma("unroll") for (int j = 0; j < NP; ++j) q[j] = fma(q[j], x[j], cf);
+                    HCVA_TAYLOR_STEP(2.4801587301587302e-5)
+                    HCVA_TAYLOR_STEP(1.9841269841269841e-4)
+                    HCVA_TAYLOR_STEP(1.3888888888888889e-3)
+                    HCVA_TAYLOR_STEP(8.3333333333333333e-3)
+                    HCVA_TAYLOR_STEP(4.1666666666666667e-2)
+                    HCVA_TAYLOR_STEP(1.6666666666666667e-1)
+                    HCVA_TAYLOR_STEP(0.5)
+                    HCVA_TAYLOR_STEP(1.0)
+#undef HCVA_TAYLOR_STEP
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) z[j] = z[j] * fma(q[j], x[j], 1.0);
+                }
+#pragma unroll
+                for (int c = 0; c < CB; c += 2)
+                    if (c0 + c < Cc) {
+                        const double2 hv = __ldg(hrow + c / 2);
+#pragma unroll
+                        for (int j = 0; j < NP; ++j) {
+                            acc[j][c] = fma(-z[j], hv.x, acc[j][c]);
+                            acc[j][c + 1] = fma(-z[j], hv.y, acc[j][c + 1]);
+                        }
+                    }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (c0 + c < Cc)
+#pragma unroll
+                for (int j = 0; j < NP; ++j)
+                    if (own[j]) a.cube[(static_cast<size_t>(i) * Cc + c0 + c) * M + kp[j]] = acc[j][c];
+    }
+}
+
 // Direct per-swap pricing in the reference's loop and summation order
 // (portfolio.cpp:58-147) for books that do not reset every pricing step.
 struct DirectArgs {
@@ -1033,7 +1135,16 @@ void launch_cube(hcva_sim* sim) {
         a.N = sim->c_N.as<double>(); a.NSsuf = sim->c_NSsuf.as<double>(); a.H = sim->c_H.as<double>();
         a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.lag0 = sim->lag0.as<double>();
         a.cube = sim->cube.as<double>();
-        k_mtm_linear<8><<<grid, 128, 0, ctx->stream>>>(a);
+        const char* env = std::getenv("HCVA_K2_NP");
+        const int np = env ? std::atoi(env) : 4;
+        if (m.Cc % 2 == 0 && np > 1) {
+            dim3 g2((sim->M + 128 * np - 1) / (128 * np), sim->n + 1);
+            if (np >= 4) k_mtm_multi<8, 4><<<g2, 128, 0, ctx->stream>>>(a);
+            else if (np == 3) k_mtm_multi<8, 3><<<g2, 128, 0, ctx->stream>>>(a);
+            else k_mtm_multi<8, 2><<<g2, 128, 0, ctx->stream>>>(a);
+        } else {
+            k_mtm_linear<8><<<grid, 128, 0, ctx->stream>>>(a);
+        }
     } else {
         DirectArgs a{};
         a.E = m.E; a.Cc = m.Cc; a.M = sim->M; a.n_local = sim->n; a.start = sim->start_step; a.n_swaps = sim->c_nswaps;
