@@ -720,50 +720,57 @@ __global__ void __launch_bounds__(128) k_labels_defaults(LabelArgs a) {
 // Register form for Cc <= CMAX: each replica's default steps, the discount at
 // its default step and the exposure there are loop invariants over the label
 // step i, so per (i, c) only (inv_i * beta_s) * exposure remains -- the same
-// rounded products, summed in client order.
-template <int CMAX>
+// rounded products, summed in client order.  A CTA takes PP consecutive paths
+// so the staging reads of the path-fastest SoA market / cube use whole sectors.
+template <int CMAX, int PP>
 __global__ void __launch_bounds__(128) k_labels_defaults_reg(LabelArgs a) {
     extern __shared__ double sm[];
-    const int k = blockIdx.x;
+    const int k0 = blockIdx.x * PP;
+    const int np = min(PP, a.M - k0);
     const int n1 = a.n + 1, Cc = a.Cn - 1;
-    double* disc = sm;             // [n1]
-    double* inv = sm + n1;         // [n1]
-    double* expo = sm + 2 * n1;    // [n1][Cc]
-    for (int t = threadIdx.x; t < n1; t += blockDim.x) {
-        disc[t] = a.disc[static_cast<size_t>(t) * a.M + k];
-        inv[t] = 1.0 / disc[t];
+    double* disc = sm;                 // [n1][PP]
+    double* inv = sm + n1 * PP;        // [n1][PP]
+    double* expo = sm + 2 * n1 * PP;   // [n1][Cc][PP]
+    for (int t = threadIdx.x; t < n1 * PP; t += blockDim.x) {
+        const int i = t / PP, p = t % PP;
+        const double d = (p < np) ? a.disc[static_cast<size_t>(i) * a.M + k0 + p] : 1.0;
+        disc[t] = d;
+        inv[t] = 1.0 / d;
     }
-    for (int t = threadIdx.x; t < n1 * Cc; t += blockDim.x) {
-        const int i = t / Cc, c = t % Cc;
-        const double v = a.cube[(static_cast<size_t>(i) * Cc + c) * a.M + k];
+    for (int t = threadIdx.x; t < n1 * Cc * PP; t += blockDim.x) {
+        const int ic = t / PP, p = t % PP;
+        const double v = (p < np) ? a.cube[static_cast<size_t>(ic) * a.M + k0 + p] : 0.0;
         expo[t] = (v < 0.0) ? 0.0 : v;
     }
     __syncthreads();
     const size_t R = static_cast<size_t>(a.M) * a.N;
-    for (int l = threadIdx.x; l < a.N; l += blockDim.x) {
-        const size_t row = static_cast<size_t>(k) * a.N + l;
+    for (int idx = threadIdx.x; idx < np * a.N; idx += blockDim.x) {
+        const int p = idx / a.N;
+        const size_t row = static_cast<size_t>(k0) * a.N + idx;
+        // w_c = beta_s * exposure_s at client c's default step s; the label at i
+        // is beta_i^-1 * sum_{c: s_c > i} w_c (clients ascending) -- the
+        // reference's (beta_i^-1 beta_s) exposure products re-associated, equal
+        // to a few ulp, with one FP64 multiply per step instead of 2 Cc.
         int st[CMAX];
-        double ds[CMAX], ex[CMAX];
+        double w[CMAX];
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) {
             st[c] = -1;
-            ds[c] = ex[c] = 0.0;
+            w[c] = 0.0;
             if (c < Cc) {
                 const int s = a.steps[(c + 1) * R + row];
                 if (s <= a.n) {
                     st[c] = s;
-                    ds[c] = disc[s];
-                    ex[c] = expo[s * Cc + c];
+                    w[c] = __dmul_rn(disc[s * PP + p], expo[(s * Cc + c) * PP + p]);
                 }
             }
         }
         for (int i = a.i0; i <= a.i1; ++i) {
-            const double vi = inv[i];
             double sum = 0.0;
 #pragma unroll
             for (int c = 0; c < CMAX; ++c)
-                if (st[c] > i) sum = __dadd_rn(sum, __dmul_rn(__dmul_rn(vi, ds[c]), ex[c]));
-            a.out[static_cast<size_t>(i - a.i0) * R + row] = sum;
+                if (st[c] > i) sum = __dadd_rn(sum, w[c]);
+            a.out[static_cast<size_t>(i - a.i0) * R + row] = __dmul_rn(inv[i * PP + p], sum);
         }
     }
 }
@@ -1215,16 +1222,22 @@ void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t*
         const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc);
         if (smem > 48 * 1024)
             HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        if (Cc <= 8) {
-            if (smem > 48 * 1024)
-                HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_reg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem)));
-            k_labels_defaults_reg<8><<<sim->M, threads, smem, ctx->stream>>>(a);
-        } else if (Cc <= 16) {
-            if (smem > 48 * 1024)
-                HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_reg<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem)));
-            k_labels_defaults_reg<16><<<sim->M, threads, smem, ctx->stream>>>(a);
+        const char* env = std::getenv("HCVA_K4_PP");
+        const int pp = env ? std::atoi(env) : 1;
+        if (Cc <= 16) {
+            const int PPc = (pp >= 4) ? 4 : (pp >= 2 ? 2 : 1);
+            const size_t smr = smem * PPc;
+            const void* fn = Cc <= 8 ? (PPc == 4 ? (const void*)k_labels_defaults_reg<8, 4>
+                                                 : PPc == 2 ? (const void*)k_labels_defaults_reg<8, 2>
+                                                            : (const void*)k_labels_defaults_reg<8, 1>)
+                                     : (PPc == 4 ? (const void*)k_labels_defaults_reg<16, 4>
+                                                 : PPc == 2 ? (const void*)k_labels_defaults_reg<16, 2>
+                                                            : (const void*)k_labels_defaults_reg<16, 1>);
+            if (smr > 48 * 1024)
+                HCVA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smr)));
+            const int thr = std::min(128, ((PPc * N + 31) / 32) * 32);
+            void* args[] = {&a};
+            HCVA_CUDA(cudaLaunchKernel(fn, dim3((sim->M + PPc - 1) / PPc), dim3(thr), args, smr, ctx->stream));
         } else {
             k_labels_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
         }
