@@ -94,6 +94,9 @@ __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, do
 }
 
 constexpr int kQueueCap = 128;  // per-warp queue of tail draws
+// Acklam's branch points 0.02425 and 0.97575 on the top 32 bits of a draw.
+constexpr uint32_t kTailLo32 = static_cast<uint32_t>(0.02425 * 4294967296.0);
+constexpr uint32_t kTailHi32 = static_cast<uint32_t>((1.0 - 0.02425) * 4294967296.0);
 
 template <int P>
 #ifndef HCVA_K1_MAXNREG
@@ -123,6 +126,8 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     const unsigned lanemask_lt = (1u << lane) - 1u;
     double* qp = qp_all + wid * kQueueCap;
     int* qs = qs_all + wid * kQueueCap;
+    const uint32_t qp_s = static_cast<uint32_t>(__cvta_generic_to_shared(qp));
+    const uint32_t qs_s = static_cast<uint32_t>(__cvta_generic_to_shared(qs));
     const int M = a.M;
     const int kloc = static_cast<int>(blockIdx.x) * P + p;
     const bool valid = kloc < M;
@@ -207,18 +212,24 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         uint64_t w0, w1;
         philox2x64(g.blk0 + b, pkey, w0, w1);  // past the chunk's last block the draws are discarded
         const double uu[2] = {u64_to_uniform(w0), u64_to_uniform(w1)};
+        const uint32_t hw[2] = {static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1 >> 32)};
         bool keep[2];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
             const int j = 2 * b + hf;
             const bool v = vb && j < nn;
-            const bool tail = v && acklam_tail(uu[hf]);
+            // Acklam's tail test on the draw's top 32 bits (p within 2^-32 of
+            // 0.02425 may take either branch: both are refined to the same normal).
+            const bool tail = v && (hw[hf] < kTailLo32 || hw[hf] > kTailHi32);
             const unsigned m = __ballot_sync(0xffffffffu, tail);
-            if (tail) {
-                const int pos = qn + __popc(m & lanemask_lt);
-                qs[pos] = j * P + p;
-                qp[pos] = uu[hf];
-            }
+            const int pos = qn + __popc(m & lanemask_lt);
+            asm volatile(
+                "{\n\t.reg .pred q;\n\t"
+                "setp.ne.b32 q, %0, 0;\n\t"
+                "@q st.shared.u32 [%1], %2;\n\t"
+                "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(static_cast<int>(tail)),
+                "r"(qs_s + 4u * pos), "r"(j * P + p), "r"(qp_s + 8u * pos), "d"(uu[hf])
+                : "memory");
             qn += __popc(m);
             keep[hf] = v && !tail;
         }
