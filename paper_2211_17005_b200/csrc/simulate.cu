@@ -786,6 +786,82 @@ __global__ void __launch_bounds__(128) k_labels_defaults_reg(LabelArgs a) {
     }
 }
 
+// CVA profile without materialising the labels (defaults kind): the register
+// form of k_labels_defaults_reg per path, each step's labels summed over the
+// path's replicas (warp shuffles, then the warps in fixed order) into
+// part[i][k]; k_profile_paths sums the paths.  1.7 GB of label stores and
+// re-reads at C2 become 13 MB of per-path sums.
+template <int CMAX>
+__global__ void __launch_bounds__(128) k_profile_defaults(LabelArgs a, double* part) {
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cc = a.Cn - 1;
+    constexpr int NW = 4;              // 128 threads
+    double* disc = sm;                 // [n1]
+    double* inv = sm + n1;             // [n1]
+    double* expo = sm + 2 * n1;        // [n1][Cc]
+    double* red = expo + n1 * Cc;      // [n1][NW]
+    for (int t = threadIdx.x; t < n1; t += blockDim.x) {
+        const double d = a.disc[static_cast<size_t>(t) * a.M + k];
+        disc[t] = d;
+        inv[t] = 1.0 / d;
+    }
+    for (int t = threadIdx.x; t < n1 * Cc; t += blockDim.x) {
+        const double v = a.cube[static_cast<size_t>(t) * a.M + k];
+        expo[t] = (v < 0.0) ? 0.0 : v;
+    }
+    for (int t = threadIdx.x; t < n1 * NW; t += blockDim.x) red[t] = 0.0;
+    __syncthreads();
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int l0 = 0; l0 < a.N; l0 += blockDim.x) {  // block-uniform passes over the replicas
+        const int l = l0 + threadIdx.x;
+        const bool live = l < a.N;
+        const size_t row = static_cast<size_t>(k) * a.N + (live ? l : 0);
+        int st[CMAX];
+        double w[CMAX];
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) {
+            st[c] = -1;
+            w[c] = 0.0;
+            if (live && c < Cc) {
+                const int s = a.steps[(c + 1) * R + row];
+                if (s <= a.n) {
+                    st[c] = s;
+                    w[c] = __dmul_rn(disc[s], expo[s * Cc + c]);
+                }
+            }
+        }
+        for (int i = a.i0; i <= a.i1; ++i) {
+            double sum = 0.0;
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c)
+                if (st[c] > i) sum = __dadd_rn(sum, w[c]);
+            double v = __dmul_rn(inv[i], sum);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[i * NW + warp] += v;
+        }
+    }
+    __syncthreads();
+    for (int i = a.i0 + threadIdx.x; i <= a.i1; i += blockDim.x)
+        part[static_cast<size_t>(i - a.i0) * a.M + k] = red[i * NW] + red[i * NW + 1] + red[i * NW + 2] + red[i * NW + 3];
+}
+
+__global__ void __launch_bounds__(256) k_profile_paths(const double* part, int M, double R, double* out) {
+    __shared__ double red[256];
+    const double* row = part + static_cast<size_t>(blockIdx.x) * M;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < M; k += 256) s += row[k];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = red[0] / R;
+}
+
 // Intensity labels (labels.cpp:50-88).  Phase 1: survivor values per
 // (step, client) in the reference's loop order; phase 2: per replica sum over
 // surviving clients.
@@ -1633,9 +1709,34 @@ hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
         StreamScope sc__(sim->ctx->stream);
         if (kind != 0 && kind != 1) throw config_error("label_kind must be 'defaults' or 'intensity'");
         HCVA_CUDA(cudaSetDevice(sim->ctx->device));
-        if (sim->labels_kind != kind) launch_labels_all(sim, kind);
         const size_t R = static_cast<size_t>(sim->M) * sim->N;
         if (!sim->profile.p) sim->profile.alloc(sizeof(double) * (sim->n + 1));
+        const int Cc = sim->model.Cc, n1 = sim->n + 1;
+        if (kind == 0 && Cc <= 16 && sim->labels_kind != kind) {  // fused: no label array
+            if (!sim->has_cube) throw contract_error("labels: no MtM cube");
+            if (!sim->has_defaults) throw contract_error("labels: no default block");
+            if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
+            LabelArgs a{};
+            a.M = sim->M; a.N = sim->N; a.n = sim->n; a.Cn = sim->model.Cn; a.E = sim->model.E; a.dt = sim->model.dt;
+            a.disc = sim->disc.as<double>(); a.cube = sim->cube.as<double>(); a.steps = sim->steps.as<uint16_t>();
+            a.i0 = 0; a.i1 = sim->n;
+            DeviceBuf part;
+            part.alloc(sizeof(double) * n1 * sim->M);
+            const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc + 4 * n1);
+            const void* fn = Cc <= 8 ? (const void*)k_profile_defaults<8> : (const void*)k_profile_defaults<16>;
+            if (smem > 48 * 1024)
+                HCVA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            double* pp = part.as<double>();
+            void* args[] = {&a, &pp};
+            HCVA_CUDA(cudaLaunchKernel(fn, dim3(sim->M), dim3(128), args, smem, sim->ctx->stream));
+            check_launch(sim->ctx);
+            k_profile_paths<<<n1, 256, 0, sim->ctx->stream>>>(pp, sim->M, static_cast<double>(R),
+                                                              sim->profile.as<double>());
+            check_launch(sim->ctx);
+            copy_out(sim->ctx, out, sim->profile.p, sizeof(double) * n1);
+            return;
+        }
+        if (sim->labels_kind != kind) launch_labels_all(sim, kind);
         k_profile<<<sim->n + 1, 256, 0, sim->ctx->stream>>>(sim->labels.as<double>(), R, sim->profile.as<double>());
         check_launch(sim->ctx);
         copy_out(sim->ctx, out, sim->profile.p, sizeof(double) * (sim->n + 1));

@@ -252,3 +252,22 @@ def test_nested_batching_is_per_state_pure():
     v4, _ = hcva.nested_cva(cfg, z["book"], {k: v[3:7] for k, v in st.items()}, surv[3:7], step, 16, parent,
                             first_state=3)
     assert np.array_equal(v4, all_v[3:7])
+
+
+@pytest.mark.parametrize("name,M,N", [("c1", 64, 16), ("c1", 40, 200), ("desk_corr", 24, 17)])
+def test_cva_profile_fused_equals_label_mean(name, M, N):
+    """cva_profile (defaults kind) sums the labels per path inside the label
+    kernel without storing them; it equals the mean of the materialised labels
+    (labels.cpp:21-48 averaged per step) up to summation order."""
+    cfg = hcva.parse_config(cases.text(name)) if name != "desk_corr" else hcva.parse_config(str(golden(name)["config"]))
+    book = hcva.generate_book(cfg)
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    fused = hcva.simulate_set(cfg, book, M, N, root).cva_profile("defaults")
+    lab = hcva.simulate_set(cfg, book, M, N, root).labels_all("defaults")
+    want = lab.reshape(lab.shape[0], -1).mean(axis=1)
+    assert fused.shape == want.shape
+    np.testing.assert_allclose(fused, want, rtol=1e-12, atol=1e-14 * np.abs(want).max())
+    # once the labels exist the profile is their mean as well
+    sim = hcva.simulate_set(cfg, book, M, N, root)
+    sim.labels_all("defaults", to_host=False)
+    np.testing.assert_allclose(sim.cva_profile("defaults"), want, rtol=1e-12, atol=1e-14 * np.abs(want).max())
