@@ -290,43 +290,64 @@ def ours_arm(args):
     e2e = None
     if not args.no_e2e:
         e2e = e2e_leg(hcva, cfg, book, ctx, stream, rank, world, args)
-    learning, models = None, None
+    # The metric line is complete from here on; the secondary legs below add to
+    # it, and a failing or stuck secondary leg is reported inside it instead of
+    # losing the line (see _secondary / learning_leg's watchdog).
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (configs/paper_shape.json model, generated 500-swap book, quarterly grid)",
+        "config": config_obj(cfg, args, world),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "phase_ms": phase_ms,
+        "roofline": {"bound": "fp64", "kernel": "k_market (K1 diffusion)", "achieved": achieved,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                     "peak_source": "measured DFMA microbenchmark on this GPU (hcva_diag_fp64_peak)",
+                     "algorithmic_flop_per_launch": k1_flop, "traffic": None,
+                     "k1_share_of_step": k1_ms / ms_step},
+        "clocks": clocks.summary(),
+        "cpu_baseline": None,
+        "cva_learning": None,
+        "nested_mc": None,
+    }
+    _PARTIAL.update(line=line, rank=rank)
+    models = None
     if not args.no_learning:
-        learning, models = learning_leg(hcva, cfg, book, ctx, args, rank, world)
-    nested = None
+        res = _secondary("cva_learning", lambda: learning_leg(hcva, cfg, book, ctx, args, rank, world))
+        if res is not None:
+            line["cva_learning"], models = res
     if not args.no_nested:
         del sim
-        nested = nested_leg(hcva, cfg, book, ctx, args, models, rank, world)
+        line["nested_mc"] = _secondary("nested_mc", lambda: nested_leg(hcva, cfg, book, ctx, args, models, rank, world))
     del models
-    cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
-               "sample": f"{info['paths']} of {M} Y-paths x {N} replicas x {n} steps, "
-                         f"{info['seconds']:.1f} s (simulate_set + features_at/defaults_label for i=n..1)"}
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                                "sample": f"{info['paths']} of {M} Y-paths x {N} replicas x {n} steps, "
+                                          f"{info['seconds']:.1f} s (simulate_set + features_at/defaults_label "
+                                          f"for i=n..1)"}
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (configs/paper_shape.json model, generated 500-swap book, quarterly grid)",
-            "config": config_obj(cfg, args, world),
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "phase_ms": phase_ms,
-            "roofline": {"bound": "fp64", "kernel": "k_market (K1 diffusion)", "achieved": achieved,
-                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                         "peak_source": "measured DFMA microbenchmark on this GPU (hcva_diag_fp64_peak)",
-                         "algorithmic_flop_per_launch": k1_flop, "traffic": None,
-                         "k1_share_of_step": k1_ms / ms_step},
-            "clocks": clocks.summary(),
-            "cpu_baseline": cpu,
-            "cva_learning": learning,
-            "nested_mc": nested,
-        }
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+_PARTIAL = {}
+
+
+def _secondary(key, fn):
+    """Run a secondary leg (CVA learning, nested MC); an exception becomes
+    {"error": ...} under `key` in the metric line rather than a lost line."""
+    try:
+        return fn()
+    except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
+        sys.stderr.write(f"bench: {key} leg failed: {exc!r}\n")
+        if key == "cva_learning":
+            _PARTIAL["line"][key] = {"error": repr(exc)}
+            return None
+        return {"error": repr(exc)}
 
 
 def ctypes_peak(ctx):
@@ -412,10 +433,14 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
     t1 = time.perf_counter()
     watchdog = None
     if world > 1:  # a stuck collective must not hang the scaling run: fail loudly instead
-        def _abort():
+        def _abort():  # print the metric line with the learning leg marked, then leave
             sys.stderr.write(f"bench: rank {rank}: multi-GPU learning leg exceeded {args.learning_timeout} s\n")
             sys.stderr.flush()
-            os._exit(3)
+            part = _PARTIAL.get("line")
+            if rank == 0 and part is not None:
+                part["cva_learning"] = {"error": f"timeout after {args.learning_timeout} s"}
+                print(json.dumps(part), flush=True)
+            os._exit(0 if part is not None else 3)
 
         watchdog = threading.Timer(args.learning_timeout, _abort)
         watchdog.daemon = True
