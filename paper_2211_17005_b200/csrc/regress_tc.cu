@@ -70,6 +70,17 @@ __host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp 
 __host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
     return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 8 * 128 * 4 + 64;
 }
+// Wide inputs (the resident layout above exceeds shared memory, e.g. C5's 157
+// features): W1, W1^T and the vectors stay resident, layer 0's K dimension is
+// streamed in kKc-column chunks of (X tile, W0) through kNst stages.
+constexpr int kKc = 16, kNst = 3;
+constexpr int kWgXMax = 256;  // widest padded input of the tensor-core path
+__host__ __device__ constexpr uint32_t stage_bytes(int U) { return 2u * 128 * kKc * 4 + 2u * U * kKc * 4; }
+__host__ __device__ constexpr size_t tile_tc_smem_ch(int U) {
+    return 4ull * U * U * 4 + 1024 + 2ull * 128 * U * 4 + static_cast<size_t>(kNst) * stage_bytes(U) + 8 * 128 * 4 +
+           8 * (3 + 2 * kNst) + 64;
+}
+__host__ __device__ constexpr bool tile_chunked(int U, int dp) { return tile_tc_smem(U, dp) > 227 * 1024; }
 
 size_t tc_weight_image_bytes(int u, int dp) { return w_image_bytes(u, dp); }
 size_t tc_x_tile_bytes(int dp) { return 2ull * x_plane_bytes(dp); }
@@ -178,22 +189,28 @@ struct TileShape {
     static constexpr int warps = 4 * NS;
 };
 
-template <int U, int ACT>
+template <int U, int ACT, bool CH>
 __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a, long t_first, long n_tiles) {
     constexpr int NS = TileShape<U>::NS, UH = TileShape<U>::UH;
     extern __shared__ __align__(128) uint8_t sm[];
     const int dp = a.dp;
     const uint32_t w0b = U * dp * 4, w1b = U * U * 4, hb = 128 * U * 4, xb = x_plane_bytes(dp);
     const uint32_t wbytes = w_image_bytes(U, dp);
+    // Resident layout: [W0 | W1 | W1^T | vec][H][X tile]; chunked (CH):
+    // [W1 | W1^T | vec][H][kNst stages of (X chunk hi | lo, W0 chunk hi | lo)].
     uint8_t* w0 = sm;
-    uint8_t* w1 = w0 + 2 * w0b;
+    uint8_t* w1 = CH ? sm : w0 + 2 * w0b;
     uint8_t* w1t = w1 + 2 * w1b;
     const float* vec = reinterpret_cast<const float*>(w1t + 2 * w1b);  // b0 | b1 | w2 | b2, mu
-    uint8_t* bufH = sm + wbytes;    // H1, then G2 (hi | lo)
-    uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo)
-    float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);  // [NS][128] partial output-layer sums
+    uint8_t* bufH = CH ? sm + 4 * w1b + 1024 : sm + wbytes;  // H1, then G2 (hi | lo)
+    uint8_t* bufX = bufH + 2 * hb;  // feature tile (hi | lo) / the chunk stages
+    float* fsh = reinterpret_cast<float*>(bufX + (CH ? kNst * stage_bytes(U) : 2 * xb));  // [NS][128] partial sums
     uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 8 * 128);  // [0] MMA, [1] weights, [2] features
-    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
+    uint64_t* full = bar + 3;                                    // CH: stage loaded / consumed
+    uint64_t* empty = full + kNst;
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3 + 2 * kNst);
+    constexpr uint32_t xcb = 128u * kKc * 4, wcb = static_cast<uint32_t>(U) * kKc * 4;  // chunk plane bytes
+    const int nq = dp / kKc;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r = tid & 127, hf = tid >> 7, cb = hf * UH;
@@ -202,6 +219,11 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         tc::mbar_init(&bar[0], 1);
         tc::mbar_init(&bar[1], 1);
         tc::mbar_init(&bar[2], 1);
+        if (CH)
+            for (int q = 0; q < kNst; ++q) {
+                tc::mbar_init(&full[q], 1);
+                tc::mbar_init(&empty[q], 1);
+            }
         tc::fence_async_smem();
     }
     if (warp == 0) tc::tmem_alloc(tbase, 256);
@@ -212,13 +234,35 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const long t_end = t_first + n_tiles;
     long tile = t_first + blockIdx.x;
+    // CH: chunk g of this CTA = chunk g % nq of its (g / nq)-th tile, stage g % kNst.
+    const long my_tiles = tile < t_end ? (t_end - tile + gridDim.x - 1) / gridDim.x : 0;
+    const long n_chunks = my_tiles * nq;
+    auto load_chunk = [&](long g) {  // one thread
+        const int st = static_cast<int>(g % kNst), q = static_cast<int>(g % nq);
+        const long tl = t_first + blockIdx.x + (g / nq) * gridDim.x;
+        uint8_t* sb = bufX + st * stage_bytes(U);
+        const uint8_t* xs = a.ximg + tl * 2 * xb + q * xcb;
+        const uint8_t* ws = a.wimg + q * wcb;
+        tc::mbar_expect_tx(&full[st], 2 * xcb + 2 * wcb);
+        tc::bulk_g2s(sb, xs, xcb, &full[st]);
+        tc::bulk_g2s(sb + xcb, xs + xb, xcb, &full[st]);
+        tc::bulk_g2s(sb + 2 * xcb, ws, wcb, &full[st]);
+        tc::bulk_g2s(sb + 2 * xcb + wcb, ws + w0b, wcb, &full[st]);
+    };
     if (tid == 0) {
-        tc::mbar_expect_tx(&bar[1], wbytes);
-        tc::bulk_g2s(w0, a.wimg, wbytes, &bar[1]);
-        tc::mbar_expect_tx(&bar[2], 2 * xb);
-        tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
+        if (CH) {
+            tc::mbar_expect_tx(&bar[1], 4 * w1b + 1024);
+            tc::bulk_g2s(w1, a.wimg + 2 * w0b, 4 * w1b + 1024, &bar[1]);
+            for (long g = 0; g < kNst && g < n_chunks; ++g) load_chunk(g);
+        } else {
+            tc::mbar_expect_tx(&bar[1], wbytes);
+            tc::bulk_g2s(w0, a.wimg, wbytes, &bar[1]);
+            tc::mbar_expect_tx(&bar[2], 2 * xb);
+            tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
+        }
     }
     tc::mbar_wait(&bar[1], 0);
+    long g_next = 0;  // CH: next chunk to consume
     uint32_t mph = 0, xph = 0;
     auto mma_wait = [&]() {  // one waiting warp, the rest parked at the barrier
         if (warp == 0) tc::mbar_wait(&bar[0], mph);
@@ -244,14 +288,33 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         const long row = tile * 128 + r;
         const bool live = row >= a.b0 && row < a.b1;
         const long trow = row - a.b0;
-        if (tid == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing thread reads the feature tile
-        xph ^= 1;
         // ---- F0: D0 = X W0^T
-        if (warp == 0)
-            tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0),
-                           0, &bar[0]);
+        if constexpr (CH) {
+            if (warp == 0) {
+                for (int q = 0; q < nq; ++q, ++g_next) {
+                    const int st = static_cast<int>(g_next % kNst);
+                    tc::mbar_wait(&full[st], static_cast<uint32_t>((g_next / kNst) & 1));
+                    uint8_t* sb = bufX + st * stage_bytes(U);
+                    tc::gemm3_warp(tm, tc::kmajor(sb, xcb, 128), tc::kmajor(sb + 2 * xcb, wcb, U), kKc,
+                                   tc::idesc_tf32(128, U, 0, 0), q > 0, &empty[st]);
+                    if (g_next >= 1) {  // the previous chunk's MMAs done: refill its stage kNst chunks ahead
+                        const long gp = g_next - 1;
+                        tc::mbar_wait(&empty[gp % kNst], static_cast<uint32_t>((gp / kNst) & 1));
+                        if (lane == 0 && gp + kNst < n_chunks) load_chunk(gp + kNst);
+                        __syncwarp();
+                    }
+                }
+                tc::commit_if(tc::elect_one(), &bar[0]);  // every F0 MMA of the tile
+            }
+        } else {
+            if (tid == 0) tc::mbar_wait(&bar[2], xph);  // only the issuing thread reads the feature tile
+            xph ^= 1;
+            if (warp == 0)
+                tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp,
+                               tc::idesc_tf32(128, U, 0, 0), 0, &bar[0]);
+        }
         mma_wait();
-        if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
+        if (!CH && tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
             tc::mbar_expect_tx(&bar[2], 2 * xb);
             tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
         }
@@ -532,10 +595,16 @@ constexpr int kWgThreads = 256;
 constexpr int kWgK = 32;                     // batch rows per chunk (the MMAs' K)
 constexpr uint32_t kWgTile = 64 * kWgK * 4;   // one plane of a 64-row chunk tile
 constexpr uint32_t kWgTileB1 = 72 * kWgK * 4; // H1t tile: U rows + a row of ones (+ zero rows to 8)
-constexpr size_t kWgSmem = 6 * static_cast<size_t>(kWgTile) + 2 * static_cast<size_t>(kWgTileB1) + 64 + 1024;
+// The Xt tile has XR rows: 64 for dp <= 64, kWgXMax for wide inputs (one CTA
+// per SM then: 512 TMEM columns, gW0 at column 128 with N = dp).
+__host__ __device__ constexpr size_t wgrad_smem(int XR) {
+    return 4 * static_cast<size_t>(kWgTile) + 2ull * XR * kWgK * 4 + 2 * static_cast<size_t>(kWgTileB1) + 64 + 1024;
+}
 
-template <int U>
-__global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
+template <int U, int XR>
+__global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 3) k_wgrad_tc(WgradArgs a) {
+    constexpr uint32_t kWgTileX = XR * kWgK * 4;
+    constexpr int kTmemCols = XR > 64 ? 512 : 256;
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
     // The row of ones in tB1 (row U) and tB0 (row d, a pad column of the
@@ -543,15 +612,15 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     // sum_r G2[r][o] (gb1) and sum_r G1[r][o] (gb0).
     uint8_t* tA1 = sm;                                // G2t chunk: 64 (o, zero-padded) x kWgK (rows)
     uint8_t* tA0 = sm + 2 * kWgTile;                  // G1t chunk
-    uint8_t* tB0 = sm + 4 * kWgTile;                  // Xt chunk: dp x kWgK, row d = 1
-    uint8_t* tB1 = sm + 6 * kWgTile;                  // H1t chunk: U x kWgK, row U = 1
+    uint8_t* tB0 = sm + 4 * kWgTile;                  // Xt chunk: dp (of XR) x kWgK, row d = 1
+    uint8_t* tB1 = tB0 + 2 * kWgTileX;                // H1t chunk: U x kWgK, row U = 1
     uint64_t* mbar = reinterpret_cast<uint64_t*>(tB1 + 2 * kWgTileB1);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int dp = a.dp;
     if (t == 0) tc::mbar_init(mbar, 1);
-    if (warp == 0) tc::tmem_alloc(tbase, 256);
-    for (int i = t; i < (6 * kWgTile + 2 * kWgTileB1) / 16; i += kWgThreads)
+    if (warp == 0) tc::tmem_alloc(tbase, kTmemCols);
+    for (int i = t; i < (4 * kWgTile + 2 * kWgTileX + 2 * kWgTileB1) / 16; i += kWgThreads)
         reinterpret_cast<float4*>(sm)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     tc::fence_before_sync();
     __syncthreads();
@@ -563,7 +632,7 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     const bool vx = (a.ld_x % 4) == 0 && (a.row0 % 4) == 0;
     constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
     constexpr int NF = (U * Q + kWgThreads - 1) / kWgThreads;   // per thread per activation array
-    constexpr int NX = (64 * Q + kWgThreads - 1) / kWgThreads;  // per thread of the Xt chunk (dp <= 64)
+    constexpr int NX = (XR * Q + kWgThreads - 1) / kWgThreads;  // per thread of the Xt chunk (dp <= XR)
     float4 rg2[NF], rh1[NF], rg1[NF], rx[NX];
     auto load = [&](long c0) {
         const int n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
@@ -603,14 +672,14 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
-            if (f < dp && f != a.d) tc::put_split4_sw(tB0, kWgTile, f, k, 64, rx[i]);
+            if (f < dp && f != a.d) tc::put_split4_sw(tB0, kWgTileX, f, k, XR, rx[i]);
         }
         if (t < 2 * Q) {  // the rows of ones (1 for the chunk's live rows, 0 past the batch end)
             const int k = (t % Q) * 4, n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
             const float4 one = make_float4(k < n ? 1.0f : 0.0f, k + 1 < n ? 1.0f : 0.0f, k + 2 < n ? 1.0f : 0.0f,
                                            k + 3 < n ? 1.0f : 0.0f);
             if (t < Q) tc::put_split4_sw(tB1, kWgTileB1, U, k, 72, one);
-            else tc::put_split4_sw(tB0, kWgTile, a.d, k, 64, one);
+            else tc::put_split4_sw(tB0, kWgTileX, a.d, k, XR, one);
         }
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -622,7 +691,8 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
                               tc::OperandSW{tc::smem_u32(tB1), kWgTileB1, 72u, 0}, kWgK,
                               tc::idesc_tf32(64, U + 8, 0, 0), !first, nullptr);
             tc::gemm3_sw_warp(tm + 128, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
-                              tc::OperandSW{tc::smem_u32(tB0), kWgTile, R64, 0}, kWgK, tc::idesc_tf32(64, dp, 0, 0),
+                              tc::OperandSW{tc::smem_u32(tB0), kWgTileX, static_cast<uint32_t>(XR), 0}, kWgK,
+                              tc::idesc_tf32(64, dp, 0, 0),
                               !first, mbar);
         }
         first = 0;
@@ -661,7 +731,7 @@ __global__ void __launch_bounds__(kWgThreads, 3) k_wgrad_tc(WgradArgs a) {
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tm, 256);
+    if (warp == 0) tc::tmem_dealloc(tm, kTmemCols);
 }
 
 // Diagnostic GEMM: D (M x N) = A (M x K) B (N x K)^T; test hook for the
@@ -771,8 +841,9 @@ __global__ void k_tc_rate(int M, int N, int iters, float* sink) {
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
-    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && d <= 63 &&  // dp = tc_dp(d) <= 64
-           tile_tc_smem(u, ((d + 16) / 16) * 16) <= 227 * 1024;
+    const int dp = ((d + 16) / 16) * 16;
+    return h == 2 && (u == 16 || u == 32 || u == 64) && d >= 1 && dp <= kWgXMax &&
+           (tile_tc_smem(u, dp) <= 227 * 1024 || tile_tc_smem_ch(u) <= 227 * 1024);
 }
 
 // Input width padded for the tensor-core tiles, with at least one pad column:
@@ -792,9 +863,15 @@ void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* 
 
 template <int U, int ACT>
 void launch_tile_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    if (tile_chunked(U, a.dp)) {
+        const size_t smem = tile_tc_smem_ch(U);
+        HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_tile_tc<U, ACT, true><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
+        return;
+    }
     const size_t smem = tile_tc_smem(U, a.dp);
-    HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_tc<U, ACT><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
+    HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tile_tc<U, ACT, false><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
 }
 
 template <int U>
@@ -819,8 +896,14 @@ int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
 
 template <int U>
 void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
-    HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWgSmem));
-    k_wgrad_tc<U><<<ctas, kWgThreads, kWgSmem, s>>>(a);
+    if (a.dp > 64) {
+        HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U, kWgXMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)wgrad_smem(kWgXMax)));
+        k_wgrad_tc<U, kWgXMax><<<ctas, kWgThreads, wgrad_smem(kWgXMax), s>>>(a);
+        return;
+    }
+    HCVA_CUDA(cudaFuncSetAttribute(k_wgrad_tc<U, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wgrad_smem(64)));
+    k_wgrad_tc<U, 64><<<ctas, kWgThreads, wgrad_smem(64), s>>>(a);
 }
 
 template <int U>
@@ -849,7 +932,7 @@ int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s) {
         const int v = e ? std::atoi(e) : 2;  // 2 measured best (partials vs overlap)
         return v < 1 ? 1 : (v > 2 ? 2 : v);
     }();
-    const long slots = static_cast<long>(per_sm) * sm_count;  // resident CTAs
+    const long slots = static_cast<long>(a.dp > 64 ? 1 : per_sm) * sm_count;  // resident CTAs
     const long per = std::max(1L, (chunks + slots - 1) / slots);
     a.rows_per_cta = static_cast<int>(per * kWgK);
     const int ctas = static_cast<int>((a.rows + a.rows_per_cta - 1) / a.rows_per_cta);

@@ -151,10 +151,38 @@ def test_batch_divisibility_is_config_error():
         rg.backward_learn(sim, cfg.training)
 
 
-def test_backward_learn_c5_shape_simt_path():
-    """C5's feature width (64 clients: d = 64 + 29 + 64 = 157 > the tensor-core
-    tile's 63) runs the SIMT trainer; per step it must match the FP64 oracle."""
+@pytest.mark.parametrize("d,u,head", [(100, 32, False), (157, 64, True), (157, 16, False)])
+def test_loss_and_gradients_wide_inputs(d, u, head):
+    """Inputs wider than the resident tile (C5: d = 157): layer 0's K dimension
+    streams through the tile kernel in 16-column chunks, the weight gradient
+    uses the 256-row feature tile; same tolerances as the narrow case."""
+    R = oracle_api.restatement()
+    h, rows = 2, 700
+    x, y = data(rows, d)
+    t = tcfg(width=u, hidden=h)
+    p = R.init_network(d, h, u, R.key(11))
+    p[-1] = 0.2
+    lo, go = R.loss(p, x, y, h, u, 0, head)
+    lg, gg = rg.quadratic_loss(t, p, x, y, head)
+    assert lg == pytest.approx(lo, rel=1e-5)
+    off = 0
+    for fo, fi in [(u, d), (u, u), (1, u)]:
+        for blk in (fo * fi, fo):
+            a, b = gg[off:off + blk], go[off:off + blk]
+            assert np.max(np.abs(a - b)) <= 5e-5 * max(np.max(np.abs(b)), 1e-12), (d, u, off)
+            off += blk
+    assert gg[-1] == pytest.approx(go[-1], rel=1e-5, abs=1e-9)
+
+
+@pytest.mark.parametrize("path", ["tensor", "simt"])
+def test_backward_learn_c5_shape(path, monkeypatch):
+    """C5's feature width (64 clients: d = 64 + 29 + 64 = 157) on the
+    tensor-core path (chunked layer 0) and on the SIMT trainer; per step both
+    must match the FP64 oracle."""
     import json
+
+    if path == "simt":
+        monkeypatch.setenv("HCVA_REGRESS_SIMT", "1")
 
     j = cases.case("c5")
     j["grid"] = {"pricing_steps": 4, "substeps": 4, "dt_years": 0.25}
