@@ -786,6 +786,83 @@ __global__ void __launch_bounds__(128) k_labels_defaults_reg(LabelArgs a) {
     }
 }
 
+// Defaults labels for many clients (Cc > 16, e.g. C5's 64): per replica the
+// clients are chained by default step (head[s] -> next[c], one byte each in
+// shared memory), then one sweep over the steps from n down to 0 adds each
+// client's beta_s * exposure_s as the step passes its default step:
+// label_i = beta_i^-1 * sum_{c: s_c > i} beta_{s_c} (MtM_{s_c,c})^+ -- the
+// reference's terms, summed by descending default step (equal to a few ulp),
+// in O(n + Cc) per replica instead of O(n Cc).  PROFILE: per-path sums of each
+// step's labels (as k_profile_defaults) instead of the labels.
+template <bool PROFILE>
+__global__ void __launch_bounds__(128) k_labels_defaults_sweep(LabelArgs a, double* part) {
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;
+    const int n1 = a.n + 1, Cc = a.Cn - 1, nt = blockDim.x;
+    constexpr int NW = 4;
+    double* disc = sm;                                         // [n1]
+    double* inv = disc + n1;                                   // [n1]
+    double* expo = inv + n1;                                   // [n1][Cc]
+    double* red = expo + static_cast<size_t>(n1) * Cc;         // [n1][NW] (PROFILE)
+    uint8_t* head = reinterpret_cast<uint8_t*>(red + (PROFILE ? n1 * NW : 0));  // [n1][nt]
+    uint8_t* next = head + static_cast<size_t>(n1) * nt;                         // [Cc][nt]
+    for (int t = threadIdx.x; t < n1; t += nt) {
+        const double d = a.disc[static_cast<size_t>(t) * a.M + k];
+        disc[t] = d;
+        inv[t] = 1.0 / d;
+    }
+    for (int t = threadIdx.x; t < n1 * Cc; t += nt) {
+        const double v = a.cube[static_cast<size_t>(t) * a.M + k];
+        expo[t] = (v < 0.0) ? 0.0 : v;
+    }
+    if (PROFILE)
+        for (int t = threadIdx.x; t < n1 * NW; t += nt) red[t] = 0.0;
+    const size_t R = static_cast<size_t>(a.M) * a.N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int l0 = 0; l0 < a.N; l0 += nt) {  // block-uniform passes over the replicas
+        __syncthreads();
+        for (int t = tid; t < n1 * nt; t += nt) head[t] = 0xFF;
+        __syncthreads();
+        const int l = l0 + tid;
+        const bool live = l < a.N;
+        const size_t row = static_cast<size_t>(k) * a.N + (live ? l : 0);
+        if (live)
+            for (int c = 0; c < Cc; ++c) {  // chain client c under its default step
+                const int st = a.steps[(c + 1) * R + row];
+                if (st <= a.n) {
+                    next[c * nt + tid] = head[st * nt + tid];
+                    head[st * nt + tid] = static_cast<uint8_t>(c);
+                }
+            }
+        double S = 0.0;  // sum over clients defaulting after step i
+        for (int i = a.n; i >= 0; --i) {
+            if (i < a.n)
+                for (int c = head[(i + 1) * nt + tid]; c != 0xFF; c = next[c * nt + tid])
+                    S = __dadd_rn(S, __dmul_rn(disc[i + 1], expo[(i + 1) * Cc + c]));
+            if (i < a.i0 || i > a.i1) continue;
+            double v = live ? __dmul_rn(inv[i], S) : 0.0;
+            if (PROFILE) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[i * NW + warp] += v;
+            } else if (live) {
+                a.out[static_cast<size_t>(i - a.i0) * R + row] = v;
+            }
+        }
+    }
+    if (PROFILE) {
+        __syncthreads();
+        for (int i = a.i0 + tid; i <= a.i1; i += nt)
+            part[static_cast<size_t>(i - a.i0) * a.M + k] =
+                red[i * NW] + red[i * NW + 1] + red[i * NW + 2] + red[i * NW + 3];
+    }
+}
+
+inline size_t sweep_smem(int n1, int Cc, int nt, bool profile) {
+    return sizeof(double) * (2 * static_cast<size_t>(n1) + static_cast<size_t>(n1) * Cc + (profile ? 4 * n1 : 0)) +
+           static_cast<size_t>(n1) * nt + static_cast<size_t>(Cc) * nt;
+}
+
 // CVA profile without materialising the labels (defaults kind): the register
 // form of k_labels_defaults_reg per path, each step's labels summed over the
 // path's replicas (warp shuffles, then the warps in fixed order) into
@@ -1325,6 +1402,11 @@ void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t*
             const int thr = std::min(128, ((PPc * N + 31) / 32) * 32);
             void* args[] = {&a};
             HCVA_CUDA(cudaLaunchKernel(fn, dim3((sim->M + PPc - 1) / PPc), dim3(thr), args, smr, ctx->stream));
+        } else if (Cc < 255) {
+            const size_t sm2 = sweep_smem(n1, Cc, 128, false);
+            HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(sm2)));
+            k_labels_defaults_sweep<false><<<sim->M, 128, sm2, ctx->stream>>>(a, nullptr);
         } else {
             k_labels_defaults<<<sim->M, threads, smem, ctx->stream>>>(a);
         }
@@ -1712,7 +1794,7 @@ hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
         const size_t R = static_cast<size_t>(sim->M) * sim->N;
         if (!sim->profile.p) sim->profile.alloc(sizeof(double) * (sim->n + 1));
         const int Cc = sim->model.Cc, n1 = sim->n + 1;
-        if (kind == 0 && Cc <= 16 && sim->labels_kind != kind) {  // fused: no label array
+        if (kind == 0 && Cc < 255 && sim->labels_kind != kind) {  // fused: no label array
             if (!sim->has_cube) throw contract_error("labels: no MtM cube");
             if (!sim->has_defaults) throw contract_error("labels: no default block");
             if (sim->start_step != 0) throw contract_error("labels expect an outer (non-rebased) market block");
@@ -1722,8 +1804,11 @@ hcva_status hcva_cva_profile(hcva_sim* sim, int kind, double* out) {
             a.i0 = 0; a.i1 = sim->n;
             DeviceBuf part;
             part.alloc(sizeof(double) * n1 * sim->M);
-            const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc + 4 * n1);
-            const void* fn = Cc <= 8 ? (const void*)k_profile_defaults<8> : (const void*)k_profile_defaults<16>;
+            const size_t smem = Cc <= 16 ? sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc + 4 * n1)
+                                         : sweep_smem(n1, Cc, 128, true);
+            const void* fn = Cc <= 8    ? (const void*)k_profile_defaults<8>
+                             : Cc <= 16 ? (const void*)k_profile_defaults<16>
+                                        : (const void*)k_labels_defaults_sweep<true>;
             if (smem > 48 * 1024)
                 HCVA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             double* pp = part.as<double>();

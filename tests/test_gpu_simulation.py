@@ -254,7 +254,7 @@ def test_nested_batching_is_per_state_pure():
     assert np.array_equal(v4, all_v[3:7])
 
 
-@pytest.mark.parametrize("name,M,N", [("c1", 64, 16), ("c1", 40, 200), ("desk_corr", 24, 17)])
+@pytest.mark.parametrize("name,M,N", [("c1", 64, 16), ("c1", 40, 200), ("desk_corr", 24, 17), ("c5", 12, 150)])
 def test_cva_profile_fused_equals_label_mean(name, M, N):
     """cva_profile (defaults kind) sums the labels per path inside the label
     kernel without storing them; it equals the mean of the materialised labels
