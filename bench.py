@@ -305,7 +305,7 @@ def ours_arm(args):
         "roofline": {"bound": "fp64", "kernel": "k_market (K1 diffusion)", "achieved": achieved,
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                      "peak_source": "measured DFMA microbenchmark on this GPU (hcva_diag_fp64_peak)",
-                     "algorithmic_flop_per_launch": k1_flop, "traffic": None,
+                     "algorithmic_flop_per_launch": k1_flop, "traffic": k1_traffic(),
                      "k1_share_of_step": k1_ms / ms_step},
         "clocks": clocks.summary(),
         "cpu_baseline": None,
@@ -348,6 +348,24 @@ def _secondary(key, fn):
             _PARTIAL["line"][key] = {"error": repr(exc)}
             return None
         return {"error": repr(exc)}
+
+
+def k1_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch at C2, from
+    the committed ncu --set full capture (profiles/r1/ncu_K1_k_market.txt):
+    the FP64-bound kernel's only DRAM traffic is its market stores."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "ncu_K1_k_market.txt")
+    try:
+        vals = {}
+        for ln in open(path):
+            if "dram__bytes_" in ln and "=" in ln:
+                k, v = ln.split("=")
+                num, unit = v.split()[0], v.split()[1]
+                vals[k.strip()] = float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+        return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                "source": "profiles/r1/ncu_K1_k_market.txt (ncu --set full, C2)"}
+    except (OSError, KeyError, ValueError, IndexError):
+        return None
 
 
 def ctypes_peak(ctx):
