@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <utility>
 
 #include "../../include/hcva_gpu.h"
 
@@ -155,6 +156,28 @@ struct hcva_sim {
 namespace hcva {
 
 inline unsigned grid1(size_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+// Programmatic dependent launch: a kernel launched by pdl_launch may become
+// resident while its predecessor drains (the predecessor calls pdl_trigger()),
+// runs its prologue, and blocks in pdl_wait() until the predecessor has
+// completed and its writes are visible.  No-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HCVA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Small host table -> device buffer (stream-ordered, synchronised).
 template <typename T>

@@ -344,6 +344,7 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
     __shared__ double part[G][33];
     const int x = threadIdx.x, grp = threadIdx.y;
     const int i = blockIdx.x * 32 + x;
+    pdl_trigger();  // the next tile kernel may run its prologue now (it waits for this grid)
     if (blockIdx.x == 0 && grp == 0) {
         double s = 0.0;
         for (int c = x; c < nct; c += 32) s += lpart[c];

@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const long t_end = t_first + n_tiles;
     long tile = t_first + blockIdx.x;
+    pdl_wait();  // the optimizer's weight image / the previous weight gradient's reads of H1t, G2t, G1t
     // CH: chunk g of this CTA = chunk g % nq of its (g / nq)-th tile, stage g % kNst.
     const long my_tiles = tile < t_end ? (t_end - tile + gridDim.x - 1) / gridDim.x : 0;
     const long n_chunks = my_tiles * nq;
@@ -838,6 +839,14 @@ __global__ void k_tc_rate(int M, int N, int iters, float* sink) {
 
 // ------------------------------------------------------------------ host
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HCVA_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
@@ -866,12 +875,12 @@ void launch_tile_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cud
     if (tile_chunked(U, a.dp)) {
         const size_t smem = tile_tc_smem_ch(U);
         HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_tile_tc<U, ACT, true><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
+        pdl_launch(k_tile_tc<U, ACT, true>, dim3(ctas), dim3(TileShape<U>::threads), smem, s, a, t_first, n_tiles);
         return;
     }
     const size_t smem = tile_tc_smem(U, a.dp);
     HCVA_CUDA(cudaFuncSetAttribute(k_tile_tc<U, ACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tile_tc<U, ACT, false><<<ctas, TileShape<U>::threads, smem, s>>>(a, t_first, n_tiles);
+    pdl_launch(k_tile_tc<U, ACT, false>, dim3(ctas), dim3(TileShape<U>::threads), smem, s, a, t_first, n_tiles);
 }
 
 template <int U>
