@@ -289,6 +289,8 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         const long row = tile * 128 + r;
         const bool live = row >= a.b0 && row < a.b1;
         const long trow = row - a.b0;
+        // the label of this row, loaded under the layer-0 GEMM (SGD and loss evaluation)
+        const double yrow = (live && (sgd || ((a.mode & 1) && hf == 0))) ? __ldg(a.y + row) : 0.0;
         // ---- F0: D0 = X W0^T
         if constexpr (CH) {
             if (warp == 0) {
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             if (live && hf == 0) {
                 const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
                 if (a.mode & 1) {
-                    const double res = ph - a.y[row];
+                    const double res = ph - yrow;
                     loss += res * res;
                 }
                 if (a.mode & 2) mn = fmin(mn, static_cast<double>(f + mu));
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
         float dd = 0.0f;
         if (live) {
             const float pr = ((a.head && f < 0.0f) ? 0.0f : f) + mu;
-            const double res = static_cast<double>(pr) - a.y[row];
+            const double res = static_cast<double>(pr) - yrow;
             const double dm = 2.0 * res / a.nb;
             if (hf == 0) {
                 loss += res * res;
