@@ -67,18 +67,21 @@ __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
     return 2u * U * dp * 4 + 4u * U * U * 4 + 1024;
 }
 __host__ __device__ constexpr uint32_t x_plane_bytes(int dp) { return 128u * dp * 4; }
-__host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
-    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 8 * 128 * 4 + 64;
-}
-// Wide inputs (the resident layout above exceeds shared memory, e.g. C5's 157
+// Wide inputs (the resident layout below exceeds shared memory, e.g. C5's 157
 // features): W1, W1^T and the vectors stay resident, layer 0's K dimension is
 // streamed in kKc-column chunks of (X tile, W0) through kNst stages.
 constexpr int kKc = 16, kNst = 3;
+// mbarriers (MMA, weights, features, kNst full + kNst empty) and the TMEM base
+// word, after the partial-sum scratch.
+constexpr size_t kTileBarBytes = 8 * (3 + 2 * kNst) + 16;
+__host__ __device__ constexpr size_t tile_tc_smem(int U, int dp) {
+    return w_image_bytes(U, dp) + 2ull * 128 * U * 4 + 2ull * x_plane_bytes(dp) + 8 * 128 * 4 + kTileBarBytes;
+}
 constexpr int kWgXMax = 256;  // widest padded input of the tensor-core path
 __host__ __device__ constexpr uint32_t stage_bytes(int U) { return 2u * 128 * kKc * 4 + 2u * U * kKc * 4; }
 __host__ __device__ constexpr size_t tile_tc_smem_ch(int U) {
     return 4ull * U * U * 4 + 1024 + 2ull * 128 * U * 4 + static_cast<size_t>(kNst) * stage_bytes(U) + 8 * 128 * 4 +
-           8 * (3 + 2 * kNst) + 64;
+           kTileBarBytes;
 }
 __host__ __device__ constexpr bool tile_chunked(int U, int dp) { return tile_tc_smem(U, dp) > 227 * 1024; }
 
