@@ -608,7 +608,7 @@ __host__ __device__ constexpr size_t wgrad_smem(int XR) {
 }
 
 template <int U, int XR>
-__global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 3) k_wgrad_tc(WgradArgs a) {
+__global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 2) k_wgrad_tc(WgradArgs a) {
     constexpr uint32_t kWgTileX = XR * kWgK * 4;
     constexpr int kTmemCols = XR > 64 ? 512 : 256;
     extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -639,29 +639,30 @@ __global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 3) k_wgrad_tc(WgradA
     constexpr int Q = kWgK / 4;                                 // float4 per feature row of a chunk
     constexpr int NF = (U * Q + kWgThreads - 1) / kWgThreads;   // per thread per activation array
     constexpr int NX = (XR * Q + kWgThreads - 1) / kWgThreads;  // per thread of the Xt chunk (dp <= XR)
-    float4 rg2[NF], rh1[NF], rg1[NF], rx[NX];
-    auto load = [&](long c0) {
+    struct Regs {
+        float4 g2[NF], h1[NF], g1[NF], x[NX];
+    };
+    auto load = [&](Regs& q, long c0) {
         const int n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
 #pragma unroll
         for (int i = 0; i < NF; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
             if (f < U) {
                 const size_t o = static_cast<size_t>(f) * a.ld_t + c0 + k;
-                rg2[i] = ld4(a.G2t + o, vt, n - k);
-                rh1[i] = ld4(a.H1t + o, vt, n - k);
-                rg1[i] = ld4(a.G1t + o, vt, n - k);
+                q.g2[i] = ld4(a.G2t + o, vt, n - k);
+                q.h1[i] = ld4(a.H1t + o, vt, n - k);
+                q.g1[i] = ld4(a.G1t + o, vt, n - k);
             }
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
-            if (f < dp && f != a.d) rx[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
+            if (f < dp && f != a.d) q.x[i] = ld4(a.Xt + static_cast<size_t>(f) * a.ld_x + a.row0 + c0 + k, vx, n - k);
         }
     };
     uint32_t phase = 0;
     int first = 1;
-    if (r_begin < r_end) load(r_begin);
-    for (long c0 = r_begin; c0 < r_end; c0 += kWgK) {
+    auto consume = [&](const Regs& q, long c0) {
         if (!first) {  // previous chunk's MMAs done reading the tiles
             tc::mbar_wait(mbar, phase);
             phase ^= 1;
@@ -670,15 +671,15 @@ __global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 3) k_wgrad_tc(WgradA
         for (int i = 0; i < NF; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
             if (f < U) {
-                tc::put_split4_sw(tA1, kWgTile, f, k, 64, rg2[i]);
-                tc::put_split4_sw(tB1, kWgTileB1, f, k, 72, rh1[i]);
-                tc::put_split4_sw(tA0, kWgTile, f, k, 64, rg1[i]);
+                tc::put_split4_sw(tA1, kWgTile, f, k, 64, q.g2[i]);
+                tc::put_split4_sw(tB1, kWgTileB1, f, k, 72, q.h1[i]);
+                tc::put_split4_sw(tA0, kWgTile, f, k, 64, q.g1[i]);
             }
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const int idx = t + i * kWgThreads, f = idx / Q, k = (idx % Q) * 4;
-            if (f < dp && f != a.d) tc::put_split4_sw(tB0, kWgTileX, f, k, XR, rx[i]);
+            if (f < dp && f != a.d) tc::put_split4_sw(tB0, kWgTileX, f, k, XR, q.x[i]);
         }
         if (t < 2 * Q) {  // the rows of ones (1 for the chunk's live rows, 0 past the batch end)
             const int k = (t % Q) * 4, n = static_cast<int>(min(static_cast<long>(kWgK), r_end - c0));
@@ -698,11 +699,22 @@ __global__ void __launch_bounds__(kWgThreads, XR > 64 ? 1 : 3) k_wgrad_tc(WgradA
                               tc::idesc_tf32(64, U + 8, 0, 0), !first, nullptr);
             tc::gemm3_sw_warp(tm + 128, tc::OperandSW{tc::smem_u32(tA0), kWgTile, R64, 0},
                               tc::OperandSW{tc::smem_u32(tB0), kWgTileX, static_cast<uint32_t>(XR), 0}, kWgK,
-                              tc::idesc_tf32(64, dp, 0, 0),
-                              !first, mbar);
+                              tc::idesc_tf32(64, dp, 0, 0), !first, mbar);
         }
         first = 0;
-        if (c0 + kWgK < r_end) load(c0 + kWgK);  // in flight while the MMAs run
+    };
+    // Two register sets: chunk c+2's loads are in flight while chunk c is
+    // split into shared memory and its MMAs run.
+    Regs ra, rb;
+    if (r_begin < r_end) load(ra, r_begin);
+    if (r_begin + kWgK < r_end) load(rb, r_begin + kWgK);
+    for (long c0 = r_begin; c0 < r_end; c0 += 2 * kWgK) {
+        consume(ra, c0);
+        if (c0 + 2 * kWgK < r_end) load(ra, c0 + 2 * kWgK);
+        if (c0 + kWgK < r_end) {
+            consume(rb, c0 + kWgK);
+            if (c0 + 3 * kWgK < r_end) load(rb, c0 + 3 * kWgK);
+        }
     }
     if (!first) {
         tc::mbar_wait(mbar, phase);
