@@ -295,11 +295,10 @@ __device__ __forceinline__ void img_store(const ImgArgs& im, int P, int i, float
 
 // Adam / SGD update of parameter i (regressor.cpp:236-261).
 __device__ __forceinline__ void optimizer_step(int i, double g, int P, double* p64, float* p32, double* m, double* v,
-                                               long t, double lr, int adam, const ImgArgs& im) {
+                                               double c1, double c2, double lr, int adam, const ImgArgs& im) {
     double w = p64[i];
     if (adam) {
         const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-        const double c1 = 1.0 - pow(b1, static_cast<double>(t)), c2 = 1.0 - pow(b2, static_cast<double>(t));
         const double mi = b1 * m[i] + (1.0 - b1) * g;
         const double vi = b2 * v[i] + (1.0 - b2) * g * g;
         m[i] = mi;
@@ -338,7 +337,8 @@ __host__ __device__ inline size_t split_index(const SplitPartials& sp, int i) {
 }
 
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
-                       double* p64, float* p32, double* m, double* v, long t, double lr, int adam, int* nonfinite,
+                       double* p64, float* p32, double* m, double* v, double c1, double c2, double lr, int adam,
+                       int* nonfinite,
                        ImgArgs im) {
     constexpr int G = 16;
     __shared__ double part[G][33];
@@ -368,7 +368,7 @@ __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, con
         __syncthreads();
     }
     if (grp != 0 || i >= P) return;
-    optimizer_step(i, part[0][x], P, p64, p32, m, v, t, lr, adam, im);
+    optimizer_step(i, part[0][x], P, p64, p32, m, v, c1, c2, lr, adam, im);
 }
 
 // Multi-GPU: this rank's gradient (FP64, fixed-order sum of its partials) and
@@ -405,7 +405,7 @@ __global__ void k_rank_sum(int P, const float* gpart, int nct, SplitPartials sp,
 
 // Update from the gathered per-rank vectors all[G][stride], summed in rank order.
 __global__ void k_adam_dist(int P, const double* all, int G, int stride, double nb, double* p64, float* p32, double* m,
-                            double* v, long t, double lr, int adam, int* nonfinite, ImgArgs im) {
+                            double* v, double c1, double c2, double lr, int adam, int* nonfinite, ImgArgs im) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
         double s = 0.0;
@@ -415,7 +415,7 @@ __global__ void k_adam_dist(int P, const double* all, int G, int stride, double 
     if (i >= P) return;
     double g = 0.0;
     for (int r = 0; r < G; ++r) g += all[static_cast<size_t>(r) * stride + i];
-    optimizer_step(i, g, P, p64, p32, m, v, t, lr, adam, im);
+    optimizer_step(i, g, P, p64, p32, m, v, c1, c2, lr, adam, im);
 }
 
 // out[0] = sum (op 0) or min (op 1) of parts[0..n), fixed order (one warp).
@@ -842,21 +842,24 @@ struct Trainer {
         SplitPartials sp;
         const double nb = static_cast<double>(b1 - b0) * world;  // the global batch
         const int tiles = grad_tiles(X, y, b0, b1, head, nb, &sp);
+        // Adam bias corrections 1 - beta^t on the host with the host libm, as
+        // the reference's adam_update (regressor.cpp:236-252).
+        const double c1 = 1.0 - std::pow(0.9, static_cast<double>(t)), c2 = 1.0 - std::pow(0.999, static_cast<double>(t));
         if (comm) {
             k_rank_sum<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp,
                                                                            lpart.as<double>(), red.as<double>());
             check_launch(ctx);
             const double* all = gather(red.as<double>(), n.P + 1);
             k_adam_dist<<<grid1(n.P, 128), 128, 0, ctx->stream>>>(n.P, all, world, n.P + 1, nb, p64.as<double>(),
-                                                                  p32.as<float>(), m.as<double>(), v.as<double>(), t,
-                                                                  lr, adam, flag.as<int>(), img_args());
+                                                                  p32.as<float>(), m.as<double>(), v.as<double>(), c1,
+                                                                  c2, lr, adam, flag.as<int>(), img_args());
             check_launch(ctx);
             return;
         }
         k_adam<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
-                                                         m.as<double>(), v.as<double>(), t, lr, adam, flag.as<int>(),
-                                                         img_args());
+                                                         m.as<double>(), v.as<double>(), c1, c2, lr, adam,
+                                                         flag.as<int>(), img_args());
         check_launch(ctx);
     }
 
