@@ -532,7 +532,7 @@ def nested_leg(hcva, cfg, book, ctx, args, models=None, rank=0, world=1):
     parent = vroot.split(3).split(step)
     # untimed warm-up on one batch worth of states (the engine batches by a
     # 12 GB budget): first-touch of the memory pool and module loading
-    warm = max(1, min(hi - lo, int(12e9 / (inner * (cfg.n_steps - step + 1) * (5 * cfg.n_economies + 3 * cfg.n_clients + 2) * 8))))
+    warm = max(1, min(hi - lo, int(12e9 / (inner * (cfg.n_steps - step + 1) * (3 * cfg.n_economies + 3 * cfg.n_clients + 2) * 8))))
     hcva.nested_cva(cfg, book, {k: v[:warm] for k, v in st.items()}, surv[:warm], step, inner, parent, ctx=ctx,
                     first_state=lo)
     if world > 1:
