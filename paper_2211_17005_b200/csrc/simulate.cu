@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(128) k_labels_defaults(LabelArgs a) {
 // its default step and the exposure there are loop invariants over the label
 // step i, so per (i, c) only (inv_i * beta_s) * exposure remains -- the same
 // rounded products, summed in client order.  A CTA takes PP consecutive paths
-// so the staging reads of the path-fastest SoA market / cube use whole sectors.
+// (PP = 1 is used: wider CTAs measured no faster).
 template <int CMAX, int PP>
 __global__ void __launch_bounds__(128) k_labels_defaults_reg(LabelArgs a) {
     extern __shared__ double sm[];
@@ -1306,13 +1306,8 @@ void launch_cube(hcva_sim* sim) {
         a.N = sim->c_N.as<double>(); a.NSsuf = sim->c_NSsuf.as<double>(); a.H = sim->c_H.as<double>();
         a.rates = sim->rates.as<double>(); a.fx = sim->fx.as<double>(); a.lag0 = sim->lag0.as<double>();
         a.cube = sim->cube.as<double>();
-        const char* env = std::getenv("HCVA_K2_NP");
-        const int np = env ? std::atoi(env) : 4;
-        if (m.Cc % 2 == 0 && np > 1) {
-            dim3 g2((sim->M + 128 * np - 1) / (128 * np), sim->n + 1);
-            if (np >= 4) k_mtm_multi<8, 4><<<g2, 128, 0, ctx->stream>>>(a);
-            else if (np == 3) k_mtm_multi<8, 3><<<g2, 128, 0, ctx->stream>>>(a);
-            else k_mtm_multi<8, 2><<<g2, 128, 0, ctx->stream>>>(a);
+        if (m.Cc % 2 == 0) {  // four paths per thread (measured best for 8 and 64 clients)
+            k_mtm_multi<8, 4><<<dim3((sim->M + 511) / 512, sim->n + 1), 128, 0, ctx->stream>>>(a);
         } else {
             k_mtm_linear<8><<<grid, 128, 0, ctx->stream>>>(a);
         }
@@ -1386,22 +1381,12 @@ void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t*
         const size_t smem = sizeof(double) * (2 * n1 + static_cast<size_t>(n1) * Cc);
         if (smem > 48 * 1024)
             HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        const char* env = std::getenv("HCVA_K4_PP");
-        const int pp = env ? std::atoi(env) : 1;
         if (Cc <= 16) {
-            const int PPc = (pp >= 4) ? 4 : (pp >= 2 ? 2 : 1);
-            const size_t smr = smem * PPc;
-            const void* fn = Cc <= 8 ? (PPc == 4 ? (const void*)k_labels_defaults_reg<8, 4>
-                                                 : PPc == 2 ? (const void*)k_labels_defaults_reg<8, 2>
-                                                            : (const void*)k_labels_defaults_reg<8, 1>)
-                                     : (PPc == 4 ? (const void*)k_labels_defaults_reg<16, 4>
-                                                 : PPc == 2 ? (const void*)k_labels_defaults_reg<16, 2>
-                                                            : (const void*)k_labels_defaults_reg<16, 1>);
-            if (smr > 48 * 1024)
-                HCVA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smr)));
-            const int thr = std::min(128, ((PPc * N + 31) / 32) * 32);
+            const void* fn = Cc <= 8 ? (const void*)k_labels_defaults_reg<8, 1> : (const void*)k_labels_defaults_reg<16, 1>;
+            if (smem > 48 * 1024)
+                HCVA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             void* args[] = {&a};
-            HCVA_CUDA(cudaLaunchKernel(fn, dim3((sim->M + PPc - 1) / PPc), dim3(thr), args, smr, ctx->stream));
+            HCVA_CUDA(cudaLaunchKernel(fn, dim3(sim->M), dim3(threads), args, smem, ctx->stream));
         } else if (Cc < 255) {
             const size_t sm2 = sweep_smem(n1, Cc, 128, false);
             HCVA_CUDA(cudaFuncSetAttribute(k_labels_defaults_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
