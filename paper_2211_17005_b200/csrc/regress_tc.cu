@@ -497,10 +497,12 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
 // chunk c -> CTA c % gridDim.x (fixed), one partial per CTA.
 template <int U>
 struct GramShape {
-    static constexpr int MP = ((U + 2 + 3) / 4) * 4;
-    static constexpr int NBK = MP / 4;
+    static constexpr int B = 8;                           // register block edge
+    static constexpr int MP = ((U + 2 + B - 1) / B) * B;  // [h2, 1, y - mu] padded
+    static constexpr int NBK = MP / B;
     static constexpr int pairs = NBK * (NBK + 1) / 2;
-    static constexpr int threads = ((pairs + 31) / 32) * 32;
+    static constexpr int G = pairs <= 16 ? 8 : 4;        // row groups per CTA (fixed order at the end)
+    static constexpr int threads = ((pairs * G + 31) / 32) * 32;
     static constexpr int CH = 64;
     static constexpr int LD = MP + 2;  // padded row (doubles)
 };
@@ -511,19 +513,21 @@ __global__ void __launch_bounds__(GramShape<U>::threads) k_gram_h2(const float* 
                                                                     const float* __restrict__ params, int P,
                                                                     double* __restrict__ gpart) {
     using S = GramShape<U>;
+    constexpr int B = S::B;
     __shared__ __align__(16) double zs[S::CH * S::LD];
     const int t = threadIdx.x;
-    int bi = 0, rem = t;  // t -> (bi, bj), bi <= bj
+    const int grp = t / S::pairs, pt = t % S::pairs;  // row group, block pair
+    int bi = 0, rem = pt;  // pt -> (bi, bj), bi <= bj
     while (bi < S::NBK && rem >= S::NBK - bi) {
         rem -= S::NBK - bi;
         ++bi;
     }
-    const bool act = t < S::pairs;
+    const bool act = grp < S::G;
     const int bj = bi + rem;
     const double mu = static_cast<double>(params[P - 1]);
-    double acc[16];
+    double acc[B * B];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    for (int k = 0; k < B * B; ++k) acc[k] = 0.0;
     const long nch = (R + S::CH - 1) / S::CH;
     for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
         const long base = ch * S::CH;
@@ -548,28 +552,48 @@ __global__ void __launch_bounds__(GramShape<U>::threads) k_gram_h2(const float* 
         }
         __syncthreads();
         if (act)
-            for (int r = 0; r < rows; ++r) {
-                const double2* zi = reinterpret_cast<const double2*>(zs + r * S::LD + 4 * bi);
-                const double2* zj = reinterpret_cast<const double2*>(zs + r * S::LD + 4 * bj);
-                const double2 a0 = zi[0], a1 = zi[1], b0 = zj[0], b1 = zj[1];
-                const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+            for (int r = grp; r < rows; r += S::G) {
+                const double2* zi = reinterpret_cast<const double2*>(zs + r * S::LD + B * bi);
+                const double2* zj = reinterpret_cast<const double2*>(zs + r * S::LD + B * bj);
+                double av[B], bv[B];
 #pragma unroll
-                for (int p = 0; p < 4; ++p)
+                for (int h = 0; h < B / 2; ++h) {
+                    const double2 x = zi[h], w = zj[h];
+                    av[2 * h] = x.x;
+                    av[2 * h + 1] = x.y;
+                    bv[2 * h] = w.x;
+                    bv[2 * h + 1] = w.y;
+                }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[p * 4 + q] = fma(av[p], bv[q], acc[p * 4 + q]);
+                for (int p = 0; p < B; ++p)
+#pragma unroll
+                    for (int q = 0; q < B; ++q) acc[p * B + q] = fma(av[p], bv[q], acc[p * B + q]);
             }
     }
-    if (!act) return;
+    // Row groups summed in group order through shared memory (reusing the chunk buffer).
+    __syncthreads();
+    double* red = zs;  // [G-1][pairs][B*B] would exceed it: accumulate group by group instead
+    for (int g = 1; g < S::G; ++g) {
+        if (grp == g && act)
+#pragma unroll
+            for (int k = 0; k < B * B; ++k) red[pt * B * B + k] = acc[k];
+        __syncthreads();
+        if (grp == 0)
+#pragma unroll
+            for (int k = 0; k < B * B; ++k) acc[k] += red[pt * B * B + k];
+        __syncthreads();
+    }
+    if (grp != 0) return;
     // Packed output: (a, b) a <= b < m = U+1 -> upper-triangle index; rhs c = (c, U+1).
     constexpr int m = U + 1, tri = m * (m + 1) / 2;
     double* out = gpart + static_cast<size_t>(blockIdx.x) * (tri + m);
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int p = 0; p < B; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int ra = 4 * bi + p, cb = 4 * bj + q;
-            if (ra < m && cb < m && ra <= cb) out[ra * m - ra * (ra - 1) / 2 + (cb - ra)] = acc[p * 4 + q];
-            else if (ra < m && cb == m) out[tri + ra] = acc[p * 4 + q];
+        for (int q = 0; q < B; ++q) {
+            const int ra = B * bi + p, cb = B * bj + q;
+            if (ra < m && cb < m && ra <= cb) out[ra * m - ra * (ra - 1) / 2 + (cb - ra)] = acc[p * B + q];
+            else if (ra < m && cb == m) out[tri + ra] = acc[p * B + q];
         }
 }
 
