@@ -439,17 +439,6 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
         book = hcva.generate_book(cfg)
     root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
     spec = dist.shard_spec(cfg.paths, t.n_batches, world, rank)
-    comm = None
-    if world > 1:
-        comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
-        torch.distributed.barrier()
-    ctx.synchronize()
-    t0 = time.perf_counter()
-    sim = hcva.simulate_set(cfg, book, spec["n_paths"], cfg.replicas, root, path_offset=spec["path_offset"],
-                            ctx=ctx, shard=spec["shard"])
-    sim.labels_all(cfg.label_kind, to_host=False)
-    ctx.synchronize()
-    t1 = time.perf_counter()
     watchdog = None
     if world > 1:  # a stuck collective must not hang the scaling run: fail loudly instead
         def _abort():  # print the metric line with the learning leg marked, then leave
@@ -464,11 +453,24 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
         watchdog = threading.Timer(args.learning_timeout, _abort)
         watchdog.daemon = True
         watchdog.start()
-    models = rg.backward_learn(sim, t, cfg.label_kind, comm=comm)
-    p, mean, scale, rep = models.get(1)
-    t2 = time.perf_counter()
-    if watchdog is not None:
-        watchdog.cancel()
+    comm = None
+    try:
+        if world > 1:
+            comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
+            torch.distributed.barrier()
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        sim = hcva.simulate_set(cfg, book, spec["n_paths"], cfg.replicas, root, path_offset=spec["path_offset"],
+                                ctx=ctx, shard=spec["shard"])
+        sim.labels_all(cfg.label_kind, to_host=False)
+        ctx.synchronize()
+        t1 = time.perf_counter()
+        models = rg.backward_learn(sim, t, cfg.label_kind, comm=comm)
+        p, mean, scale, rep = models.get(1)
+        t2 = time.perf_counter()
+    finally:
+        if watchdog is not None:
+            watchdog.cancel()
     total, sim_s, train_s = t2 - t0, t1 - t0, t2 - t1
     if world > 1:  # max over ranks
         tt = torch.tensor([total, sim_s, train_s], device="cuda", dtype=torch.float64)
