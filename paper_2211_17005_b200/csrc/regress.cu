@@ -738,7 +738,7 @@ struct Trainer {
         long parts = std::max<long>(max_tiles, eval_ctas);
         if (use_tc) {
             dp = tc_dp(n.d);
-            parts = std::max<long>(parts, ctx->sm_count);
+            parts = std::max<long>(parts, std::max(ctx->sm_count, tc_eval_max_ctas(ctx->sm_count)));
             ld_tmax = ((std::max<long>(max_batch, 1) + 63) / 64) * 64;
             const size_t tsz = static_cast<size_t>(n.u) * ld_tmax * 4;
             h1t.alloc(tsz);

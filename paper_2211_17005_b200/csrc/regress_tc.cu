@@ -491,6 +491,155 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
+// Full-sample evaluation (loss / head-switch minimum / predictions / layer-2
+// activations) for the resident-input shapes, two CTAs per SM: the layer-1
+// operand H1 (hi | lo) goes from the layer-0 epilogue straight into tensor
+// memory (tcgen05.st) and layer 1 reads it from there (A-in-TMEM MMA), so a
+// CTA needs no H tile in shared memory (W0, W1, vectors and the feature tile:
+// ~82 KB), and two CTAs per SM interleave their GEMM -> epilogue chains.
+template <int U>
+struct EvalShape {
+    static constexpr int UH = U < 32 ? U : 32;  // columns per thread
+    static constexpr int NS = U / UH;           // warpgroups
+    static constexpr int threads = 128 * NS;
+};
+
+__host__ __device__ constexpr size_t eval_tc_smem(int U, int dp) {
+    return 2ull * U * dp * 4 + 2ull * U * U * 4 + 1024 + 2ull * 128 * dp * 4 + 2 * 128 * 4 + 64;
+}
+
+template <int U, int ACT>
+__global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a, long t_first, long n_tiles) {
+    constexpr int NS = EvalShape<U>::NS, UH = EvalShape<U>::UH;
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int dp = a.dp;
+    const uint32_t w0b = U * dp * 4, w1b = U * U * 4, xb = x_plane_bytes(dp);
+    uint8_t* w0 = sm;                                         // W0 hi | lo
+    uint8_t* w1 = w0 + 2 * w0b;                               // W1 hi | lo
+    float* vec = reinterpret_cast<float*>(w1 + 2 * w1b);      // b0 | b1 | w2 | b2, mu
+    uint8_t* bufX = reinterpret_cast<uint8_t*>(vec) + 1024;   // feature tile hi | lo
+    float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);     // [NS][128] partial output sums
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);  // [0] MMA, [1] weights, [2] features
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid & 127, hf = tid >> 7, cb = hf * UH;
+    if (tid == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::mbar_init(&bar[2], 1);
+        tc::fence_async_smem();
+    }
+    if (warp == 0) tc::tmem_alloc(tbase, 256);  // D0 | D1 | H1 hi | H1 lo
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = *tbase;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const long t_end = t_first + n_tiles;
+    long tile = t_first + blockIdx.x;
+    pdl_wait();  // the optimizer's weight image
+    if (tid == 0) {
+        tc::mbar_expect_tx(&bar[1], 2 * w0b + 2 * w1b + 1024);
+        tc::bulk_g2s(w0, a.wimg, 2 * w0b + 2 * w1b, &bar[1]);  // W0 | W1 (W1^T not needed)
+        tc::bulk_g2s(vec, a.wimg + 2 * w0b + 4 * w1b, 1024, &bar[1]);
+        tc::mbar_expect_tx(&bar[2], 2 * xb);
+        tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
+    }
+    tc::mbar_wait(&bar[1], 0);
+    const float b2 = vec[192], mu = vec[193];
+    uint32_t mph = 0, xph = 0;
+    auto mma_wait = [&]() {
+        if (warp == 0) tc::mbar_wait(&bar[0], mph);
+        mph ^= 1;
+        __syncthreads();
+        tc::fence_after_sync();
+    };
+    double loss = 0.0, mn = INFINITY;
+    for (; tile < t_end; tile += gridDim.x) {
+        const long row = tile * 128 + r;
+        const bool live = row >= a.b0 && row < a.b1;
+        const double yrow = (live && (a.mode & 1) && hf == 0) ? __ldg(a.y + row) : 0.0;
+        if (tid == 0) tc::mbar_wait(&bar[2], xph);
+        xph ^= 1;
+        if (warp == 0)  // ---- F0: D0 = X W0^T
+            tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0),
+                           0, &bar[0]);
+        mma_wait();
+        if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
+            tc::mbar_expect_tx(&bar[2], 2 * xb);
+            tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
+        }
+#pragma unroll
+        for (int c = 0; c < UH; c += 16) {  // H1 = act(D0 + b0) -> tensor memory, hi | lo
+            float v[16], lo[16];
+            tc::tmem_ld16(tm + lb + cb + c, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const float h = act_f<ACT>(v[q] + vec[cb + c + q]);
+                v[q] = tc::tf32_rna(h);
+                lo[q] = h - v[q];
+            }
+            tc::tmem_st16(tm + lb + 128 + cb + c, v);
+            tc::tmem_st16(tm + lb + 192 + cb + c, lo);
+        }
+        tc::tmem_wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        if (tid == 0) {  // ---- F1: D1 = H1 W1^T, H1 from tensor memory
+            tc::gemm3_ts(tm + 64, tm + 128, tm + 192, tc::kmajor(w1, w1b, U), U, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+        float h2[UH];
+#pragma unroll
+        for (int c = 0; c < UH; c += 16) tc::tmem_ld16(tm + lb + 64 + cb + c, h2 + c);
+#pragma unroll
+        for (int q = 0; q < UH; ++q) h2[q] = act_f<ACT>(h2[q] + vec[64 + cb + q]);
+        float fp = 0.0f;
+#pragma unroll
+        for (int j = 0; j < UH; ++j) fp = fmaf(h2[j], vec[128 + cb + j], fp);
+        float f = b2 + fp;
+        if (NS > 1) {
+            fsh[hf * 128 + r] = fp;
+            __syncthreads();
+            float fs = fsh[r];
+#pragma unroll
+            for (int h = 1; h < NS; ++h) fs += fsh[h * 128 + r];
+            f = b2 + fs;
+        }
+        if ((a.mode & 8) && live)
+#pragma unroll
+            for (int j = 0; j < UH; j += 4)
+                *reinterpret_cast<float4*>(a.H2 + row * U + cb + j) = make_float4(h2[j], h2[j + 1], h2[j + 2], h2[j + 3]);
+        if (live && hf == 0) {
+            const double ph = static_cast<double>((f < 0.0f ? 0.0f : f) + mu);
+            if (a.mode & 1) {
+                const double res = ph - yrow;
+                loss += res * res;
+            }
+            if (a.mode & 2) mn = fmin(mn, static_cast<double>(f + mu));
+            if (a.mode & 4) a.pred[row] = ph;
+        }
+    }
+    // per-CTA partials: warpgroup 0 holds the per-row terms (fixed order over its warps)
+    tc::fence_before_sync();
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(bufX);
+    loss = warp_sum(loss);
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0 && warp < 4) {
+        red[warp] = loss;
+        red[4 + warp] = mn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (a.mode & 1) a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
+        if (a.mode & 2) a.mpart[blockIdx.x] = fmin(fmin(red[4], red[5]), fmin(red[6], red[7]));
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
 // Refit Gram (regressor.cpp:191-213) in FP64 from the FP32 layer-2
 // activations: z = [h2, 1, y - mu] padded to MP = 4 * NBK, one thread per
 // 4x4 block (bi <= bj) of z z^T, 64-row chunks staged in shared memory,
@@ -790,7 +939,7 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
     uint64_t* mbar = reinterpret_cast<uint64_t*>(tb + 2 * bbytes);
     uint32_t* tbase = reinterpret_cast<uint32_t*>(mbar + 1);
     const int t = threadIdx.x, warp = t >> 5;
-    const bool swz = variant == 1 || variant >= 5;
+    const bool swz = variant == 1 || (variant >= 5 && variant <= 7);
     const bool amn = variant == 2 || variant == 4 || variant == 5 || variant == 7;
     const bool bmn = variant == 3 || variant == 4 || variant == 6 || variant == 7;
     if (t == 0) tc::mbar_init(mbar, 1);
@@ -814,7 +963,27 @@ __global__ void k_tc_gemm_diag(int M, int N, int K, const float* A, const float*
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tm = *tbase;
-    if (t == 0) {
+    if (variant == 8) {  // A (hi | lo) from tensor memory at columns 128 / 192 (M = 128, K <= 64)
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        for (int c0 = 0; c0 < K; c0 += 16) {
+            float hi[16], lo[16];
+            for (int q = 0; q < 16; ++q) {
+                const float a = (t < M && c0 + q < K) ? A[t * K + c0 + q] : 0.0f;
+                hi[q] = tc::tf32_rna(a);
+                lo[q] = a - hi[q];
+            }
+            tc::tmem_st16(tm + lane_base + 128 + c0, hi);
+            tc::tmem_st16(tm + lane_base + 192 + c0, lo);
+        }
+        tc::tmem_wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        if (t == 0) {
+            tc::gemm3_ts(tm, tm + 128, tm + 192, tc::kmajor(tb, bbytes, N), K, tc::idesc_tf32(M, N, 0, 0), 0);
+            tc::commit(mbar);
+        }
+    } else if (t == 0) {
         if (swz) {
             // MN-major SW128 tiles hold K rows x MN columns (R = K).
             tc::gemm3_sw(tm, tc::OperandSW{tc::smem_u32(ta), abytes, static_cast<uint32_t>(amn ? K : M), amn},
@@ -934,9 +1103,39 @@ void launch_tile_u(const TileArgs& a, long t_first, long n_tiles, int ctas, cuda
     }
 }
 
+template <int U, int ACT>
+void launch_eval_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = eval_tc_smem(U, a.dp);
+    HCVA_CUDA(cudaFuncSetAttribute(k_eval_tc<U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pdl_launch(k_eval_tc<U, ACT>, dim3(ctas), dim3(EvalShape<U>::threads), smem, s, a, t_first, n_tiles);
+}
+
+template <int U>
+void launch_eval_u(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    switch (a.act) {
+        case 0: launch_eval_ua<U, 0>(a, t_first, n_tiles, ctas, s); break;
+        case 1: launch_eval_ua<U, 1>(a, t_first, n_tiles, ctas, s); break;
+        case 2: launch_eval_ua<U, 2>(a, t_first, n_tiles, ctas, s); break;
+        default: launch_eval_ua<U, 3>(a, t_first, n_tiles, ctas, s); break;
+    }
+}
+
+int tc_eval_max_ctas(int sm_count) { return 2 * sm_count; }
+
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
     if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
     const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
+    static const bool eval2 = [] {
+        const char* e = std::getenv("HCVA_EVAL_TMEM");
+        return !(e && e[0] == '0');
+    }();
+    if (a.mode != 0 && eval2 && u >= 16 && !tile_chunked(u, a.dp) && eval_tc_smem(u, a.dp) <= 113 * 1024) {
+        const int ctas = static_cast<int>(std::min<long>(n_tiles, tc_eval_max_ctas(sm_count)));
+        if (u == 16) launch_eval_u<16>(a, t_first, n_tiles, ctas, s);
+        else if (u == 32) launch_eval_u<32>(a, t_first, n_tiles, ctas, s);
+        else launch_eval_u<64>(a, t_first, n_tiles, ctas, s);
+        return ctas;
+    }
     const int ctas = static_cast<int>(std::min<long>(n_tiles, sm_count));
     if (u == 16) launch_tile_u<16>(a, t_first, n_tiles, ctas, s);
     else if (u == 32) launch_tile_u<32>(a, t_first, n_tiles, ctas, s);

@@ -50,7 +50,8 @@ void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* 
 // Returns the number of per-CTA partials written (gpart / lpart / mpart rows).
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s);
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s);
-int tc_wgrad_max_ctas(int sm_count);  // rows of WgradArgs::gpart the launcher may write
+int tc_wgrad_max_ctas(int sm_count);
+int tc_eval_max_ctas(int sm_count);  // partial rows an evaluation launch may write  // rows of WgradArgs::gpart the launcher may write
 // FP64 Gram partials of z = [H2 row, 1] and rhs z (y - mu) in k_refit's packed
 // layout (upper triangle, then rhs); returns the partial count (<= max_parts).
 int launch_gram_h2(int u, const float* H2, const double* y, long R, const float* params, int P, double* gpart,

@@ -244,6 +244,25 @@ __device__ __forceinline__ void gemm3_warp(uint32_t d_tmem, const Operand& A, co
     if (mbar) commit_if(issue, mbar);
 }
 
+// A operand from tensor memory (TS form): M rows in lanes, K tf32 columns.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, int accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// 3xTF32 with A (hi at a_hi, lo at a_lo columns) in tensor memory, B K-major in shared memory.
+__device__ __forceinline__ void gemm3_ts(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, const Operand& B, int K,
+                                         uint32_t idesc, int accumulate) {
+    for (int ks = 0; ks < K / 8; ++ks) {
+        mma_tf32_ts(d_tmem, a_hi + 8 * ks, B.desc(0, ks), idesc, (ks > 0 || accumulate) ? 1 : 0);
+        mma_tf32_ts(d_tmem, a_lo + 8 * ks, B.desc(0, ks), idesc, 1);
+        mma_tf32_ts(d_tmem, a_hi + 8 * ks, B.desc(1, ks), idesc, 1);
+    }
+}
+
 __device__ __forceinline__ void gemm3(uint32_t d_tmem, const Operand& A, const Operand& B, int K, uint32_t idesc,
                                       int accumulate) {
     for (int ks = 0; ks < K / 8; ++ks) {
