@@ -700,7 +700,7 @@ struct Trainer {
     // Tensor-core path: weight-gradient partials, transposed activations, packed operand images.
     DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2, gram_sum;
     int max_tiles = 0, last_parts = 0, dp = 0, gram_parts = 0;
-    bool use_tc = false;
+    bool use_tc = false, xf32 = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
     bool wimg_valid = false;  // weight image matches p32
     const uint8_t* ximg_over = nullptr;    // evaluation on another feature image (Q/R probe)
@@ -738,6 +738,7 @@ struct Trainer {
         long parts = std::max<long>(max_tiles, eval_ctas);
         if (use_tc) {
             dp = tc_dp(n.d);
+            xf32 = tc_two_cta(n.u, dp);
             parts = std::max<long>(parts, std::max(ctx->sm_count, tc_eval_max_ctas(ctx->sm_count)));
             ld_tmax = ((std::max<long>(max_batch, 1) + 63) / 64) * 64;
             const size_t tsz = static_cast<size_t>(n.u) * ld_tmax * 4;
@@ -781,7 +782,7 @@ struct Trainer {
     void prepare_x(const float* X, long R) {
         if (!use_tc) return;
         if (R > x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
-        launch_pack_x(X, R, n.d, dp, ximg.as<uint8_t>(), xt.as<float>(), ld_x, ctx->stream);
+        launch_pack_x(X, R, n.d, dp, ximg.as<uint8_t>(), xt.as<float>(), ld_x, xf32 ? 1 : 0, ctx->stream);
         check_launch(ctx);
     }
 
@@ -803,6 +804,7 @@ struct Trainer {
         ta.H2 = h2.as<float>();
         ta.H1t = h1t.as<float>(); ta.G2t = g2t.as<float>(); ta.G1t = g1t.as<float>();
         ta.ld_t = ((b1 - b0 + 63) / 64) * 64;
+        ta.xf32 = xf32 ? 1 : 0;
         const int ctas = launch_tile_tc(n.u, ta, ctx->sm_count, ctx->stream);
         check_launch(ctx);
         return ctas;
@@ -984,6 +986,7 @@ struct FeatArgs {
     float* Xt;         // ... and the transposed copy [dp][ld_x]
     long ld_x;
     int dp;
+    int xf32;          // feature tiles as one FP32 plane (tc_two_cta) instead of hi | lo planes
 };
 
 __device__ __forceinline__ double state_col(const FeatArgs& a, int k, int j) {
@@ -1007,7 +1010,7 @@ __global__ void k_build_x(FeatArgs a) {
         const bool in = row < R;
         const int k = in ? static_cast<int>(row / a.N) : 0;
         const uint32_t xb = 128u * a.dp * 4;
-        uint8_t* tb = a.ximg + (row / 128) * 2 * xb;
+        uint8_t* tb = a.ximg + (row / 128) * (a.xf32 ? 1 : 2) * xb;
         for (int c = 0; c < a.dp; c += 4) {
             float v[4];
 #pragma unroll
@@ -1020,7 +1023,11 @@ __global__ void k_build_x(FeatArgs a) {
                 v[qq] = x;
                 if (in && a.Xt) a.Xt[col * a.ld_x + row] = x;
             }
-            tc::put_split4(tb, xb, static_cast<int>(row % 128), c, 128, make_float4(v[0], v[1], v[2], v[3]));
+            if (a.xf32)
+                *reinterpret_cast<float4*>(tb + tc::core_off(static_cast<int>(row % 128), c, 128)) =
+                    make_float4(v[0], v[1], v[2], v[3]);
+            else
+                tc::put_split4(tb, xb, static_cast<int>(row % 128), c, 128, make_float4(v[0], v[1], v[2], v[3]));
         }
         return;
     }
@@ -1168,6 +1175,7 @@ void build_features(Trainer& tr, FeatArgs fa, DeviceBuf& X, long R, DeviceBuf* i
     if (tr.use_tc) {
         if (!img && R > tr.x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
         fa.ximg = img ? img->as<uint8_t>() : tr.ximg.as<uint8_t>();
+        fa.xf32 = tr.xf32 ? 1 : 0;
         fa.Xt = img ? nullptr : tr.xt.as<float>();
         fa.ld_x = tr.ld_x;
         fa.dp = tr.dp;

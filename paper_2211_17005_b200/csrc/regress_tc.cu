@@ -162,9 +162,9 @@ __global__ void k_pack_w(int U, int d, int dp, int off0, int off1, int off2, int
 }
 
 __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uint8_t* __restrict__ img,
-                         float* __restrict__ Xt, long ld_x) {
+                         float* __restrict__ Xt, long ld_x, int xf32) {
     const uint32_t xb = x_plane_bytes(dp);
-    uint8_t* tile = img + static_cast<size_t>(blockIdx.x) * 2 * xb;
+    uint8_t* tile = img + static_cast<size_t>(blockIdx.x) * (xf32 ? 1 : 2) * xb;
     const int r = threadIdx.x;
     const long row = static_cast<long>(blockIdx.x) * 128 + r;
     const bool in = row < R;
@@ -172,7 +172,8 @@ __global__ void k_pack_x(const float* __restrict__ X, long R, int d, int dp, uin
         float v[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) v[q] = (in && c + q < d) ? X[row * d + c + q] : 0.0f;
-        tc::put_split4(tile, xb, r, c, 128, make_float4(v[0], v[1], v[2], v[3]));
+        if (xf32) *reinterpret_cast<float4*>(tile + tc::core_off(r, c, 128)) = make_float4(v[0], v[1], v[2], v[3]);
+        else tc::put_split4(tile, xb, r, c, 128, make_float4(v[0], v[1], v[2], v[3]));
         if (in)
 #pragma unroll
             for (int q = 0; q < 4; ++q) Xt[(c + q) * ld_x + row] = v[q];
@@ -491,6 +492,27 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
+// The FP32 feature tile (core layout, one plane) -> tensor memory as the A
+// operand of layer 0: hi at column 128, lo at 128 + dp.  The NS warpgroups
+// split the 8-column groups between them; rows = TMEM lanes of each warp.
+template <int NS>
+__device__ __forceinline__ void x_to_tmem(const uint8_t* bufX, int dp, uint32_t tm, uint32_t lb, int r, int hf) {
+    const int groups = dp / 8, per = (groups + NS - 1) / NS;
+    for (int gi = hf * per; gi < min(groups, (hf + 1) * per); ++gi) {
+        const float4 x0 = *reinterpret_cast<const float4*>(bufX + tc::core_off(r, 8 * gi, 128));
+        const float4 x1 = *reinterpret_cast<const float4*>(bufX + tc::core_off(r, 8 * gi + 4, 128));
+        float hi[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w}, lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float v = hi[q];
+            hi[q] = tc::tf32_rna(v);
+            lo[q] = v - hi[q];
+        }
+        tc::tmem_st8(tm + lb + 128 + 8 * gi, hi);
+        tc::tmem_st8(tm + lb + 128 + dp + 8 * gi, lo);
+    }
+}
+
 // Full-sample evaluation (loss / head-switch minimum / predictions / layer-2
 // activations) for the resident-input shapes, two CTAs per SM: the layer-1
 // operand H1 (hi | lo) goes from the layer-0 epilogue straight into tensor
@@ -505,7 +527,7 @@ struct EvalShape {
 };
 
 __host__ __device__ constexpr size_t eval_tc_smem(int U, int dp) {
-    return 2ull * U * dp * 4 + 2ull * U * U * 4 + 1024 + 2ull * 128 * dp * 4 + 2 * 128 * 4 + 64;
+    return 2ull * U * dp * 4 + 2ull * U * U * 4 + 1024 + 1ull * 128 * dp * 4 + 2 * 128 * 4 + 64;
 }
 
 template <int U, int ACT>
@@ -517,8 +539,8 @@ __global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a
     uint8_t* w0 = sm;                                         // W0 hi | lo
     uint8_t* w1 = w0 + 2 * w0b;                               // W1 hi | lo
     float* vec = reinterpret_cast<float*>(w1 + 2 * w1b);      // b0 | b1 | w2 | b2, mu
-    uint8_t* bufX = reinterpret_cast<uint8_t*>(vec) + 1024;   // feature tile hi | lo
-    float* fsh = reinterpret_cast<float*>(bufX + 2 * xb);     // [NS][128] partial output sums
+    uint8_t* bufX = reinterpret_cast<uint8_t*>(vec) + 1024;   // feature tile, FP32
+    float* fsh = reinterpret_cast<float*>(bufX + xb);         // [NS][128] partial output sums
     uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);  // [0] MMA, [1] weights, [2] features
     uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -542,8 +564,8 @@ __global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a
         tc::mbar_expect_tx(&bar[1], 2 * w0b + 2 * w1b + 1024);
         tc::bulk_g2s(w0, a.wimg, 2 * w0b + 2 * w1b, &bar[1]);  // W0 | W1 (W1^T not needed)
         tc::bulk_g2s(vec, a.wimg + 2 * w0b + 4 * w1b, 1024, &bar[1]);
-        tc::mbar_expect_tx(&bar[2], 2 * xb);
-        tc::bulk_g2s(bufX, a.ximg + tile * 2 * xb, 2 * xb, &bar[2]);
+        tc::mbar_expect_tx(&bar[2], xb);
+        tc::bulk_g2s(bufX, a.ximg + tile * xb, xb, &bar[2]);
     }
     tc::mbar_wait(&bar[1], 0);
     const float b2 = vec[192], mu = vec[193];
@@ -559,16 +581,23 @@ __global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a
         const long row = tile * 128 + r;
         const bool live = row >= a.b0 && row < a.b1;
         const double yrow = (live && (a.mode & 1) && hf == 0) ? __ldg(a.y + row) : 0.0;
-        if (tid == 0) tc::mbar_wait(&bar[2], xph);
+        tc::mbar_wait(&bar[2], xph);
         xph ^= 1;
-        if (warp == 0)  // ---- F0: D0 = X W0^T
-            tc::gemm3_warp(tm, tc::kmajor(bufX, xb, 128), tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0),
-                           0, &bar[0]);
-        mma_wait();
-        if (tid == 0 && tile + gridDim.x < t_end) {  // feature tile consumed: stream in the next one
-            tc::mbar_expect_tx(&bar[2], 2 * xb);
-            tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
+        x_to_tmem<NS>(bufX, dp, tm, lb, r, hf);  // the feature tile, split, into tensor memory
+        tc::tmem_wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+        if (tid == 0) {
+            if (tile + gridDim.x < t_end) {  // feature tile read: stream in the next one
+                tc::mbar_expect_tx(&bar[2], xb);
+                tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * xb, xb, &bar[2]);
+            }
+            // ---- F0: D0 = X W0^T, X from tensor memory
+            tc::gemm3_ts(tm, tm + 128, tm + 128 + dp, tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
         }
+        mma_wait();
 #pragma unroll
         for (int c = 0; c < UH; c += 16) {  // H1 = act(D0 + b0) -> tensor memory, hi | lo
             float v[16], lo[16];
@@ -636,6 +665,245 @@ __global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a
     if (tid == 0) {
         if (a.mode & 1) a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
         if (a.mode & 2) a.mpart[blockIdx.x] = fmin(fmin(red[4], red[5]), fmin(red[6], red[7]));
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
+// SGD tile kernel, two CTAs per SM (resident inputs, dp <= 32 at U = 64): the
+// A operands of layer 1 (H1) and of the backward GEMM (G2) go through tensor
+// memory instead of a shared H tile, the vectors are read through L1, and each
+// thread covers 32 columns in two 16-column passes (layer 2's activations are
+// recomputed from D1 for the gradient pass) -- <= 113 KB of shared memory and
+// <= 128 registers, so two CTAs per SM interleave their GEMM -> epilogue
+// chains.  Same arithmetic and outputs as k_tile_tc's SGD mode.
+template <int U>
+struct SgdShape {
+    static constexpr int UH = U < 32 ? U : 32;  // columns per thread
+    static constexpr int NS = U / UH;           // warpgroups
+    static constexpr int CP = 16;               // columns per pass
+    static constexpr int NP = UH / CP;
+    static constexpr int threads = 128 * NS;
+    static constexpr int warps = 4 * NS;
+};
+
+__host__ __device__ constexpr size_t sgd_tc_smem(int U, int dp) {
+    return 2ull * U * dp * 4 + 4ull * U * U * 4 + 1ull * 128 * dp * 4 + 128 * 4 + 64;
+}
+
+template <int U, int ACT>
+__global__ void __launch_bounds__(SgdShape<U>::threads, 2) k_sgd_tc(TileArgs a, long t_first, long n_tiles) {
+    using S = SgdShape<U>;
+    constexpr int NS = S::NS, UH = S::UH, CP = S::CP, NP = S::NP;
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int dp = a.dp;
+    const uint32_t w0b = U * dp * 4, w1b = U * U * 4, xb = x_plane_bytes(dp);
+    uint8_t* w0 = sm;                                        // W0 hi | lo
+    uint8_t* w1 = w0 + 2 * w0b;                              // W1 hi | lo
+    uint8_t* w1t = w1 + 2 * w1b;                             // W1^T hi | lo
+    uint8_t* bufX = w1t + 2 * w1b;                           // feature tile, FP32
+    float* fsh = reinterpret_cast<float*>(bufX + xb);        // [128] output-sum exchange
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 128);  // [0] MMA, [1] weights, [2] features
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 3);
+    const float* vec = reinterpret_cast<const float*>(a.wimg + 2 * w0b + 4 * w1b);  // b0 | b1 | w2 | b2, mu
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid & 127, hf = tid >> 7, cb = hf * UH;
+    if (tid == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::mbar_init(&bar[2], 1);
+        tc::fence_async_smem();
+    }
+    if (warp == 0) tc::tmem_alloc(tbase, 256);  // D0 | D1, then Dbp | A hi | A lo
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = *tbase;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const long t_end = t_first + n_tiles;
+    long tile = t_first + blockIdx.x;
+    pdl_wait();  // the optimizer's weight image, the previous weight gradient's reads of H1t, G2t, G1t
+    if (tid == 0) {
+        tc::mbar_expect_tx(&bar[1], 2 * w0b + 4 * w1b);
+        tc::bulk_g2s(w0, a.wimg, 2 * w0b + 4 * w1b, &bar[1]);  // W0 | W1 | W1^T
+        tc::mbar_expect_tx(&bar[2], xb);
+        tc::bulk_g2s(bufX, a.ximg + tile * xb, xb, &bar[2]);
+    }
+    const float b2 = __ldg(vec + 192), mu = __ldg(vec + 193);
+    tc::mbar_wait(&bar[1], 0);
+    uint32_t mph = 0, xph = 0;
+    auto mma_wait = [&]() {
+        if (warp == 0) tc::mbar_wait(&bar[0], mph);
+        mph ^= 1;
+        __syncthreads();
+        tc::fence_after_sync();
+    };
+    auto cta_sync = [&]() {
+        tc::fence_before_sync();
+        __syncthreads();
+        tc::fence_after_sync();
+    };
+    double loss = 0.0, dmu = 0.0;
+    float gb2 = 0.0f;
+    float acc_w2[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc_w2[p] = 0.0f;
+
+    for (; tile < t_end; tile += gridDim.x) {
+        const long row = tile * 128 + r;
+        const bool live = row >= a.b0 && row < a.b1;
+        const long trow = row - a.b0;
+        const double yrow = live ? __ldg(a.y + row) : 0.0;
+        tc::mbar_wait(&bar[2], xph);
+        xph ^= 1;
+        x_to_tmem<NS>(bufX, dp, tm, lb, r, hf);  // the feature tile, split, into tensor memory
+        tc::tmem_wait_st();
+        cta_sync();
+        if (tid == 0) {
+            if (tile + gridDim.x < t_end) {  // feature tile read: stream in the next one
+                tc::mbar_expect_tx(&bar[2], xb);
+                tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * xb, xb, &bar[2]);
+            }
+            // ---- F0: D0 = X W0^T, X from tensor memory
+            tc::gemm3_ts(tm, tm + 128, tm + 128 + dp, tc::kmajor(w0, w0b, U), dp, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+        // H1 = act(D0 + b0) -> A (hi | lo), H1t; act'(H1) back into D0
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int c0 = cb + p * CP;
+            float v[CP], hi[CP];
+            tc::tmem_ld16(tm + lb + c0, v);
+#pragma unroll
+            for (int q = 0; q < CP; ++q) {
+                v[q] = act_f<ACT>(v[q] + __ldg(vec + c0 + q));
+                hi[q] = tc::tf32_rna(v[q]);
+            }
+            if (live)
+#pragma unroll
+                for (int q = 0; q < CP; ++q) a.H1t[(c0 + q) * a.ld_t + trow] = v[q];
+            tc::tmem_st16(tm + lb + 128 + c0, hi);
+#pragma unroll
+            for (int q = 0; q < CP; ++q) {
+                hi[q] = v[q] - hi[q];  // lo
+                v[q] = act_d<ACT>(v[q]);
+            }
+            tc::tmem_st16(tm + lb + 192 + c0, hi);
+            tc::tmem_st16(tm + lb + c0, v);
+        }
+        tc::tmem_wait_st();
+        cta_sync();
+        if (tid == 0) {  // ---- F1: D1 = H1 W1^T, H1 from tensor memory
+            tc::gemm3_ts(tm + 64, tm + 128, tm + 192, tc::kmajor(w1, w1b, U), U, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+        // f = b2 + H2 w2 (warpgroup partials summed in order 0, 1)
+        float fp = 0.0f;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int c0 = cb + p * CP;
+            float h[CP];
+            tc::tmem_ld16(tm + lb + 64 + c0, h);
+#pragma unroll
+            for (int j = 0; j < CP; ++j) fp = fmaf(act_f<ACT>(h[j] + __ldg(vec + 64 + c0 + j)), __ldg(vec + 128 + c0 + j), fp);
+        }
+        float f = b2 + fp;
+        if (NS > 1) {
+            if (hf == 1) fsh[r] = fp;
+            __syncthreads();
+            if (hf == 0) {
+                f = b2 + (fp + fsh[r]);
+                fsh[r] = f;
+            }
+            __syncthreads();
+            f = fsh[r];
+        }
+        // residual, output layer, mu
+        float dd = 0.0f;
+        if (live) {
+            const float pr = ((a.head && f < 0.0f) ? 0.0f : f) + mu;
+            const double res = static_cast<double>(pr) - yrow;
+            const double dm = 2.0 * res / a.nb;
+            if (hf == 0) {
+                loss += res * res;
+                dmu += dm;
+            }
+            dd = static_cast<float>(dm);
+            if (a.head && !(f > 0.0f)) dd = 0.0f;
+        }
+        if (hf == 0) gb2 += dd;
+        // G2 = dd w2 act'(H2) -> A (hi | lo; layer 1 has consumed H1), G2t; output-layer gradient
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int c0 = cb + p * CP;
+            float h[CP], g[CP];
+            tc::tmem_ld16(tm + lb + 64 + c0, h);
+#pragma unroll
+            for (int j = 0; j < CP; ++j) {
+                h[j] = act_f<ACT>(h[j] + __ldg(vec + 64 + c0 + j));
+                g[j] = dd * h[j];
+            }
+            acc_w2[p] += bfly_sum<CP>(g, lane);
+#pragma unroll
+            for (int j = 0; j < CP; ++j) g[j] = dd * __ldg(vec + 128 + c0 + j) * act_d<ACT>(h[j]);
+            if (live)
+#pragma unroll
+                for (int j = 0; j < CP; ++j) a.G2t[(c0 + j) * a.ld_t + trow] = g[j];
+#pragma unroll
+            for (int j = 0; j < CP; ++j) h[j] = tc::tf32_rna(g[j]);
+            tc::tmem_st16(tm + lb + 128 + c0, h);
+#pragma unroll
+            for (int j = 0; j < CP; ++j) h[j] = g[j] - h[j];
+            tc::tmem_st16(tm + lb + 192 + c0, h);
+        }
+        tc::tmem_wait_st();
+        cta_sync();  // every D1 read done: the backward GEMM reuses its columns
+        if (tid == 0) {  // ---- B: Dbp = G2 W1 (B: the W1^T tile), G2 from tensor memory
+            tc::gemm3_ts(tm + 64, tm + 128, tm + 192, tc::kmajor(w1t, w1b, U), U, tc::idesc_tf32(128, U, 0, 0), 0);
+            tc::commit(&bar[0]);
+        }
+        mma_wait();
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {  // G1 = Dbp act'(H1) -> G1t
+            const int c0 = cb + p * CP;
+            float g[CP], dv[CP];
+            tc::tmem_ld16(tm + lb + 64 + c0, g);
+            tc::tmem_ld16(tm + lb + c0, dv);
+            if (live)
+#pragma unroll
+                for (int j = 0; j < CP; ++j) a.G1t[(c0 + j) * a.ld_t + trow] = g[j] * dv[j];
+        }
+        cta_sync();  // TMEM reads of D0 / Dbp done before the next tile's F0
+    }
+
+    // ---- per-CTA partials (fixed order over the warps), scratch in the feature tile
+    cta_sync();
+    constexpr int NWP = S::warps;
+    float* part = reinterpret_cast<float*>(bufX);                    // [warp][64]
+    double* red = reinterpret_cast<double*>(part + NWP * 64);        // [3][warps]
+    if (lane < CP)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) part[warp * 64 + cb + p * CP + lane] = acc_w2[p];
+    loss = warp_sum(loss);
+    dmu = warp_sum(dmu);
+    gb2 = warp_sum(gb2);
+    if (lane == 0) {
+        red[warp] = loss;
+        red[NWP + warp] = dmu;
+        red[2 * NWP + warp] = gb2;
+    }
+    __syncthreads();
+    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
+    if (tid < U) {
+        const int w0q = (tid / UH) * 4;  // first warp of the owning warpgroup
+        gout[a.off2 + tid] = part[(w0q + 0) * 64 + tid] + part[(w0q + 1) * 64 + tid] + part[(w0q + 2) * 64 + tid] +
+                             part[(w0q + 3) * 64 + tid];
+    }
+    if (tid == 0) {
+        a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];  // warpgroup 0 holds the per-row terms
+        gout[a.P - 1] = static_cast<float>(red[NWP] + red[NWP + 1] + red[NWP + 2] + red[NWP + 3]);
+        gout[a.off2 + U] = static_cast<float>(red[2 * NWP] + red[2 * NWP + 1] + red[2 * NWP + 2] + red[2 * NWP + 3]);
     }
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
@@ -1057,6 +1325,14 @@ bool pdl_enabled() {
     return on;
 }
 
+bool tc_two_cta(int u, int dp) {
+    static const bool on = [] {
+        const char* e = std::getenv("HCVA_TWO_CTA");
+        return !(e && e[0] == '0');
+    }();
+    return on && u >= 16 && dp <= 64 && sgd_tc_smem(u, dp) <= 113 * 1024 && eval_tc_smem(u, dp) <= 113 * 1024;
+}
+
 bool tc_eligible(int d, int h, int u) {
     if (const char* e = std::getenv("HCVA_REGRESS_SIMT"))
         if (std::atoi(e)) return false;
@@ -1075,9 +1351,10 @@ void launch_pack_w(int u, int d, int dp, int off0, int off1, int off2, int P, co
     k_pack_w<<<(n + 255) / 256, 256, 0, s>>>(u, d, dp, off0, off1, off2, P, params, wimg);
 }
 
-void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, cudaStream_t s) {
+void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, int xf32,
+                   cudaStream_t s) {
     const long tiles = (R + 127) / 128;
-    if (tiles > 0) k_pack_x<<<static_cast<unsigned>(tiles), 128, 0, s>>>(X, R, d, dp, ximg, Xt, ld_x);
+    if (tiles > 0) k_pack_x<<<static_cast<unsigned>(tiles), 128, 0, s>>>(X, R, d, dp, ximg, Xt, ld_x, xf32);
 }
 
 template <int U, int ACT>
@@ -1122,14 +1399,34 @@ void launch_eval_u(const TileArgs& a, long t_first, long n_tiles, int ctas, cuda
 
 int tc_eval_max_ctas(int sm_count) { return 2 * sm_count; }
 
+template <int U, int ACT>
+void launch_sgd_ua(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = sgd_tc_smem(U, a.dp);
+    HCVA_CUDA(cudaFuncSetAttribute(k_sgd_tc<U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pdl_launch(k_sgd_tc<U, ACT>, dim3(ctas), dim3(SgdShape<U>::threads), smem, s, a, t_first, n_tiles);
+}
+
+template <int U>
+void launch_sgd_u(const TileArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    switch (a.act) {
+        case 0: launch_sgd_ua<U, 0>(a, t_first, n_tiles, ctas, s); break;
+        case 1: launch_sgd_ua<U, 1>(a, t_first, n_tiles, ctas, s); break;
+        case 2: launch_sgd_ua<U, 2>(a, t_first, n_tiles, ctas, s); break;
+        default: launch_sgd_ua<U, 3>(a, t_first, n_tiles, ctas, s); break;
+    }
+}
+
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s) {
     if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
     const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
-    static const bool eval2 = [] {
-        const char* e = std::getenv("HCVA_EVAL_TMEM");
-        return !(e && e[0] == '0');
-    }();
-    if (a.mode != 0 && eval2 && u >= 16 && !tile_chunked(u, a.dp) && eval_tc_smem(u, a.dp) <= 113 * 1024) {
+    if (a.xf32 && a.mode == 0) {  // two CTAs per SM (tc_two_cta shapes)
+        const int ctas = static_cast<int>(std::min<long>(n_tiles, tc_eval_max_ctas(sm_count)));
+        if (u == 16) launch_sgd_u<16>(a, t_first, n_tiles, ctas, s);
+        else if (u == 32) launch_sgd_u<32>(a, t_first, n_tiles, ctas, s);
+        else launch_sgd_u<64>(a, t_first, n_tiles, ctas, s);
+        return ctas;
+    }
+    if (a.xf32) {
         const int ctas = static_cast<int>(std::min<long>(n_tiles, tc_eval_max_ctas(sm_count)));
         if (u == 16) launch_eval_u<16>(a, t_first, n_tiles, ctas, s);
         else if (u == 32) launch_eval_u<32>(a, t_first, n_tiles, ctas, s);

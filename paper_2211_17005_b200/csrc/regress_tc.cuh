@@ -27,6 +27,7 @@ struct TileArgs {
     float* H2;       // [R][U] layer-2 activations (mode bit 8)
     float *H1t, *G2t, *G1t;  // SGD: [U][ld_t] transposed, row index relative to b0
     long ld_t;
+    int xf32;                // feature tiles are one FP32 plane (tc_two_cta shapes), else hi | lo planes
 };
 
 struct WgradArgs {
@@ -41,12 +42,16 @@ struct WgradArgs {
 };
 
 bool tc_eligible(int d, int h, int u);
+// Shapes served by the two-CTA-per-SM kernels (k_sgd_tc / k_eval_tc): their
+// feature tiles are one FP32 plane, split into tensor memory in the kernel.
+bool tc_two_cta(int u, int dp);
 int tc_dp(int d);  // input dimension padded for the tensor-core tiles
 // Pack the FP32 parameters into the weight image.
 void launch_pack_w(int u, int d, int dp, int off0, int off1, int off2, int P, const float* params, uint8_t* wimg,
                    cudaStream_t s);
 // Pack X [R][d] into 128-row tiles and the transposed copy Xt [dp][ld_x] (pad rows zero).
-void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, cudaStream_t s);
+void launch_pack_x(const float* X, long R, int d, int dp, uint8_t* ximg, float* Xt, long ld_x, int xf32,
+                   cudaStream_t s);
 // Returns the number of per-CTA partials written (gpart / lpart / mpart rows).
 int launch_tile_tc(int u, const TileArgs& a, int sm_count, cudaStream_t s);
 int launch_wgrad_tc(int u, WgradArgs a, int sm_count, cudaStream_t s);
