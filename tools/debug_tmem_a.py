@@ -1,3 +1,5 @@
+"""Check the A-operand-in-tensor-memory tcgen05.mma (variant 8 of hcva_diag_tc_gemm,
+used by k_sgd_tc / k_eval_tc) against the shared-memory K-major form (variant 0)."""
 import ctypes as C, os, sys
 sys.path.insert(0, "/root/repo")
 import numpy as np
