@@ -206,3 +206,26 @@ def test_backward_learn_c5_shape(path, monkeypatch):
         bo, ro = R.train_base(x, y, start, t.hidden_layers, t.width, t.n_batches, t.epochs, t.learning_rate)
         assert rep["best_loss"] == pytest.approx(ro["best_loss"], rel=1e-3, abs=1e-12), i
 
+
+
+@pytest.mark.parametrize("n,k", [(32, 16), (64, 48), (64, 64), (128, 64)])
+def test_tcgen05_operand_forms(n, k):
+    """The two 3xTF32 tcgen05.mma forms the regression kernels use: A and B
+    K-major in shared memory (variant 0) and A in tensor memory (variant 8,
+    k_sgd_tc / k_eval_tc), M = 128, against an FP64 product (~1e-6 relative:
+    3xTF32 is FP32-accurate)."""
+    import ctypes as C
+
+    from paper_2211_17005_b200 import _lib
+
+    L = _lib.lib()
+    L.hcva_diag_tc_gemm.argtypes = [C.c_void_p] + [C.c_int] * 4 + [C.c_void_p] * 3
+    rng = np.random.default_rng(k)
+    A = rng.standard_normal((128, k)).astype(np.float32)
+    B = rng.standard_normal((n, k)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    for var in (0, 8):
+        D = np.zeros((128, n), dtype=np.float32)
+        assert L.hcva_diag_tc_gemm(hcva.context().handle, 128, n, k, var, A.ctypes.data, B.ctypes.data,
+                                   D.ctypes.data) == 0
+        assert np.max(np.abs(D - ref)) <= 2e-6 * np.max(np.abs(ref)), var
