@@ -1,29 +1,34 @@
 // regress_tc.cu -- K5 on the 5th-generation tensor cores: the SGD step and the
 // full-sample evaluation of the backward regression (regressor.cpp:97-158) as
 // tcgen05 kind::tf32 GEMMs (3xTF32, FP32 accumulation in TMEM) for the paper's
-// network shape: two hidden layers of width U in {16, 32, 64}, input d <= 64.
-// All operands are K-major (canonical no-swizzle core tiles, tc.cuh).
+// network shape: two hidden layers of width U in {16, 32, 64}, input d <= 255.
+// Shared-memory operands are K-major (canonical no-swizzle core tiles, tc.cuh).
 //
 // k_pack_w      parameters -> weight image (W0, W1, W1^T hi/lo planes + biases),
 //               one bulk copy per CTA.
-// k_pack_x      features X [R][d] -> 128-row operand tiles (hi/lo) + Xt [dp][R].
-// k_tile_tc<U, ACT>  persistent: one CTA per SM walks 128-row tiles (thread r
-//               = row r = TMEM lane r); thread 0 issues the MMAs, tcgen05.commit
-//               signals an mbarrier, epilogues read TMEM with tcgen05.ld; the
-//               next tile's features stream in by cp.async.bulk during the
-//               current tile's layer-1 and backward GEMMs.
+// k_pack_x      features X [R][d] -> 128-row operand tiles + Xt [dp][R]: one
+//               FP32 plane for the two-CTA kernels, hi/lo planes otherwise.
+// The per-tile GEMM chain (thread r = row r = TMEM lane r; one thread issues
+// the MMAs, tcgen05.commit signals an mbarrier, epilogues read TMEM):
 //     F0   D0  = X  W0^T   (M=128, N=U, K=dp)  -> H1 = act(D0 + b0); act'(H1) -> D0
 //     F1   D1  = H1 W1^T   (M=128, N=U, K=U)   -> H2, f, loss, G2
 //     B    Dbp = G2 W1     (M=128, N=U, K=U; B operand = W1^T tile)
 //                                              -> G1 = Dbp act'(H1)
-//   SGD mode also writes H1, G2, G1 transposed ([feature][row]) for the
-//   weight-gradient kernel; the bias / output-layer / mu gradients are column
-//   sums (butterfly reduce-scatter across the warp, accumulated per CTA).
-//   Eval mode produces the loss / min fit / predictions.
-// k_wgrad_tc<U>  split-K weight gradients over the batch rows: each CTA
-//                accumulates  gW1 = G2^T H1 (M=64, N=U)  and
-//                gW0 = G1^T X (M=64, N=dp) over its rows in TMEM, 64-row
-//                chunks with the next chunk's loads in flight, one partial.
+//   SGD also writes H1, G2, G1 transposed ([feature][row]) for the weight-
+//   gradient kernel; bias / output-layer / mu gradients are column sums
+//   (butterfly reduce-scatter across the warp, accumulated per CTA).
+// k_sgd_tc<U, ACT>   SGD, two CTAs per SM (tc_two_cta shapes): the A operands
+//               X, H1, G2 live in tensor memory (A-in-TMEM MMAs), shared memory
+//               holds W0, W1, W1^T and the FP32 feature tile.
+// k_eval_tc<U, ACT>  evaluation (loss / min fit / predictions / H2), two CTAs
+//               per SM, X and H1 in tensor memory.
+// k_tile_tc<U, ACT, CH>  the general one-CTA-per-SM kernel (both modes) with
+//               A operands in shared memory; CH streams layer 0's K dimension
+//               in 16-column chunks for wide inputs (C5).
+// k_wgrad_tc<U, XR>  split-K weight gradients over the batch rows: each CTA
+//               accumulates gW1 = G2^T H1 (M=64, N=U) and gW0 = G1^T X
+//               (M=64, N=dp) over its rows in TMEM, 32-row chunks with two
+//               chunks of loads in flight, one partial per CTA.
 // Reductions of the per-CTA partials are fixed-order FP64 (k_adam in regress.cu).
 #include <algorithm>
 #include <cmath>
