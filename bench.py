@@ -423,16 +423,16 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
     time is the max over ranks."""
     import torch
 
+    import copy
+    import json as _json
+
+    import cases
     from paper_2211_17005_b200 import dist
     from paper_2211_17005_b200 import regression as rg
 
     t = cfg.training
     steps = args.learning_steps or cfg.n_steps
     if steps != cfg.n_steps:
-        import json as _json
-
-        import cases
-
         j = cases.case(args.config)
         j["grid"]["pricing_steps"] = steps
         cfg = hcva.parse_config(_json.dumps(j))
@@ -457,6 +457,20 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
     try:
         if world > 1:
             comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
+            torch.distributed.barrier()
+        # untimed warm-up: the same trainer path over the last two pricing steps of a
+        # small set (module loading, memory-pool growth, host-side first calls)
+        wt = copy.copy(t)
+        wj = _json.loads(_json.dumps(cases.case(args.config)))
+        wj["grid"]["pricing_steps"] = 2
+        wcfg = hcva.parse_config(_json.dumps(wj))
+        wspec = dist.shard_spec(min(cfg.paths, 1024), wt.n_batches, world, rank)
+        wsim = hcva.simulate_set(wcfg, hcva.generate_book(wcfg), wspec["n_paths"], cfg.replicas, root,
+                                 path_offset=wspec["path_offset"], ctx=ctx, shard=wspec["shard"])
+        wsim.labels_all(cfg.label_kind, to_host=False)
+        rg.backward_learn(wsim, wt, cfg.label_kind, comm=comm)
+        del wsim
+        if world > 1:
             torch.distributed.barrier()
         ctx.synchronize()
         t0 = time.perf_counter()
