@@ -66,7 +66,6 @@ __device__ __forceinline__ float act_d(float v) {
     else return v > 0.0f ? 1.0f : 0.0f;
 }
 
-constexpr int kTcThreads = 128;
 
 __host__ __device__ constexpr uint32_t w_image_bytes(int U, int dp) {
     return 2u * U * dp * 4 + 4u * U * U * 4 + 1024;
@@ -331,7 +330,6 @@ __global__ void __launch_bounds__(TileShape<U>::threads, 1) k_tile_tc(TileArgs a
             tc::bulk_g2s(bufX, a.ximg + (tile + gridDim.x) * 2 * xb, 2 * xb, &bar[2]);
         }
         // H1 = act(D0 + b0) -> bufH (+ H1t); act'(H1) back into D0
-#pragma unroll
         {
             const int c0 = cb;
             float v[UH];
