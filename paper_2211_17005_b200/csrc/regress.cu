@@ -336,11 +336,14 @@ __host__ __device__ inline size_t split_index(const SplitPartials& sp, int i) {
                         : base + static_cast<size_t>(k - U * sp.d) * sp.dp + sp.d;
 }
 
+#ifndef HCVA_ADAM_G
+#define HCVA_ADAM_G 8  // partial groups per parameter (8 measured best of 8, 16, 32)
+#endif
 __global__ void k_adam(int P, const float* gpart, int nct, SplitPartials sp, const double* lpart, double nb,
                        double* p64, float* p32, double* m, double* v, double c1, double c2, double lr, int adam,
                        int* nonfinite,
                        ImgArgs im) {
-    constexpr int G = 16;
+    constexpr int G = HCVA_ADAM_G;
     __shared__ double part[G][33];
     const int x = threadIdx.x, grp = threadIdx.y;
     const int i = blockIdx.x * 32 + x;
@@ -858,7 +861,7 @@ struct Trainer {
             check_launch(ctx);
             return;
         }
-        k_adam<<<(n.P + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
+        k_adam<<<(n.P + 31) / 32, dim3(32, HCVA_ADAM_G), 0, ctx->stream>>>(n.P, gpart.as<float>(), tiles, sp, lpart.as<double>(),
                                                          static_cast<double>(b1 - b0), p64.as<double>(), p32.as<float>(),
                                                          m.as<double>(), v.as<double>(), c1, c2, lr, adam,
                                                          flag.as<int>(), img_args());
