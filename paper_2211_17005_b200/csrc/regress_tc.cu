@@ -44,10 +44,10 @@ namespace hcva {
 // absolute error ~1e-7 (FP32 rounding level of the O(1) activations that
 // feed the next layer), a third of tanhf's instruction count.
 __device__ __forceinline__ float tanh_fast(float z) {
-    float t;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(-2.8853900817779268f * fabsf(z)));
-    const float y = __fdividef(1.0f - t, 1.0f + t);
-    return copysignf(y, z);
+    float e, r;  // 1 - 2 / (e^{2z} + 1): saturates to +-1 through e^{2z} = inf / 0
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * z));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+    return fmaf(-2.0f, r, 1.0f);
 }
 
 // Activations (regressor.cpp:35-57), derivative from the activation value.
