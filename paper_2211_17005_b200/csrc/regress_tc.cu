@@ -809,8 +809,13 @@ __global__ void __launch_bounds__(SgdShape<U>::threads, 2) k_sgd_tc(TileArgs a, 
             float h[CP];
             tc::tmem_ld16(tm + lb + 64 + c0, h);
 #pragma unroll
-            for (int j = 0; j < CP; ++j) fp = fmaf(act_f<ACT>(h[j] + __ldg(vec + 64 + c0 + j)), __ldg(vec + 128 + c0 + j), fp);
+            for (int j = 0; j < CP; ++j) {
+                h[j] = act_f<ACT>(h[j] + __ldg(vec + 64 + c0 + j));
+                fp = fmaf(h[j], __ldg(vec + 128 + c0 + j), fp);
+            }
+            tc::tmem_st16(tm + lb + 64 + c0, h);  // H2 back into D1 for the gradient pass
         }
+        tc::tmem_wait_st();
         float f = b2 + fp;
         if (NS > 1) {
             if (hf == 1) fsh[r] = fp;
@@ -841,12 +846,9 @@ __global__ void __launch_bounds__(SgdShape<U>::threads, 2) k_sgd_tc(TileArgs a, 
         for (int p = 0; p < NP; ++p) {
             const int c0 = cb + p * CP;
             float h[CP], g[CP];
-            tc::tmem_ld16(tm + lb + 64 + c0, h);
+            tc::tmem_ld16(tm + lb + 64 + c0, h);  // H2
 #pragma unroll
-            for (int j = 0; j < CP; ++j) {
-                h[j] = act_f<ACT>(h[j] + __ldg(vec + 64 + c0 + j));
-                g[j] = dd * h[j];
-            }
+            for (int j = 0; j < CP; ++j) g[j] = dd * h[j];
             acc_w2[p] += bfly_sum<CP>(g, lane);
 #pragma unroll
             for (int j = 0; j < CP; ++j) g[j] = dd * __ldg(vec + 128 + c0 + j) * act_d<ACT>(h[j]);
