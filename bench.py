@@ -464,15 +464,15 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
         if world > 1:
             comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
             torch.distributed.barrier()
-        # untimed warm-up: the same trainer path over the last two pricing steps of a
-        # small set (module loading, memory-pool growth, host-side first calls)
+        # untimed warm-up: the same trainer path at full size over two pricing steps
+        # (module loading, host-side first calls, and the stream-ordered memory pool
+        # grown to the run's footprint, which it keeps for the timed run)
         wt = copy.copy(t)
         wj = _json.loads(_json.dumps(cases.case(args.config)))
         wj["grid"]["pricing_steps"] = 2
         wcfg = hcva.parse_config(_json.dumps(wj))
-        wspec = dist.shard_spec(min(cfg.paths, 1024), wt.n_batches, world, rank)
-        wsim = hcva.simulate_set(wcfg, hcva.generate_book(wcfg), wspec["n_paths"], cfg.replicas, root,
-                                 path_offset=wspec["path_offset"], ctx=ctx, shard=wspec["shard"])
+        wsim = hcva.simulate_set(wcfg, hcva.generate_book(wcfg), spec["n_paths"], cfg.replicas, root,
+                                 path_offset=spec["path_offset"], ctx=ctx, shard=spec["shard"])
         wsim.labels_all(cfg.label_kind, to_host=False)
         rg.backward_learn(wsim, wt, cfg.label_kind, comm=comm)
         del wsim
