@@ -223,13 +223,20 @@ hcva_status hcva_twin_labels(hcva_sim* sim, const hcva_swap* book, int n_swaps, 
                              double* twin1, double* twin2);
 /* twin_l2_error / twin_relative_rmse / twin_relative_rmse_std_error
  * (validation.cpp:41-117); block = paths_per_block of the clustered s.e.
- * twin_relative_rmse fails with HCVA_ERR_NUMERIC when E[xi1 xi2] <= 0. */
-hcva_status hcva_twin_l2_error(const double* pred, const double* twin1, const double* twin2, size_t n, int block,
-                               double* value, double* std_error);
-hcva_status hcva_twin_relative_rmse(const double* pred, const double* twin1, const double* twin2, size_t n,
-                                    double* out);
-hcva_status hcva_twin_relative_rmse_se(const double* pred, const double* twin1, const double* twin2, size_t n,
-                                       int block, double* out);
+ * Inputs are host or device arrays of n rows, reduced on the context's GPU in
+ * a fixed order (estimators.cu).  twin_relative_rmse fails with
+ * HCVA_ERR_NUMERIC when E[xi1 xi2] <= 0. */
+hcva_status hcva_twin_l2_error(hcva_ctx* ctx, const double* pred, const double* twin1, const double* twin2,
+                               size_t n, int block, double* value, double* std_error);
+hcva_status hcva_twin_relative_rmse(hcva_ctx* ctx, const double* pred, const double* twin1, const double* twin2,
+                                    size_t n, double* out);
+hcva_status hcva_twin_relative_rmse_se(hcva_ctx* ctx, const double* pred, const double* twin1,
+                                       const double* twin2, size_t n, int block, double* out);
+/* nested_relative_rmse (validation.cpp:181-210) over host or device arrays:
+ * out = value, std_error, excluded_zero, used.  HCVA_ERR_NUMERIC when every
+ * benchmark is zero. */
+hcva_status hcva_nested_relative_rmse(hcva_ctx* ctx, const double* pred, const double* nested, size_t n,
+                                      double* out /* [4] */);
 
 /* --- regression (regressor.hpp:33-139) ----------------------------------- */
 typedef struct {              /* TrainConfig, regressor.hpp:33-44 */
@@ -276,8 +283,9 @@ hcva_status hcva_backward_learn_qr(hcva_sim* sim, const hcva_train_cfg* cfg, int
  * NULL skips either. */
 hcva_status hcva_probe_block(hcva_sim* sim, uint64_t probe_key, int label_kind, uint16_t* steps_out,
                              double* labels_out);
-/* estimate_qr (planner.cpp:11-70): out = Q, R, total, n_pairs, Q s.e., R s.e. */
-hcva_status hcva_estimate_qr(const double* g1, const double* g2, size_t n, double* out /* [6] */);
+/* estimate_qr (planner.cpp:11-70) on host or device loss pairs:
+ * out = Q, R, total, n_pairs, Q s.e., R s.e. */
+hcva_status hcva_estimate_qr(hcva_ctx* ctx, const double* g1, const double* g2, size_t n, double* out /* [6] */);
 
 /* --- multi-GPU regression -------------------------------------
  * Y-paths shard by hcva_simulate_set_sharded (rank g owns slice g of every
@@ -307,6 +315,10 @@ hcva_status hcva_models_get(const hcva_models* m, int step, double* params, doub
                             double* epoch_losses, double* best_loss, int* best_epoch);
 /* TrainedModelSequence::predict (regressor.cpp:349-352) on sim's features at step. */
 hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* out /* [M*N] */);
+/* percentile_table (pipeline.cpp:138-156): per step i = 1..n of the models,
+ * the predictions on sim (the validation set) reduced on the device to
+ * out [n][6] = step, mean, p1, p2.5, p97.5, p99. */
+hcva_status hcva_percentile_table(const hcva_models* m, hcva_sim* sim, double* out);
 hcva_status hcva_models_destroy(hcva_models* m);
 /* TrainedModelSequence::save / load (regressor.cpp:397-481), the HCVAMDL1
  * format byte for byte (weights column-major as Eigen writes them).  Loaded

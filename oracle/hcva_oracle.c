@@ -981,7 +981,6 @@ int or_pipeline_bench(const or_model* m, const or_swap* book, int n_swaps, int M
                       uint64_t key_sim, int kind, double* seconds, double* checksum) {
     const int E = m->n_economies, Cn = m->n_clients + 1, n = m->n_steps, C = m->n_clients;
     const size_t rows = (size_t)M * (n + 1);
-    const int cols = (Cn - 1) + E + (E - 1) + (Cn - 1) + E;
     double* rates = malloc(sizeof(double) * rows * E);
     double* fx = malloc(sizeof(double) * rows * (E > 1 ? E - 1 : 1));
     double* intens = malloc(sizeof(double) * rows * Cn);
@@ -991,22 +990,74 @@ int or_pipeline_bench(const or_model* m, const or_swap* book, int n_swaps, int M
     double* cube = malloc(sizeof(double) * rows * C);
     uint16_t* steps = malloc(sizeof(uint16_t) * (size_t)M * N * Cn);
     double* lab = malloc(sizeof(double) * (size_t)M * N);
-    double* feat = malloc(sizeof(double) * (size_t)M * N * cols);
     const double t0 = now_s();
     int rc = or_simulate_market(m, M, or_split_key(key_sim, 0), rates, fx, intens, lagged, disc, hazard);
     if (!rc) rc = or_sample_defaults(M, n, Cn, hazard, N, or_split_key(key_sim, 1), steps);
     if (!rc) rc = or_build_cube(m, M, n, 0, rates, fx, lagged, book, n_swaps, cube);
     double sum = 0.0;
     for (int i = n; i >= 1 && !rc; --i) {
-        rc = or_features(i, M, n, E, Cn, N, rates, fx, intens, lagged, steps, feat);
-        if (!rc)
-            rc = (kind ? or_intensity_label : or_defaults_label)(i, M, n, E, Cn, N, m->dt, disc, intens,
+        rc = (kind ? or_intensity_label : or_defaults_label)(i, M, n, E, Cn, N, m->dt, disc, intens,
                                                                  steps, cube, lab);
         for (size_t r = 0; r < (size_t)M * N && !rc; ++r) sum += lab[r];
     }
     *seconds = now_s() - t0;
     *checksum = sum;
     free(rates), free(fx), free(intens), free(lagged), free(disc), free(hazard), free(cube);
-    free(steps), free(lab), free(feat);
+    free(steps), free(lab);
     return rc;
+}
+
+/* nested_relative_rmse (validation.cpp:181-210): squared relative errors over
+ * the nonzero benchmarks; out = value, std_error, excluded_zero, used. */
+int or_nested_relative_rmse(const double* pred, const double* nested, size_t n, double* out) {
+    if (n == 0) return fail(2, "nested_relative_rmse: size mismatch or empty input");
+    size_t used = 0;
+    double m = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+        if (nested[j] == 0.0) continue;
+        const double e = (pred[j] - nested[j]) / nested[j];
+        m += e * e;
+        ++used;
+    }
+    if (used == 0) return fail(3, "nested_relative_rmse: all benchmarks are zero");
+    m /= (double)used;
+    out[0] = sqrt(m);
+    out[1] = 0.0;
+    if (used > 1 && m > 0.0) {
+        double v = 0.0;
+        for (size_t j = 0; j < n; ++j) {
+            if (nested[j] == 0.0) continue;
+            const double e = (pred[j] - nested[j]) / nested[j];
+            v += (e * e - m) * (e * e - m);
+        }
+        v /= (double)(used - 1);
+        out[1] = sqrt(v / (double)used) / (2.0 * out[0]);
+    }
+    out[2] = (double)(n - used);
+    out[3] = (double)used;
+    return 0;
+}
+
+/* One row of percentile_table (pipeline.cpp:138-156) with percentile_sorted's
+ * linear interpolation (pipeline.cpp:41-47): v is sorted in place; out =
+ * mean (sequential sum of the sorted values), p1, p2.5, p97.5, p99. */
+static int cmp_double(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+
+int or_percentile_bands(double* v, size_t n, double* out) {
+    if (n == 0) return fail(2, "percentile_table: no predictions");
+    qsort(v, n, sizeof(double), cmp_double);
+    double s = 0.0;
+    for (size_t j = 0; j < n; ++j) s += v[j];
+    out[0] = s / (double)n;
+    const double q[4] = {0.01, 0.025, 0.975, 0.99};
+    for (int t = 0; t < 4; ++t) {
+        const double pos = q[t] * ((double)n - 1.0);
+        const size_t i = (size_t)pos;
+        const double f = pos - (double)i;
+        out[1 + t] = i + 1 < n ? v[i] * (1.0 - f) + v[i + 1] * f : v[i];
+    }
+    return 0;
 }

@@ -131,6 +131,14 @@ int or_save_book_csv(const char* path, const or_swap* book, int n_swaps);
 /* --- Q/R probe (planner.cpp:11-70): out = q, r, total, n_pairs, q_se, r_se --- */
 int or_estimate_qr(const double* g1, const double* g2, size_t n, double* out);
 
+/* --- nested_relative_rmse (validation.cpp:181-210): out = value, std_error,
+ * excluded_zero, used --- */
+int or_nested_relative_rmse(const double* pred, const double* nested, size_t n, double* out);
+/* --- percentile_table row (pipeline.cpp:41-47,138-156); restatement only
+ * (the reference's pipeline.cpp needs Eigen): v sorted in place, out = mean,
+ * p1, p2.5, p97.5, p99 --- */
+int or_percentile_bands(double* v, size_t n, double* out);
+
 /* --- regression (regressor.cpp, restated in regress_oracle.c) ---
  * activation: 0 tanh, 1 sigmoid, 2 softplus, 3 relu.  Flat parameters: for
  * l = 0..hidden, W_l [fan_out][fan_in] then b_l [fan_out]; then mu. */
@@ -154,9 +162,11 @@ int or_train_base(const or_net_shape* s, const double* x, const double* y, int r
 
 /* --- timed CPU baseline of the scenario pipeline ---
  * simulate_set (pipeline.cpp:63-70) with market = split(0), defaults =
- * split(1) of `key_sim`, then for every step i = n..1 the label source
- * (pipeline.cpp:83-90): features_at + defaults_label (kind 0) or
- * intensity_label (kind 1).  *seconds = wall time of exactly that work;
+ * split(1) of `key_sim`, then for every step i = n..1 the label of the
+ * label source (pipeline.cpp:83-90): defaults_label (kind 0) or
+ * intensity_label (kind 1).  features_at is not timed: the engine never
+ * materialises the feature matrix (it is built inside the regression), so
+ * both arms time the same work.  *seconds = wall time of exactly that work;
  * *checksum = sum of all labels (to keep the work observable). */
 int or_pipeline_bench(const or_model* m, const or_swap* book, int n_swaps, int n_paths,
                       int n_replicas, uint64_t key_sim, int kind, double* seconds,

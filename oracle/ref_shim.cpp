@@ -380,6 +380,17 @@ int or_twin_relative_rmse_se(const double* pred, const double* t1, const double*
     });
 }
 
+int or_nested_relative_rmse(const double* pred, const double* nested, std::size_t n, double* out) {
+    return guarded([&] {
+        NestedRmse r = nested_relative_rmse(std::vector<double>(pred, pred + n),
+                                            std::vector<double>(nested, nested + n));
+        out[0] = r.value;
+        out[1] = r.std_error;
+        out[2] = static_cast<double>(r.excluded_zero);
+        out[3] = static_cast<double>(r.used);
+    });
+}
+
 int or_save_book_csv(const char* path, const or_swap* book, int n_swaps) {
     return guarded([&] { save_book_csv(path, to_book(book, n_swaps)); });
 }
@@ -399,8 +410,9 @@ int or_estimate_qr(const double* g1, const double* g2, std::size_t n, double* ou
 }  // extern "C"
 
 // Timed CPU baseline through the reference's own functions, exactly the work
-// of simulate_set (pipeline.cpp:63-70) + the label source for i = n..1
-// (pipeline.cpp:83-90); parallel_for uses HIERCVA_THREADS workers.
+// of simulate_set (pipeline.cpp:63-70) + the labels of the label source for
+// i = n..1 (pipeline.cpp:83-90; features_at is not timed, as on the GPU arm);
+// parallel_for uses HIERCVA_THREADS workers.
 #include <chrono>
 extern "C" int or_pipeline_bench(const or_model* m, const or_swap* book, int n_swaps, int M, int N,
                                  std::uint64_t key_sim, int kind, double* seconds, double* checksum) {
@@ -415,10 +427,8 @@ extern "C" int or_pipeline_bench(const or_model* m, const or_swap* book, int n_s
         MtMCube cube = build_mtm_cube(market, bk, p);
         double sum = 0.0;
         for (int i = g.n_steps; i >= 1; --i) {
-            FeatureMatrix f = features_at(i, market, defaults);
             LabelSet l = kind ? intensity_label(i, market, defaults, cube) : defaults_label(i, market, defaults, cube);
             for (double v : l.values) sum += v;
-            if (f.values.empty()) sum += 1.0;
         }
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         *checksum = sum;

@@ -148,16 +148,18 @@ def lib():
         "hcva_twin_labels": [vp, C.POINTER(Swap), C.c_int, C.c_int, u64, dptr, dptr],
         "hcva_backward_learn_qr": [vp, C.POINTER(TrainCfg), C.c_int, u64, dptr, C.POINTER(vp)],
         "hcva_probe_block": [vp, u64, C.c_int, C.POINTER(C.c_uint16), dptr],
-        "hcva_estimate_qr": [dptr, dptr, C.c_size_t, dptr],
+        "hcva_estimate_qr": [vp, dptr, dptr, C.c_size_t, dptr],
+        "hcva_nested_relative_rmse": [vp, dptr, dptr, C.c_size_t, dptr],
+        "hcva_percentile_table": [vp, vp, dptr],
         "hcva_ard_sample_variances": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
                                       C.c_int, C.c_int, u64, dptr, dptr, dptr, C.POINTER(C.c_int)],
         "hcva_models_save": [vp, C.c_char_p, u64, C.c_char_p],
         "hcva_models_load": [vp, C.c_char_p, C.POINTER(u64), C.c_char_p, C.c_int, C.POINTER(vp)],
         "hcva_sim_save_market": [vp, C.c_char_p, u64],
         "hcva_market_load": [vp, C.POINTER(Model), C.POINTER(Grid), C.c_char_p, C.POINTER(u64), C.POINTER(vp)],
-        "hcva_twin_l2_error": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr, dptr],
-        "hcva_twin_relative_rmse": [dptr, dptr, dptr, C.c_size_t, dptr],
-        "hcva_twin_relative_rmse_se": [dptr, dptr, dptr, C.c_size_t, C.c_int, dptr],
+        "hcva_twin_l2_error": [vp, dptr, dptr, dptr, C.c_size_t, C.c_int, dptr, dptr],
+        "hcva_twin_relative_rmse": [vp, dptr, dptr, dptr, C.c_size_t, dptr],
+        "hcva_twin_relative_rmse_se": [vp, dptr, dptr, dptr, C.c_size_t, C.c_int, dptr],
         "hcva_comm_nccl_id": [C.c_char_p],
         "hcva_comm_create_nccl": [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)],
         "hcva_group_create": [C.c_int, C.POINTER(vp)],
@@ -200,5 +202,5 @@ EXPORTED = [
     "hcva_backward_learn_dist", "hcva_twin_labels", "hcva_twin_l2_error", "hcva_twin_relative_rmse",
     "hcva_twin_relative_rmse_se", "hcva_backward_learn_qr", "hcva_probe_block", "hcva_estimate_qr",
     "hcva_models_save", "hcva_models_load", "hcva_sim_save_market", "hcva_market_load",
-    "hcva_ard_sample_variances",
+    "hcva_ard_sample_variances", "hcva_nested_relative_rmse", "hcva_percentile_table",
 ]

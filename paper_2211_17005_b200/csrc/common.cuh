@@ -193,7 +193,8 @@ void stage(DeviceBuf& buf, const std::vector<T>& v) {
 void check_launch(hcva_ctx* ctx);
 void launch_labels_from(hcva_sim* sim, int kind, int i0, int i1, const uint16_t* steps, int N, double* dev_out);
 void probe_block(hcva_sim* sim, uint64_t key, int kind, DeviceBuf& steps, DeviceBuf& labels);
-void estimate_qr_host(const double* g1, const double* g2, size_t n, double* out);  // validation.cpp
+void estimate_qr_device(hcva_ctx* ctx, const double* g /* [n][2] */, size_t n, double* out);  // estimators.cu
+void percentile_bands(hcva_ctx* ctx, const double* dev_values, size_t n, double* out /* [5] */);
 hcva_sim* new_sim(hcva_ctx* ctx, const hcva_model* model, const hcva_grid* grid);
 hcva_sim* new_sim(hcva_ctx* ctx, const Model& model);
 void prepare_market(hcva_sim* sim, const std::vector<uint64_t>& group_keys, const std::vector<double>& init_state,

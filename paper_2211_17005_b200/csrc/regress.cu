@@ -685,6 +685,14 @@ __global__ void k_set_mu_from(const double* all, int G, double R_total, double* 
     p32[P - 1] = static_cast<float>(s / R_total);
 }
 
+__global__ void k_sq_err(const double* pred, const double* y, long n, double* out) {
+    const long j = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (j < n) {
+        const double e = pred[j] - y[j];
+        out[j] = e * e;
+    }
+}
+
 __global__ void k_local_sum(const double* y, long R, double* out) {
     __shared__ double red[32];
     double s = 0.0;
@@ -1325,9 +1333,9 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
         // head) predicts both, g_t = squared errors, estimate_qr on the host.
         const bool probe = qr_trace != nullptr;
         if (probe && comm) throw contract_error("Q/R probe: single-GPU runs only");
-        DeviceBuf p_steps, p_labels, p_img, p_X, p_pred;
+        DeviceBuf p_steps, p_labels, p_img, p_X, p_pred, p_g;
         const long R2 = 2L * sim->M;
-        std::vector<double> p_y(R2), p_p(R2), g1(sim->M), g2(sim->M);
+        const double* p_y = nullptr;  // this step's probe labels (device)
         size_t trace_row = 0;
         int cur_step = 0;
         if (probe) {
@@ -1335,18 +1343,16 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
             if (tr.use_tc) p_img.alloc(static_cast<size_t>((R2 + 127) / 128) * tc_x_tile_bytes(tr.dp));
             else p_X.alloc(sizeof(float) * R2 * d);
             p_pred.alloc(sizeof(double) * R2);
+            p_g.alloc(sizeof(double) * R2);
             tr.on_epoch = [&](int epoch) {
                 tr.ximg_over = tr.use_tc ? p_img.as<uint8_t>() : nullptr;
                 tr.eval(p_X.as<float>(), nullptr, R2, 4, p_pred.as<double>());
                 tr.ximg_over = nullptr;
-                copy_out(ctx, p_p.data(), p_pred.p, sizeof(double) * R2);
-                for (int k = 0; k < sim->M; ++k) {
-                    const double e1 = p_p[2 * k] - p_y[2 * k], e2 = p_p[2 * k + 1] - p_y[2 * k + 1];
-                    g1[k] = e1 * e1;
-                    g2[k] = e2 * e2;
-                }
+                // g[k] = (squared error of replica 0, of replica 1): already the pair layout
+                k_sq_err<<<grid1(R2, 256), 256, 0, ctx->stream>>>(p_pred.as<double>(), p_y, R2, p_g.as<double>());
+                ctx->launches++;
                 double qr[6];
-                estimate_qr_host(g1.data(), g2.data(), sim->M, qr);
+                estimate_qr_device(ctx, p_g.as<double>(), sim->M, qr);
                 double* row = qr_trace + 4 * trace_row++;
                 row[0] = cur_step;
                 row[1] = epoch;
@@ -1378,7 +1384,7 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
                 fp.N = 2;
                 fp.steps = p_steps.as<uint16_t>();
                 build_features(tr, fp, p_X, R2, &p_img);
-                copy_out(ctx, p_y.data(), p_labels.as<double>() + static_cast<size_t>(i) * R2, sizeof(double) * R2);
+                p_y = p_labels.as<double>() + static_cast<size_t>(i) * R2;
                 cur_step = i;
             }
             const double* y = sim->labels.as<double>() + static_cast<size_t>(i) * R;
@@ -1460,6 +1466,36 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         build_features(tr, fa, X, R);
         tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
         copy_out(ctx, out, pred.p, R * 8);
+    });
+}
+
+// percentile_table (pipeline.cpp:138-156): per step i = 1..n the out-of-sample
+// predictions on the validation set, sorted on the device; out [n][6] = step,
+// mean, p1, p2.5, p97.5, p99 (percentile_sorted's linear interpolation).
+hcva_status hcva_percentile_table(const hcva_models* m, hcva_sim* sim, double* out) {
+    return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (!sim->has_defaults) throw contract_error("predict: no default block");
+        const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
+        if (d != m->n.d) throw contract_error("forward: feature dimension mismatch");
+        const long R = static_cast<long>(sim->M) * sim->N;
+        Trainer tr(ctx, m->n, 1, R);
+        DeviceBuf X, pred;
+        if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
+        pred.alloc(sizeof(double) * R);
+        for (int i = 1; i <= m->n_steps; ++i) {
+            tr.set_params(m->params.as<double>() + static_cast<size_t>(i - 1) * m->n.P);
+            FeatArgs fa = feat_args(sim, i);
+            fa.mean = m->mean.as<double>() + static_cast<size_t>(i - 1) * d;
+            fa.scale = m->scale.as<double>() + static_cast<size_t>(i - 1) * d;
+            build_features(tr, fa, X, R);
+            tr.eval(X.as<float>(), nullptr, R, 4, pred.as<double>());
+            double* row = out + 6 * static_cast<size_t>(i - 1);
+            row[0] = i;
+            percentile_bands(ctx, pred.as<double>(), R, row + 1);
+        }
     });
 }
 

@@ -466,7 +466,7 @@ def twin_l2_error(predictions, twin1, twin2, paths_per_block: int = 1):
     """twin_l2_error (validation.cpp:41-56): (value, clustered std error)."""
     p, a, b = _triplet(predictions, twin1, twin2)
     v, se = C.c_double(), C.c_double()
-    _lib.check(_lib.lib().hcva_twin_l2_error(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+    _lib.check(_lib.lib().hcva_twin_l2_error(context().handle, p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
                                              b.ctypes.data_as(_lib.dptr), p.size, int(paths_per_block),
                                              C.byref(v), C.byref(se)))
     return v.value, se.value
@@ -476,7 +476,7 @@ def twin_relative_rmse(predictions, twin1, twin2) -> float:
     """twin_relative_rmse (validation.cpp:58-69); NumericError when E[xi1 xi2] <= 0."""
     p, a, b = _triplet(predictions, twin1, twin2)
     v = C.c_double()
-    _lib.check(_lib.lib().hcva_twin_relative_rmse(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+    _lib.check(_lib.lib().hcva_twin_relative_rmse(context().handle, p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
                                                   b.ctypes.data_as(_lib.dptr), p.size, C.byref(v)))
     return v.value
 
@@ -485,7 +485,7 @@ def twin_relative_rmse_std_error(predictions, twin1, twin2, paths_per_block: int
     """twin_relative_rmse_std_error (validation.cpp:71-117)."""
     p, a, b = _triplet(predictions, twin1, twin2)
     v = C.c_double()
-    _lib.check(_lib.lib().hcva_twin_relative_rmse_se(p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
+    _lib.check(_lib.lib().hcva_twin_relative_rmse_se(context().handle, p.ctypes.data_as(_lib.dptr), a.ctypes.data_as(_lib.dptr),
                                                      b.ctypes.data_as(_lib.dptr), p.size, int(paths_per_block),
                                                      C.byref(v)))
     return v.value
@@ -514,21 +514,17 @@ def ard_sample_variances(cfg: PipelineConfig, book: np.ndarray, n_dgp: int, path
 
 
 def nested_relative_rmse(predictions: np.ndarray, nested: np.ndarray):
-    """nested_relative_rmse (validation.cpp:181-210): (value, std_error, excluded_zero, used)."""
-    pred = np.asarray(predictions, dtype=np.float64)
-    nest = np.asarray(nested, dtype=np.float64)
+    """nested_relative_rmse (validation.cpp:181-210): (value, std_error, excluded_zero, used),
+    reduced on the GPU (estimators.cu)."""
+    pred = np.ascontiguousarray(np.ravel(predictions), dtype=np.float64)
+    nest = np.ascontiguousarray(np.ravel(nested), dtype=np.float64)
     if pred.shape != nest.shape or pred.size == 0:
         raise _lib.ContractError("nested_relative_rmse: size mismatch or empty input")
-    keep = nest != 0.0
-    if not keep.any():
-        raise _lib.NumericError("nested_relative_rmse: all benchmarks are zero")
-    sq = ((pred[keep] - nest[keep]) / nest[keep]) ** 2
-    m = float(np.mean(sq))
-    value = float(np.sqrt(m))
-    se = 0.0
-    if sq.size > 1 and m > 0.0:
-        se = float(np.sqrt(np.var(sq, ddof=1) / sq.size) / (2.0 * value))
-    return value, se, int((~keep).sum()), int(keep.sum())
+    out = np.zeros(4)
+    _lib.check(_lib.lib().hcva_nested_relative_rmse(context().handle, pred.ctypes.data_as(_lib.dptr),
+                                                    nest.ctypes.data_as(_lib.dptr), pred.size,
+                                                    out.ctypes.data_as(_lib.dptr)))
+    return float(out[0]), float(out[1]), int(out[2]), int(out[3])
 
 
 # ---- pybind-surface mirror (hiercva_module.cpp:99-139) ---------------------

@@ -165,22 +165,14 @@ def estimate_qr(g1, g2) -> Dict[str, float]:
     if a.size != b.size:
         raise _lib.ContractError("estimate_qr: pair length mismatch")
     out = np.zeros(6)
-    _lib.check(_lib.lib().hcva_estimate_qr(a.ctypes.data_as(_lib.dptr), b.ctypes.data_as(_lib.dptr), a.size,
+    _lib.check(_lib.lib().hcva_estimate_qr(context().handle, a.ctypes.data_as(_lib.dptr), b.ctypes.data_as(_lib.dptr), a.size,
                                            out.ctypes.data_as(_lib.dptr)))
     return dict(q=out[0], r=out[1], total=out[2], n_pairs=int(out[3]), q_std_error=out[4], r_std_error=out[5])
 
 
 def percentile_table(models: Models, validation: SimulationSet) -> Dict[int, Dict[str, float]]:
-    """percentile_table (pipeline.cpp:138-156): out-of-sample mean and percentile bands per step."""
-    rows = {}
-    for i in range(1, models.n_steps + 1):
-        v = np.sort(models.predict(i, validation))
-
-        def pct(q):
-            pos = q * (v.size - 1)
-            idx = int(pos)
-            frac = pos - idx
-            return v[idx] * (1 - frac) + v[idx + 1] * frac if idx + 1 < v.size else v[idx]
-
-        rows[i] = dict(mean=float(np.sum(v) / v.size), p1=pct(0.01), p2_5=pct(0.025), p97_5=pct(0.975), p99=pct(0.99))
-    return rows
+    """percentile_table (pipeline.cpp:138-156): out-of-sample mean and percentile bands per step,
+    predicted, sorted and reduced on the GPU."""
+    out = np.zeros((models.n_steps, 6))
+    _lib.check(_lib.lib().hcva_percentile_table(models.handle, validation.handle, out.ctypes.data_as(_lib.dptr)))
+    return {int(r[0]): dict(mean=r[1], p1=r[2], p2_5=r[3], p97_5=r[4], p99=r[5]) for r in out}

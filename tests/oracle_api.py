@@ -317,6 +317,21 @@ class Oracle:
         self._check(self.lib.or_estimate_qr(_ptr(a), _ptr(b), C.c_size_t(a.size), _ptr(out)))
         return dict(q=out[0], r=out[1], total=out[2], n_pairs=int(out[3]), q_std_error=out[4], r_std_error=out[5])
 
+    def nested_relative_rmse(self, pred, nested):
+        """validation.cpp:181-210 -> (value, std_error, excluded_zero, used)."""
+        p = np.ascontiguousarray(np.ravel(pred), dtype=np.float64)
+        v = np.ascontiguousarray(np.ravel(nested), dtype=np.float64)
+        out = np.zeros(4)
+        self._check(self.lib.or_nested_relative_rmse(_ptr(p), _ptr(v), C.c_size_t(p.size), _ptr(out)))
+        return float(out[0]), float(out[1]), int(out[2]), int(out[3])
+
+    def percentile_bands(self, values):
+        """One percentile_table row (pipeline.cpp:41-47,138-156): mean, p1, p2.5, p97.5, p99."""
+        v = np.array(np.ravel(values), dtype=np.float64)
+        out = np.zeros(5)
+        self._check(self.lib.or_percentile_bands(_ptr(v), C.c_size_t(v.size), _ptr(out)))
+        return out
+
     # -- regression (regressor.cpp restated) -------------------------------
     def _shape(self, d, hidden, width, activation=0):
         class S(C.Structure):

@@ -1,7 +1,6 @@
-"""Twin-MC validator: the host estimators of
-validation.cpp:41-117 against the compiled reference's values (golden
-fixtures, bit-exact) and the restatement; twin_labels on the GPU against the
-golden labels and, at larger sizes, the restatement."""
+"""Twin-MC validator: twin_labels on the GPU against the
+golden labels and, at larger sizes, the restatement.  The estimators of
+validation.cpp:41-117 are tested in test_estimators.py."""
 import numpy as np
 import pytest
 
@@ -14,50 +13,6 @@ GOLDEN = ["minimal", "c1", "desk_corr", "c2", "c5"]
 
 def golden(name):
     return np.load(f"{oracle_api.ROOT}/tests/golden/{name}.npz")
-
-
-def estimators(t1, t2, N):
-    pred = cases.twin_prediction(t1, t2)
-    out = []
-    for block in (1, N):
-        out += list(hcva.twin_l2_error(pred, t1, t2, block))
-    try:
-        out.append(hcva.twin_relative_rmse(pred, t1, t2))
-    except hcva.NumericError:
-        out.append(float("nan"))
-    out += [hcva.twin_relative_rmse_std_error(pred, t1, t2, b) for b in (1, N)]
-    return np.array(out)
-
-
-@pytest.mark.parametrize("name", GOLDEN)
-def test_twin_estimators_bit_exact(name):
-    z = golden(name)
-    got = estimators(z["twin1"], z["twin2"], int(z["N"]))
-    assert np.array_equal(got, z["twin_stats"], equal_nan=True)
-
-
-def test_twin_estimators_random_vs_restatement():
-    R = oracle_api.restatement()
-    rng = np.random.default_rng(4)
-    for n, block in ((1000, 8), (97, 1), (64, 64), (2, 1)):
-        t1 = rng.exponential(size=n) * (rng.random(n) < 0.6)
-        t2 = rng.exponential(size=n) * (rng.random(n) < 0.6)
-        pred = rng.random(n)
-        assert hcva.twin_l2_error(pred, t1, t2, block) == R.twin_l2_error(pred, t1, t2, block)
-        if np.mean(t1 * t2) > 0:
-            assert hcva.twin_relative_rmse(pred, t1, t2) == R.twin_relative_rmse(pred, t1, t2)
-        else:
-            with pytest.raises(hcva.NumericError):
-                hcva.twin_relative_rmse(pred, t1, t2)
-        assert hcva.twin_relative_rmse_std_error(pred, t1, t2, block) == \
-            R.twin_relative_rmse_std_error(pred, t1, t2, block)
-
-
-def test_twin_estimator_errors():
-    with pytest.raises(hcva.ContractError):
-        hcva.twin_l2_error(np.zeros(3), np.zeros(3), np.zeros(2))
-    with pytest.raises(hcva.NumericError):
-        hcva.twin_relative_rmse(np.ones(4), np.zeros(4), np.ones(4))
 
 
 def gpu_twin(name, M, N, step):
