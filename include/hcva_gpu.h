@@ -261,6 +261,15 @@ hcva_status hcva_init_network(const hcva_train_cfg* cfg, int input_dim, uint64_t
  * grads may be NULL. */
 hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
                                 int head, const double* x, const double* y, int rows, double* loss, double* grads);
+/* forward (regressor.cpp:97-113) with the positive head on (as
+ * TrainedModelSequence::predict, regressor.cpp:349-352) on standardised host
+ * rows x [rows][input_dim]: out [rows]. */
+hcva_status hcva_forward(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                         const double* x, int rows, double* out);
+/* refit_output_layer (regressor.cpp:191-213): params' output layer replaced by
+ * the ridge (cfg->ridge) least-squares fit of y - mu on [z_h, 1]. */
+hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, double* params,
+                                    const double* x, const double* y, int rows);
 /* train_base (regressor.cpp:265-347) on host rows, contiguous batches. */
 hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
                             const double* y, int rows, const double* init, double* best, double* epoch_losses,

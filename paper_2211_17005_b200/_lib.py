@@ -141,6 +141,8 @@ def lib():
         "hcva_net_size": [C.POINTER(TrainCfg), C.c_int, C.POINTER(C.c_int)],
         "hcva_init_network": [C.POINTER(TrainCfg), C.c_int, u64, dptr],
         "hcva_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, dptr, dptr],
+        "hcva_forward": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr],
+        "hcva_refit_output_layer": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, dptr, C.c_int],
         "hcva_train_base": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr, dptr, dptr, dptr,
                             C.POINTER(C.c_int)],
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
@@ -203,4 +205,5 @@ EXPORTED = [
     "hcva_twin_relative_rmse_se", "hcva_backward_learn_qr", "hcva_probe_block", "hcva_estimate_qr",
     "hcva_models_save", "hcva_models_load", "hcva_sim_save_market", "hcva_market_load",
     "hcva_ard_sample_variances", "hcva_nested_relative_rmse", "hcva_percentile_table",
+    "hcva_forward", "hcva_refit_output_layer",
 ]

@@ -1249,6 +1249,47 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
     });
 }
 
+// forward (regressor.cpp:97-113) with the positive head on, as
+// TrainedModelSequence::predict applies it (regressor.cpp:349-352), on host
+// rows that are already standardised.
+hcva_status hcva_forward(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                         const double* x, int rows, double* out) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (rows < 1) throw contract_error("forward: no rows");
+        const NetDims n = dims_from(cfg, input_dim);
+        Trainer tr(ctx, n, 1, rows);
+        DeviceBuf dX, pred;
+        stage_features(tr, x, rows, input_dim, dX);
+        pred.alloc(static_cast<size_t>(rows) * 8);
+        tr.set_params(params);
+        tr.eval(dX.as<float>(), nullptr, rows, 4, pred.as<double>());
+        copy_out(ctx, out, pred.p, static_cast<size_t>(rows) * 8);
+    });
+}
+
+// refit_output_layer (regressor.cpp:191-213): the output layer of `params`
+// (positive head off) replaced by the ridge least-squares fit on [z_h, 1]
+// against y - mu: Gram on the device in FP64 from the FP32 activations, LDL^T
+// solve in FP64.
+hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, double* params,
+                                    const double* x, const double* y, int rows) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (rows < 1) throw contract_error("refit_output_layer: no rows");
+        const NetDims n = dims_from(cfg, input_dim);
+        Trainer tr(ctx, n, 1, rows);
+        DeviceBuf dX, dy;
+        stage_features(tr, x, rows, input_dim, dX);
+        stage(dy, std::vector<double>(y, y + rows));
+        tr.set_params(params);
+        tr.refit(dX.as<float>(), dy.as<double>(), rows, cfg->ridge);
+        copy_out(ctx, params, tr.p64.p, static_cast<size_t>(n.P) * 8);
+    });
+}
+
 hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
                             const double* y, int rows, const double* init, double* best, double* epoch_losses,
                             double* best_loss, int* best_epoch) {

@@ -56,6 +56,28 @@ def quadratic_loss(t: TrainConfig, params: np.ndarray, x: np.ndarray, y: np.ndar
     return loss.value, g
 
 
+def forward(t: TrainConfig, params: np.ndarray, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
+    """forward (regressor.cpp:97-113) with the positive head on, on standardised rows: predictions."""
+    ctx = ctx or context()
+    x, params = _f64(x), _f64(params)
+    out = np.zeros(x.shape[0])
+    _lib.check(_lib.lib().hcva_forward(ctx.handle, C.byref(train_cfg(t)), x.shape[1], params.ctypes.data_as(_lib.dptr),
+                                       x.ctypes.data_as(_lib.dptr), x.shape[0], out.ctypes.data_as(_lib.dptr)))
+    return out
+
+
+def refit_output_layer(t: TrainConfig, params: np.ndarray, x: np.ndarray, y: np.ndarray,
+                       ctx: Optional[Context] = None) -> np.ndarray:
+    """refit_output_layer (regressor.cpp:191-213): a copy of params with the output layer refit."""
+    ctx = ctx or context()
+    x, y = _f64(x), _f64(y)
+    p = np.array(params, dtype=np.float64)
+    _lib.check(_lib.lib().hcva_refit_output_layer(ctx.handle, C.byref(train_cfg(t)), x.shape[1],
+                                                  p.ctypes.data_as(_lib.dptr), x.ctypes.data_as(_lib.dptr),
+                                                  y.ctypes.data_as(_lib.dptr), x.shape[0]))
+    return p
+
+
 def train_base(t: TrainConfig, x: np.ndarray, y: np.ndarray, init: np.ndarray, ctx: Optional[Context] = None):
     """train_base (regressor.cpp:265-347) with contiguous batches: (best params, report)."""
     ctx = ctx or context()

@@ -10,6 +10,8 @@ default indicators; the FP64 engine is held far tighter):
     per-client book sum); labels 1e-9 relative + 1e-12 of scale; features as
     market (indicator columns exact).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -271,3 +273,44 @@ def test_cva_profile_fused_equals_label_mean(name, M, N):
     sim = hcva.simulate_set(cfg, book, M, N, root)
     sim.labels_all("defaults", to_host=False)
     np.testing.assert_allclose(sim.cva_profile("defaults"), want, rtol=1e-12, atol=1e-14 * np.abs(want).max())
+
+
+@pytest.mark.slow
+def test_c2_full_default_indicators_vs_reference():
+    """The headline configuration pinned against the compiled reference
+    (defaults.cpp:20-45 on market.cpp:161-234's market, run on this host's
+    cores): every one of the 2^14 x 2^7 x 9 default steps equal, every market
+    factor of every path at the market tolerance; cube and labels on the first
+    2048 paths.  The counts are printed (pytest -s) together with the engine's
+    threshold-tie counters."""
+    F = oracle_api.reference()
+    if F is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    os.environ["HIERCVA_THREADS"] = str(len(os.sched_getaffinity(0)))
+    M, N = 16384, 128
+    cfg, book, sim = gpu_case("c2", M, N)
+    assert (cfg.n_steps, cfg.substeps, cfg.n_clients, cfg.n_economies) == (100, 25, 8, 10)
+    m = cases.oracle_model(cfg)
+    sk = F.split(F.key(cfg.seed), 1)
+    mk = F.simulate_market(m, M, F.split(sk, 0))
+    st = F.sample_defaults(mk["hazard"], N, F.split(sk, 1))
+    got = sim.default_steps()
+    assert got.shape == st.shape == (M, N, cfg.n_clients + 1)
+    mism = int((got != st).sum())
+    ties = sim.tie_counts()
+    print(f"\nC2 default steps: {got.size} compared, {mism} mismatches, ties within 1 ulp {ties[0]}, "
+          f"within 1e-12 {ties[1]}, defaulted {(st != 0xFFFF).sum()}")
+    assert mism == 0, f"{mism} default-step mismatches (ties within 1 ulp: {ties[0]})"
+    g = sim.market_arrays()
+    for key in ("rates", "fx", "intens", "lagged", "disc", "hazard"):
+        # short rates cross zero on a few of the 16.5M entries: a 1e-12-of-scale floor
+        close(g[key], mk[key], MARKET_RTOL, 1e-12, key)
+    del g
+    P = 2048
+    sub = {k: np.ascontiguousarray(v[:P]) for k, v in mk.items()}
+    cube = F.build_cube(m, sub, book)
+    gc = sim.cube_values()[:P]
+    close(gc, cube, 1e-10, 1e-10, "cube")
+    for i in (0, 1, 37, 99):
+        want = F.defaults_label(i, sub, st[:P], cube, cfg.dt)
+        close(sim.labels(i, "defaults")[:P], want, 1e-9, 1e-12, f"label {i}")
