@@ -13,7 +13,8 @@ needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Multi-GPU (torchrun): weak scaling -- rank r simulates its own 2^14 paths
+--gpus N > 1 without torchrun starts N ranks itself (torch.distributed.run on
+127.0.0.1, one process per GPU, device = local rank).  Multi-GPU: weak scaling -- rank r simulates its own 2^14 paths
 (global path offset r * 2^14); no collective on the data path.  Device time
 is the max over ranks.
 """
@@ -55,6 +56,7 @@ def parse_args():
     ap.add_argument("--nested-step", type=int, default=5)
     ap.add_argument("--nested-inner", type=int, default=128)
     ap.add_argument("--nested-states", type=int, default=0, help="outer states (default: all validation paths)")
+    ap.add_argument("--launch-probe", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--learning-timeout", type=float, default=240.0,
                     help="N > 1: if the sharded learning leg (~3 s at C2) exceeds this many seconds, print the "
                          "metric line with the leg marked as timed out and exit")
@@ -79,6 +81,16 @@ def workload(args):
         j["simulation"]["replicas"] = args.replicas
     cfg = hcva.parse_config(json.dumps(j))
     return cfg, j
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
 
 
 def cpu_threads() -> int:
@@ -141,7 +153,8 @@ def reference_arm(args):
             vals.append(v)
     value = float(np.mean(vals))
     sample = (f"{info['paths']} of {cfg.paths} Y-paths x {cfg.replicas} X-replicas x {cfg.n_steps} steps "
-              f"per step ({info['seconds']:.1f} s; simulate_set + features_at/defaults_label for i=n..1)")
+              f"per step ({info['seconds']:.1f} s; simulate_set + defaults_label for i=n..1; features_at is not "
+              f"timed on either arm) on {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * info["seconds"],
@@ -161,7 +174,16 @@ def config_obj(cfg, args, world):
             "paths_per_gpu": cfg.paths, "replicas": cfg.replicas, "pricing_steps": cfg.n_steps,
             "substeps": cfg.substeps, "dt_years": cfg.dt, "n_factors": cfg.n_factors,
             "global_paths": cfg.paths * world, "parallelism": f"y-path shards x{world}",
-            "l2": "per-step working set ~2.5 GB/GPU >> 126 MB L2 (no flush needed)"}
+            "l2": "per-step working set ~2.5 GB/GPU >> 126 MB L2 (no flush needed)",
+            "step_work": "Y diffusion + MtM cube + X default steps + defaults labels of all n steps (features "
+                         "are not materialised on either arm: the regression builds them per batch)",
+            "deviations": {
+                "mtm_not_fused_with_diffusion": "K1 and K2 are both FP64-issue bound; fusing saves only the "
+                                                "0.6 GB market re-read, and labels/features/nested/twin re-read "
+                                                "the 106 MB cube (DESIGN.md section 3)",
+                "default_steps_not_bitmasks": "X indicators stored as one uint16 default step per (replica, "
+                                              "name), which encodes 1{s <= i} for every step i (DESIGN.md "
+                                              "section 3)"}}
 
 
 # ----------------------------------------------------------------- clocks
@@ -244,6 +266,8 @@ def ours_arm(args):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2211_17005_b200 as hcva
 
@@ -277,6 +301,7 @@ def ours_arm(args):
         torch.cuda.synchronize()
     launches = ctx.launch_count() - launches0
     ms = e0.elapsed_time(e1)
+    ties = sim.tie_counts()
     phases = np.array([sim.phase_times(s) for s in range(args.steps)])  # ms [K, 4]
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -315,7 +340,10 @@ def ours_arm(args):
                      "algorithmic_flop_per_launch": k1_flop, "traffic": k1_traffic(),
                      "k1_share_of_step": k1_ms / ms_step},
         "clocks": clocks.summary(),
+        "threshold_ties_last_step": {"within_1ulp": int(ties[0]), "within_1e-12": int(ties[1]),
+                                     "comparisons": int(M * N * (cfg.n_clients + 1))},
         "cpu_baseline": None,
+        "parity": None,
         "cva_learning": None,
         "nested_mc": None,
     }
@@ -333,8 +361,9 @@ def ours_arm(args):
         v, info = run_reference_sample(cfg, args.cpu_baseline_seconds)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                                 "sample": f"{info['paths']} of {M} Y-paths x {N} replicas x {n} steps, "
-                                          f"{info['seconds']:.1f} s (simulate_set + features_at/defaults_label "
-                                          f"for i=n..1)"}
+                                          f"{info['seconds']:.1f} s (simulate_set + defaults_label for i=n..1; "
+                                          f"features_at is not timed on either arm) on {cpu_model()}"}
+        line["parity"] = _secondary("parity", lambda: parity_leg(hcva, cfg, book, ctx))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -355,6 +384,89 @@ def _secondary(key, fn):
             _PARTIAL["line"][key] = {"error": repr(exc)}
             return None
         return {"error": repr(exc)}
+
+
+def parity_leg(hcva, cfg, book, ctx):
+    """Untimed checker, run with the CPU baseline (rank 0, N=1): the reference's
+    own simulate_market + sample_default_block (oracle/_ref, compiled from
+    /root/reference's sources, HIERCVA_THREADS = host cores) on the FULL
+    workload against the engine's default block for the same stream keys --
+    every one of M x N x Cn default steps must be equal (defaults.cpp:20-45);
+    threshold ties within 1 ulp / 1e-12 are the engine's counters."""
+    import cases
+    import oracle_api
+
+    ref = oracle_api.reference()
+    kind = "reference"
+    if ref is None:
+        ref, kind = oracle_api.restatement(), "port"
+    os.environ["HIERCVA_THREADS"] = str(cpu_threads())
+    M, N = cfg.paths, cfg.replicas
+    root = hcva.RandomStream(cfg.seed).split(hcva.K_TRAIN_SIM)
+    sim = hcva.simulate_set(cfg, book, M, N, root, ctx=ctx)
+    got = sim.default_steps()
+    ties = sim.tie_counts()
+    gmk = sim.market_arrays()
+    del sim
+    m = cases.oracle_model(cfg)
+    sk = ref.split(ref.key(cfg.seed), 1)
+    c0 = time.perf_counter()
+    mk = ref.simulate_market(m, M, ref.split(sk, 0))
+    want = ref.sample_defaults(mk["hazard"], N, ref.split(sk, 1))
+    sec = time.perf_counter() - c0
+    rel = 0.0
+    for k in ("rates", "intens", "hazard", "disc"):
+        a, b = gmk[k], mk[k]
+        rel = max(rel, float(np.max(np.abs(a - b) / (np.abs(b) + 1e-12 * np.max(np.abs(b))))))
+    return {"default_mismatches": int((got != want).sum()), "default_steps_compared": int(got.size),
+            "ties_1ulp": int(ties[0]), "ties_1e-12": int(ties[1]),
+            "defaulted": int((want != 0xFFFF).sum()), "market_max_rel_err": rel,
+            "against": f"{kind}: simulate_market + sample_default_block on all {M} x {N} x {cfg.n_clients + 1} "
+                       f"(path, replica, name) of the bench workload, same stream keys ({sec:.1f} s on "
+                       f"{cpu_threads()} host threads)"}
+
+
+def sgd_roofline(hcva, cfg, ctx):
+    """Roofline of the regression's dominant kernel chain, the SGD step
+    (k_sgd_tc + k_wgrad_tc + optimizer) at the bench network and batch: CUDA
+    events on the engine's stream (hcva_diag_sgd_timing) around steps on one
+    synthetic batch of the workload's shape; algorithmic tensor flop per row =
+    forward 2dU + 2U^2, backward G1 = G2 W1 2U^2, weight gradients 2U^2 + 2dU
+    (d = 2Cc + 3E - 1 features, U hidden units) -- the 3xTF32 products issue
+    three MMAs per algorithmic one, so TF32/3 is the attainable ceiling."""
+    import ctypes as C
+
+    from paper_2211_17005_b200 import _lib
+    from paper_2211_17005_b200 import regression as rg
+
+    t = cfg.training
+    d = 2 * cfg.n_clients + 3 * cfg.n_economies - 1
+    U = t.width
+    rows = cfg.paths * cfg.replicas // t.n_batches
+    rng = np.random.default_rng(0)
+    x = np.hstack([(rng.random((rows, cfg.n_clients)) < 0.3).astype(np.float64),
+                   rng.standard_normal((rows, d - cfg.n_clients))])
+    y = np.abs(rng.standard_normal(rows)) * 10.0
+    p = rg.init_network(t, d, 12345)
+    p[-1] = float(np.mean(y))
+    out = np.zeros(3)
+    L = _lib.lib()
+    _lib.check(L.hcva_diag_sgd_timing(ctx.handle, C.byref(rg.train_cfg(t)), d, p.ctypes.data_as(_lib.dptr),
+                                      x.ctypes.data_as(_lib.dptr), y.ctypes.data_as(_lib.dptr), rows, 50,
+                                      out.ctypes.data_as(_lib.dptr)))
+    peak = C.c_double()
+    _lib.check(L.hcva_diag_tc_rate(ctx.handle, 128, 256, 4096, C.byref(peak)))
+    flop_row = 4 * d * U + 6 * U * U
+    flop = flop_row * rows
+    achieved = flop / (out[0] * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "SGD step (k_sgd_tc + k_wgrad_tc + k_adam)", "unit": "TFLOP/s",
+            "achieved": achieved, "peak": peak.value, "frac": achieved / peak.value,
+            "frac_of_tf32_div3": achieved / (peak.value / 3.0),
+            "peak_source": "measured kind::tf32 tcgen05.mma rate, M=128 N=256 chains on every SM "
+                           "(hcva_diag_tc_rate)",
+            "algorithmic_flop_per_step": flop, "flop_per_row": flop_row, "rows_per_step": rows,
+            "d": d, "width": U, "step_ms": out[0], "gradient_kernels_ms": out[1], "optimizer_ms": out[2],
+            "traffic": None}
 
 
 def k1_traffic():
@@ -526,6 +638,8 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
             "scaling": "strong (global C2 problem sharded by Y-path)" if world > 1 else None,
             "net": f"{t.hidden_layers}x{t.width} {t.activation}", "best_loss_step1": rep["best_loss"],
             "path": "hcva_simulate_set + hcva_labels_all + hcva_backward_learn (K1-K5, device resident)"}
+    if rank == 0:
+        out["roofline"] = _secondary("sgd_roofline", lambda: sgd_roofline(hcva, cfg, ctx))
     return out, (models if steps == cfg.n_steps and world == 1 else None)
 
 
@@ -613,8 +727,37 @@ def nested_reference_sample(cfg, book, st, surv, step, inner, gpu_sec, states, s
             "ratio_vs_gpu": full / gpu_sec}
 
 
+def self_launch(args):
+    """`--gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 with this same command line, and return
+    their exit status; None when already a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator creation shows nranks
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.launch_probe:  # launcher test hook: which rank am I
+        rank, world, local = dist_env()
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "pid": os.getpid()}), flush=True)
+        return
+    rank, world, _ = dist_env()
+    if world != args.gpus and rank == 0:
+        sys.stderr.write(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} rank(s)\n")
     if args.impl == "reference":
         reference_arm(args)
     else:

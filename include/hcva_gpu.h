@@ -88,6 +88,14 @@ hcva_status hcva_diag_fp64_peak(hcva_ctx* ctx, double* tflops);
 /* Diagnostic: the device special functions of the normal transform on host
  * arguments (fn 0 erfc, 1 exp(z<=0), 2 uniform->normal, 3 exp(-y^2)). */
 hcva_status hcva_diag_special(hcva_ctx* ctx, int fn, const double* x, size_t n, double* out);
+/* Diagnostic: one 3xTF32 tcgen05 GEMM D[M][N] = A[M][K] B[N][K]^T in the
+ * regression kernels' operand forms (variant 0: A, B in shared memory; 8: A in
+ * tensor memory). */
+hcva_status hcva_diag_tc_gemm(hcva_ctx* ctx, int M, int N, int K, int variant, const float* A, const float* B,
+                              float* D);
+/* Diagnostic: measured kind::tf32 tcgen05.mma throughput (TFLOP/s) of an
+ * M x N x 8 MMA chain on every SM (the regression's tensor roofline). */
+hcva_status hcva_diag_tc_rate(hcva_ctx* ctx, int M, int N, int iters, double* tflops);
 
 /* --- RNG (rng.hpp:16-52, rng.cpp:44-130) --------------------------------- */
 uint64_t hcva_rng_root_key(uint64_t seed);               /* RandomStream(seed) */
@@ -270,6 +278,11 @@ hcva_status hcva_forward(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim
  * the ridge (cfg->ridge) least-squares fit of y - mu on [z_h, 1]. */
 hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, double* params,
                                     const double* x, const double* y, int rows);
+/* Profiling probe (bench.py roofline): `steps` SGD steps on one batch of host
+ * rows, CUDA events on the context's stream; out = mean ms of [step,
+ * gradient kernels, optimizer]. */
+hcva_status hcva_diag_sgd_timing(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                                 const double* x, const double* y, int rows, int steps, double* out /* [3] */);
 /* train_base (regressor.cpp:265-347) on host rows, contiguous batches. */
 hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
                             const double* y, int rows, const double* init, double* best, double* epoch_losses,

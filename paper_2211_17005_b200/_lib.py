@@ -134,6 +134,8 @@ def lib():
         "hcva_cva_profile": [vp, C.c_int, vp],
         "hcva_diag_fp64_peak": [vp, dptr],
         "hcva_diag_special": [vp, C.c_int, vp, C.c_size_t, vp],
+        "hcva_diag_tc_gemm": [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp],
+        "hcva_diag_tc_rate": [vp, C.c_int, C.c_int, C.c_int, dptr],
         "hcva_nested_cva_batch": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
                                   C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, u64, dptr, dptr],
         "hcva_nested_cva_range": [vp, C.POINTER(Model), C.POINTER(Grid), C.POINTER(Swap), C.c_int, dptr,
@@ -143,6 +145,7 @@ def lib():
         "hcva_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, dptr, dptr],
         "hcva_forward": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr],
         "hcva_refit_output_layer": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, dptr, C.c_int],
+        "hcva_diag_sgd_timing": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, dptr, C.c_int, C.c_int, dptr],
         "hcva_train_base": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr, dptr, dptr, dptr,
                             C.POINTER(C.c_int)],
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
@@ -197,7 +200,7 @@ EXPORTED = [
     "hcva_sim_destroy", "hcva_sim_dims", "hcva_sim_tie_counts", "hcva_sim_export_market",
     "hcva_sim_export_defaults", "hcva_sim_export_cube", "hcva_labels", "hcva_labels_all",
     "hcva_features", "hcva_sim_rerun", "hcva_sim_phase_times", "hcva_cva_profile",
-    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_nested_cva_batch", "hcva_nested_cva_range", "hcva_net_size",
+    "hcva_diag_fp64_peak", "hcva_diag_special", "hcva_diag_tc_gemm", "hcva_diag_tc_rate", "hcva_nested_cva_batch", "hcva_nested_cva_range", "hcva_net_size",
     "hcva_init_network", "hcva_quadratic_loss", "hcva_train_base", "hcva_backward_learn", "hcva_models_info",
     "hcva_models_get", "hcva_predict", "hcva_models_destroy", "hcva_comm_nccl_id", "hcva_comm_create_nccl",
     "hcva_group_create", "hcva_group_destroy", "hcva_comm_create_local", "hcva_comm_info", "hcva_comm_destroy",
@@ -205,5 +208,5 @@ EXPORTED = [
     "hcva_twin_relative_rmse_se", "hcva_backward_learn_qr", "hcva_probe_block", "hcva_estimate_qr",
     "hcva_models_save", "hcva_models_load", "hcva_sim_save_market", "hcva_market_load",
     "hcva_ard_sample_variances", "hcva_nested_relative_rmse", "hcva_percentile_table",
-    "hcva_forward", "hcva_refit_output_layer",
+    "hcva_forward", "hcva_refit_output_layer", "hcva_diag_sgd_timing",
 ]

@@ -851,10 +851,13 @@ struct Trainer {
         return tiles;
     }
 
+    cudaEvent_t* phase_ev = nullptr;  // profiling: events after the gradient kernels and after the update
+
     void sgd_step(const float* X, const double* y, long b0, long b1, int head, long t, double lr, int adam) {
         SplitPartials sp;
         const double nb = static_cast<double>(b1 - b0) * world;  // the global batch
         const int tiles = grad_tiles(X, y, b0, b1, head, nb, &sp);
+        if (phase_ev) HCVA_CUDA(cudaEventRecord(phase_ev[0], ctx->stream));
         // Adam bias corrections 1 - beta^t on the host with the host libm, as
         // the reference's adam_update (regressor.cpp:236-252).
         const double c1 = 1.0 - std::pow(0.9, static_cast<double>(t)), c2 = 1.0 - std::pow(0.999, static_cast<double>(t));
@@ -874,6 +877,7 @@ struct Trainer {
                                                          m.as<double>(), v.as<double>(), c1, c2, lr, adam,
                                                          flag.as<int>(), img_args());
         check_launch(ctx);
+        if (phase_ev) HCVA_CUDA(cudaEventRecord(phase_ev[1], ctx->stream));
     }
 
     ImgArgs img_args() {
@@ -1287,6 +1291,46 @@ hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, in
         tr.set_params(params);
         tr.refit(dX.as<float>(), dy.as<double>(), rows, cfg->ridge);
         copy_out(ctx, params, tr.p64.p, static_cast<size_t>(n.P) * 8);
+    });
+}
+
+// Roofline probe of the SGD step (bench.py): `steps` SGD steps of train_base's
+// inner loop on one batch of `rows` host rows, CUDA events on the engine's
+// stream around every step and after its gradient kernels.  out = mean ms of
+// [whole step, gradient kernels (tile + weight gradient), optimizer].
+hcva_status hcva_diag_sgd_timing(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
+                                 const double* x, const double* y, int rows, int steps, double* out) {
+    return guarded([&] {
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (rows < 1 || steps < 1) throw contract_error("sgd timing: no rows or steps");
+        const NetDims n = dims_from(cfg, input_dim);
+        Trainer tr(ctx, n, rows, rows);
+        DeviceBuf dX, dy;
+        stage_features(tr, x, rows, input_dim, dX);
+        stage(dy, std::vector<double>(y, y + rows));
+        tr.set_params(params);
+        HCVA_CUDA(cudaMemsetAsync(tr.m.p, 0, n.P * 8, ctx->stream));
+        HCVA_CUDA(cudaMemsetAsync(tr.v.p, 0, n.P * 8, ctx->stream));
+        for (int w = 0; w < 3; ++w) tr.sgd_step(dX.as<float>(), dy.as<double>(), 0, rows, 0, w + 1, cfg->learning_rate, cfg->adam);
+        std::vector<cudaEvent_t> ev(3 * steps);
+        for (auto& e : ev) HCVA_CUDA(cudaEventCreate(&e));
+        for (int s = 0; s < steps; ++s) {
+            HCVA_CUDA(cudaEventRecord(ev[3 * s], ctx->stream));
+            tr.phase_ev = &ev[3 * s + 1];
+            tr.sgd_step(dX.as<float>(), dy.as<double>(), 0, rows, 0, s + 4, cfg->learning_rate, cfg->adam);
+        }
+        tr.phase_ev = nullptr;
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        double tot = 0.0, grad = 0.0, opt = 0.0;
+        for (int s = 0; s < steps; ++s) {
+            float a = 0.f, b = 0.f;
+            HCVA_CUDA(cudaEventElapsedTime(&a, ev[3 * s], ev[3 * s + 1]));
+            HCVA_CUDA(cudaEventElapsedTime(&b, ev[3 * s + 1], ev[3 * s + 2]));
+            grad += a, opt += b, tot += a + b;
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        out[0] = tot / steps, out[1] = grad / steps, out[2] = opt / steps;
     });
 }
 

@@ -132,3 +132,26 @@ def test_rank_ordered_allgather_training_gloo():
     ref = _sgd_epochs(R, x, y, p0.copy(), 4, 3)
     assert np.allclose(ps[0], ref, rtol=1e-10, atol=1e-13)
     assert not np.array_equal(ref, p0)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_self_launch_starts_n_ranks(n):
+    """`python bench.py --gpus N` without torchrun starts N rank processes
+    (torch.distributed.run on 127.0.0.1) with distinct RANK / LOCAL_RANK and
+    WORLD_SIZE = N (the launcher only: --launch-probe prints each rank's
+    environment and exits before any device work)."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(oracle_api.ROOT, "bench.py"), "--gpus", str(n),
+                          "--launch-probe"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import re
+
+    ranks = [json.loads(m) for m in re.findall(r'\{"rank"[^{}]*\}', out.stdout)]
+    assert sorted(r["rank"] for r in ranks) == list(range(n))
+    assert sorted(r["local_rank"] for r in ranks) == list(range(n))
+    assert {r["world"] for r in ranks} == {n}
+    assert len({r["pid"] for r in ranks}) == n
