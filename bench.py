@@ -426,14 +426,15 @@ def parity_leg(hcva, cfg, book, ctx):
                        f"{cpu_threads()} host threads)"}
 
 
-def sgd_roofline(hcva, cfg, ctx):
+def sgd_roofline(hcva, cfg, sim):
     """Roofline of the regression's dominant kernel chain, the SGD step
-    (k_sgd_tc + k_wgrad_tc + optimizer) at the bench network and batch: CUDA
-    events on the engine's stream (hcva_diag_sgd_timing) around steps on one
-    synthetic batch of the workload's shape; algorithmic tensor flop per row =
-    forward 2dU + 2U^2, backward G1 = G2 W1 2U^2, weight gradients 2U^2 + 2dU
-    (d = 2Cc + 3E - 1 features, U hidden units) -- the 3xTF32 products issue
-    three MMAs per algorithmic one, so TF32/3 is the attainable ceiling."""
+    (gradient kernel(s) + optimizer) at the bench network and batch: CUDA
+    events on the engine's stream (hcva_diag_sgd_timing) around SGD steps of
+    train_base at pricing step n of the learning set; algorithmic tensor flop
+    per row = forward 2dU + 2U^2, backward G1 = G2 W1 2U^2, weight gradients
+    2U^2 + 2dU (d = 2Cc + 3E - 1 features, U hidden units) -- the 3xTF32
+    products issue three MMAs per algorithmic one, so TF32/3 is the attainable
+    ceiling."""
     import ctypes as C
 
     from paper_2211_17005_b200 import _lib
@@ -443,30 +444,22 @@ def sgd_roofline(hcva, cfg, ctx):
     d = 2 * cfg.n_clients + 3 * cfg.n_economies - 1
     U = t.width
     rows = cfg.paths * cfg.replicas // t.n_batches
-    rng = np.random.default_rng(0)
-    x = np.hstack([(rng.random((rows, cfg.n_clients)) < 0.3).astype(np.float64),
-                   rng.standard_normal((rows, d - cfg.n_clients))])
-    y = np.abs(rng.standard_normal(rows)) * 10.0
-    p = rg.init_network(t, d, 12345)
-    p[-1] = float(np.mean(y))
-    out = np.zeros(3)
-    L = _lib.lib()
-    _lib.check(L.hcva_diag_sgd_timing(ctx.handle, C.byref(rg.train_cfg(t)), d, p.ctypes.data_as(_lib.dptr),
-                                      x.ctypes.data_as(_lib.dptr), y.ctypes.data_as(_lib.dptr), rows, 50,
-                                      out.ctypes.data_as(_lib.dptr)))
+    tm = rg.sgd_timing(sim, t, cfg.n_steps, steps=50, label_kind=cfg.label_kind)
     peak = C.c_double()
-    _lib.check(L.hcva_diag_tc_rate(ctx.handle, 128, 256, 4096, C.byref(peak)))
+    _lib.check(_lib.lib().hcva_diag_tc_rate(sim.ctx.handle, 128, 256, 4096, C.byref(peak)))
     flop_row = 4 * d * U + 6 * U * U
     flop = flop_row * rows
-    achieved = flop / (out[0] * 1e-3) / 1e12
-    return {"bound": "tensor", "kernel": "SGD step (k_sgd_tc + k_wgrad_tc + k_adam)", "unit": "TFLOP/s",
+    achieved = flop / (tm["step_ms"] * 1e-3) / 1e12
+    kern = "k_sgd_split (fused gradient, layer-0 split) + k_adam" if tm["split"] else \
+        "k_sgd_tc + k_wgrad_tc + k_adam"
+    return {"bound": "tensor", "kernel": f"SGD step ({kern})", "unit": "TFLOP/s",
             "achieved": achieved, "peak": peak.value, "frac": achieved / peak.value,
             "frac_of_tf32_div3": achieved / (peak.value / 3.0),
             "peak_source": "measured kind::tf32 tcgen05.mma rate, M=128 N=256 chains on every SM "
                            "(hcva_diag_tc_rate)",
             "algorithmic_flop_per_step": flop, "flop_per_row": flop_row, "rows_per_step": rows,
-            "d": d, "width": U, "step_ms": out[0], "gradient_kernels_ms": out[1], "optimizer_ms": out[2],
-            "traffic": None}
+            "d": d, "width": U, "step_ms": tm["step_ms"], "gradient_kernels_ms": tm["gradient_ms"],
+            "optimizer_ms": tm["optimizer_ms"], "traffic": None}
 
 
 def k1_traffic():
@@ -639,7 +632,7 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
             "net": f"{t.hidden_layers}x{t.width} {t.activation}", "best_loss_step1": rep["best_loss"],
             "path": "hcva_simulate_set + hcva_labels_all + hcva_backward_learn (K1-K5, device resident)"}
     if rank == 0:
-        out["roofline"] = _secondary("sgd_roofline", lambda: sgd_roofline(hcva, cfg, ctx))
+        out["roofline"] = _secondary("sgd_roofline", lambda: sgd_roofline(hcva, cfg, sim))
     return out, (models if steps == cfg.n_steps and world == 1 else None)
 
 

@@ -278,11 +278,19 @@ hcva_status hcva_forward(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim
  * the ridge (cfg->ridge) least-squares fit of y - mu on [z_h, 1]. */
 hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, double* params,
                                     const double* x, const double* y, int rows);
-/* Profiling probe (bench.py roofline): `steps` SGD steps on one batch of host
- * rows, CUDA events on the context's stream; out = mean ms of [step,
- * gradient kernels, optimizer]. */
-hcva_status hcva_diag_sgd_timing(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
-                                 const double* x, const double* y, int rows, int steps, double* out /* [3] */);
+/* Profiling probe (bench.py roofline): train_base's SGD steps at pricing step
+ * `step` of a simulated set (scaler, features, init as backward_learn), CUDA
+ * events on the context's stream; out = mean ms of [step, gradient kernels,
+ * optimizer], 1 if the layer-0 split kernels ran. */
+hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int step, int label_kind, int steps,
+                                 double* out /* [4] */);
+/* quadratic_loss (regressor.cpp:115-158) on rows [b0, b1) of the label
+ * source at pricing step `step` (pipeline.cpp:72-111): the set's features
+ * standardised with mean / scale [input_dim], its labels of label_kind,
+ * through the kernels backward_learn runs on this set. */
+hcva_status hcva_sim_quadratic_loss(hcva_sim* sim, const hcva_train_cfg* cfg, int step, int label_kind,
+                                    const double* params, const double* mean, const double* scale, int head,
+                                    long b0, long b1, double* loss, double* grads);
 /* train_base (regressor.cpp:265-347) on host rows, contiguous batches. */
 hcva_status hcva_train_base(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* x,
                             const double* y, int rows, const double* init, double* best, double* epoch_losses,

@@ -145,7 +145,9 @@ def lib():
         "hcva_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, dptr, C.c_int, dptr, dptr, C.c_int, dptr, dptr],
         "hcva_forward": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr],
         "hcva_refit_output_layer": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, dptr, C.c_int],
-        "hcva_diag_sgd_timing": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, dptr, C.c_int, C.c_int, dptr],
+        "hcva_diag_sgd_timing": [vp, C.POINTER(TrainCfg), C.c_int, C.c_int, C.c_int, dptr],
+        "hcva_sim_quadratic_loss": [vp, C.POINTER(TrainCfg), C.c_int, C.c_int, dptr, dptr, dptr, C.c_int, C.c_long,
+                                    C.c_long, dptr, dptr],
         "hcva_train_base": [vp, C.POINTER(TrainCfg), C.c_int, dptr, dptr, C.c_int, dptr, dptr, dptr, dptr,
                             C.POINTER(C.c_int)],
         "hcva_backward_learn": [vp, C.POINTER(TrainCfg), C.c_int, C.POINTER(vp)],
@@ -208,5 +210,5 @@ EXPORTED = [
     "hcva_twin_relative_rmse_se", "hcva_backward_learn_qr", "hcva_probe_block", "hcva_estimate_qr",
     "hcva_models_save", "hcva_models_load", "hcva_sim_save_market", "hcva_market_load",
     "hcva_ard_sample_variances", "hcva_nested_relative_rmse", "hcva_percentile_table",
-    "hcva_forward", "hcva_refit_output_layer", "hcva_diag_sgd_timing",
+    "hcva_forward", "hcva_refit_output_layer", "hcva_diag_sgd_timing", "hcva_sim_quadratic_loss",
 ]

@@ -24,6 +24,7 @@
 // Reductions are over fixed CTA partitions in fixed order: results are
 // deterministic and independent of scheduling.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -719,6 +720,12 @@ struct Trainer {
     hcva_comm* comm = nullptr;  // multi-GPU: rank-ordered allgather of the FP64 partials
     int world = 1;
     DeviceBuf red, gath;
+    // Layer-0 split (regress_split.cu): per-path columns yhat [M][qp] of the
+    // current step + the default steps instead of a feature matrix.
+    bool split = false;
+    SplitArgs sa{};
+    DeviceBuf yhat;
+    const SplitArgs* sa_over = nullptr;  // evaluation on other rows of the same paths (Q/R probe)
 
     void set_comm(hcva_comm* c, size_t max_len) {
         comm = c;  // an explicit comm always takes the gather path (world 1 included)
@@ -733,8 +740,10 @@ struct Trainer {
         return gath.as<double>();
     }
 
-    Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0) : ctx(c), n(dims) {
+    Trainer(hcva_ctx* c, const NetDims& dims, long max_batch, long max_rows = 0, bool split_mode = false)
+        : ctx(c), n(dims) {
         use_tc = tc_eligible(n.d, n.h, n.u);
+        split = split_mode && use_tc;
         while (TR > 32 && tile_smem(n, TR) > 200 * 1024) TR /= 2;
         if (tile_smem(n, TR) > 227 * 1024) throw config_error("training: network too wide for the tile kernel");
         const size_t smem = tile_smem(n, TR);
@@ -747,7 +756,11 @@ struct Trainer {
         max_tiles = static_cast<int>((max_batch + TR - 1) / TR);
         const size_t P = n.P;
         long parts = std::max<long>(max_tiles, eval_ctas);
-        if (use_tc) {
+        if (use_tc && split) {
+            dp = tc_dp(n.d);
+            parts = std::max<long>(parts, std::max(ctx->sm_count, split_max_ctas(ctx->sm_count)));
+            wimg.alloc(tc_weight_image_bytes(n.u, dp));
+        } else if (use_tc) {
             dp = tc_dp(n.d);
             xf32 = tc_two_cta(n.u, dp);
             parts = std::max<long>(parts, std::max(ctx->sm_count, tc_eval_max_ctas(ctx->sm_count)));
@@ -789,6 +802,39 @@ struct Trainer {
         wimg_valid = false;
     }
 
+    // The split source of a simulated set (paths M, replicas N): the per-path
+    // columns are rebuilt for every step by build_yhat.
+    void split_source(const hcva_sim* sim) {
+        const int Cc = sim->model.Cc, q = n.d - Cc;
+        sa = SplitArgs{};
+        sa.d = n.d; sa.Cc = Cc; sa.q = q; sa.qp = ((q + 3) / 4) * 4; sa.N = sim->N;
+        sa.P = n.P; sa.off0 = n.off[0]; sa.off1 = n.off[1]; sa.off2 = n.off[2]; sa.act = n.act;
+        sa.M = sim->M; sa.R = static_cast<long>(sim->M) * sim->N;
+        sa.steps = sim->steps.as<uint16_t>();
+        yhat.alloc(static_cast<size_t>(sim->M) * sa.qp * 4);
+        sa.yhat = yhat.as<float>();
+    }
+
+    SplitArgs split_args(const SplitArgs& base, const double* y, long b0, long b1, int head, int mode, double nb,
+                         double* pred) {
+        if (!wimg_valid) {
+            launch_pack_w(n.u, n.d, dp, n.off[0], n.off[1], n.off[2], n.P, p32.as<float>(), wimg.as<uint8_t>(),
+                          ctx->stream);
+            check_launch(ctx);
+            wimg_valid = true;
+        }
+        SplitArgs a = base;
+        const size_t w0b = static_cast<size_t>(n.u) * dp * 4, w1b = static_cast<size_t>(n.u) * n.u * 4;
+        a.w1img = wimg.as<uint8_t>() + 2 * w0b;
+        a.vec = reinterpret_cast<const float*>(wimg.as<uint8_t>() + 2 * w0b + 4 * w1b);
+        a.p32 = p32.as<float>();
+        a.mu64 = p64.as<double>() + n.P - 1;
+        a.y = y; a.b0 = b0; a.b1 = b1; a.head = head; a.mode = mode; a.nb = nb;
+        a.gpart = gpart.as<float>(); a.lpart = lpart.as<double>(); a.mpart = mpart.as<double>(); a.pred = pred;
+        a.H2 = h2.as<float>();
+        return a;
+    }
+
     // Features of the sample (X [R][d], device) -> the tensor-core operand images.
     void prepare_x(const float* X, long R) {
         if (!use_tc) return;
@@ -824,6 +870,13 @@ struct Trainer {
     // Gradient partials of rows [b0, b1): per-tile partials (+ weight-gradient
     // partials on the tensor-core path, described by sp); returns the tile count.
     int grad_tiles(const float* X, const double* y, long b0, long b1, int head, double nb, SplitPartials* sp) {
+        if (split) {
+            const int ctas = launch_sgd_split(split_args(sa, y, b0, b1, head, 0, nb, nullptr), ctx->sm_count,
+                                              ctx->stream);
+            check_launch(ctx);
+            if (sp) *sp = SplitPartials{};
+            return ctas;
+        }
         if (use_tc) {
             const int ctas = tile_launch(y, b0, b1, head, 0, nb, nullptr);
             WgradArgs wa{};
@@ -888,6 +941,12 @@ struct Trainer {
 
     // Full-sample forward; sets last_parts = number of loss / min partials written.
     void eval(const float* X, const double* y, long R, int mode, double* pred) {
+        if (split) {
+            const SplitArgs& base = sa_over ? *sa_over : sa;
+            last_parts = launch_eval_split(split_args(base, y, 0, R, 1, mode, 1.0, pred), ctx->sm_count, ctx->stream);
+            check_launch(ctx);
+            return;
+        }
         if (use_tc) {
             last_parts = tile_launch(y, 0, R, 1, mode, 1.0, pred);
             return;
@@ -903,7 +962,12 @@ struct Trainer {
         if (use_tc) {
             const size_t hbytes = static_cast<size_t>(R) * n.u * 4;
             if (h2.bytes < hbytes) h2.alloc(hbytes);  // layer-2 activations, first refit only
-            tile_launch(y, 0, R, 1, 8, 1.0, nullptr);
+            if (split) {
+                launch_eval_split(split_args(sa, y, 0, R, 1, 8, 1.0, nullptr), ctx->sm_count, ctx->stream);
+                check_launch(ctx);
+            } else {
+                tile_launch(y, 0, R, 1, 8, 1.0, nullptr);
+            }
             nct = launch_gram_h2(n.u, h2.as<float>(), y, R, p32.as<float>(), n.P, gram.as<double>(), gram_parts,
                                  ctx->sm_count, ctx->stream);
         } else {
@@ -1054,6 +1118,17 @@ __global__ void k_build_x(FeatArgs a) {
         o[Cc + j] = static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]);
 }
 
+// Layer-0 split: the standardised per-path columns of step i, yhat [M][qp]
+// (FP32 of the FP64 standardisation, the values k_build_x writes; zero pad).
+__global__ void k_build_yhat(FeatArgs a, float* yhat, int q, int qp) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<size_t>(a.M) * qp) return;
+    const int k = static_cast<int>(i % a.M), j = static_cast<int>(i / a.M);
+    const int Cc = a.Cn - 1;
+    yhat[static_cast<size_t>(k) * qp + j] =
+        j < q ? static_cast<float>((state_col(a, k, j) - a.mean[Cc + j]) / a.scale[Cc + j]) : 0.0f;
+}
+
 // Scaler (regressor.cpp:84-95) over the rows: the state columns repeat per path,
 // so mean / population variance over rows equal those over paths.  One CTA per
 // column, fixed-order FP64 reduction; indicator columns pass through.
@@ -1181,12 +1256,55 @@ void stage_features(Trainer& tr, const double* x, int rows, int d, DeviceBuf& dX
     tr.prepare_x(dX.as<float>(), rows);
 }
 
+// Whether a trainer on this simulated set takes the layer-0 split path (the
+// SGD kernel needs N >= 16 replicas per path, the evaluation any N).
+bool use_split(const NetDims& n, const hcva_sim* sim, bool sgd = true) {
+    const int Cc = sim->model.Cc;
+    return tc_eligible(n.d, n.h, n.u) && n.d == 2 * Cc + 3 * sim->model.E - 1 && (!sgd || sim->N >= 16) &&
+           split_eligible(n.u, n.h, sim->N, Cc, n.d - Cc);
+}
+
+// Loss and gradient of the mean loss from a launch's partials, summed on the
+// host in fixed order (FP64).
+void reduce_partials(Trainer& tr, int tiles, const SplitPartials& sp, long rows, double* loss, double* grads) {
+    hcva_ctx* ctx = tr.ctx;
+    const NetDims& n = tr.n;
+    std::vector<float> gp(static_cast<size_t>(tiles) * n.P), gb(static_cast<size_t>(sp.nB) * sp.stride);
+    std::vector<double> lp(tiles);
+    copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);
+    if (sp.nB) copy_out(ctx, gb.data(), sp.gpartB, gb.size() * 4);
+    copy_out(ctx, lp.data(), tr.lpart.p, lp.size() * 8);
+    double l = 0.0;
+    for (double v : lp) l += v;
+    *loss = l / rows;
+    if (grads)
+        for (int i = 0; i < n.P; ++i) {
+            const bool split = (i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1);
+            const bool fromB = split && sp.nB;
+            const float* src = fromB ? gb.data() + split_index(sp, i) : gp.data() + i;
+            const size_t stride = fromB ? sp.stride : n.P;
+            const int cnt = fromB ? sp.nB : tiles;
+            double g = 0.0;
+            for (int c = 0; c < cnt; ++c) g += src[static_cast<size_t>(c) * stride];
+            grads[i] = g;
+        }
+}
+
 // Standardised features of one step (fa with mean / scale set): straight into
 // the tensor-core operand images, or into X [R][d] for the SIMT path.
 // With `img` (tensor-core path) the features go to that operand image only
 // (evaluation rows, e.g. the Q/R probe), not to the trainer's own.
 void build_features(Trainer& tr, FeatArgs fa, DeviceBuf& X, long R, DeviceBuf* img = nullptr) {
     hcva_ctx* ctx = tr.ctx;
+    if (tr.split) {  // no feature matrix: the per-path columns of this step (shared by other rows of the paths)
+        if (!img) {
+            k_build_yhat<<<grid1(static_cast<size_t>(fa.M) * tr.sa.qp, 256), 256, 0, ctx->stream>>>(
+                fa, tr.yhat.as<float>(), tr.sa.q, tr.sa.qp);
+            tr.sa.step = fa.step;
+            check_launch(ctx);
+        }
+        return;
+    }
     if (tr.use_tc) {
         if (!img && R > tr.x_rows) throw contract_error("training: feature rows exceed the trainer's capacity");
         fa.ximg = img ? img->as<uint8_t>() : tr.ximg.as<uint8_t>();
@@ -1231,25 +1349,44 @@ hcva_status hcva_quadratic_loss(hcva_ctx* ctx, const hcva_train_cfg* cfg, int in
         SplitPartials sp;
         const int tiles =
             tr.grad_tiles(dX.as<float>(), dy.as<double>(), 0, rows, head, static_cast<double>(rows), &sp);
-        std::vector<float> gp(static_cast<size_t>(tiles) * n.P), gb(static_cast<size_t>(sp.nB) * sp.stride);
-        std::vector<double> lp(tiles);
-        copy_out(ctx, gp.data(), tr.gpart.p, gp.size() * 4);
-        if (sp.nB) copy_out(ctx, gb.data(), sp.gpartB, gb.size() * 4);
-        copy_out(ctx, lp.data(), tr.lpart.p, lp.size() * 8);
-        double l = 0.0;
-        for (double v : lp) l += v;
-        *loss = l / rows;
-        if (grads)
-            for (int i = 0; i < n.P; ++i) {
-                const bool split = (i >= sp.lo0 && i < sp.hi0) || (i >= sp.lo1 && i < sp.hi1);
-                const bool fromB = split && sp.nB;
-                const float* src = fromB ? gb.data() + split_index(sp, i) : gp.data() + i;
-                const size_t stride = fromB ? sp.stride : n.P;
-                const int cnt = fromB ? sp.nB : tiles;
-                double g = 0.0;
-                for (int c = 0; c < cnt; ++c) g += src[static_cast<size_t>(c) * stride];
-                grads[i] = g;
-            }
+        reduce_partials(tr, tiles, sp, rows, loss, grads);
+    });
+}
+
+// quadratic_loss (regressor.cpp:115-158) on rows [b0, b1) of the label
+// source's data at step i (make_label_source, pipeline.cpp:72-111): features
+// of the simulated set standardised with host mean / scale [d], labels of
+// label_kind -- through the kernels backward_learn runs on this set (the
+// layer-0 split kernel where eligible).
+hcva_status hcva_sim_quadratic_loss(hcva_sim* sim, const hcva_train_cfg* cfg, int step, int label_kind,
+                                    const double* params, const double* mean, const double* scale, int head,
+                                    long b0, long b1, double* loss, double* grads) {
+    return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
+        StreamScope sc__(ctx->stream);
+        HCVA_CUDA(cudaSetDevice(ctx->device));
+        if (!sim->has_defaults || !sim->has_cube) throw contract_error("quadratic_loss: set has no defaults / cube");
+        if (step < 1 || step > sim->n) throw contract_error("label step out of range");
+        const long R = static_cast<long>(sim->M) * sim->N;
+        if (b0 < 0 || b1 > R || b1 <= b0) throw contract_error("quadratic_loss: bad row range");
+        const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
+        const NetDims n = dims_from(cfg, d);
+        if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
+        Trainer tr(ctx, n, b1 - b0, R, use_split(n, sim));
+        if (tr.split) tr.split_source(sim);
+        DeviceBuf dmean, dscale, X;
+        stage(dmean, std::vector<double>(mean, mean + d));
+        stage(dscale, std::vector<double>(scale, scale + d));
+        FeatArgs fa = feat_args(sim, step);
+        fa.mean = dmean.as<double>();
+        fa.scale = dscale.as<double>();
+        if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
+        build_features(tr, fa, X, R);
+        tr.set_params(params);
+        SplitPartials sp;
+        const double* y = sim->labels.as<double>() + static_cast<size_t>(step) * R;
+        const int tiles = tr.grad_tiles(X.as<float>(), y, b0, b1, head, static_cast<double>(b1 - b0), &sp);
+        reduce_partials(tr, tiles, sp, b1 - b0, loss, grads);
     });
 }
 
@@ -1294,33 +1431,77 @@ hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, in
     });
 }
 
-// Roofline probe of the SGD step (bench.py): `steps` SGD steps of train_base's
-// inner loop on one batch of `rows` host rows, CUDA events on the engine's
-// stream around every step and after its gradient kernels.  out = mean ms of
-// [whole step, gradient kernels (tile + weight gradient), optimizer].
-hcva_status hcva_diag_sgd_timing(hcva_ctx* ctx, const hcva_train_cfg* cfg, int input_dim, const double* params,
-                                 const double* x, const double* y, int rows, int steps, double* out) {
+// Roofline probe of the SGD step (bench.py): train_base's inner loop at step
+// `step` of a simulated set (scaler, features, Glorot init with mu = label
+// mean), three untimed SGD steps, then `steps` SGD steps over consecutive
+// batches with CUDA events on the engine's stream around every step and after
+// its gradient kernels.  out = mean ms of [whole step, gradient kernels,
+// optimizer], and the number of gradient partial rows per step.
+hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int step, int label_kind, int steps,
+                                 double* out) {
     return guarded([&] {
+        hcva_ctx* ctx = sim->ctx;
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
-        if (rows < 1 || steps < 1) throw contract_error("sgd timing: no rows or steps");
-        const NetDims n = dims_from(cfg, input_dim);
-        Trainer tr(ctx, n, rows, rows);
-        DeviceBuf dX, dy;
-        stage_features(tr, x, rows, input_dim, dX);
-        stage(dy, std::vector<double>(y, y + rows));
-        tr.set_params(params);
+        if (steps < 1 || step < 1 || step > sim->n) throw contract_error("sgd timing: bad step / count");
+        const long R = static_cast<long>(sim->M) * sim->N;
+        if (cfg->n_batches < 1 || R % cfg->n_batches) throw config_error("make_batches: batch count must divide M*N");
+        const long bs = R / cfg->n_batches;
+        const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
+        const NetDims n = dims_from(cfg, d);
+        if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
+        Trainer tr(ctx, n, bs, R, use_split(n, sim));
+        if (tr.split) tr.split_source(sim);
+        DeviceBuf mean, scale, X;
+        mean.alloc(static_cast<size_t>(d) * 8);
+        scale.alloc(static_cast<size_t>(d) * 8);
+        FeatArgs fa = feat_args(sim, step);
+        k_scaler<<<d, 256, 0, ctx->stream>>>(fa, mean.as<double>(), scale.as<double>());
+        fa.mean = mean.as<double>();
+        fa.scale = scale.as<double>();
+        if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
+        build_features(tr, fa, X, R);
+        const double* y = sim->labels.as<double>() + static_cast<size_t>(step) * R;
+        const auto p = init_params(n, split_key(split_key(root_key(cfg->seed), 0xBEEF), step));
+        tr.set_params(p.data());
+        HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
+        k_set_mu_mean<<<1, 1024, 0, ctx->stream>>>(y, R, tr.p64.as<double>(), tr.p32.as<float>(), n.P);
         HCVA_CUDA(cudaMemsetAsync(tr.m.p, 0, n.P * 8, ctx->stream));
         HCVA_CUDA(cudaMemsetAsync(tr.v.p, 0, n.P * 8, ctx->stream));
-        for (int w = 0; w < 3; ++w) tr.sgd_step(dX.as<float>(), dy.as<double>(), 0, rows, 0, w + 1, cfg->learning_rate, cfg->adam);
-        std::vector<cudaEvent_t> ev(3 * steps);
+        tr.wimg_valid = false;
+        auto run = [&](long t) {
+            const long b = t % cfg->n_batches;
+            tr.sgd_step(X.as<float>(), y, b * bs, (b + 1) * bs, 0, t + 1, cfg->learning_rate, cfg->adam);
+        };
+        for (long w = 0; w < 3; ++w) run(w);
+        std::vector<cudaEvent_t> ev(3 * static_cast<size_t>(steps));
         for (auto& e : ev) HCVA_CUDA(cudaEventCreate(&e));
         for (int s = 0; s < steps; ++s) {
             HCVA_CUDA(cudaEventRecord(ev[3 * s], ctx->stream));
             tr.phase_ev = &ev[3 * s + 1];
-            tr.sgd_step(dX.as<float>(), dy.as<double>(), 0, rows, 0, s + 4, cfg->learning_rate, cfg->adam);
+            run(3 + s);
         }
         tr.phase_ev = nullptr;
+        if (tr.split && std::getenv("HCVA_SPLIT_TRACE")) {  // profiling: phase clocks of one more step
+            DeviceBuf tb;
+            tb.alloc(80 * 8);
+            HCVA_CUDA(cudaMemsetAsync(tb.p, 0, 80 * 8, ctx->stream));
+            tr.sa.trace = tb.as<long long>();
+            run(3 + steps);
+            tr.sa.trace = nullptr;
+            long long h[80];
+            copy_out(ctx, h, tb.p, sizeof h);
+            for (int t = 0; t < 4; ++t) {
+                std::fprintf(stderr, "tile %d:", t);
+                for (int k = 1; k <= 10; ++k) std::fprintf(stderr, " %lld", h[t * 16 + k] - h[t * 16 + k - 1]);
+                std::fprintf(stderr, "\n");
+            }
+            std::fprintf(stderr, "fixed:");
+            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %lld", h[64 + k] - h[64 + k - 1]);
+            std::fprintf(stderr, " | tail:");
+            for (int k = 8; k < 13; ++k) std::fprintf(stderr, " %lld", h[64 + k] - h[64 + 5]);
+            std::fprintf(stderr, "  entry->tile0 %lld, tile3 end->final %lld\n", h[0] - h[64], h[67] - h[3 * 16 + 10]);
+        }
         HCVA_CUDA(cudaStreamSynchronize(ctx->stream));
         double tot = 0.0, grad = 0.0, opt = 0.0;
         for (int s = 0; s < steps; ++s) {
@@ -1330,7 +1511,8 @@ hcva_status hcva_diag_sgd_timing(hcva_ctx* ctx, const hcva_train_cfg* cfg, int i
             grad += a, opt += b, tot += a + b;
         }
         for (auto e : ev) cudaEventDestroy(e);
-        out[0] = tot / steps, out[1] = grad / steps, out[2] = opt / steps;
+        tr.check_finite();
+        out[0] = tot / steps, out[1] = grad / steps, out[2] = opt / steps, out[3] = tr.split ? 1.0 : 0.0;
     });
 }
 
@@ -1405,7 +1587,8 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
         models->best_loss.alloc(static_cast<size_t>(nsteps) * 8);
         models->best_epoch.alloc(static_cast<size_t>(nsteps) * 4);
         if (sim->labels_kind != label_kind) launch_labels_all(sim, label_kind);
-        Trainer tr(ctx, n, R / cfg->n_batches, R);
+        Trainer tr(ctx, n, R / cfg->n_batches, R, use_split(n, sim));
+        if (tr.split) tr.split_source(sim);
         const int mm = n.u + 1;
         tr.set_comm(comm, std::max<size_t>({static_cast<size_t>(n.P) + 1, static_cast<size_t>(mm * (mm + 1) / 2 + mm),
                                             static_cast<size_t>(d)}));
@@ -1425,14 +1608,21 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
         int cur_step = 0;
         if (probe) {
             probe_block(sim, probe_key, label_kind, p_steps, p_labels);
-            if (tr.use_tc) p_img.alloc(static_cast<size_t>((R2 + 127) / 128) * tc_x_tile_bytes(tr.dp));
+            if (tr.split) { /* the probe rows reuse this step's per-path columns */ }
+            else if (tr.use_tc) p_img.alloc(static_cast<size_t>((R2 + 127) / 128) * tc_x_tile_bytes(tr.dp));
             else p_X.alloc(sizeof(float) * R2 * d);
             p_pred.alloc(sizeof(double) * R2);
             p_g.alloc(sizeof(double) * R2);
             tr.on_epoch = [&](int epoch) {
-                tr.ximg_over = tr.use_tc ? p_img.as<uint8_t>() : nullptr;
+                tr.ximg_over = tr.use_tc && !tr.split ? p_img.as<uint8_t>() : nullptr;
+                SplitArgs p_sa = tr.sa;  // the probe's two replicas per path
+                p_sa.steps = p_steps.as<uint16_t>();
+                p_sa.N = 2;
+                p_sa.R = R2;
+                tr.sa_over = tr.split ? &p_sa : nullptr;
                 tr.eval(p_X.as<float>(), nullptr, R2, 4, p_pred.as<double>());
                 tr.ximg_over = nullptr;
+                tr.sa_over = nullptr;
                 // g[k] = (squared error of replica 0, of replica 1): already the pair layout
                 k_sq_err<<<grid1(R2, 256), 256, 0, ctx->stream>>>(p_pred.as<double>(), p_y, R2, p_g.as<double>());
                 ctx->launches++;
@@ -1540,7 +1730,8 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
         const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
         if (d != m->n.d) throw contract_error("forward: feature dimension mismatch");
         const long R = static_cast<long>(sim->M) * sim->N;
-        Trainer tr(ctx, m->n, 1, R);
+        Trainer tr(ctx, m->n, 1, R, use_split(m->n, sim, false));
+        if (tr.split) tr.split_source(sim);
         tr.set_params(m->params.as<double>() + static_cast<size_t>(step - 1) * m->n.P);
         FeatArgs fa = feat_args(sim, step);
         fa.mean = m->mean.as<double>() + static_cast<size_t>(step - 1) * d;
@@ -1566,7 +1757,8 @@ hcva_status hcva_percentile_table(const hcva_models* m, hcva_sim* sim, double* o
         const int d = sim->model.Cc * 2 + 3 * sim->model.E - 1;
         if (d != m->n.d) throw contract_error("forward: feature dimension mismatch");
         const long R = static_cast<long>(sim->M) * sim->N;
-        Trainer tr(ctx, m->n, 1, R);
+        Trainer tr(ctx, m->n, 1, R, use_split(m->n, sim, false));
+        if (tr.split) tr.split_source(sim);
         DeviceBuf X, pred;
         if (!tr.use_tc) X.alloc(sizeof(float) * R * d);
         pred.alloc(sizeof(double) * R);

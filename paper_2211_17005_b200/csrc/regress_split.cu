@@ -1,0 +1,787 @@
+// regress_split.cu -- K5 with the layer-0 split: the SGD step
+// and the full-sample evaluation of the backward regression (regressor.cpp:
+// 97-158, 191-213) for the paper's network (two hidden layers of U = 64),
+// without a feature matrix.
+//
+// A feature row of replica (k, l) at step i (labels.cpp:142-167) is
+// [1{s_klc <= i} for the Cc clients, y_k] where y_k -- rates, FX, client
+// intensities, lagged rates, standardised -- is the same for all N replicas
+// of path k.  So layer 0 splits:
+//     z0 = (b0 + W0_y y_k) + W0_ind 1{s_kl <= i}
+// P_k = b0 + W0_y y_k is computed once per path of a tile (FP32 FMA chains
+// over the q columns), the indicator part from the replica's default steps
+// (uint16 per name).  Per 128-row tile the kernel reads 8 default steps and a
+// label per row plus one y_k per path -- ~3 KB instead of a 24 KB feature
+// tile -- and the step never materialises the 2M x 48 feature matrix.
+//
+// k_sgd_split<ACT>  the whole SGD gradient in one launch, one CTA per SM
+//   (persistent over the batch's tiles, 512 TMEM columns, ~226 KB of shared
+//   memory).  Per tile (thread r = row r = TMEM lane r, two warpgroups of 32
+//   columns):
+//     H1 = act(P_k + W0_ind ind)     SIMT; act'(H1) kept in registers;
+//                                    H1 hi|lo -> TMEM (A), H1^T hi|lo -> smem
+//     F1   D  = H1 W1^T              (M=128, N=64, K=64, A in TMEM)
+//          H2, f, residual, G2 = dd w2 act'(H2); G2 hi|lo -> TMEM, G2^T -> smem
+//     B    D  = G2 W1                (B: the W1^T tile)
+//     gW1 += G2^T [H1^T; 1]          (M=64, N=72, K=128 rows, both SW128 smem)
+//          G1 = D act'(H1); G1^T hi|lo -> smem
+//     Dind = G1^T [ind; member]      (M=64, N=32, K=128: indicator columns and
+//                                     per-path row sums, exact 0/1 operand)
+//          gW0_ind += Dind[:, c];  s_p = Dind[:, 8+p];  gb0 += s_p;
+//          gW0_y += s_p (x) y_p      (SIMT, 64 owner threads)
+//   so the weight gradients accumulate in tensor memory / registers across
+//   the CTA's tiles and leave once, as one FP32 partial row per CTA (no
+//   transposed activations in HBM, no second kernel).  3xTF32 throughout.
+// k_eval_split<ACT>  loss / head-switch minimum / predictions / layer-2
+//   activations, two CTAs per SM: P for every path of the tile (N >= 1),
+//   H1 -> TMEM, F1, epilogue as k_eval_tc.
+// Reductions are over fixed tile -> CTA maps in fixed order: deterministic.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "regress_act.cuh"
+#include "regress_tc.cuh"
+#include "tc.cuh"
+
+namespace hcva {
+namespace {
+
+constexpr int kU = 64;           // hidden width served here
+constexpr int kQ = 48;           // per-path columns (q <= 48), row stride of ysh
+constexpr int kInd = 8;          // indicator columns (Cc <= 8)
+constexpr int kPaths = 9;        // distinct paths per 128-row tile in the SGD kernel (N >= 16)
+constexpr int kEvPaths = 128;    // ... in the evaluation kernel (N >= 1)
+constexpr uint32_t kW1 = kU * kU * 4;        // one plane of W1 / W1^T (16 KB)
+constexpr uint32_t kW0i = kU * kInd * 4;     // one plane of the W0 indicator block (2 KB)
+constexpr uint32_t kH = kU * 128 * 4;        // one H1^T plane (32 KB)
+constexpr uint32_t kG = 128 * 128 * 4;       // G^T stacked [hi rows 0..63; lo rows 64..127] (64 KB)
+constexpr uint32_t kGlo = 8 * 1024;          // row 64 + o of a 128-row SW128 tile: 8 atoms past row o
+constexpr int kBR = 32;                      // rows of the [indicators; path membership; 0] operand
+constexpr uint32_t kB = kBR * 128 * 4;       // its single (exact) plane (16 KB)
+constexpr int kSgdThreads = 512;             // 4 warpgroups x 16 columns
+constexpr int kSlots = 5;                    // per-tile indicator / path-sum blocks kept in TMEM
+// TMEM columns of the SGD kernel: D (layer-0 indicator part, layer 1, backward),
+// A hi | lo (H1, then G2), gW1 [hi rows; lo rows] x 64, the indicator A
+// operand, kSlots blocks of per-tile [128 x 32] indicator / path sums, and
+// act'(H1) (then G1) of the current tile.
+constexpr uint32_t kTD = 0, kTAh = 64, kTAl = 128, kTW1 = 192, kTInd = 256, kTSlot = 288, kTDh = 448;
+static_assert(kTSlot + 32 * kSlots <= kTDh, "TMEM columns");
+
+constexpr size_t sgd_split_smem() {
+    return 2ull * kH + kG + kB + 4ull * kW1 + 2ull * kW0i + 4ull * (kPaths * kQ + 2 * kPaths * kU + 4 * 128 + 2 * kU) +
+           128 + 1024;
+}
+
+__device__ __forceinline__ long lmin(long x, long y) { return x < y ? x : y; }
+
+__device__ __forceinline__ void cta_sync() {
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+}
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ void sts(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// Per-path part of layer 0 for the paths of a tile: P[p][o] = b0[o] + W0_y[o] . y_p,
+// eight threads per output (strided partial sums, then a fixed shuffle tree).
+__device__ __forceinline__ void path_projection8(const SplitArgs& a, const float* ysh, float* Psh, int np, int tid,
+                                                 int nthreads) {
+    const int sub = tid & 7;
+    for (int i = tid >> 3; i < np * kU; i += nthreads >> 3) {
+        const int p = i / kU, o = i % kU;
+        const float* w = a.p32 + a.off0 + o * a.d + a.Cc;
+        float s = 0.0f;
+        for (int j = sub; j < a.q; j += 8) s = fmaf(__ldg(w + j), ysh[p * kQ + j], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (sub == 0) Psh[p * kU + o] = __ldg(a.vec + o) + s;
+    }
+}
+
+// Row state of one 128-row tile for thread row r.
+struct RowState {
+    unsigned kfirst;  // first path of the tile
+    int np;           // paths in the tile
+    int p;            // this row's path (tile-local)
+    unsigned ind;     // indicator bits 1{s_c <= i}
+    double y;         // label
+    bool live;
+};
+
+// The global loads of a tile's row state (issued early, consumed later): the
+// row's default steps and label, and this thread's share of the tile's path
+// columns (element tid of np x q).
+struct RowLoads {
+    unsigned short st[kInd];
+    double y;
+    float yv;
+};
+
+__device__ __forceinline__ RowLoads row_loads(const SplitArgs& a, long tile, int r, int tid) {
+    RowLoads l;
+    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
+    const unsigned row = row0 + r;
+    const bool live = row >= a.b0 && row < a.b1;
+#pragma unroll
+    for (int c = 0; c < kInd; ++c)
+        l.st[c] = (live && c < a.Cc) ? __ldg(a.steps + static_cast<size_t>(c + 1) * a.R + row) : 0xFFFF;
+    l.y = live ? __ldg(a.y + row) : 0.0;
+    const unsigned kfirst = row0 / N;
+    const int np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - kfirst + 1);
+    l.yv = tid < np * a.q ? __ldg(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q) : 0.0f;
+    return l;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// The same rows' lines pulled into L2 (no registers held).
+__device__ __forceinline__ void row_prefetch(const SplitArgs& a, long tile, int r, int tid) {
+    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
+    const unsigned row = row0 + r;
+    if (row < a.b1) {
+        if ((r & 31) == 0) {  // one lane per 32 rows: 64 B of steps per name, 256 B of labels
+#pragma unroll
+            for (int c = 0; c < kInd; ++c)
+                if (c < a.Cc) prefetch_l2(a.steps + static_cast<size_t>(c + 1) * a.R + row);
+            prefetch_l2(a.y + row);
+        }
+    }
+    const unsigned kfirst = row0 / N;
+    const int np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - kfirst + 1);
+    if (tid < np * a.q && tid % 32 == 0) prefetch_l2(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q);
+}
+
+__device__ __forceinline__ RowState row_state(const SplitArgs& a, long tile, int r, const RowLoads& l) {
+    RowState s;
+    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
+    s.kfirst = row0 / N;
+    s.np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - s.kfirst + 1);
+    const unsigned row = row0 + r;
+    s.live = row >= a.b0 && row < a.b1;
+    s.p = s.live ? static_cast<int>(row / N - s.kfirst) : 0;
+    s.ind = 0;
+#pragma unroll
+    for (int c = 0; c < kInd; ++c) s.ind |= (l.st[c] <= a.step ? 1u : 0u) << c;
+    s.y = l.y;
+    return s;
+}
+
+// Profiling: per-phase clock64 stamps of CTA 0's first tiles (SplitArgs::trace).
+#define TRACE(k) \
+    if (a.trace && blockIdx.x == 0 && tid == 0 && nt < 4) a.trace[nt * 16 + (k)] = clock64()
+#define TRACE_FIX(k) \
+    if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[64 + (k)] = clock64()
+
+template <int ACT>
+__global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, long t_first, long n_tiles) {
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = align1k(sm_raw);
+    uint8_t* tH = sm;              // H1^T hi | lo planes, SW128 K-major, 64 x 128
+    uint8_t* tG = tH + 2 * kH;     // G2^T, then G1^T, stacked hi | lo rows, 128 x 128
+    uint8_t* tB = tG + kG;         // [indicators (8); path membership (9); 0] x 128, exact
+    uint8_t* w1 = tB + kB;         // W1 hi | lo
+    uint8_t* w1t = w1 + 2 * kW1;   // W1^T hi | lo
+    uint8_t* w0b = w1t + 2 * kW1;  // W0 indicator columns [64 x 8] hi | lo (B operand)
+    float* ysh = reinterpret_cast<float*>(w0b + 2 * kW0i);  // [p][kQ] y of a tile's paths
+    float* Psh = ysh + kPaths * kQ;                        // [2][p][kU] layer-0 path parts, double buffered
+    float* fsh = Psh + 2 * kPaths * kU;                    // [4][128] output-sum exchange
+    float* vsh = fsh + 4 * 128;                            // b1 | w2
+    // mbarriers: MMA completions 0 Z (D0), 1 F (F1), 2 X (B), 3 Y (gW1); 4 W (weights);
+    // 5..8 operands ready for D0 / F1 / B + gW1 / slot + next D0 (one arrival per epilogue warp)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(vsh + 2 * kU);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 9);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool issuer = warp == kSgdThreads / 32;  // warp 16 issues every MMA; warps 0-15 are rows x columns
+    const int r = tid & 127, hf = (tid >> 7) & 3, cb = hf * 16;
+    if (tid == 0) {
+        for (int i = 0; i < 5; ++i) tc::mbar_init(&bar[i], 1);
+        for (int i = 5; i < 9; ++i) tc::mbar_init(&bar[i], kSgdThreads / 32);
+        tc::fence_async_smem();
+    }
+    TRACE_FIX(0);
+    if (warp == 0) tc::tmem_alloc(tbase, 512);
+    for (int i = tid; i < kPaths * kQ; i += kSgdThreads + 32) ysh[i] = 0.0f;
+    // transposed-store addresses of this thread: element (feature cb + q, batch row r)
+    // of a SW128 K-major tile with R rows sits at base + x[q & 7] + (q >> 3) * 1024
+    uint32_t xH[8], xG[8];
+    {
+        const uint32_t cr = (r & 31) >> 2;
+        const uint32_t bH = tc::smem_u32(tH) + ((r >> 5) * (kU / 8) + cb / 8) * 1024u + (r & 3) * 4u;
+        const uint32_t bG = tc::smem_u32(tG) + ((r >> 5) * (128 / 8) + cb / 8) * 1024u + (r & 3) * 4u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            xH[k] = bH + k * 128u + ((cr ^ k) << 4);
+            xG[k] = bG + k * 128u + ((cr ^ k) << 4);
+        }
+    }
+    // the first tile's row loads do not depend on the optimizer: before the dependency wait
+    const RowLoads l0 = (!issuer && t_first + blockIdx.x < t_first + n_tiles) ? row_loads(a, t_first + blockIdx.x, r, tid)
+                                                                            : RowLoads{};
+    cta_sync();
+    const uint32_t tm = *tbase;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    pdl_wait();  // the optimizer's parameters and weight image
+    if (tid == 0) {
+        tc::mbar_expect_tx(&bar[4], 4 * kW1);
+        tc::bulk_g2s(w1, a.w1img, 4 * kW1, &bar[4]);
+    }
+    const uint32_t id128 = tc::idesc_tf32(128, kU, 0, 0);
+    const long t_end = t_first + n_tiles;
+    double loss = 0.0, dmu = 0.0;
+    float gb2 = 0.0f, acc_w2 = 0.0f, acc_b1 = 0.0f;
+    int nt = 0;
+
+    if (issuer) {
+        // ================= MMA issue (one lane), paced by the epilogue warps' ready barriers
+        uint32_t rph[4] = {0, 0, 0, 0};
+        auto wait_ready = [&](int k) {
+            tc::mbar_wait(&bar[5 + k], rph[k]);
+            rph[k] ^= 1;
+            tc::fence_after_sync();
+        };
+        auto issue_d0 = [&]() {  // D0 = ind W0_ind^T (exact A: two MMAs), commit Z
+            const tc::Operand B = tc::kmajor(w0b, kW0i, kU);
+            tc::mma_tf32_ts(tm + kTD, tm + kTInd, B.desc(0, 0), id128, 0);
+            tc::mma_tf32_ts(tm + kTD, tm + kTInd, B.desc(1, 0), id128, 1);
+            tc::commit(&bar[0]);
+        };
+        tc::mbar_wait(&bar[4], 0);  // W1 / W1^T in shared memory
+        long t = t_first + blockIdx.x;
+        if (t < t_end) {
+            wait_ready(0);
+            if (lane == 0) issue_d0();
+        }
+        for (int n = 0; t < t_end; t += gridDim.x, ++n) {
+            const bool more = t + gridDim.x < t_end;
+            wait_ready(1);
+            if (lane == 0) {  // ---- F1: D = H1 W1^T, H1 from tensor memory (also covers the last slot MMAs)
+                tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, id128, 0);
+                tc::commit(&bar[1]);
+            }
+            wait_ready(2);
+            if (lane == 0) {
+                // ---- B: D = G2 W1 (the W1^T tile), G2 from tensor memory; commit X
+                tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1t, kW1, kU), kU, id128, 0);
+                tc::commit(&bar[2]);
+                // ---- gW1 += [G2^T hi; G2^T lo] (H1^T hi + H1^T lo): M = 128, two MMAs per K step; commit Y
+                const tc::OperandSW A{tc::smem_u32(tG), 0, 128, 0};
+                const tc::OperandSW Bh{tc::smem_u32(tH), 0, kU, 0}, Bl{tc::smem_u32(tH) + kH, 0, kU, 0};
+                const uint32_t id = tc::idesc_tf32(128, kU, 0, 0);
+#pragma unroll 1
+                for (int ks = 0; ks < 16; ++ks) {
+                    tc::mma_tf32(tm + kTW1, A.desc(0, ks), Bh.desc(0, ks), id, (ks > 0 || n > 0) ? 1 : 0);
+                    tc::mma_tf32(tm + kTW1, A.desc(0, ks), Bl.desc(0, ks), id, 1);
+                }
+                tc::commit(&bar[3]);
+            }
+            wait_ready(3);
+            if (lane == 0) {
+                if (more) issue_d0();  // the next tile's D0 first (the epilogue waits on it next)
+                // ---- slot = [G1^T hi; G1^T lo] [ind; member] (exact B, M = 128): read at the end
+                const tc::OperandSW A{tc::smem_u32(tG), 0, 128, 0}, Bm{tc::smem_u32(tB), 0, kBR, 0};
+                const uint32_t id = tc::idesc_tf32(128, kBR, 0, 0), slot = tm + kTSlot + 32u * n;
+#pragma unroll 1
+                for (int ks = 0; ks < 16; ++ks) tc::mma_tf32(slot, A.desc(0, ks), Bm.desc(0, ks), id, ks > 0 ? 1 : 0);
+            }
+            nt = n + 1;
+        }
+        if (lane == 0) tc::commit(&bar[1]);  // the last slot MMAs
+        __syncwarp();
+    } else {
+        // ================= epilogue warps: 128 rows x 4 column groups of 16
+        for (int i = tid; i < kInd * kU; i += kSgdThreads) {
+            const int o = i / kInd, c = i % kInd;
+            tc::put_split(w0b, kW0i, o, c, kU, c < a.Cc ? a.p32[a.off0 + o * a.d + c] : 0.0f);
+        }
+        const float b2 = __ldg(a.vec + 192);
+        const double mu = a.mu64[0], two_nb = 2.0 / a.nb;
+        if (tid < 2 * kU) vsh[tid] = __ldg(a.vec + 64 + tid);  // b1 | w2
+        const float* b1v = vsh + cb;
+        const float* w2v = vsh + kU + cb;
+        uint32_t ph[4] = {0, 0, 0, 0};
+        auto epi_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kSgdThreads) : "memory"); };
+        auto wait_done = [&](int b) {
+            tc::mbar_wait(&bar[b], ph[b]);
+            ph[b] ^= 1;
+            tc::fence_after_sync();
+        };
+        auto ready = [&](int k) {  // this warp's operand writes for the next MMAs are complete
+            tc::tmem_wait_st();
+            tc::fence_async_smem();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&bar[5 + k])) : "memory");
+        };
+        // layer-0 inputs of a tile: its paths' y, P into Psh[buf], the indicator A operand
+        auto stage_tile = [&](const RowState& st, float yv, int buf) {
+            if (tid < st.np * a.q) ysh[(tid / a.q) * kQ + tid % a.q] = yv;
+            if (hf == 0) {
+                float iv[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) iv[c] = ((st.ind >> c) & 1u) ? 1.0f : 0.0f;
+                tc::tmem_st8(tm + lb + kTInd, iv);
+            }
+            epi_sync();
+            path_projection8(a, ysh, Psh + buf * kPaths * kU, st.np, tid, kSgdThreads);
+        };
+        int buf = 0;
+        long tile = t_first + blockIdx.x;
+        RowState cur{};
+        if (tile < t_end) {
+            cur = row_state(a, tile, r, l0);
+            stage_tile(cur, l0.yv, 0);
+            ready(0);
+        }
+        TRACE_FIX(1);
+        TRACE_FIX(2);
+        for (; tile < t_end; tile += gridDim.x, ++nt, buf ^= 1) {
+            const bool more = tile + gridDim.x < t_end;
+            TRACE(0);
+            epi_sync();  // Psh of this tile complete
+            wait_done(0);  // D0 of this tile
+            TRACE(1);
+            // ---- layer 0 -> H1 (TMEM A, H1^T), act'(H1) -> TMEM
+            {
+                float dh[16];
+                float z[16], hi[16], lo[16];
+                const float* P = Psh + buf * kPaths * kU + cur.p * kU + cb;
+                tc::tmem_ld16(tm + lb + kTD + cb, z);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const float h = act_f<ACT>(z[q] + P[q]);
+                    hi[q] = tc::tf32_rna(h);
+                    lo[q] = h - hi[q];
+                    dh[q] = act_d<ACT>(h);
+                    sts(xH[q & 7] + (q >> 3) * 1024u, hi[q]);
+                    sts(xH[q & 7] + (q >> 3) * 1024u + kH, lo[q]);
+                }
+                tc::tmem_st16(tm + lb + kTAh + cb, hi);
+                tc::tmem_st16(tm + lb + kTAl + cb, lo);
+                tc::tmem_st16(tm + lb + kTDh + cb, dh);
+            }
+            ready(1);
+            TRACE(2);
+            if (more) row_prefetch(a, tile + gridDim.x, r, tid);  // to L2 under F1; loaded after B
+            TRACE(3);
+            TRACE(4);
+            wait_done(1);
+            TRACE(5);
+            // ---- epilogue 2: this row's column of [ind; member] (8 rows per warpgroup), H2, f, residual, G2
+#pragma unroll
+            for (int n = 0; n < kBR / 4; ++n) {
+                const int br = hf * (kBR / 4) + n;
+                float v = 0.0f;
+                if (br < kInd) v = ((cur.ind >> br) & 1u) ? 1.0f : 0.0f;
+                else if (br < kInd + kPaths) v = (cur.live && cur.p == br - kInd) ? 1.0f : 0.0f;
+                *reinterpret_cast<float*>(tB + tc::sw_off(br, r, kBR)) = v;
+            }
+            float h2[16];
+            tc::tmem_ld16(tm + lb + kTD + cb, h2);
+            float fp = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                h2[j] = act_f<ACT>(h2[j] + b1v[j]);
+                fp = fmaf(h2[j], w2v[j], fp);
+            }
+            fsh[hf * 128 + r] = fp;
+            epi_sync();
+            const float f = b2 + ((fsh[r] + fsh[128 + r]) + (fsh[256 + r] + fsh[384 + r]));
+            float dd = 0.0f;
+            if (cur.live) {
+                const double pr = ((a.head && f < 0.0f) ? 0.0 : static_cast<double>(f)) + mu;
+                const double res = pr - cur.y;
+                const double dm = res * two_nb;
+                if (hf == 0) {
+                    loss += res * res;
+                    dmu += dm;
+                }
+                dd = static_cast<float>(dm);
+                if (a.head && !(f > 0.0f)) dd = 0.0f;
+            }
+            if (hf == 0) gb2 += dd;
+            {
+                float g[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) g[j] = dd * h2[j];
+                acc_w2 += bfly_sum<16>(g, lane);  // lane: column cb + lane % 16 over the warp's rows
+            }
+            {
+                float gv[16], hi[16], lo[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    gv[q] = dd * w2v[q] * act_d<ACT>(h2[q]);
+                    hi[q] = tc::tf32_rna(gv[q]);
+                    lo[q] = gv[q] - hi[q];
+                    sts(xG[q & 7] + (q >> 3) * 1024u, hi[q]);
+                    sts(xG[q & 7] + (q >> 3) * 1024u + kGlo, lo[q]);
+                }
+                tc::tmem_st16(tm + lb + kTAh + cb, hi);
+                tc::tmem_st16(tm + lb + kTAl + cb, lo);
+                acc_b1 += bfly_sum<16>(gv, lane);  // gb1: column sums of G2
+            }
+            ready(2);
+            TRACE(6);
+            wait_done(2);
+            TRACE(7);
+            {  // ---- G1 = D act'(H1) (tensor memory until gW1 has read G2^T)
+                float g1[16], dh[16];
+                tc::tmem_ld16(tm + lb + kTD + cb, g1);
+                tc::tmem_ld16(tm + lb + kTDh + cb, dh);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) g1[q] *= dh[q];
+                tc::tmem_st16(tm + lb + kTDh + cb, g1);
+            }
+            RowState nxt{};
+            if (more) {  // the next tile's layer-0 inputs, under gW1
+                const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid);
+                nxt = row_state(a, tile + gridDim.x, r, ln);
+                stage_tile(nxt, ln.yv, buf ^ 1);
+            }
+            TRACE(8);
+            wait_done(3);
+            TRACE(9);
+            {
+                float g1[16];
+                tc::tmem_ld16(tm + lb + kTDh + cb, g1);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const float hi = tc::tf32_rna(g1[q]);
+                    sts(xG[q & 7] + (q >> 3) * 1024u, hi);
+                    sts(xG[q & 7] + (q >> 3) * 1024u + kGlo, g1[q] - hi);
+                }
+            }
+            ready(3);
+            TRACE(10);
+            cur = nxt;
+        }
+        wait_done(1);  // the issuer's final commit: every MMA done
+    }
+    __syncthreads();
+    TRACE_FIX(3);
+    TRACE_FIX(4);
+
+    // ---- this CTA's partial row of the gradient (every parameter); scratch in tH / tG
+    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
+    constexpr int L1 = kU + 1;                 // padded rows: conflict-free column stores
+    float* s1 = reinterpret_cast<float*>(tH);  // [128][L1] gW1 rows: hi part, lo part
+    float* s2 = reinterpret_cast<float*>(tG);  // [128][kInd + 1 + kQ + 1] gW0 rows: hi part, lo part
+    if (warp < 4) {
+#pragma unroll
+        for (int c = 0; c < kU; c += 16) {
+            float v[16];
+            tc::tmem_ld16(tm + lb + kTW1 + c, v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) s1[r * L1 + c + q] = v[q];
+        }
+    }
+    TRACE_FIX(5);
+    float* part = fsh;                                      // [warp][32] w2, then b1 partials
+    double* red = reinterpret_cast<double*>(Psh);          // [3][16]
+    if (!issuer) part[warp * 32 + lane] = acc_w2;
+    loss = warp_sum(loss);
+    dmu = warp_sum(dmu);
+    const float gb2w = warp_sum(gb2);
+    if (lane == 0 && !issuer) {
+        red[warp] = loss;
+        red[16 + warp] = dmu;
+        red[32 + warp] = gb2w;
+    }
+    __syncthreads();
+    if (tid < kU) {  // column tid: warpgroup tid / 16, lane tid % 16 of its four warps
+        const int w0q = (tid / 16) * 4, c = tid % 16;
+        gout[a.off2 + tid] = part[(w0q + 0) * 32 + c] + part[(w0q + 1) * 32 + c] + part[(w0q + 2) * 32 + c] +
+                             part[(w0q + 3) * 32 + c];
+    }
+    if (tid == 0) {  // warpgroup 0 holds the per-row terms
+        a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
+        gout[a.P - 1] = static_cast<float>(red[16] + red[17] + red[18] + red[19]);
+        gout[a.off2 + kU] = static_cast<float>(red[32] + red[33] + red[34] + red[35]);
+    }
+    __syncthreads();
+    TRACE_FIX(8);
+    if (!issuer) part[warp * 32 + lane] = acc_b1;
+    __syncthreads();
+    if (tid < kU) {
+        const int w0q = (tid / 16) * 4, c = tid % 16;
+        gout[a.off1 + kU * kU + tid] = part[(w0q + 0) * 32 + c] + part[(w0q + 1) * 32 + c] +
+                                       part[(w0q + 2) * 32 + c] + part[(w0q + 3) * 32 + c];
+    }
+    TRACE_FIX(9);
+    // gW1[o][i] = hi-row + lo-row of the stacked accumulator
+    for (int i = tid; i < kU * kU; i += kSgdThreads + 32) {
+        const int o = i / kU, c = i % kU;
+        gout[a.off1 + i] = nt == 0 ? 0.0f : s1[o * L1 + c] + s1[(kU + o) * L1 + c];
+    }
+    TRACE_FIX(10);
+    // gW0 from the slots: accumulator row r' (TMEM lane r', warps 0-3) is output
+    // row r' % 64, hi part for r' < 64, lo part above.  Per slot (tile order):
+    // the indicator columns, and per path (path order) s_p -> b0 and s_p y_p.
+    int* snp = reinterpret_cast<int*>(red + 48);                          // [kSlots] paths per slot
+    float* yh = reinterpret_cast<float*>(tH + 128 * (kU + 1) * 4 + 64);  // [slot][kPaths][kQ]
+    if (tid < nt) {
+        const unsigned row0 = static_cast<unsigned>((t_first + blockIdx.x + static_cast<long>(tid) * gridDim.x) * 128);
+        const unsigned N = static_cast<unsigned>(a.N);
+        snp[tid] = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - row0 / N + 1);
+    }
+    for (int i = tid; i < nt * kPaths * kQ; i += kSgdThreads + 32) {
+        const int s = i / (kPaths * kQ), p = (i / kQ) % kPaths, j = i % kQ;
+        const unsigned row0 = static_cast<unsigned>((t_first + blockIdx.x + static_cast<long>(s) * gridDim.x) * 128);
+        const unsigned kf = row0 / static_cast<unsigned>(a.N);
+        const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
+        yh[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
+    }
+    __syncthreads();
+    TRACE_FIX(11);
+    constexpr int LW = kInd + 1 + kQ + 1;  // s2 row: indicators, b0, y columns (padded)
+    if (warp < 4) {
+        float acc_i[kInd], acc_y[kQ], acc_b0 = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kInd; ++c) acc_i[c] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) acc_y[j] = 0.0f;
+        for (int sl = 0; sl < nt; ++sl) {
+            float v[32];
+            tc::tmem_ld16(tm + lb + kTSlot + 32u * sl, v);
+            tc::tmem_ld16(tm + lb + kTSlot + 32u * sl + 16, v + 16);
+#pragma unroll
+            for (int c = 0; c < kInd; ++c) acc_i[c] += v[c];
+            const int np = snp[sl];
+#pragma unroll
+            for (int p = 0; p < kPaths; ++p) {
+                if (p >= np) break;
+                const float sp = v[kInd + p];
+                acc_b0 += sp;
+                const float* y = yh + (sl * kPaths + p) * kQ;
+#pragma unroll
+                for (int j = 0; j < kQ; ++j) acc_y[j] = fmaf(sp, y[j], acc_y[j]);
+            }
+        }
+        float* row = s2 + r * LW;
+#pragma unroll
+        for (int c = 0; c < kInd; ++c) row[c] = acc_i[c];
+        row[kInd] = acc_b0;
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) row[kInd + 1 + j] = acc_y[j];
+    }
+    __syncthreads();
+    TRACE_FIX(12);
+    if (tid < kSgdThreads) {  // output row o = tid / 8, columns c = tid % 8, +8, ...
+        const int o = tid >> 3, W = kInd + 1 + a.q;
+        for (int c = tid & 7; c < W; c += 8) {
+            const float v = s2[o * LW + c] + s2[(kU + o) * LW + c];
+            if (c < kInd) {
+                if (c < a.Cc) gout[a.off0 + o * a.d + c] = v;
+            } else if (c == kInd) {
+                gout[a.off0 + kU * a.d + o] = v;
+            } else {
+                gout[a.off0 + o * a.d + a.Cc + (c - kInd - 1)] = v;
+            }
+        }
+    }
+    TRACE_FIX(6);
+    tc::fence_before_sync();
+    __syncthreads();
+    TRACE_FIX(7);
+    if (warp == 0) tc::tmem_dealloc(tm, 512);
+}
+
+// ---------------------------------------------------------------- evaluation
+constexpr size_t eval_split_smem() {
+    return 2ull * kW1 + 4ull * (kInd * kU + kEvPaths * kQ + kEvPaths * kU + 2 * 128) + 64 + 128;
+}
+
+template <int ACT>
+__global__ void __launch_bounds__(256, 2) k_eval_split(SplitArgs a, long t_first, long n_tiles) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* w1 = sm;                                       // W1 hi | lo
+    float* w0i = reinterpret_cast<float*>(w1 + 2 * kW1);    // [c][o]
+    float* ysh = w0i + kInd * kU;                           // [p][kQ]
+    float* Psh = ysh + kEvPaths * kQ;                       // [p][kU]
+    float* fsh = Psh + kEvPaths * kU;                       // [2][128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid & 127, hf = tid >> 7, cb = hf * 32;
+    if (tid == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::fence_async_smem();
+    }
+    if (warp == 0) tc::tmem_alloc(tbase, 256);  // D | H1 hi | H1 lo
+    cta_sync();
+    const uint32_t tm = *tbase;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    pdl_wait();
+    if (tid == 0) {
+        tc::mbar_expect_tx(&bar[1], 2 * kW1);
+        tc::bulk_g2s(w1, a.w1img, 2 * kW1, &bar[1]);
+    }
+    for (int i = tid; i < kInd * kU; i += 256) {
+        const int c = i / kU, o = i % kU;
+        w0i[i] = c < a.Cc ? a.p32[a.off0 + o * a.d + c] : 0.0f;
+    }
+    const float b2 = __ldg(a.vec + 192);
+    const double mu = a.mu64[0];
+    tc::mbar_wait(&bar[1], 0);
+    __syncthreads();
+    uint32_t mph = 0;
+    double loss = 0.0, mn = INFINITY;
+    const long t_end = t_first + n_tiles;
+    for (long tile = t_first + blockIdx.x; tile < t_end; tile += gridDim.x) {
+        const long row0 = tile * 128;
+        const long kfirst = row0 / a.N;
+        const int np = static_cast<int>(lmin(row0 + 127, a.R - 1) / a.N - kfirst + 1);
+        for (int i = tid; i < np * a.q; i += 256) {
+            const int p = i / a.q, j = i % a.q;
+            ysh[p * kQ + j] = __ldg(a.yhat + (kfirst + p) * a.qp + j);
+        }
+        const long row = row0 + r;
+        const bool live = row >= a.b0 && row < a.b1;
+        const int p = live ? static_cast<int>(row / a.N - kfirst) : 0;
+        uint32_t ind = 0;
+        if (live)
+            for (int c = 0; c < a.Cc; ++c) ind |= (__ldg(a.steps + static_cast<size_t>(c + 1) * a.R + row) <= a.step) << c;
+        const double yrow = (live && (a.mode & 1) && hf == 0) ? __ldg(a.y + row) : 0.0;
+        __syncthreads();
+        path_projection8(a, ysh, Psh, np, tid, 256);
+        __syncthreads();
+#pragma unroll
+        for (int c16 = 0; c16 < 32; c16 += 16) {
+            float hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int o = cb + c16 + q;
+                float z = Psh[p * kU + o];
+#pragma unroll
+                for (int c = 0; c < kInd; ++c)
+                    if ((ind >> c) & 1u) z += w0i[c * kU + o];
+                const float h = act_f<ACT>(z);
+                hi[q] = tc::tf32_rna(h);
+                lo[q] = h - hi[q];
+            }
+            tc::tmem_st16(tm + lb + kTAh + cb + c16, hi);
+            tc::tmem_st16(tm + lb + kTAl + cb + c16, lo);
+        }
+        tc::tmem_wait_st();
+        cta_sync();
+        if (tid == 0) {
+            tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, tc::idesc_tf32(128, kU, 0, 0), 0);
+            tc::commit(&bar[0]);
+        }
+        if (warp == 0) tc::mbar_wait(&bar[0], mph);
+        mph ^= 1;
+        __syncthreads();
+        tc::fence_after_sync();
+        float h2[32];
+        tc::tmem_ld16(tm + lb + kTD + cb, h2);
+        tc::tmem_ld16(tm + lb + kTD + cb + 16, h2 + 16);
+        float fp = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            h2[j] = act_f<ACT>(h2[j] + __ldg(a.vec + 64 + cb + j));
+            fp = fmaf(h2[j], __ldg(a.vec + 128 + cb + j), fp);
+        }
+        fsh[hf * 128 + r] = fp;
+        __syncthreads();
+        const float f = b2 + (fsh[r] + fsh[128 + r]);
+        if ((a.mode & 8) && live)
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(a.H2 + row * kU + cb + j) = make_float4(h2[j], h2[j + 1], h2[j + 2], h2[j + 3]);
+        if (live && hf == 0) {
+            const double ph = (f < 0.0f ? 0.0 : static_cast<double>(f)) + mu;
+            if (a.mode & 1) {
+                const double res = ph - yrow;
+                loss += res * res;
+            }
+            if (a.mode & 2) mn = fmin(mn, static_cast<double>(f) + mu);
+            if (a.mode & 4) a.pred[row] = ph;
+        }
+        tc::fence_before_sync();
+        __syncthreads();  // TMEM reads, ysh / Psh / fsh free for the next tile
+    }
+    double* red = reinterpret_cast<double*>(Psh);
+    loss = warp_sum(loss);
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0 && warp < 4) {
+        red[warp] = loss;
+        red[4 + warp] = mn;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (a.mode & 1) a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
+        if (a.mode & 2) a.mpart[blockIdx.x] = fmin(fmin(red[4], red[5]), fmin(red[6], red[7]));
+    }
+    if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
+template <int ACT>
+void launch_sgd_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = sgd_split_smem();
+    HCVA_CUDA(cudaFuncSetAttribute(k_sgd_split<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pdl_launch(k_sgd_split<ACT>, dim3(ctas), dim3(kSgdThreads + 32), smem, s, a, t_first, n_tiles);
+}
+
+template <int ACT>
+void launch_eval_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = eval_split_smem();
+    HCVA_CUDA(cudaFuncSetAttribute(k_eval_split<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pdl_launch(k_eval_split<ACT>, dim3(ctas), dim3(256), smem, s, a, t_first, n_tiles);
+}
+
+}  // namespace
+
+static_assert(sgd_split_smem() <= 227 * 1024, "split SGD kernel exceeds shared memory");
+static_assert(2ull * kH >= 128ull * (kU + 1) * 4 + 64 + 4ull * kSlots * kPaths * kQ &&
+                  kG >= 128ull * (kInd + kQ + 2) * 4,
+              "readout scratch exceeds the operand tiles");
+static_assert(eval_split_smem() <= 113 * 1024, "split evaluation kernel must fit two CTAs per SM");
+
+bool split_eligible(int u, int h, int N, int Cc, int q) {
+    static const bool on = [] {
+        const char* e = std::getenv("HCVA_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on && u == kU && h == 2 && N >= 1 && Cc >= 0 && Cc <= kInd && q >= 1 && q <= kQ;
+}
+
+int split_max_ctas(int sm_count) { return 2 * sm_count; }
+
+int launch_sgd_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
+    if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
+    const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
+    // one CTA per SM, at most kSlots tiles each (more CTAs run in later waves)
+    const long per = std::min<long>(kSlots, (n_tiles + sm_count - 1) / sm_count);
+    const int ctas = static_cast<int>((n_tiles + per - 1) / per);
+    switch (a.act) {
+        case 0: launch_sgd_act<0>(a, t_first, n_tiles, ctas, s); break;
+        case 1: launch_sgd_act<1>(a, t_first, n_tiles, ctas, s); break;
+        case 2: launch_sgd_act<2>(a, t_first, n_tiles, ctas, s); break;
+        default: launch_sgd_act<3>(a, t_first, n_tiles, ctas, s); break;
+    }
+    return ctas;
+}
+
+int launch_eval_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
+    if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
+    const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
+    const int ctas = static_cast<int>(std::min<long>(n_tiles, split_max_ctas(sm_count)));
+    switch (a.act) {
+        case 0: launch_eval_act<0>(a, t_first, n_tiles, ctas, s); break;
+        case 1: launch_eval_act<1>(a, t_first, n_tiles, ctas, s); break;
+        case 2: launch_eval_act<2>(a, t_first, n_tiles, ctas, s); break;
+        default: launch_eval_act<3>(a, t_first, n_tiles, ctas, s); break;
+    }
+    return ctas;
+}
+
+}  // namespace hcva

@@ -41,6 +41,40 @@ struct WgradArgs {
     float* gpart;                  // [cta][U*U + U*dp]: W1 rows, then W0 rows padded to dp
 };
 
+// Layer-0 split (regress_split.cu): the feature row of replica (k, l) at
+// step i is [1{s_klc <= i} (c = 1..Cc), y_k (q per-path market columns)], so
+// W0 x = W0_ind 1{s <= i} + (b0 + W0_y y_k): the per-path part is computed
+// once per path per tile, the indicator part from the default steps; the
+// feature matrix is never built.
+struct SplitArgs {
+    int d, Cc, q, qp, N, step, P, off0, off1, off2, act;
+    long M, R;                 // paths and rows of the set
+    const float* yhat;         // [M][qp] standardised per-path columns of this step
+    const uint16_t* steps;     // [Cn][R] default steps (name 0 = bank)
+    const uint8_t* w1img;      // W1 hi | lo, W1^T hi | lo planes of the weight image
+    const float* vec;          // b0 | b1 | w2 | b2, mu of the weight image
+    const float* p32;          // FP32 parameters (W0 columns)
+    const double* mu64;        // FP64 master copy of mu
+    const double* y;           // labels [R]
+    long b0, b1;               // live rows
+    int head, mode;            // mode 0: SGD; else TileArgs::mode bits (1 loss, 2 min, 4 pred, 8 H2)
+    double nb;
+    float* gpart;              // SGD: [cta][P] gradient partials (every parameter)
+    double* lpart;             // [cta] sum of squared residuals
+    double* mpart;             // [cta] min of f + mu
+    double* pred;              // predictions, absolute row
+    float* H2;                 // [R][U] layer-2 activations (mode 8)
+    long long* trace;          // profiling: phase clocks of CTA 0 (HCVA_SPLIT_TRACE), or null
+};
+// Shapes served by the split kernels: U = 64, two hidden layers, Cc <= 8,
+// q <= 48; the SGD kernel also needs N >= 16 replicas per path (<= 9 paths
+// per 128-row tile), the evaluation kernel any N.
+bool split_eligible(int u, int h, int N, int Cc, int q);
+// Returns the number of per-CTA partials written.
+int launch_sgd_split(const SplitArgs& a, int sm_count, cudaStream_t s);
+int launch_eval_split(const SplitArgs& a, int sm_count, cudaStream_t s);
+int split_max_ctas(int sm_count);
+
 bool tc_eligible(int d, int h, int u);
 // Shapes served by the two-CTA-per-SM kernels (k_sgd_tc / k_eval_tc): their
 // feature tiles are one FP32 plane, split into tensor memory in the kernel.

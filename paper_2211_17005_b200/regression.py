@@ -56,6 +56,32 @@ def quadratic_loss(t: TrainConfig, params: np.ndarray, x: np.ndarray, y: np.ndar
     return loss.value, g
 
 
+def sim_quadratic_loss(sim: SimulationSet, t: TrainConfig, step: int, params: np.ndarray, mean: np.ndarray,
+                       scale: np.ndarray, head: bool = False, rows: Optional[Tuple[int, int]] = None,
+                       label_kind: str = "defaults") -> Tuple[float, np.ndarray]:
+    """quadratic_loss (regressor.cpp:115-158) on the label source's rows of a simulated set at `step`
+    (features standardised with mean / scale) through the kernels backward_learn runs on it."""
+    params, mean, scale = _f64(params), _f64(mean), _f64(scale)
+    b0, b1 = rows if rows is not None else (0, sim.n_paths * sim.n_replicas)
+    g = np.zeros_like(params)
+    loss = C.c_double()
+    kind = {"defaults": 0, "intensity": 1}[label_kind]
+    _lib.check(_lib.lib().hcva_sim_quadratic_loss(sim.handle, C.byref(train_cfg(t)), int(step), kind,
+                                                  params.ctypes.data_as(_lib.dptr), mean.ctypes.data_as(_lib.dptr),
+                                                  scale.ctypes.data_as(_lib.dptr), int(head), int(b0), int(b1),
+                                                  C.byref(loss), g.ctypes.data_as(_lib.dptr)))
+    return loss.value, g
+
+
+def sgd_timing(sim: SimulationSet, t: TrainConfig, step: int, steps: int = 50, label_kind: str = "defaults"):
+    """Mean ms of [SGD step, gradient kernels, optimizer] and whether the split kernels ran (hcva_diag_sgd_timing)."""
+    out = np.zeros(4)
+    kind = {"defaults": 0, "intensity": 1}[label_kind]
+    _lib.check(_lib.lib().hcva_diag_sgd_timing(sim.handle, C.byref(train_cfg(t)), int(step), kind, int(steps),
+                                               out.ctypes.data_as(_lib.dptr)))
+    return dict(step_ms=out[0], gradient_ms=out[1], optimizer_ms=out[2], split=bool(out[3]))
+
+
 def forward(t: TrainConfig, params: np.ndarray, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
     """forward (regressor.cpp:97-113) with the positive head on, on standardised rows: predictions."""
     ctx = ctx or context()
