@@ -724,7 +724,7 @@ struct Trainer {
     // current step + the default steps instead of a feature matrix.
     bool split = false;
     SplitArgs sa{};
-    DeviceBuf yhat;
+    DeviceBuf yhat, pg;  // per-path columns of the step; layer-0 path parts (evaluations)
     const SplitArgs* sa_over = nullptr;  // evaluation on other rows of the same paths (Q/R probe)
 
     void set_comm(hcva_comm* c, size_t max_len) {
@@ -813,6 +813,7 @@ struct Trainer {
         sa.steps = sim->steps.as<uint16_t>();
         yhat.alloc(static_cast<size_t>(sim->M) * sa.qp * 4);
         sa.yhat = yhat.as<float>();
+        pg.alloc(static_cast<size_t>(sim->M) * n.u * 4);
     }
 
     SplitArgs split_args(const SplitArgs& base, const double* y, long b0, long b1, int head, int mode, double nb,
@@ -832,6 +833,7 @@ struct Trainer {
         a.y = y; a.b0 = b0; a.b1 = b1; a.head = head; a.mode = mode; a.nb = nb;
         a.gpart = gpart.as<float>(); a.lpart = lpart.as<double>(); a.mpart = mpart.as<double>(); a.pred = pred;
         a.H2 = h2.as<float>();
+        a.Pg_out = pg.as<float>();
         return a;
     }
 

@@ -594,122 +594,240 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     if (warp == 0) tc::tmem_dealloc(tm, 512);
 }
 
-// ---------------------------------------------------------------- evaluation
-constexpr size_t eval_split_smem() {
-    return 2ull * kW1 + 4ull * (kInd * kU + kEvPaths * kQ + kEvPaths * kU + 2 * 128) + 64 + 128;
+// Layer-0 path parts of every path for an evaluation (W0 fixed during it):
+// Pg[k][o] = b0[o] + W0_y[o] . y_k.  A CTA takes 64 paths: thread (o, g) keeps
+// W0_y row o in registers and walks paths g, g + 4, ... of the block (the y
+// rows staged in shared memory), sequential FMA order over j as elsewhere.
+constexpr int kPjPaths = 64;
+__global__ void __launch_bounds__(256) k_path_proj(SplitArgs a, float* Pg) {
+    __shared__ float ys[kPjPaths * kQ];
+    const long k0 = static_cast<long>(blockIdx.x) * kPjPaths;
+    const int np = static_cast<int>(min(static_cast<long>(kPjPaths), a.M - k0));
+    for (int i = threadIdx.x; i < np * a.q; i += blockDim.x)
+        ys[(i / a.q) * kQ + i % a.q] = __ldg(a.yhat + (k0 + i / a.q) * a.qp + i % a.q);
+    const int o = threadIdx.x & (kU - 1), g = threadIdx.x / kU;
+    float w[kQ];
+#pragma unroll
+    for (int j = 0; j < kQ; ++j) w[j] = j < a.q ? __ldg(a.p32 + a.off0 + o * a.d + a.Cc + j) : 0.0f;
+    const float b0 = __ldg(a.vec + o);
+    __syncthreads();
+    for (int p = g; p < np; p += 256 / kU) {
+        float s = 0.0f;
+#pragma unroll
+        for (int j = 0; j < kQ; ++j)
+            if (j < a.q) s = fmaf(w[j], ys[p * kQ + j], s);
+        Pg[(k0 + p) * kU + o] = b0 + s;
+    }
 }
 
+// ---------------------------------------------------------------- evaluation
+// k_eval_split: one CTA per SM, 16 epilogue warps (128 rows x 4 groups of 16
+// columns) and an MMA-issue warp, two tiles in flight: while F1 of tile n
+// runs on the tensor cores, the epilogue finishes tile n-1 (H2, f, outputs)
+// and prepares tile n+1 (default steps, path columns, P, the indicator
+// operand whose D0 MMA follows).  Per TMEM buffer b = n & 1: D (D0, then F1's
+// accumulator), H1 hi | lo (A operand), indicators.
+constexpr int kEvThreads = 512;
+constexpr uint32_t kEvBuf = 256;  // TMEM columns per buffer: D 0, A hi 64, A lo 128, indicators 192
+constexpr size_t eval_split_smem() { return 2ull * kW1 + 2ull * kW0i + 4ull * (4 * 128 + 2 * kU) + 128 + 128; }
+
 template <int ACT>
-__global__ void __launch_bounds__(256, 2) k_eval_split(SplitArgs a, long t_first, long n_tiles) {
+__global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, long t_first, long n_tiles) {
     extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* w1 = sm;                                       // W1 hi | lo
-    float* w0i = reinterpret_cast<float*>(w1 + 2 * kW1);    // [c][o]
-    float* ysh = w0i + kInd * kU;                           // [p][kQ]
-    float* Psh = ysh + kEvPaths * kQ;                       // [p][kU]
-    float* fsh = Psh + kEvPaths * kU;                       // [2][128]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(fsh + 2 * 128);
-    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 2);
+    uint8_t* w1 = sm;                                        // W1 hi | lo
+    uint8_t* w0b = w1 + 2 * kW1;                             // W0 indicator columns [64 x 8] hi | lo
+    float* fsh = reinterpret_cast<float*>(w0b + 2 * kW0i);  // [4][128]
+    float* vsh = fsh + 4 * 128;                              // b1 | w2
+    // mbarriers: 0/1 D0 done, 2/3 F1 done, 4/5 D0 operands ready, 6/7 F1 operands ready, 8 weights
+    uint64_t* bar = reinterpret_cast<uint64_t*>(vsh + 2 * kU);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 9);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int r = tid & 127, hf = tid >> 7, cb = hf * 32;
+    const bool issuer = warp == kEvThreads / 32;
+    const int r = tid & 127, hf = (tid >> 7) & 3, cb = hf * 16;
     if (tid == 0) {
-        tc::mbar_init(&bar[0], 1);
-        tc::mbar_init(&bar[1], 1);
+        for (int i = 0; i < 4; ++i) tc::mbar_init(&bar[i], 1);
+        for (int i = 4; i < 8; ++i) tc::mbar_init(&bar[i], kEvThreads / 32);
+        tc::mbar_init(&bar[8], 1);
         tc::fence_async_smem();
     }
-    if (warp == 0) tc::tmem_alloc(tbase, 256);  // D | H1 hi | H1 lo
+    if (warp == 0) tc::tmem_alloc(tbase, 512);
     cta_sync();
     const uint32_t tm = *tbase;
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     pdl_wait();
     if (tid == 0) {
-        tc::mbar_expect_tx(&bar[1], 2 * kW1);
-        tc::bulk_g2s(w1, a.w1img, 2 * kW1, &bar[1]);
+        tc::mbar_expect_tx(&bar[8], 2 * kW1);
+        tc::bulk_g2s(w1, a.w1img, 2 * kW1, &bar[8]);
     }
-    for (int i = tid; i < kInd * kU; i += 256) {
-        const int c = i / kU, o = i % kU;
-        w0i[i] = c < a.Cc ? a.p32[a.off0 + o * a.d + c] : 0.0f;
-    }
-    const float b2 = __ldg(a.vec + 192);
-    const double mu = a.mu64[0];
-    tc::mbar_wait(&bar[1], 0);
-    __syncthreads();
-    uint32_t mph = 0;
+    const uint32_t id128 = tc::idesc_tf32(128, kU, 0, 0);
+    const int nt = n_tiles > blockIdx.x ? static_cast<int>((n_tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
     double loss = 0.0, mn = INFINITY;
-    const long t_end = t_first + n_tiles;
-    for (long tile = t_first + blockIdx.x; tile < t_end; tile += gridDim.x) {
-        const long row0 = tile * 128;
-        const long kfirst = row0 / a.N;
-        const int np = static_cast<int>(lmin(row0 + 127, a.R - 1) / a.N - kfirst + 1);
-        for (int i = tid; i < np * a.q; i += 256) {
-            const int p = i / a.q, j = i % a.q;
-            ysh[p * kQ + j] = __ldg(a.yhat + (kfirst + p) * a.qp + j);
+    if (issuer) {
+        uint32_t rph[4] = {0, 0, 0, 0};
+        auto wait_ready = [&](int k) {
+            tc::mbar_wait(&bar[4 + k], rph[k]);
+            rph[k] ^= 1;
+            tc::fence_after_sync();
+        };
+        auto d0 = [&](int b) {
+            const tc::Operand B = tc::kmajor(w0b, kW0i, kU);
+            const uint32_t base = tm + b * kEvBuf;
+            tc::mma_tf32_ts(base, base + 192, B.desc(0, 0), id128, 0);
+            tc::mma_tf32_ts(base, base + 192, B.desc(1, 0), id128, 1);
+            tc::commit(&bar[b]);
+        };
+        tc::mbar_wait(&bar[8], 0);
+        if (nt > 0) {
+            wait_ready(0);
+            if (lane == 0) d0(0);
         }
-        const long row = row0 + r;
-        const bool live = row >= a.b0 && row < a.b1;
-        const int p = live ? static_cast<int>(row / a.N - kfirst) : 0;
-        uint32_t ind = 0;
-        if (live)
-            for (int c = 0; c < a.Cc; ++c) ind |= (__ldg(a.steps + static_cast<size_t>(c + 1) * a.R + row) <= a.step) << c;
-        const double yrow = (live && (a.mode & 1) && hf == 0) ? __ldg(a.y + row) : 0.0;
-        __syncthreads();
-        path_projection8(a, ysh, Psh, np, tid, 256);
-        __syncthreads();
-#pragma unroll
-        for (int c16 = 0; c16 < 32; c16 += 16) {
-            float hi[16], lo[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int o = cb + c16 + q;
-                float z = Psh[p * kU + o];
+        for (int n = 0; n < nt; ++n) {
+            const int b = n & 1;
+            wait_ready(2 + b);
+            if (lane == 0) {
+                const uint32_t base = tm + b * kEvBuf;
+                tc::gemm3_ts(base, base + 64, base + 128, tc::kmajor(w1, kW1, kU), kU, id128, 0);
+                tc::commit(&bar[2 + b]);
+            }
+            if (n + 1 < nt) {
+                wait_ready(b ^ 1);
+                if (lane == 0) d0(b ^ 1);
+            }
+        }
+        __syncwarp();
+    } else {
+        for (int i = tid; i < kInd * kU; i += kEvThreads) {
+            const int o = i / kInd, c = i % kInd;
+            tc::put_split(w0b, kW0i, o, c, kU, c < a.Cc ? a.p32[a.off0 + o * a.d + c] : 0.0f);
+        }
+        if (tid < 2 * kU) vsh[tid] = __ldg(a.vec + 64 + tid);  // b1 | w2
+        const float b2 = __ldg(a.vec + 192);
+        const double mu = a.mu64[0];
+        uint32_t ph[4] = {0, 0, 0, 0};
+        auto epi_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kEvThreads) : "memory"); };
+        auto wait_done = [&](int k) {
+            tc::mbar_wait(&bar[k], ph[k]);
+            ph[k] ^= 1;
+            tc::fence_after_sync();
+        };
+        auto ready = [&](int k) {
+            tc::tmem_wait_st();
+            tc::fence_async_smem();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&bar[4 + k])) : "memory");
+        };
+        long rk0 = 0, rk1 = 0;  // this row's path, buffers 0 / 1
+        bool rl0 = false, rl1 = false;
+        double ry0 = 0.0, ry1 = 0.0;
+        const uint32_t rbar = tc::smem_u32(&bar[4]), dbar = tc::smem_u32(&bar[0]);
+        // register prefetch of a tile's global inputs (issued one iteration ahead)
+        struct Pre {
+            unsigned short st[kInd];
+            double y;
+            long k;
+            bool live;
+        };
+        auto fetch = [&](int n) {
+            Pre f;
+            const long tile = t_first + blockIdx.x + static_cast<long>(n) * gridDim.x;
+            const unsigned rw = static_cast<unsigned>(tile * 128) + r;
+            f.live = rw >= a.b0 && rw < a.b1;
+            f.k = f.live ? rw / static_cast<unsigned>(a.N) : 0;
+            f.y = 0.0;
+            if (hf == 0) {
 #pragma unroll
                 for (int c = 0; c < kInd; ++c)
-                    if ((ind >> c) & 1u) z += w0i[c * kU + o];
-                const float h = act_f<ACT>(z);
-                hi[q] = tc::tf32_rna(h);
-                lo[q] = h - hi[q];
+                    f.st[c] = (f.live && c < a.Cc) ? __ldg(a.steps + static_cast<size_t>(c + 1) * a.R + rw) : 0xFFFF;
+                if (f.live && (a.mode & 1)) f.y = __ldg(a.y + rw);
             }
-            tc::tmem_st16(tm + lb + kTAh + cb + c16, hi);
-            tc::tmem_st16(tm + lb + kTAl + cb + c16, lo);
-        }
-        tc::tmem_wait_st();
-        cta_sync();
-        if (tid == 0) {
-            tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, tc::idesc_tf32(128, kU, 0, 0), 0);
-            tc::commit(&bar[0]);
-        }
-        if (warp == 0) tc::mbar_wait(&bar[0], mph);
-        mph ^= 1;
-        __syncthreads();
-        tc::fence_after_sync();
-        float h2[32];
-        tc::tmem_ld16(tm + lb + kTD + cb, h2);
-        tc::tmem_ld16(tm + lb + kTD + cb + 16, h2 + 16);
-        float fp = 0.0f;
+            return f;
+        };
+        // tile n's inputs: default steps -> indicator operand (TMEM)
+        auto prep = [&](int n, const Pre& f) {
+            const int b = n & 1;
+            if (hf == 0) {
+                float iv[8];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            h2[j] = act_f<ACT>(h2[j] + __ldg(a.vec + 64 + cb + j));
-            fp = fmaf(h2[j], __ldg(a.vec + 128 + cb + j), fp);
-        }
-        fsh[hf * 128 + r] = fp;
-        __syncthreads();
-        const float f = b2 + (fsh[r] + fsh[128 + r]);
-        if ((a.mode & 8) && live)
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(a.H2 + row * kU + cb + j) = make_float4(h2[j], h2[j + 1], h2[j + 2], h2[j + 3]);
-        if (live && hf == 0) {
-            const double ph = (f < 0.0f ? 0.0 : static_cast<double>(f)) + mu;
-            if (a.mode & 1) {
-                const double res = ph - yrow;
-                loss += res * res;
+                for (int c = 0; c < kInd; ++c) iv[c] = f.st[c] <= a.step ? 1.0f : 0.0f;
+                tc::tmem_st8(tm + b * kEvBuf + lb + 192, iv);
             }
-            if (a.mode & 2) mn = fmin(mn, static_cast<double>(f) + mu);
-            if (a.mode & 4) a.pred[row] = ph;
+            if (b) rk1 = f.k, rl1 = f.live, ry1 = f.y;
+            else rk0 = f.k, rl0 = f.live, ry0 = f.y;
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rbar + 8 * b) : "memory");
+        };
+        auto layer0 = [&](int n) {  // H1 of tile n -> A[b]
+            const int b = n & 1;
+            tc::mbar_wait_addr(dbar + 8 * b, ph[b]);
+            ph[b] ^= 1;
+            tc::fence_after_sync();
+            float z[16], hi[16], lo[16];
+            const float4* P = reinterpret_cast<const float4*>(a.Pg + (b ? rk1 : rk0) * kU + cb);
+            tc::tmem_ld16(tm + b * kEvBuf + lb + cb, z);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 pv = __ldg(P + q4);
+                const float pz[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = 4 * q4 + u;
+                    const float h = act_f<ACT>(z[q] + pz[u]);
+                    hi[q] = tc::tf32_rna(h);
+                    lo[q] = h - hi[q];
+                }
+            }
+            tc::tmem_st16(tm + b * kEvBuf + lb + 64 + cb, hi);
+            tc::tmem_st16(tm + b * kEvBuf + lb + 128 + cb, lo);
+            ready(2 + b);
+        };
+        auto outputs = [&](int n) {  // H2, f and the requested outputs of tile n
+            const int b = n & 1;
+            const long tile = t_first + blockIdx.x + static_cast<long>(n) * gridDim.x;
+            const long rw = tile * 128 + r;
+            wait_done(2 + b);
+            float h2[16];
+            tc::tmem_ld16(tm + b * kEvBuf + lb + cb, h2);
+            epi_sync();  // the previous tile's fsh reads are done
+            float fp = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                h2[j] = act_f<ACT>(h2[j] + vsh[cb + j]);
+                fp = fmaf(h2[j], vsh[kU + cb + j], fp);
+            }
+            fsh[hf * 128 + r] = fp;
+            epi_sync();
+            const float f = b2 + ((fsh[r] + fsh[128 + r]) + (fsh[256 + r] + fsh[384 + r]));
+            const bool live = b ? rl1 : rl0;
+            if ((a.mode & 8) && live)
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(a.H2 + rw * kU + cb + j) = make_float4(h2[j], h2[j + 1], h2[j + 2], h2[j + 3]);
+            if (live && hf == 0) {
+                const double ph = (f < 0.0f ? 0.0 : static_cast<double>(f)) + mu;
+                if (a.mode & 1) {
+                    const double res = ph - (b ? ry1 : ry0);
+                    loss += res * res;
+                }
+                if (a.mode & 2) mn = fmin(mn, static_cast<double>(f) + mu);
+                if (a.mode & 4) a.pred[rw] = ph;
+            }
+        };
+        epi_sync();  // b1 | w2 staged
+        if (nt > 0) prep(0, fetch(0));
+        for (int n = 0; n < nt; ++n) {
+            Pre f{};
+            if (n + 1 < nt) f = fetch(n + 1);  // in flight under layer 0 of n and the outputs of n-1
+            layer0(n);
+            if (n > 0) outputs(n - 1);
+            if (n + 1 < nt) prep(n + 1, f);
         }
-        tc::fence_before_sync();
-        __syncthreads();  // TMEM reads, ysh / Psh / fsh free for the next tile
+        if (nt > 0) outputs(nt - 1);
     }
-    double* red = reinterpret_cast<double*>(Psh);
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(fsh);
     loss = warp_sum(loss);
     for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if (lane == 0 && warp < 4) {
@@ -721,7 +839,9 @@ __global__ void __launch_bounds__(256, 2) k_eval_split(SplitArgs a, long t_first
         if (a.mode & 1) a.lpart[blockIdx.x] = red[0] + red[1] + red[2] + red[3];
         if (a.mode & 2) a.mpart[blockIdx.x] = fmin(fmin(red[4], red[5]), fmin(red[6], red[7]));
     }
-    if (warp == 0) tc::tmem_dealloc(tm, 256);
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tm, 512);
 }
 
 template <int ACT>
@@ -735,7 +855,7 @@ template <int ACT>
 void launch_eval_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
     const size_t smem = eval_split_smem();
     HCVA_CUDA(cudaFuncSetAttribute(k_eval_split<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    pdl_launch(k_eval_split<ACT>, dim3(ctas), dim3(256), smem, s, a, t_first, n_tiles);
+    pdl_launch(k_eval_split<ACT>, dim3(ctas), dim3(kEvThreads + 32), smem, s, a, t_first, n_tiles);
 }
 
 }  // namespace
@@ -744,7 +864,7 @@ static_assert(sgd_split_smem() <= 227 * 1024, "split SGD kernel exceeds shared m
 static_assert(2ull * kH >= 128ull * (kU + 1) * 4 + 64 + 4ull * kSlots * kPaths * kQ &&
                   kG >= 128ull * (kInd + kQ + 2) * 4,
               "readout scratch exceeds the operand tiles");
-static_assert(eval_split_smem() <= 113 * 1024, "split evaluation kernel must fit two CTAs per SM");
+static_assert(eval_split_smem() <= 227 * 1024, "split evaluation kernel exceeds shared memory");
 
 bool split_eligible(int u, int h, int N, int Cc, int q) {
     static const bool on = [] {
@@ -771,10 +891,13 @@ int launch_sgd_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
     return ctas;
 }
 
-int launch_eval_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
-    if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
+int launch_eval_split(const SplitArgs& a_in, int sm_count, cudaStream_t s) {
+    if (a_in.b1 <= a_in.b0) throw contract_error("regression tile: empty row range");
+    SplitArgs a = a_in;
+    k_path_proj<<<static_cast<unsigned>((a.M + kPjPaths - 1) / kPjPaths), 256, 0, s>>>(a, a.Pg_out);
+    a.Pg = a.Pg_out;
     const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
-    const int ctas = static_cast<int>(std::min<long>(n_tiles, split_max_ctas(sm_count)));
+    const int ctas = static_cast<int>(std::min<long>(n_tiles, sm_count));
     switch (a.act) {
         case 0: launch_eval_act<0>(a, t_first, n_tiles, ctas, s); break;
         case 1: launch_eval_act<1>(a, t_first, n_tiles, ctas, s); break;

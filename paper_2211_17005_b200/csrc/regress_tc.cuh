@@ -65,6 +65,8 @@ struct SplitArgs {
     double* pred;              // predictions, absolute row
     float* H2;                 // [R][U] layer-2 activations (mode 8)
     long long* trace;          // profiling: phase clocks of CTA 0 (HCVA_SPLIT_TRACE), or null
+    const float* Pg;           // evaluation: layer-0 path parts [M][64] (k_path_proj)
+    float* Pg_out;             // evaluation: where the launcher writes them
 };
 // Shapes served by the split kernels: U = 64, two hidden layers, Cc <= 8,
 // q <= 48; the SGD kernel also needs N >= 16 replicas per path (<= 9 paths
