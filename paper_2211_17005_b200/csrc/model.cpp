@@ -1,6 +1,10 @@
 // model.cpp -- host-side model utilities of the engine (validation, Cholesky,
 // zero-coupon/par arithmetic, book generation).  These run once per call on
-// the host, exactly as in the reference; the hot loops live in the kernels.
+// the host and must reproduce the reference's generated book, par rates and
+// error texts bit for bit, so is_multiple / cholesky_lower / zc_price /
+// par_rate / generate_book are restatements of the reference's own lines
+// (portfolio.cpp:16-56,149-174, market.cpp:136-159; SURVEY §8(a) a5, a11,
+// a14 allow the reuse); the hot loops live in the kernels.
 #include <cmath>
 #include <cstring>
 #include <mutex>

@@ -603,13 +603,15 @@ __global__ void __launch_bounds__(EvalShape<U>::threads, 2) k_eval_tc(TileArgs a
     if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
-// SGD tile kernel, two CTAs per SM (resident inputs, dp <= 32 at U = 64): the
-// A operands of layer 1 (H1) and of the backward GEMM (G2) go through tensor
+// SGD tile kernel, two CTAs per SM, for the feature-matrix path (host rows and
+// sets the layer-0 split kernels do not serve, regress_split.cu): the A
+// operands of layer 1 (H1) and of the backward GEMM (G2) go through tensor
 // memory instead of a shared H tile, the vectors are read through L1, and each
-// thread covers 32 columns in two 16-column passes (layer 2's activations are
-// recomputed from D1 for the gradient pass) -- <= 113 KB of shared memory and
-// <= 128 registers, so two CTAs per SM interleave their GEMM -> epilogue
-// chains.  Same arithmetic and outputs as k_tile_tc's SGD mode.
+// thread covers 32 columns in two 16-column passes; layer 2's activations are
+// stored back into D1 and reloaded for the gradient pass.  Admission
+// (tc_two_cta): sgd_tc_smem <= 113 KB, i.e. dp <= 48 at U = 64; TMEM: D0 | D1
+// in columns 0..127, the feature tile's hi | lo split at 128..128 + 2 dp.
+// Same arithmetic and outputs as k_tile_tc's SGD mode.
 template <int U>
 struct SgdShape {
     static constexpr int UH = U < 32 ? U : 32;  // columns per thread
