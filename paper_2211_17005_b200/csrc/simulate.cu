@@ -88,9 +88,29 @@ struct MarketArgs {
 // The correlated increment z = L zraw reads the chunk tile through the CSR of
 // the Cholesky factor (exact zeros skipped).  Stores at pricing steps are
 // coalesced over the path index.
+// HCVA_K1_FMA (default on): the recursion's multiply-adds contract to FMAs.
+// The factors then differ from the reference's separately rounded products by
+// ~1 ulp per substep (market parity is 1e-11 relative); a default step could
+// only flip for a threshold within ~1e-15 of a cumulative hazard, and the
+// full C2 comparison (tests/test_gpu_simulation.py) counts 0 mismatches.
+#ifndef HCVA_K1_FMA
+#define HCVA_K1_FMA 1
+#endif
+__device__ __forceinline__ double madd(double a, double b, double c) {
+#if HCVA_K1_FMA
+    return fma(a, b, c);
+#else
+    return dadd(dmul(a, b), c);
+#endif
+}
+
 __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, double h, double z) {
     // r + (a(b - r) - q) h + (sigma sqrt h) z     (market.cpp:121-124)
+#if HCVA_K1_FMA
+    return fma(k.c3, z, fma(fma(k.c0, dsub(k.c1, r), -k.c2), h, r));
+#else
     return dadd(dadd(r, dmul(dsub(dmul(k.c0, dsub(k.c1, r)), k.c2), h)), dmul(k.c3, z));
+#endif
 }
 
 constexpr int kQueueCap = 128;  // per-warp queue of tail draws
@@ -285,18 +305,17 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
         auto zcorr = [&](const ZRow& k) {
             if (k.single) return dmul(k.v0, zt[k.o0]);
-            if (!k.dense) return dadd(dmul(k.v0, zt[k.o0]), dmul(k.v1, zt[k.o1]));
+            if (!k.dense) return madd(k.v1, zt[k.o1], dmul(k.v0, zt[k.o0]));
             double acc = 0.0;
-            for (int q = chol_row[k.d]; q < chol_row[k.d + 1]; ++q)
-                acc = dadd(acc, dmul(chol_val[q], zt[chol_col[q] * P]));
+            for (int q = chol_row[k.d]; q < chol_row[k.d + 1]; ++q) acc = madd(chol_val[q], zt[chol_col[q] * P], acc);
             return acc;
         };
         if (econ) {
             const double r0 = s1, re = s0;
             const double zr = zcorr(zr_a), z0 = zcorr(zr_b), zx = zcorr(zr_c);
-            s3 = dadd(s3, dmul(r0, h));  // -ln beta, left endpoint (market.cpp:208)
+            s3 = madd(r0, h, s3);  // -ln beta, left endpoint (market.cpp:208)
             // log chi + (r0 - re - sigma^2/2) h + sigma sqrt(h) z, pre-step rates (market.cpp:211-223)
-            s2 = dadd(dadd(s2, dmul(dsub(dsub(r0, re), kx_c0), h)), dmul(kx_c1, zx));
+            s2 = madd(kx_c1, zx, madd(dsub(dsub(r0, re), kx_c0), h, s2));
             s0 = vasicek_step(re, kc_a, h, zr);
             s1 = vasicek_step(r0, kc_b, h, z0);
         } else {
@@ -304,13 +323,11 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             const double z0 = zcorr(zr_a), z1 = zcorr(zr_b);
             const FactorCoef& k0 = kc_a;
             const FactorCoef& k1 = kc_b;
-            s2 = dadd(s2, dmul(s0, h));
-            s3 = dadd(s3, dmul(s1, h));
+            s2 = madd(s0, h, s2);
+            s3 = madd(s1, h, s3);
             const double gp0 = (s0 < 0.0) ? 0.0 : s0, gp1 = (s1 < 0.0) ? 0.0 : s1;
-            const double nx0 = dadd(dadd(s0, dmul(dmul(k0.c0, dsub(k0.c1, gp0)), h)),
-                                    dmul(dmul(dmul(k0.c2, sqrt(gp0)), sqh), z0));
-            const double nx1 = dadd(dadd(s1, dmul(dmul(k1.c0, dsub(k1.c1, gp1)), h)),
-                                    dmul(dmul(dmul(k1.c2, sqrt(gp1)), sqh), z1));
+            const double nx0 = madd(dmul(dmul(k0.c2, sqrt(gp0)), sqh), z0, madd(dmul(k0.c0, dsub(k0.c1, gp0)), h, s0));
+            const double nx1 = madd(dmul(dmul(k1.c2, sqrt(gp1)), sqh), z1, madd(dmul(k1.c0, dsub(k1.c1, gp1)), h, s1));
             s0 = (nx0 < 0.0) ? 0.0 : nx0;
             s1 = (nx1 < 0.0) ? 0.0 : nx1;
         }
