@@ -281,9 +281,10 @@ hcva_status hcva_refit_output_layer(hcva_ctx* ctx, const hcva_train_cfg* cfg, in
 /* Profiling probe (bench.py roofline): train_base's SGD steps at pricing step
  * `step` of a simulated set (scaler, features, init as backward_learn), CUDA
  * events on the context's stream; out = mean ms of [step, gradient kernels,
- * optimizer], 1 if the layer-0 split kernels ran. */
+ * optimizer], 1 if the layer-0 split kernels ran, and the mean ms per step of
+ * the persistent epoch kernel (0 when the shape does not take it). */
 hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int step, int label_kind, int steps,
-                                 double* out /* [4] */);
+                                 double* out /* [5] */);
 /* quadratic_loss (regressor.cpp:115-158) on rows [b0, b1) of the label
  * source at pricing step `step` (pipeline.cpp:72-111): the set's features
  * standardised with mean / scale [input_dim], its labels of label_kind,

@@ -42,6 +42,7 @@
 
 #include "common.cuh"
 #include "regress_act.cuh"
+#include "regress_opt.cuh"
 #include "regress_tc.cuh"
 #include "tc.cuh"
 
@@ -99,11 +100,11 @@ __device__ __forceinline__ void path_projection8(const SplitArgs& a, const float
         const int p = i / kU, o = i % kU;
         const float* w = a.p32 + a.off0 + o * a.d + a.Cc;
         float s = 0.0f;
-        for (int j = sub; j < a.q; j += 8) s = fmaf(__ldg(w + j), ysh[p * kQ + j], s);
+        for (int j = sub; j < a.q; j += 8) s = fmaf(__ldcg(w + j), ysh[p * kQ + j], s);
         s += __shfl_xor_sync(0xffffffffu, s, 4);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
-        if (sub == 0) Psh[p * kU + o] = __ldg(a.vec + o) + s;
+        if (sub == 0) Psh[p * kU + o] = __ldcg(a.vec + o) + s;
     }
 }
 
@@ -117,6 +118,27 @@ struct RowState {
     bool live;
 };
 
+// Grid-wide barrier of the persistent SGD kernel (cooperative launch: every
+// CTA is resident).  `count` is zeroed before the launch; barrier k of the
+// launch waits for (k + 1) * gridDim.x arrivals.  A CTA that is never joined
+// traps instead of hanging the GPU.
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(count, 1u);
+        const long long t0 = clock64();
+        unsigned v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+            if (clock64() - t0 > (1ll << 35)) __trap();
+        }
+    }
+    __syncthreads();
+}
+
 // The global loads of a tile's row state (issued early, consumed later): the
 // row's default steps and label, and this thread's share of the tile's path
 // columns (element tid of np x q).
@@ -126,11 +148,11 @@ struct RowLoads {
     float yv;
 };
 
-__device__ __forceinline__ RowLoads row_loads(const SplitArgs& a, long tile, int r, int tid) {
+__device__ __forceinline__ RowLoads row_loads(const SplitArgs& a, long tile, int r, int tid, long b0, long b1) {
     RowLoads l;
     const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
     const unsigned row = row0 + r;
-    const bool live = row >= a.b0 && row < a.b1;
+    const bool live = row >= b0 && row < b1;
 #pragma unroll
     for (int c = 0; c < kInd; ++c)
         l.st[c] = (live && c < a.Cc) ? __ldg(a.steps + static_cast<size_t>(c + 1) * a.R + row) : 0xFFFF;
@@ -144,10 +166,10 @@ __device__ __forceinline__ RowLoads row_loads(const SplitArgs& a, long tile, int
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // The same rows' lines pulled into L2 (no registers held).
-__device__ __forceinline__ void row_prefetch(const SplitArgs& a, long tile, int r, int tid) {
+__device__ __forceinline__ void row_prefetch(const SplitArgs& a, long tile, int r, int tid, long b1) {
     const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
     const unsigned row = row0 + r;
-    if (row < a.b1) {
+    if (row < b1) {
         if ((r & 31) == 0) {  // one lane per 32 rows: 64 B of steps per name, 256 B of labels
 #pragma unroll
             for (int c = 0; c < kInd; ++c)
@@ -160,13 +182,14 @@ __device__ __forceinline__ void row_prefetch(const SplitArgs& a, long tile, int 
     if (tid < np * a.q && tid % 32 == 0) prefetch_l2(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q);
 }
 
-__device__ __forceinline__ RowState row_state(const SplitArgs& a, long tile, int r, const RowLoads& l) {
+__device__ __forceinline__ RowState row_state(const SplitArgs& a, long tile, int r, const RowLoads& l, long b0,
+                                              long b1) {
     RowState s;
     const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
     s.kfirst = row0 / N;
     s.np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - s.kfirst + 1);
     const unsigned row = row0 + r;
-    s.live = row >= a.b0 && row < a.b1;
+    s.live = row >= b0 && row < b1;
     s.p = s.live ? static_cast<int>(row / N - s.kfirst) : 0;
     s.ind = 0;
 #pragma unroll
@@ -223,26 +246,34 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             xG[k] = bG + k * 128u + ((cr ^ k) << 4);
         }
     }
+    // Persistent mode (a.fuse): a.nsteps SGD steps over consecutive batches of a.bs
+    // rows from a.b0, the optimizer fused behind two grid barriers per step.
+    const int nsteps = a.fuse ? a.nsteps : 1;
     // the first tile's row loads do not depend on the optimizer: before the dependency wait
-    const RowLoads l0 = (!issuer && t_first + blockIdx.x < t_first + n_tiles) ? row_loads(a, t_first + blockIdx.x, r, tid)
-                                                                            : RowLoads{};
+    const long b1_0 = a.fuse ? a.b0 + a.bs : a.b1;
+    const RowLoads l0pre = (!issuer && blockIdx.x < n_tiles) ? row_loads(a, t_first + blockIdx.x, r, tid, a.b0, b1_0)
+                                                             : RowLoads{};
     cta_sync();
     const uint32_t tm = *tbase;
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     pdl_wait();  // the optimizer's parameters and weight image
+    const uint32_t id128 = tc::idesc_tf32(128, kU, 0, 0);
+    uint32_t ph[4] = {0, 0, 0, 0}, rph[4] = {0, 0, 0, 0};
+    unsigned gsyncs = 0;
+    for (int step = 0; step < nsteps; ++step) {
+    const long sb0 = a.fuse ? a.b0 + step * a.bs : a.b0, sb1 = a.fuse ? sb0 + a.bs : a.b1;
+    const long tf = sb0 / 128, t_end = (sb1 - 1) / 128 + 1;
     if (tid == 0) {
+        if (step > 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // the image the optimizer wrote
         tc::mbar_expect_tx(&bar[4], 4 * kW1);
         tc::bulk_g2s(w1, a.w1img, 4 * kW1, &bar[4]);
     }
-    const uint32_t id128 = tc::idesc_tf32(128, kU, 0, 0);
-    const long t_end = t_first + n_tiles;
     double loss = 0.0, dmu = 0.0;
     float gb2 = 0.0f, acc_w2 = 0.0f, acc_b1 = 0.0f;
     int nt = 0;
 
     if (issuer) {
         // ================= MMA issue (one lane), paced by the epilogue warps' ready barriers
-        uint32_t rph[4] = {0, 0, 0, 0};
         auto wait_ready = [&](int k) {
             tc::mbar_wait(&bar[5 + k], rph[k]);
             rph[k] ^= 1;
@@ -254,8 +285,8 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             tc::mma_tf32_ts(tm + kTD, tm + kTInd, B.desc(1, 0), id128, 1);
             tc::commit(&bar[0]);
         };
-        tc::mbar_wait(&bar[4], 0);  // W1 / W1^T in shared memory
-        long t = t_first + blockIdx.x;
+        tc::mbar_wait(&bar[4], step & 1);  // W1 / W1^T in shared memory
+        long t = tf + blockIdx.x;
         if (t < t_end) {
             wait_ready(0);
             if (lane == 0) issue_d0();
@@ -300,14 +331,13 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         // ================= epilogue warps: 128 rows x 4 column groups of 16
         for (int i = tid; i < kInd * kU; i += kSgdThreads) {
             const int o = i / kInd, c = i % kInd;
-            tc::put_split(w0b, kW0i, o, c, kU, c < a.Cc ? a.p32[a.off0 + o * a.d + c] : 0.0f);
+            tc::put_split(w0b, kW0i, o, c, kU, c < a.Cc ? __ldcg(a.p32 + a.off0 + o * a.d + c) : 0.0f);
         }
-        const float b2 = __ldg(a.vec + 192);
-        const double mu = a.mu64[0], two_nb = 2.0 / a.nb;
-        if (tid < 2 * kU) vsh[tid] = __ldg(a.vec + 64 + tid);  // b1 | w2
+        const float b2 = __ldcg(a.vec + 192);
+        const double mu = __ldcg(a.mu64), two_nb = 2.0 / a.nb;
+        if (tid < 2 * kU) vsh[tid] = __ldcg(a.vec + 64 + tid);  // b1 | w2
         const float* b1v = vsh + cb;
         const float* w2v = vsh + kU + cb;
-        uint32_t ph[4] = {0, 0, 0, 0};
         auto epi_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kSgdThreads) : "memory"); };
         auto wait_done = [&](int b) {
             tc::mbar_wait(&bar[b], ph[b]);
@@ -334,10 +364,11 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             path_projection8(a, ysh, Psh + buf * kPaths * kU, st.np, tid, kSgdThreads);
         };
         int buf = 0;
-        long tile = t_first + blockIdx.x;
+        long tile = tf + blockIdx.x;
         RowState cur{};
         if (tile < t_end) {
-            cur = row_state(a, tile, r, l0);
+            const RowLoads l0 = step == 0 ? l0pre : row_loads(a, tile, r, tid, sb0, sb1);
+            cur = row_state(a, tile, r, l0, sb0, sb1);
             stage_tile(cur, l0.yv, 0);
             ready(0);
         }
@@ -370,7 +401,7 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             }
             ready(1);
             TRACE(2);
-            if (more) row_prefetch(a, tile + gridDim.x, r, tid);  // to L2 under F1; loaded after B
+            if (more) row_prefetch(a, tile + gridDim.x, r, tid, sb1);  // to L2 under F1; loaded after B
             TRACE(3);
             TRACE(4);
             wait_done(1);
@@ -442,8 +473,8 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             }
             RowState nxt{};
             if (more) {  // the next tile's layer-0 inputs, under gW1
-                const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid);
-                nxt = row_state(a, tile + gridDim.x, r, ln);
+                const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid, sb0, sb1);
+                nxt = row_state(a, tile + gridDim.x, r, ln, sb0, sb1);
                 stage_tile(nxt, ln.yv, buf ^ 1);
             }
             TRACE(8);
@@ -528,13 +559,13 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     int* snp = reinterpret_cast<int*>(red + 48);                          // [kSlots] paths per slot
     float* yh = reinterpret_cast<float*>(tH + 128 * (kU + 1) * 4 + 64);  // [slot][kPaths][kQ]
     if (tid < nt) {
-        const unsigned row0 = static_cast<unsigned>((t_first + blockIdx.x + static_cast<long>(tid) * gridDim.x) * 128);
+        const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(tid) * gridDim.x) * 128);
         const unsigned N = static_cast<unsigned>(a.N);
         snp[tid] = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - row0 / N + 1);
     }
     for (int i = tid; i < nt * kPaths * kQ; i += kSgdThreads + 32) {
         const int s = i / (kPaths * kQ), p = (i / kQ) % kPaths, j = i % kQ;
-        const unsigned row0 = static_cast<unsigned>((t_first + blockIdx.x + static_cast<long>(s) * gridDim.x) * 128);
+        const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(s) * gridDim.x) * 128);
         const unsigned kf = row0 / static_cast<unsigned>(a.N);
         const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
         yh[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
@@ -588,6 +619,55 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         }
     }
     TRACE_FIX(6);
+    if (a.fuse) {
+        // ---- the optimizer, fused: every CTA's partial row is written; CTA c reduces
+        // parameters [c per, (c+1) per) over the rows in fixed order, updates them
+        // (regressor.cpp:236-261) and refreshes the weight image; then every CTA
+        // reloads the weights for the next step
+        __threadfence();
+        grid_sync(a.gbar, ++gsyncs * gridDim.x);
+        TRACE_FIX(13);
+        const int P = a.P, G = gridDim.x;
+        const int per = (P + G - 1) / G, i0 = blockIdx.x * per, i1 = min(P, i0 + per);
+        const double c1 = __ldcg(a.c12 + 2 * step), c2 = __ldcg(a.c12 + 2 * step + 1);
+        ImgArgs im;
+        im.img = a.img;
+        im.U = kU;
+        im.d = a.d;
+        im.dp = a.dp;
+        im.off0 = a.off0;
+        im.off1 = a.off1;
+        im.off2 = a.off2;
+        // rows split over the 16 epilogue warps (lanes = consecutive parameters: coalesced),
+        // the 16 warp sums combined in warp order in shared memory
+        double* part = reinterpret_cast<double*>(tG);  // [16][per]
+        if (warp < 16) {
+            for (int j = lane; j < per; j += 32) {
+                double g = 0.0;
+                if (i0 + j < i1)
+                    for (int c = warp; c < G; c += 16) g += static_cast<double>(__ldcg(a.gpart + static_cast<size_t>(c) * P + i0 + j));
+                part[warp * per + j] = g;
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < i1 - i0; j += kSgdThreads + 32) {
+            double g = 0.0;
+            for (int w = 0; w < 16; ++w) g += part[w * per + j];
+            optimizer_step(i0 + j, g, P, a.p64w, a.p32w, a.m, a.v, c1, c2, a.lr, a.adam, im);
+        }
+        if (blockIdx.x == 0 && warp == 0) {  // the batch loss must stay finite (regressor.cpp:291-293)
+            double l = 0.0;
+            for (int c = lane; c < G; c += 32) l += __ldcg(a.lpart + c);
+            l = warp_sum(l);
+            if (lane == 0 && !isfinite(l / a.nb)) atomicExch(a.nonfinite, 1);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        TRACE_FIX(14);
+        grid_sync(a.gbar, ++gsyncs * gridDim.x);
+        TRACE_FIX(15);
+    }
+    }  // step
     tc::fence_before_sync();
     __syncthreads();
     TRACE_FIX(7);
@@ -852,6 +932,29 @@ void launch_sgd_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cu
 }
 
 template <int ACT>
+bool launch_sgd_fused_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
+    const size_t smem = sgd_split_smem();
+    HCVA_CUDA(cudaFuncSetAttribute(k_sgd_split<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, dev = 0, sms = 0;
+    HCVA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sgd_split<ACT>, kSgdThreads + 32, smem));
+    HCVA_CUDA(cudaGetDevice(&dev));
+    HCVA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm < 1 || ctas > per_sm * sms) return false;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kSgdThreads + 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HCVA_CUDA(cudaLaunchKernelEx(&cfg, k_sgd_split<ACT>, a, t_first, n_tiles));
+    return true;
+}
+
+template <int ACT>
 void launch_eval_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, cudaStream_t s) {
     const size_t smem = eval_split_smem();
     HCVA_CUDA(cudaFuncSetAttribute(k_eval_split<ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -889,6 +992,20 @@ int launch_sgd_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
         default: launch_sgd_act<3>(a, t_first, n_tiles, ctas, s); break;
     }
     return ctas;
+}
+
+bool launch_sgd_split_fused(const SplitArgs& a, int sm_count, cudaStream_t s) {
+    if (!a.fuse || a.nsteps < 1 || a.bs < 1 || a.bs % 128 || a.b0 % 128) return false;
+    const long t_first = a.b0 / 128, n_tiles = a.bs / 128;  // tiles of each step's batch
+    const long per = (n_tiles + sm_count - 1) / sm_count;
+    if (per > kSlots) return false;
+    const int ctas = static_cast<int>((n_tiles + per - 1) / per);
+    switch (a.act) {
+        case 0: return launch_sgd_fused_act<0>(a, t_first, n_tiles, ctas, s);
+        case 1: return launch_sgd_fused_act<1>(a, t_first, n_tiles, ctas, s);
+        case 2: return launch_sgd_fused_act<2>(a, t_first, n_tiles, ctas, s);
+        default: return launch_sgd_fused_act<3>(a, t_first, n_tiles, ctas, s);
+    }
 }
 
 int launch_eval_split(const SplitArgs& a_in, int sm_count, cudaStream_t s) {

@@ -67,7 +67,21 @@ struct SplitArgs {
     long long* trace;          // profiling: phase clocks of CTA 0 (HCVA_SPLIT_TRACE), or null
     const float* Pg;           // evaluation: layer-0 path parts [M][64] (k_path_proj)
     float* Pg_out;             // evaluation: where the launcher writes them
+    // Persistent SGD (fuse != 0): nsteps steps over consecutive batches of bs rows
+    // from b0, the optimizer fused behind grid barriers (cooperative launch).
+    int fuse, nsteps;
+    long bs;
+    double lr;
+    int adam, dp;
+    double *p64w, *m, *v;      // FP64 master parameters, Adam moments
+    float* p32w;               // FP32 parameters (the same buffer as p32)
+    uint8_t* img;              // weight image (W1, W1^T planes and vectors refreshed in place)
+    unsigned* gbar;            // grid-barrier counter (zeroed before the launch)
+    int* nonfinite;
+    const double* c12;         // [nsteps][2] Adam bias corrections 1 - beta^t (host libm pow)
 };
+// Persistent SGD over a.nsteps batches; false if the grid would not be co-resident.
+bool launch_sgd_split_fused(const SplitArgs& a, int sm_count, cudaStream_t s);
 // Shapes served by the split kernels: U = 64, two hidden layers, Cc <= 8,
 // q <= 48; the SGD kernel also needs N >= 16 replicas per path (<= 9 paths
 // per 128-row tile), the evaluation kernel any N.

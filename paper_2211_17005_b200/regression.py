@@ -75,11 +75,12 @@ def sim_quadratic_loss(sim: SimulationSet, t: TrainConfig, step: int, params: np
 
 def sgd_timing(sim: SimulationSet, t: TrainConfig, step: int, steps: int = 50, label_kind: str = "defaults"):
     """Mean ms of [SGD step, gradient kernels, optimizer] and whether the split kernels ran (hcva_diag_sgd_timing)."""
-    out = np.zeros(4)
+    out = np.zeros(5)
     kind = {"defaults": 0, "intensity": 1}[label_kind]
     _lib.check(_lib.lib().hcva_diag_sgd_timing(sim.handle, C.byref(train_cfg(t)), int(step), kind, int(steps),
                                                out.ctypes.data_as(_lib.dptr)))
-    return dict(step_ms=out[0], gradient_ms=out[1], optimizer_ms=out[2], split=bool(out[3]))
+    return dict(step_ms=out[0], gradient_ms=out[1], optimizer_ms=out[2], split=bool(out[3]),
+                fused_step_ms=out[4] if out[4] > 0 else None)
 
 
 def forward(t: TrainConfig, params: np.ndarray, x: np.ndarray, ctx: Optional[Context] = None) -> np.ndarray:
