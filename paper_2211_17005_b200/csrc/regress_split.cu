@@ -352,16 +352,48 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&bar[5 + k])) : "memory");
         };
         // layer-0 inputs of a tile: its paths' y, P into Psh[buf], the indicator A operand
+        // N >= 128 (a tile holds at most 2 paths): the layer-0 path parts of every
+        // tile of this CTA's step at once, Psh [2 * tile + p][64], W0_y rows loaded once
+        const bool pre = a.N >= 128;
+        if (pre) {
+            const int ntl = static_cast<int>((t_end - (tf + blockIdx.x) + gridDim.x - 1) / gridDim.x);
+            float* ys2 = Psh + 2 * kSlots * kU;  // [2 * tile + p][kQ]
+            for (int i = tid; i < ntl * 2 * kQ; i += kSgdThreads) {
+                const int k = i / (2 * kQ), p = (i / kQ) % 2, j = i % kQ;
+                const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(k) * gridDim.x) * 128);
+                const unsigned kf = row0 / static_cast<unsigned>(a.N);
+                const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
+                ys2[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
+            }
+            const int o = tid >> 3, sub = tid & 7;
+            float w[kQ / 8];
+#pragma unroll
+            for (int m = 0; m < kQ / 8; ++m)
+                w[m] = sub + 8 * m < a.q ? __ldcg(a.p32 + a.off0 + o * a.d + a.Cc + sub + 8 * m) : 0.0f;
+            const float b0o = __ldcg(a.vec + o);
+            epi_sync();
+            for (int qi = 0; qi < 2 * ntl; ++qi) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int m = 0; m < kQ / 8; ++m) acc = fmaf(w[m], ys2[qi * kQ + sub + 8 * m], acc);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                if (sub == 0) Psh[qi * kU + o] = b0o + acc;
+            }
+        }
         auto stage_tile = [&](const RowState& st, float yv, int buf) {
-            if (tid < st.np * a.q) ysh[(tid / a.q) * kQ + tid % a.q] = yv;
+            if (!pre && tid < st.np * a.q) ysh[(tid / a.q) * kQ + tid % a.q] = yv;
             if (hf == 0) {
                 float iv[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) iv[c] = ((st.ind >> c) & 1u) ? 1.0f : 0.0f;
                 tc::tmem_st8(tm + lb + kTInd, iv);
             }
-            epi_sync();
-            path_projection8(a, ysh, Psh + buf * kPaths * kU, st.np, tid, kSgdThreads);
+            if (!pre) {
+                epi_sync();
+                path_projection8(a, ysh, Psh + buf * kPaths * kU, st.np, tid, kSgdThreads);
+            }
         };
         int buf = 0;
         long tile = tf + blockIdx.x;
@@ -384,7 +416,7 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             {
                 float dh[16];
                 float z[16], hi[16], lo[16];
-                const float* P = Psh + buf * kPaths * kU + cur.p * kU + cb;
+                const float* P = (pre ? Psh + (2 * nt + cur.p) * kU : Psh + buf * kPaths * kU + cur.p * kU) + cb;
                 tc::tmem_ld16(tm + lb + kTD + cb, z);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
@@ -460,6 +492,12 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 acc_b1 += bfly_sum<16>(gv, lane);  // gb1: column sums of G2
             }
             ready(2);
+            RowState nxt{};
+            if (more) {  // the next tile's layer-0 inputs, under the B GEMM and gW1
+                const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid, sb0, sb1);
+                nxt = row_state(a, tile + gridDim.x, r, ln, sb0, sb1);
+                stage_tile(nxt, ln.yv, buf ^ 1);
+            }
             TRACE(6);
             wait_done(2);
             TRACE(7);
@@ -470,12 +508,6 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
 #pragma unroll
                 for (int q = 0; q < 16; ++q) g1[q] *= dh[q];
                 tc::tmem_st16(tm + lb + kTDh + cb, g1);
-            }
-            RowState nxt{};
-            if (more) {  // the next tile's layer-0 inputs, under gW1
-                const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid, sb0, sb1);
-                nxt = row_state(a, tile + gridDim.x, r, ln, sb0, sb1);
-                stage_tile(nxt, ln.yv, buf ^ 1);
             }
             TRACE(8);
             wait_done(3);
@@ -964,6 +996,7 @@ void launch_eval_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, c
 }  // namespace
 
 static_assert(sgd_split_smem() <= 227 * 1024, "split SGD kernel exceeds shared memory");
+static_assert(2 * kSlots * kU + 2 * kSlots * kQ <= 2 * kPaths * kU, "per-step path parts exceed Psh");
 static_assert(2ull * kH >= 128ull * (kU + 1) * 4 + 64 + 4ull * kSlots * kPaths * kQ &&
                   kG >= 128ull * (kInd + kQ + 2) * 4,
               "readout scratch exceeds the operand tiles");

@@ -23,3 +23,5 @@ t0 = time.perf_counter()
 m = rg.backward_learn(sim, cfg.training, "defaults")
 m.get(1)
 print(json.dumps({"pricing_steps": steps, "backward_learn_s": time.perf_counter() - t0}))
+p, mean, scale, rep = m.get(1)
+print(json.dumps({"best_loss_step1": rep["best_loss"], "fused_env": os.environ.get("HCVA_FUSED_EPOCH")}))
