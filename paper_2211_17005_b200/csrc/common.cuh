@@ -9,9 +9,20 @@
 #include <vector>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hcva_gpu.h"
 
 namespace hcva {
+
+// NVTX range over an engine phase (header-only NVTX3: a no-op unless a tool
+// such as Nsight Systems is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Exception types mirroring proj/include/hiercva/errors.hpp:9-25; the C ABI
 // converts them to hcva_status codes.

@@ -139,6 +139,7 @@ extern "C" hcva_status hcva_nested_cva_range(hcva_ctx* ctx, const hcva_model* mo
                                              const int* survived, int n_states, int first_state, int step,
                                              int inner, uint64_t parent_key, double* value, double* std_error) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_nested_cva");
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
         if (inner < 1) throw contract_error("nested_cva: inner_count must be >= 1");
@@ -224,6 +225,7 @@ extern "C" hcva_status hcva_nested_cva_batch(hcva_ctx* ctx, const hcva_model* mo
 extern "C" hcva_status hcva_twin_labels(hcva_sim* outer, const hcva_swap* book, int n_swaps, int step, uint64_t key,
                                         double* twin1, double* twin2) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_twin_labels");
         hcva_ctx* ctx = outer->ctx;
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));

@@ -1682,7 +1682,9 @@ static hcva_status hcva_backward_learn_ex(hcva_sim* sim, const hcva_train_cfg* c
                 row[3] = qr[1];
             };
         }
+        NvtxRange nvtx_all("hcva_backward_learn");
         for (int i = nsteps; i >= 1; --i) {
+            NvtxRange nvtx_step("train_base (pricing step)");
             FeatArgs fa = feat_args(sim, i);
             double* mean = models->mean.as<double>() + static_cast<size_t>(i - 1) * d;
             double* scale = models->scale.as<double>() + static_cast<size_t>(i - 1) * d;
@@ -1769,6 +1771,7 @@ hcva_status hcva_models_get(const hcva_models* m, int step, double* params, doub
 // features at `step` (e.g. the validation set, pipeline.cpp:138-156).
 hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* out) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_predict");
         hcva_ctx* ctx = sim->ctx;
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));
@@ -1797,6 +1800,7 @@ hcva_status hcva_predict(const hcva_models* m, hcva_sim* sim, int step, double* 
 // mean, p1, p2.5, p97.5, p99 (percentile_sorted's linear interpolation).
 hcva_status hcva_percentile_table(const hcva_models* m, hcva_sim* sim, double* out) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_percentile_table");
         hcva_ctx* ctx = sim->ctx;
         StreamScope sc__(ctx->stream);
         HCVA_CUDA(cudaSetDevice(ctx->device));

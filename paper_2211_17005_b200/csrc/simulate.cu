@@ -1551,6 +1551,7 @@ hcva_status hcva_simulate_set_sharded(hcva_ctx* ctx, const hcva_model* model, co
                                       int shard_blk, int shard_stride, int n_replicas, uint64_t key_market,
                                       uint64_t key_defaults, hcva_sim** out) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_simulate_set");
         StreamScope sc__(ctx->stream);
         if (!grid) throw contract_error("simulate_set: null grid");
         if (n_paths < 1) throw contract_error("simulate_market: n_paths must be >= 1");
@@ -1585,6 +1586,7 @@ hcva_status hcva_simulate_set_sharded(hcva_ctx* ctx, const hcva_model* model, co
 hcva_status hcva_sim_rerun(hcva_sim* sim, uint64_t key_market, uint64_t key_defaults, int labels_kind,
                            int event_slot) {
     return guarded([&] {
+        NvtxRange nvtx__("hcva_sim_rerun");
         StreamScope sc__(sim->ctx->stream);
         if (sim->start_step != 0 || sim->n_groups != 1) throw contract_error("rerun: outer blocks only");
         if (!sim->m_coef.p) throw contract_error("rerun: the set was loaded, not simulated");
