@@ -982,7 +982,12 @@ bool launch_sgd_fused_act(const SplitArgs& a, long t_first, long n_tiles, int ct
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    HCVA_CUDA(cudaLaunchKernelEx(&cfg, k_sgd_split<ACT>, a, t_first, n_tiles));
+    const cudaError_t err = cudaLaunchKernelEx(&cfg, k_sgd_split<ACT>, a, t_first, n_tiles);
+    if (err == cudaErrorCooperativeLaunchTooLarge) {  // not co-resident here: per-step launches instead
+        (void)cudaGetLastError();
+        return false;
+    }
+    HCVA_CUDA(err);
     return true;
 }
 
