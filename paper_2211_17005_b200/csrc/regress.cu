@@ -1545,8 +1545,13 @@ hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int s
                 tr.sa.trace = nullptr;
                 long long hh[80];
                 copy_out(ctx, hh, tb.p, sizeof hh);
-                std::fprintf(stderr, "fused last step: tail->sync1 %lld, adam %lld, sync2 %lld\n", hh[77] - hh[70],
-                             hh[78] - hh[77], hh[79] - hh[78]);
+                std::fprintf(stderr, "fused last step (cycles): tiles %lld | final wait + readout %lld | partials %lld"
+                             " | sync1 %lld | adam %lld | sync2 %lld | step total %.0f\n",
+                             hh[67] - hh[66], hh[69] - hh[67], hh[70] - hh[69], hh[77] - hh[70], hh[78] - hh[77],
+                             hh[79] - hh[78], ms / nb * 1.965e6);
+                std::fprintf(stderr, "per-tile (last step):");
+                for (int t = 0; t < 4; ++t) std::fprintf(stderr, " %lld", hh[t * 16 + 10] - hh[t * 16]);
+                std::fprintf(stderr, "\n");
             }
         }
         HCVA_CUDA(cudaStreamSynchronize(ctx->stream));

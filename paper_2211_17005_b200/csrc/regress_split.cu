@@ -656,12 +656,20 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         // parameters [c per, (c+1) per) over the rows in fixed order, updates them
         // (regressor.cpp:236-261) and refreshes the weight image; then every CTA
         // reloads the weights for the next step
-        __threadfence();
-        grid_sync(a.gbar, ++gsyncs * gridDim.x);
-        TRACE_FIX(13);
         const int P = a.P, G = gridDim.x;
         const int per = (P + G - 1) / G, i0 = blockIdx.x * per, i1 = min(P, i0 + per);
         const double c1 = __ldcg(a.c12 + 2 * step), c2 = __ldcg(a.c12 + 2 * step + 1);
+        // this CTA's slice of the optimizer state: only this CTA updates it, so it is
+        // read before the barrier
+        double w_own = 0.0, m_own = 0.0, v_own = 0.0;
+        if (tid < i1 - i0) {
+            w_own = __ldcg(a.p64w + i0 + tid);
+            m_own = __ldcg(a.m + i0 + tid);
+            v_own = __ldcg(a.v + i0 + tid);
+        }
+        __threadfence();
+        grid_sync(a.gbar, ++gsyncs * gridDim.x);
+        TRACE_FIX(13);
         ImgArgs im;
         im.img = a.img;
         im.U = kU;
@@ -676,16 +684,32 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         if (warp < 16) {
             for (int j = lane; j < per; j += 32) {
                 double g = 0.0;
-                if (i0 + j < i1)
+                if (i0 + j < i1) {
+#pragma unroll 8
                     for (int c = warp; c < G; c += 16) g += static_cast<double>(__ldcg(a.gpart + static_cast<size_t>(c) * P + i0 + j));
+                }
                 part[warp * per + j] = g;
             }
         }
         __syncthreads();
-        for (int j = tid; j < i1 - i0; j += kSgdThreads + 32) {
+        if (tid < i1 - i0) {  // Adam / SGD (regressor.cpp:236-261) on the prefetched state
+            const int i = i0 + tid;
             double g = 0.0;
-            for (int w = 0; w < 16; ++w) g += part[w * per + j];
-            optimizer_step(i0 + j, g, P, a.p64w, a.p32w, a.m, a.v, c1, c2, a.lr, a.adam, im);
+            for (int w = 0; w < 16; ++w) g += part[w * per + tid];
+            double wv = w_own;
+            if (a.adam) {
+                const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+                const double mi = b1 * m_own + (1.0 - b1) * g;
+                const double vi = b2 * v_own + (1.0 - b2) * g * g;
+                a.m[i] = mi;
+                a.v[i] = vi;
+                wv -= a.lr * (mi / c1) / (sqrt(vi / c2) + eps);
+            } else {
+                wv -= a.lr * g;
+            }
+            a.p64w[i] = wv;
+            a.p32w[i] = static_cast<float>(wv);
+            img_store(im, P, i, static_cast<float>(wv));
         }
         if (blockIdx.x == 0 && warp == 0) {  // the batch loss must stay finite (regressor.cpp:291-293)
             double l = 0.0;
@@ -1038,6 +1062,10 @@ bool launch_sgd_split_fused(const SplitArgs& a, int sm_count, cudaStream_t s) {
     const long per = (n_tiles + sm_count - 1) / sm_count;
     if (per > kSlots) return false;
     const int ctas = static_cast<int>((n_tiles + per - 1) / per);
+    // the fused optimizer gives each thread of a CTA at most one parameter, and its
+    // 16 x per partial sums (FP64) live in the G^T | B operand tiles
+    const long pslice = (a.P + ctas - 1) / ctas;
+    if (pslice > kSgdThreads + 32 || 16 * 8 * pslice > static_cast<long>(kG + kB)) return false;
     switch (a.act) {
         case 0: return launch_sgd_fused_act<0>(a, t_first, n_tiles, ctas, s);
         case 1: return launch_sgd_fused_act<1>(a, t_first, n_tiles, ctas, s);
