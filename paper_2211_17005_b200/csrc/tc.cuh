@@ -118,13 +118,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// try_wait's suspend-time hint: a waiting warp is descheduled until the phase
+// completes (or this many ns pass) instead of spinning on issue slots.
+constexpr uint32_t kSuspendNs = 1000000;
+
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
@@ -132,9 +136,9 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n\t}\n" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
