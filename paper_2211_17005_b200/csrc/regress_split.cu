@@ -293,6 +293,15 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         }
         for (int n = 0; t < t_end; t += gridDim.x, ++n) {
             const bool more = t + gridDim.x < t_end;
+            if (more) {  // the next tile's rows (default steps, labels) into L2 while this tile runs
+                const unsigned row0 = static_cast<unsigned>((t + gridDim.x) * 128);
+                if (lane < kInd && lane < a.Cc) {  // 256 B of default steps per name: two lines
+                    const uint16_t* p = a.steps + static_cast<size_t>(lane + 1) * a.R + row0;
+                    prefetch_l2(p);
+                    prefetch_l2(p + 64);
+                }
+                if (lane >= 16 && lane < 24) prefetch_l2(a.y + row0 + 16 * (lane - 16));  // 1 KB of labels
+            }
             wait_ready(1);
             if (lane == 0) {  // ---- F1: D = H1 W1^T, H1 from tensor memory (also covers the last slot MMAs)
                 tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, id128, 0);
@@ -433,7 +442,6 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             }
             ready(1);
             TRACE(2);
-            if (more) row_prefetch(a, tile + gridDim.x, r, tid, sb1);  // to L2 under F1; loaded after B
             TRACE(3);
             TRACE(4);
             wait_done(1);
