@@ -139,3 +139,35 @@ def test_split_deterministic():
     b = rg.backward_learn(sim, t)
     for i in (1, 2):
         assert np.array_equal(a.get(i)[0], b.get(i)[0])
+
+
+def test_persistent_epoch_matches_per_step_launches():
+    """The persistent epoch kernel (optimizer fused behind grid barriers) and
+    per-step launches (k_sgd_split + k_adam, HCVA_FUSED_EPOCH=0) train the same
+    network: the two reduce the same FP32 partial rows in different fixed
+    orders in FP64, so they agree to rounding (and in practice bit for bit)."""
+    import os
+    import subprocess
+    import sys
+
+    script = (
+        "import json, sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
+        "import numpy as np, cases, paper_2211_17005_b200 as hcva;"
+        "from paper_2211_17005_b200 import regression as rg;"
+        "j = cases.case('c2'); j['grid']['pricing_steps'] = 2; cfg = hcva.parse_config(json.dumps(j));"
+        "t = cfg.training; t.epochs, t.n_batches = 4, 8;"
+        "sim = hcva.simulate_set(cfg, hcva.generate_book(cfg), 256, 128, hcva.RandomStream(cfg.seed).split(1));"
+        "m = rg.backward_learn(sim, t);"
+        "print(json.dumps([list(m.get(i)[0]) for i in (1, 2)] + [rg.sgd_timing(sim, t, 2, steps=2)['fused_step_ms']]))"
+    )
+    out = {}
+    for f in ("1", "0"):
+        env = dict(os.environ, HCVA_FUSED_EPOCH=f)
+        r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, env=env, timeout=600,
+                           cwd=oracle_api.ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[f] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["1"][2] is not None and out["0"][2] is None  # the fused kernel ran only when enabled
+    for i in range(2):
+        a, b = np.array(out["1"][i]), np.array(out["0"][i])
+        assert np.allclose(a, b, rtol=1e-9, atol=1e-12), np.max(np.abs(a - b))
