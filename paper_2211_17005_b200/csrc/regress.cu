@@ -488,18 +488,27 @@ __global__ void k_gram(NetDims n, const float* X, const double* y, long R, const
 
 // out[idx] = sum over c of parts[c * stride + idx], four interleaved chains
 // combined pairwise (fixed order).
+// out[i] = sum over the n partial rows of parts[.][i] in a fixed order: block
+// (32, 16), x = entry, y = group g summing rows g, g + 16, ... with four chains,
+// then the 16 group sums in a fixed pairwise tree.
 __global__ void k_sum_parts(const double* parts, int n, int stride, double* out) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= stride) return;
+    constexpr int G = 16;
+    __shared__ double part[G][33];
+    const int x = threadIdx.x, grp = threadIdx.y;
+    const int idx = blockIdx.x * 32 + x;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
-    int c = 0;
-    for (; c + 4 <= n; c += 4)
+    if (idx < stride) {
+        int c = grp, k = 0;
+        for (; c < n; c += G, k = (k + 1) & 3) a[k] += parts[static_cast<size_t>(c) * stride + idx];
+    }
+    part[grp][x] = (a[0] + a[1]) + (a[2] + a[3]);
+    __syncthreads();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] += parts[static_cast<size_t>(c + k) * stride + idx];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (c + k < n) a[k] += parts[static_cast<size_t>(c + k) * stride + idx];
-    out[idx] = (a[0] + a[1]) + (a[2] + a[3]);
+    for (int h = G / 2; h >= 1; h >>= 1) {
+        if (grp < h) part[grp][x] += part[grp + h][x];
+        __syncthreads();
+    }
+    if (grp == 0 && idx < stride) out[idx] = part[0][x];
 }
 
 // One CTA: reduce the Gram partials (fixed order), ridge lam = max(ridge tr/(u+1), 1e-300),
@@ -967,7 +976,7 @@ struct Trainer {
         if (nct > 8 || comm) {  // pre-reduce the partials across the GPU, k_refit then reads one
             const int stride = mm * (mm + 1) / 2 + mm;
             if (gram_sum.bytes < static_cast<size_t>(stride) * 8) gram_sum.alloc(static_cast<size_t>(stride) * 8);
-            k_sum_parts<<<(stride + 127) / 128, 128, 0, ctx->stream>>>(gram.as<double>(), nct, stride,
+            k_sum_parts<<<(stride + 31) / 32, dim3(32, 16), 0, ctx->stream>>>(gram.as<double>(), nct, stride,
                                                                          gram_sum.as<double>());
             check_launch(ctx);
             gsrc = gram_sum.as<double>();
