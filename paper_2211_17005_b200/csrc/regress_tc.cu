@@ -1390,6 +1390,84 @@ void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
     k_wgrad_tc<U, 64><<<ctas, kWgThreads, wgrad_smem(64), s>>>(a);
 }
 
+// Refit Gram for U = 64 on the FP64 tensor cores (mma.sync m8n8k4 .f64, FP64
+// accumulation): z = [h2, 1, y - mu, 0...] (72 columns, 9 blocks of 8); the
+// 45 upper block pairs (bi <= bj) of z^T z are split over 8 warps, each warp
+// walking the CTA's 64-row chunks in 4-row K steps (fixed order: chunk, then
+// K step), one partial per CTA in k_gram_h2's packed layout.
+constexpr int kGdRows = 64, kGdLD = 76;  // chunk rows, padded row (doubles)
+__global__ void __launch_bounds__(256) k_gram_dmma(const float* __restrict__ H2, const double* __restrict__ y,
+                                                    long R, const float* __restrict__ params, int P,
+                                                    double* __restrict__ gpart) {
+    constexpr int U = 64, NBK = 9, pairs = 45, PW = 6;  // pairs per warp (8 warps x 6 >= 45)
+    __shared__ __align__(16) double zs[kGdRows * kGdLD];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    int pbi[PW], pbj[PW];
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {  // pair index warp + 8 q -> (bi, bj), bi <= bj
+        int pt = warp + 8 * q, bi = 0;
+        if (pt >= pairs) pt = pairs - 1;  // duplicate, discarded at the end
+        while (pt >= NBK - bi) {
+            pt -= NBK - bi;
+            ++bi;
+        }
+        pbi[q] = bi;
+        pbj[q] = bi + pt;
+    }
+    const double mu = static_cast<double>(params[P - 1]);
+    double acc[PW][2];
+#pragma unroll
+    for (int q = 0; q < PW; ++q) acc[q][0] = acc[q][1] = 0.0;
+    const int fr = lane & 3, fc = lane >> 2;  // fragment: row (K) and column (M / N) of this lane
+    const long nch = (R + kGdRows - 1) / kGdRows;
+    for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const long base = ch * kGdRows;
+        const int rows = static_cast<int>(min(static_cast<long>(kGdRows), R - base));
+        __syncthreads();
+        for (int i = t; i < kGdRows * (U / 4); i += 256) {
+            const int r = i / (U / 4), c4 = (i % (U / 4)) * 4;
+            float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (r < rows) v = __ldg(reinterpret_cast<const float4*>(H2 + (base + r) * U + c4));
+            double* z = zs + r * kGdLD + c4;
+            z[0] = v.x;
+            z[1] = v.y;
+            z[2] = v.z;
+            z[3] = v.w;
+        }
+        for (int r = t; r < kGdRows; r += 256) {
+            double* z = zs + r * kGdLD;
+            const bool in = r < rows;
+            z[U] = in ? 1.0 : 0.0;
+            z[U + 1] = in ? y[base + r] - mu : 0.0;
+            for (int c = U + 2; c < 72; ++c) z[c] = 0.0;
+        }
+        __syncthreads();
+        for (int k0 = 0; k0 < kGdRows; k0 += 4) {
+            const double* zr = zs + (k0 + fr) * kGdLD + fc;
+#pragma unroll
+            for (int q = 0; q < PW; ++q) {
+                const double a = zr[8 * pbi[q]], b = zr[8 * pbj[q]];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc[q][0]), "+d"(acc[q][1])
+                             : "d"(a), "d"(b));
+            }
+        }
+    }
+    // Packed output: (a, b) a <= b < m = U+1 -> upper-triangle index; rhs c = (c, U+1).
+    constexpr int m = U + 1, tri = m * (m + 1) / 2;
+    double* out = gpart + static_cast<size_t>(blockIdx.x) * (tri + m);
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {
+        if (warp + 8 * q >= pairs) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int ra = 8 * pbi[q] + fc, cb = 8 * pbj[q] + 2 * fr + e;  // D[row = lane/4][col = 2 (lane%4) + e]
+            if (ra < m && cb < m && ra <= cb) out[ra * m - ra * (ra - 1) / 2 + (cb - ra)] = acc[q][e];
+            else if (ra < m && cb == m) out[tri + ra] = acc[q][e];
+        }
+    }
+}
+
 template <int U>
 int launch_gram_u(const float* H2, const double* y, long R, const float* params, int P, double* gpart, int ctas,
                   cudaStream_t s) {
@@ -1403,6 +1481,14 @@ int launch_gram_h2(int u, const float* H2, const double* y, long R, const float*
     const int ctas = static_cast<int>(std::max<long>(1, std::min<long>({chunks, 4L * sm_count, max_parts})));
     if (u == 16) return launch_gram_u<16>(H2, y, R, params, P, gpart, ctas, s);
     if (u == 32) return launch_gram_u<32>(H2, y, R, params, P, gpart, ctas, s);
+    static const bool dmma = [] {
+        const char* e = std::getenv("HCVA_GRAM_DMMA");
+        return !(e && e[0] == '0');
+    }();
+    if (dmma) {
+        k_gram_dmma<<<ctas, 256, 0, s>>>(H2, y, R, params, P, gpart);
+        return ctas;
+    }
     return launch_gram_u<64>(H2, y, R, params, P, gpart, ctas, s);
 }
 

@@ -1,7 +1,7 @@
 """Regression parity at the production shape of the paper case (C2): U = 64
 hidden units, two hidden layers, d = 2*Cc + 3E - 1 = 45 inputs (dp = 48), so
 the two-CTA tensor-core kernels run -- k_sgd_tc<64> + k_wgrad_tc<64,64> for
-gradients, k_eval_tc<64> for evaluations and predictions, k_gram_h2<64> +
+gradients, k_eval_tc<64> for evaluations and predictions, k_gram_dmma +
 k_refit for the refit -- on batches of more than 2 x 148 x 2 tiles of 128
 rows, so every CTA of the persistent grid walks several tiles (double-buffered
 feature prefetch, mbarrier phases across tiles) and the last tile is partial.
@@ -89,7 +89,7 @@ def test_predictions_per_path_c2_shape(act):
 
 
 def test_refit_output_layer_c2_shape():
-    """k_gram_h2<64> + k_refit (regressor.cpp:191-213) against the FP64 refit."""
+    """k_gram_dmma + k_refit (regressor.cpp:191-213) against the FP64 refit."""
     R = oracle_api.restatement()
     x, y = c2_like(ROWS, seed=3)
     p = R.init_network(D, H, U, R.key(7, 0xBEEF, 10))
