@@ -1503,8 +1503,8 @@ hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int s
         tr.phase_ev = nullptr;
         if (tr.split && std::getenv("HCVA_SPLIT_TRACE")) {  // profiling: phase clocks of one more step
             DeviceBuf tb;
-            tb.alloc(80 * 8);
-            HCVA_CUDA(cudaMemsetAsync(tb.p, 0, 80 * 8, ctx->stream));
+            tb.alloc(96 * 8);
+            HCVA_CUDA(cudaMemsetAsync(tb.p, 0, 96 * 8, ctx->stream));
             tr.sa.trace = tb.as<long long>();
             run(3 + steps);
             tr.sa.trace = nullptr;
@@ -1547,13 +1547,16 @@ hcva_status hcva_diag_sgd_timing(hcva_sim* sim, const hcva_train_cfg* cfg, int s
             if (ran) out[4] = ms / nb;
             if (ran && std::getenv("HCVA_SPLIT_TRACE")) {
                 DeviceBuf tb;
-                tb.alloc(80 * 8);
-                HCVA_CUDA(cudaMemsetAsync(tb.p, 0, 80 * 8, ctx->stream));
+                tb.alloc(96 * 8);
+                HCVA_CUDA(cudaMemsetAsync(tb.p, 0, 96 * 8, ctx->stream));
                 tr.sa.trace = tb.as<long long>();
                 tr.sgd_epoch(y, bs, nb, 0, tr.c12.as<double>(), cfg->learning_rate, cfg->adam);
                 tr.sa.trace = nullptr;
-                long long hh[80];
+                long long hh[96];
                 copy_out(ctx, hh, tb.p, sizeof hh);
+                std::fprintf(stderr, "fused last step start (cycles): weights+P %lld | first tile staged %lld | to tile 0 %lld"
+                             " | adam: gather %lld, sums %lld\n",
+                             hh[81] - hh[80], hh[65] - hh[81], hh[0] - hh[65], hh[82] - hh[77], hh[83] - hh[82]);
                 std::fprintf(stderr, "fused last step (cycles): tiles %lld | final wait + readout %lld | partials %lld"
                              " | sync1 %lld | adam %lld | sync2 %lld | step total %.0f\n",
                              hh[67] - hh[66], hh[69] - hh[67], hh[70] - hh[69], hh[77] - hh[70], hh[78] - hh[77],

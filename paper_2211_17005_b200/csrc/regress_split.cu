@@ -119,20 +119,23 @@ struct RowState {
 };
 
 // Grid-wide barrier of the persistent SGD kernel (cooperative launch: every
-// CTA is resident).  `count` is zeroed before the launch; barrier k of the
-// launch waits for (k + 1) * gridDim.x arrivals.  A CTA that is never joined
-// traps instead of hanging the GPU.
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned target) {
+// CTA is resident), split into arrive and wait so that work not depending on
+// the other CTAs can run in between.  `count` is zeroed before the launch;
+// barrier k of the launch waits for (k + 1) * gridDim.x arrivals.  The CTA
+// barrier orders every thread's writes before thread 0's release (cumulative);
+// the matching acquire is thread 0's poll.  A CTA that is never joined traps
+// instead of hanging the GPU.
+__device__ __forceinline__ void grid_arrive(unsigned* count) {
     __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned* count, unsigned target) {
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(count, 1u);
         const long long t0 = clock64();
         unsigned v;
         while (true) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
             if (v >= target) break;
-            __nanosleep(64);
             if (clock64() - t0 > (1ll << 35)) __trap();
         }
     }
@@ -148,39 +151,28 @@ struct RowLoads {
     float yv;
 };
 
+// Element tid of the tile's np x q path columns (the layer-0 inputs of its paths).
+__device__ __forceinline__ float path_col(const SplitArgs& a, long tile, int tid) {
+    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
+    const unsigned kfirst = row0 / N;
+    const int np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - kfirst + 1);
+    return tid < np * a.q ? __ldg(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q) : 0.0f;
+}
+
 __device__ __forceinline__ RowLoads row_loads(const SplitArgs& a, long tile, int r, int tid, long b0, long b1) {
     RowLoads l;
-    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
-    const unsigned row = row0 + r;
+    const unsigned row = static_cast<unsigned>(tile * 128) + r;
     const bool live = row >= b0 && row < b1;
 #pragma unroll
     for (int c = 0; c < kInd; ++c)
         l.st[c] = (live && c < a.Cc) ? __ldg(a.steps + static_cast<size_t>(c + 1) * a.R + row) : 0xFFFF;
     l.y = live ? __ldg(a.y + row) : 0.0;
-    const unsigned kfirst = row0 / N;
-    const int np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - kfirst + 1);
-    l.yv = tid < np * a.q ? __ldg(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q) : 0.0f;
+    l.yv = a.N >= 128 ? 0.0f : path_col(a, tile, tid);  // N >= 128: staged per step instead
     return l;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-// The same rows' lines pulled into L2 (no registers held).
-__device__ __forceinline__ void row_prefetch(const SplitArgs& a, long tile, int r, int tid, long b1) {
-    const unsigned row0 = static_cast<unsigned>(tile * 128), N = static_cast<unsigned>(a.N);
-    const unsigned row = row0 + r;
-    if (row < b1) {
-        if ((r & 31) == 0) {  // one lane per 32 rows: 64 B of steps per name, 256 B of labels
-#pragma unroll
-            for (int c = 0; c < kInd; ++c)
-                if (c < a.Cc) prefetch_l2(a.steps + static_cast<size_t>(c + 1) * a.R + row);
-            prefetch_l2(a.y + row);
-        }
-    }
-    const unsigned kfirst = row0 / N;
-    const int np = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - kfirst + 1);
-    if (tid < np * a.q && tid % 32 == 0) prefetch_l2(a.yhat + static_cast<size_t>(kfirst + tid / a.q) * a.qp + tid % a.q);
-}
 
 __device__ __forceinline__ RowState row_state(const SplitArgs& a, long tile, int r, const RowLoads& l, long b0,
                                               long b1) {
@@ -251,8 +243,23 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     const int nsteps = a.fuse ? a.nsteps : 1;
     // the first tile's row loads do not depend on the optimizer: before the dependency wait
     const long b1_0 = a.fuse ? a.b0 + a.bs : a.b1;
-    const RowLoads l0pre = (!issuer && blockIdx.x < n_tiles) ? row_loads(a, t_first + blockIdx.x, r, tid, a.b0, b1_0)
-                                                             : RowLoads{};
+    // (in persistent mode the next step's are loaded during the optimizer's last barrier)
+    RowLoads lfirst = (!issuer && blockIdx.x < n_tiles) ? row_loads(a, t_first + blockIdx.x, r, tid, a.b0, b1_0)
+                                                        : RowLoads{};
+    // N >= 128 (a tile holds at most 2 paths): the per-path columns of every tile of
+    // this CTA's step, staged once per step as ys2 [2 * tile + p][kQ]
+    const bool pre = a.N >= 128;
+    float* ys2 = Psh + 2 * kSlots * kU;
+    auto load_ys2 = [&](long tf_, long t_end_) {
+        const int ntl = static_cast<int>((t_end_ - (tf_ + blockIdx.x) + gridDim.x - 1) / gridDim.x);
+        for (int i = tid; i < ntl * 2 * kQ; i += kSgdThreads) {
+            const int k = i / (2 * kQ), p = (i / kQ) % 2, j = i % kQ;
+            const unsigned row0 = static_cast<unsigned>((tf_ + blockIdx.x + static_cast<long>(k) * gridDim.x) * 128);
+            const unsigned kf = row0 / static_cast<unsigned>(a.N);
+            const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
+            ys2[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
+        }
+    };
     cta_sync();
     const uint32_t tm = *tbase;
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -263,6 +270,7 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     for (int step = 0; step < nsteps; ++step) {
     const long sb0 = a.fuse ? a.b0 + step * a.bs : a.b0, sb1 = a.fuse ? sb0 + a.bs : a.b1;
     const long tf = sb0 / 128, t_end = (sb1 - 1) / 128 + 1;
+    TRACE_FIX(16);
     if (tid == 0) {
         if (step > 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // the image the optimizer wrote
         tc::mbar_expect_tx(&bar[4], 4 * kW1);
@@ -363,17 +371,9 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         // layer-0 inputs of a tile: its paths' y, P into Psh[buf], the indicator A operand
         // N >= 128 (a tile holds at most 2 paths): the layer-0 path parts of every
         // tile of this CTA's step at once, Psh [2 * tile + p][64], W0_y rows loaded once
-        const bool pre = a.N >= 128;
         if (pre) {
             const int ntl = static_cast<int>((t_end - (tf + blockIdx.x) + gridDim.x - 1) / gridDim.x);
-            float* ys2 = Psh + 2 * kSlots * kU;  // [2 * tile + p][kQ]
-            for (int i = tid; i < ntl * 2 * kQ; i += kSgdThreads) {
-                const int k = i / (2 * kQ), p = (i / kQ) % 2, j = i % kQ;
-                const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(k) * gridDim.x) * 128);
-                const unsigned kf = row0 / static_cast<unsigned>(a.N);
-                const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
-                ys2[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
-            }
+            if (step == 0) load_ys2(tf, t_end);
             const int o = tid >> 3, sub = tid & 7;
             float w[kQ / 8];
 #pragma unroll
@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 acc += __shfl_xor_sync(0xffffffffu, acc, 1);
                 if (sub == 0) Psh[qi * kU + o] = b0o + acc;
             }
+            TRACE_FIX(17);
         }
         auto stage_tile = [&](const RowState& st, float yv, int buf) {
             if (!pre && tid < st.np * a.q) ysh[(tid / a.q) * kQ + tid % a.q] = yv;
@@ -408,9 +409,8 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         long tile = tf + blockIdx.x;
         RowState cur{};
         if (tile < t_end) {
-            const RowLoads l0 = step == 0 ? l0pre : row_loads(a, tile, r, tid, sb0, sb1);
-            cur = row_state(a, tile, r, l0, sb0, sb1);
-            stage_tile(cur, l0.yv, 0);
+            cur = row_state(a, tile, r, lfirst, sb0, sb1);
+            stage_tile(cur, lfirst.yv, 0);
             ready(0);
         }
         TRACE_FIX(1);
@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     TRACE_FIX(4);
 
     // ---- this CTA's partial row of the gradient (every parameter); scratch in tH / tG
-    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * a.P;
+    // partial rows: stride P, padded to 16 bytes in persistent mode (16-byte gathers)
+    const int gld = a.fuse ? (a.P + 3) & ~3 : a.P;
+    float* gout = a.gpart + static_cast<size_t>(blockIdx.x) * gld;
     constexpr int L1 = kU + 1;                 // padded rows: conflict-free column stores
     float* s1 = reinterpret_cast<float*>(tH);  // [128][L1] gW1 rows: hi part, lo part
     float* s2 = reinterpret_cast<float*>(tG);  // [128][kInd + 1 + kQ + 1] gW0 rows: hi part, lo part
@@ -597,28 +599,37 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     // row r' % 64, hi part for r' < 64, lo part above.  Per slot (tile order):
     // the indicator columns, and per path (path order) s_p -> b0 and s_p y_p.
     int* snp = reinterpret_cast<int*>(red + 48);                          // [kSlots] paths per slot
-    float* yh = reinterpret_cast<float*>(tH + 128 * (kU + 1) * 4 + 64);  // [slot][kPaths][kQ]
+    // per-path columns of each slot's paths: ys2 when staged per step, else loaded here
+    float* yh = pre ? ys2 : reinterpret_cast<float*>(tH + 128 * (kU + 1) * 4 + 64);  // [slot][ystr][kQ]
+    const int ystr = pre ? 2 : kPaths;
     if (tid < nt) {
         const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(tid) * gridDim.x) * 128);
         const unsigned N = static_cast<unsigned>(a.N);
         snp[tid] = static_cast<int>(min(row0 + 127u, static_cast<unsigned>(a.R - 1)) / N - row0 / N + 1);
     }
-    for (int i = tid; i < nt * kPaths * kQ; i += kSgdThreads + 32) {
-        const int s = i / (kPaths * kQ), p = (i / kQ) % kPaths, j = i % kQ;
-        const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(s) * gridDim.x) * 128);
-        const unsigned kf = row0 / static_cast<unsigned>(a.N);
-        const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
-        yh[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
+    if (!pre) {
+        for (int i = tid; i < nt * kPaths * kQ; i += kSgdThreads + 32) {
+            const int s = i / (kPaths * kQ), p = (i / kQ) % kPaths, j = i % kQ;
+            const unsigned row0 = static_cast<unsigned>((tf + blockIdx.x + static_cast<long>(s) * gridDim.x) * 128);
+            const unsigned kf = row0 / static_cast<unsigned>(a.N);
+            const bool in = j < a.q && kf + p < static_cast<unsigned>(a.M);
+            yh[i] = in ? __ldg(a.yhat + static_cast<size_t>(kf + p) * a.qp + j) : 0.0f;
+        }
     }
     __syncthreads();
     TRACE_FIX(11);
+    // Slots over the four warpgroups by columns: warpgroup g accumulates the y columns
+    // [12 g, 12 g + 12) over every slot (and warpgroup 0 the indicator columns and b0),
+    // each element summed over slots and paths in order.
     constexpr int LW = kInd + 1 + kQ + 1;  // s2 row: indicators, b0, y columns (padded)
-    if (warp < 4) {
-        float acc_i[kInd], acc_y[kQ], acc_b0 = 0.0f;
+    constexpr int kQg = kQ / 4;
+    if (!issuer) {
+        const int wg = warp >> 2;
+        float acc_i[kInd], acc_y[kQg], acc_b0 = 0.0f;
 #pragma unroll
         for (int c = 0; c < kInd; ++c) acc_i[c] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < kQ; ++j) acc_y[j] = 0.0f;
+        for (int j = 0; j < kQg; ++j) acc_y[j] = 0.0f;
         for (int sl = 0; sl < nt; ++sl) {
             float v[32];
             tc::tmem_ld16(tm + lb + kTSlot + 32u * sl, v);
@@ -631,17 +642,19 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 if (p >= np) break;
                 const float sp = v[kInd + p];
                 acc_b0 += sp;
-                const float* y = yh + (sl * kPaths + p) * kQ;
+                const float* y = yh + (sl * ystr + p) * kQ + wg * kQg;
 #pragma unroll
-                for (int j = 0; j < kQ; ++j) acc_y[j] = fmaf(sp, y[j], acc_y[j]);
+                for (int j = 0; j < kQg; ++j) acc_y[j] = fmaf(sp, y[j], acc_y[j]);
             }
         }
         float* row = s2 + r * LW;
+        if (wg == 0) {
 #pragma unroll
-        for (int c = 0; c < kInd; ++c) row[c] = acc_i[c];
-        row[kInd] = acc_b0;
+            for (int c = 0; c < kInd; ++c) row[c] = acc_i[c];
+            row[kInd] = acc_b0;
+        }
 #pragma unroll
-        for (int j = 0; j < kQ; ++j) row[kInd + 1 + j] = acc_y[j];
+        for (int j = 0; j < kQg; ++j) row[kInd + 1 + wg * kQg + j] = acc_y[j];
     }
     __syncthreads();
     TRACE_FIX(12);
@@ -665,19 +678,22 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         // (regressor.cpp:236-261) and refreshes the weight image; then every CTA
         // reloads the weights for the next step
         const int P = a.P, G = gridDim.x;
-        const int per = (P + G - 1) / G, i0 = blockIdx.x * per, i1 = min(P, i0 + per);
+        const int per = ((P + G - 1) / G + 3) & ~3, i0 = blockIdx.x * per, cnt = min(P, i0 + per) - i0;
         const double c1 = __ldcg(a.c12 + 2 * step), c2 = __ldcg(a.c12 + 2 * step + 1);
         // this CTA's slice of the optimizer state: only this CTA updates it, so it is
         // read before the barrier
         double w_own = 0.0, m_own = 0.0, v_own = 0.0;
-        if (tid < i1 - i0) {
+        if (tid < cnt) {
             w_own = __ldcg(a.p64w + i0 + tid);
             m_own = __ldcg(a.m + i0 + tid);
             v_own = __ldcg(a.v + i0 + tid);
         }
-        __threadfence();
-        grid_sync(a.gbar, ++gsyncs * gridDim.x);
+        grid_arrive(a.gbar);
+        grid_wait(a.gbar, ++gsyncs * G);
         TRACE_FIX(13);
+        double lsum = 0.0;  // the batch loss (CTA 0's MMA-issue warp), consumed after the update
+        if (blockIdx.x == 0 && issuer)
+            for (int c = lane; c < G; c += 32) lsum += __ldcg(a.lpart + c);
         ImgArgs im;
         im.img = a.img;
         im.U = kU;
@@ -686,49 +702,73 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         im.off0 = a.off0;
         im.off1 = a.off1;
         im.off2 = a.off2;
-        // rows split over the 16 epilogue warps (lanes = consecutive parameters: coalesced),
-        // the 16 warp sums combined in warp order in shared memory
-        double* part = reinterpret_cast<double*>(tG);  // [16][per]
-        if (warp < 16) {
-            for (int j = lane; j < per; j += 32) {
-                double g = 0.0;
-                if (i0 + j < i1) {
-#pragma unroll 8
-                    for (int c = warp; c < G; c += 16) g += static_cast<double>(__ldcg(a.gpart + static_cast<size_t>(c) * P + i0 + j));
+        if (cnt > 0) {
+            // the slice of every partial row into shared memory (16-byte loads, four in
+            // flight per thread), then summed in FP64: ng groups of consecutive rows, the
+            // group sums in group order
+            float* rows = reinterpret_cast<float*>(tH);  // [G][per]
+            const int nq = (cnt + 3) >> 2, nall = G * nq;
+            for (int i = tid; i < nall; i += 4 * (kSgdThreads + 32)) {
+                float4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = i + u * (kSgdThreads + 32), c = k / nq, qq = k % nq;
+                    if (k < nall) v[u] = __ldcg(reinterpret_cast<const float4*>(a.gpart + static_cast<size_t>(c) * gld + i0) + qq);
                 }
-                part[warp * per + j] = g;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = i + u * (kSgdThreads + 32), c = k / nq, qq = k % nq;
+                    if (k < nall) *reinterpret_cast<float4*>(rows + c * per + 4 * qq) = v[u];
+                }
+            }
+            __syncthreads();
+            TRACE_FIX(18);
+            const int ng = min(8, (kSgdThreads + 32) / per);
+            double* part = reinterpret_cast<double*>(tG);  // [ng][per]
+            if (tid < ng * per) {
+                const int j = tid % per, k = tid / per, ca = k * G / ng, ce = (k + 1) * G / ng;
+                double g = 0.0;
+                for (int c = ca; c < ce; ++c) g += static_cast<double>(rows[c * per + j]);
+                part[k * per + j] = g;
+            }
+            __syncthreads();
+            TRACE_FIX(19);
+            if (tid < cnt) {  // Adam / SGD (regressor.cpp:236-261) on the prefetched state
+                const int i = i0 + tid;
+                double g = 0.0;
+                for (int k = 0; k < ng; ++k) g += part[k * per + tid];
+                double wv = w_own;
+                if (a.adam) {
+                    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+                    const double mi = b1 * m_own + (1.0 - b1) * g;
+                    const double vi = b2 * v_own + (1.0 - b2) * g * g;
+                    a.m[i] = mi;
+                    a.v[i] = vi;
+                    wv -= a.lr * (mi / c1) / (sqrt(vi / c2) + eps);
+                } else {
+                    wv -= a.lr * g;
+                }
+                a.p64w[i] = wv;
+                a.p32w[i] = static_cast<float>(wv);
+                img_store(im, P, i, static_cast<float>(wv));
             }
         }
-        __syncthreads();
-        if (tid < i1 - i0) {  // Adam / SGD (regressor.cpp:236-261) on the prefetched state
-            const int i = i0 + tid;
-            double g = 0.0;
-            for (int w = 0; w < 16; ++w) g += part[w * per + tid];
-            double wv = w_own;
-            if (a.adam) {
-                const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-                const double mi = b1 * m_own + (1.0 - b1) * g;
-                const double vi = b2 * v_own + (1.0 - b2) * g * g;
-                a.m[i] = mi;
-                a.v[i] = vi;
-                wv -= a.lr * (mi / c1) / (sqrt(vi / c2) + eps);
-            } else {
-                wv -= a.lr * g;
-            }
-            a.p64w[i] = wv;
-            a.p32w[i] = static_cast<float>(wv);
-            img_store(im, P, i, static_cast<float>(wv));
-        }
-        if (blockIdx.x == 0 && warp == 0) {  // the batch loss must stay finite (regressor.cpp:291-293)
-            double l = 0.0;
-            for (int c = lane; c < G; c += 32) l += __ldcg(a.lpart + c);
-            l = warp_sum(l);
+        if (blockIdx.x == 0 && issuer) {  // the batch loss must stay finite (regressor.cpp:291-293)
+            const double l = warp_sum(lsum);
             if (lane == 0 && !isfinite(l / a.nb)) atomicExch(a.nonfinite, 1);
         }
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
         TRACE_FIX(14);
-        grid_sync(a.gbar, ++gsyncs * gridDim.x);
+        grid_arrive(a.gbar);
+        ++gsyncs;
+        {  // the next step's loads that do not need the new weights (lfirst is
+           // assigned on every path: the previous value is dead during the tiles)
+            const long nb0 = sb0 + a.bs, ntf = nb0 / 128, nt_end = (nb0 + a.bs - 1) / 128 + 1;
+            const bool more = step + 1 < nsteps && !issuer;
+            lfirst = (more && ntf + blockIdx.x < nt_end) ? row_loads(a, ntf + blockIdx.x, r, tid, nb0, nb0 + a.bs)
+                                                        : RowLoads{};
+            if (more && pre) load_ys2(ntf, nt_end);
+        }
+        grid_wait(a.gbar, gsyncs * G);
         TRACE_FIX(15);
     }
     }  // step
@@ -1035,7 +1075,7 @@ void launch_eval_act(const SplitArgs& a, long t_first, long n_tiles, int ctas, c
 static_assert(sgd_split_smem() <= 227 * 1024, "split SGD kernel exceeds shared memory");
 static_assert(2 * kSlots * kU + 2 * kSlots * kQ <= 2 * kPaths * kU, "per-step path parts exceed Psh");
 static_assert(2ull * kH >= 128ull * (kU + 1) * 4 + 64 + 4ull * kSlots * kPaths * kQ &&
-                  kG >= 128ull * (kInd + kQ + 2) * 4,
+                  kG >= 128ull * (kInd + kQ + 2) * 4 && kQ % 4 == 0,
               "readout scratch exceeds the operand tiles");
 static_assert(eval_split_smem() <= 227 * 1024, "split evaluation kernel exceeds shared memory");
 
@@ -1070,10 +1110,10 @@ bool launch_sgd_split_fused(const SplitArgs& a, int sm_count, cudaStream_t s) {
     const long per = (n_tiles + sm_count - 1) / sm_count;
     if (per > kSlots) return false;
     const int ctas = static_cast<int>((n_tiles + per - 1) / per);
-    // the fused optimizer gives each thread of a CTA at most one parameter, and its
-    // 16 x per partial sums (FP64) live in the G^T | B operand tiles
-    const long pslice = (a.P + ctas - 1) / ctas;
-    if (pslice > kSgdThreads + 32 || 16 * 8 * pslice > static_cast<long>(kG + kB)) return false;
+    // the fused optimizer gives each thread of a CTA at most one parameter (slices of
+    // a multiple of 4 for 16-byte gathers); the gathered rows fill the H1^T tile
+    const long pslice = (((a.P + ctas - 1) / ctas + 3) / 4) * 4;
+    if (pslice > kSgdThreads + 32 || 4L * ctas * pslice > static_cast<long>(2 * kH)) return false;
     switch (a.act) {
         case 0: return launch_sgd_fused_act<0>(a, t_first, n_tiles, ctas, s);
         case 1: return launch_sgd_fused_act<1>(a, t_first, n_tiles, ctas, s);
