@@ -945,15 +945,18 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
         };
         auto layer0 = [&](int n) {  // H1 of tile n -> A[b]
             const int b = n & 1;
+            const float4* P = reinterpret_cast<const float4*>(a.Pg + (b ? rk1 : rk0) * kU + cb);
+            float4 pg[4];  // the path part, loaded under the D0 wait
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) pg[q4] = __ldg(P + q4);
             tc::mbar_wait_addr(dbar + 8 * b, ph[b]);
             ph[b] ^= 1;
             tc::fence_after_sync();
             float z[16], hi[16], lo[16];
-            const float4* P = reinterpret_cast<const float4*>(a.Pg + (b ? rk1 : rk0) * kU + cb);
             tc::tmem_ld16(tm + b * kEvBuf + lb + cb, z);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 pv = __ldg(P + q4);
+                const float4 pv = pg[q4];
                 const float pz[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -967,13 +970,18 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
             tc::tmem_st16(tm + b * kEvBuf + lb + 128 + cb, lo);
             ready(2 + b);
         };
-        auto outputs = [&](int n) {  // H2, f and the requested outputs of tile n
+        // H2, f and the requested outputs of tile n; once its accumulator is read, the
+        // buffer's next tile n + 2 is prepared (so its D0 runs under this epilogue)
+        auto outputs = [&](int n, bool prep_next, const Pre& fn) {
             const int b = n & 1;
             const long tile = t_first + blockIdx.x + static_cast<long>(n) * gridDim.x;
             const long rw = tile * 128 + r;
+            const bool live = b ? rl1 : rl0;  // this tile's row state (prep overwrites buffer b's)
+            const double yrow = b ? ry1 : ry0;
             wait_done(2 + b);
             float h2[16];
             tc::tmem_ld16(tm + b * kEvBuf + lb + cb, h2);
+            if (prep_next) prep(n + 2, fn);
             epi_sync();  // the previous tile's fsh reads are done
             float fp = 0.0f;
 #pragma unroll
@@ -984,7 +992,6 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
             fsh[hf * 128 + r] = fp;
             epi_sync();
             const float f = b2 + ((fsh[r] + fsh[128 + r]) + (fsh[256 + r] + fsh[384 + r]));
-            const bool live = b ? rl1 : rl0;
             if ((a.mode & 8) && live)
 #pragma unroll
                 for (int j = 0; j < 16; j += 4)
@@ -992,7 +999,7 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
             if (live && hf == 0) {
                 const double ph = (f < 0.0f ? 0.0 : static_cast<double>(f)) + mu;
                 if (a.mode & 1) {
-                    const double res = ph - (b ? ry1 : ry0);
+                    const double res = ph - yrow;
                     loss += res * res;
                 }
                 if (a.mode & 2) mn = fmin(mn, static_cast<double>(f) + mu);
@@ -1003,12 +1010,12 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
         if (nt > 0) prep(0, fetch(0));
         for (int n = 0; n < nt; ++n) {
             Pre f{};
-            if (n + 1 < nt) f = fetch(n + 1);  // in flight under layer 0 of n and the outputs of n-1
+            if (n + 1 < nt) f = fetch(n + 1);  // in flight under layer 0 of n
             layer0(n);
-            if (n > 0) outputs(n - 1);
-            if (n + 1 < nt) prep(n + 1, f);
+            if (n > 0) outputs(n - 1, n + 1 < nt, f);
+            else if (n + 1 < nt) prep(n + 1, f);
         }
-        if (nt > 0) outputs(nt - 1);
+        if (nt > 0) outputs(nt - 1, false, Pre{});
     }
     __syncthreads();
     double* red = reinterpret_cast<double*>(fsh);
