@@ -574,9 +574,14 @@ def learning_leg(hcva, cfg, book, ctx, args, rank=0, world=1):
         if world > 1:
             comm = dist.nccl_comm(ctx, world, rank, dist.share_id(dist.nccl_unique_id))
             torch.distributed.barrier()
-        # untimed warm-up: the same trainer path at full size over two pricing steps
-        # (module loading, host-side first calls, and the stream-ordered memory pool
-        # grown to the run's footprint, which it keeps for the timed run)
+        # untimed warm-up: the full set and its labels once (the stream-ordered memory
+        # pool grown to the run's footprint, which it keeps for the timed run: on a
+        # fresh box first-touch allocations cost ~0.3 s), then the same trainer path at
+        # full size over two pricing steps (module loading, host-side first calls)
+        wsim = hcva.simulate_set(cfg, book, spec["n_paths"], cfg.replicas, root, path_offset=spec["path_offset"],
+                                 ctx=ctx, shard=spec["shard"])
+        wsim.labels_all(cfg.label_kind, to_host=False)
+        del wsim
         wt = copy.copy(t)
         wj = _json.loads(_json.dumps(cases.case(args.config)))
         wj["grid"]["pricing_steps"] = 2

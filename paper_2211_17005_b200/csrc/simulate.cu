@@ -10,6 +10,7 @@
 //   k_intensity_*  K4' intensity labels (labels.cpp:50-88)
 //   k_features     K4" feature rows of one step (labels.cpp:142-167)
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -1123,6 +1124,7 @@ void choose_market_shape(hcva_sim* sim) {
         // T even, ~7 normal pairs per thread per chunk, bounded by shared memory.
         int T = std::max(2, ((2 * TPP * 7) / D) & ~1);
         T = std::min(T, 16);
+        if (const char* e = std::getenv("HCVA_K1_T")) T = std::max(2, std::atoi(e) & ~1);  // profiling knob
         size_t smem = sizeof(double) * (head + queue + 2 * static_cast<size_t>(T) * D * P);
         while (smem > 100 * 1024 && T > 2) {
             T -= 2;
