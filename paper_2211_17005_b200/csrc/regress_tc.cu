@@ -1420,28 +1420,43 @@ __global__ void __launch_bounds__(256) k_gram_dmma(const float* __restrict__ H2,
     for (int q = 0; q < PW; ++q) acc[q][0] = acc[q][1] = 0.0;
     const int fr = lane & 3, fc = lane >> 2;  // fragment: row (K) and column (M / N) of this lane
     const long nch = (R + kGdRows - 1) / kGdRows;
+    // register prefetch: the next chunk's rows are in flight while this chunk's MMAs run
+    constexpr int kPer = kGdRows * (U / 4) / 256;  // float4 per thread per chunk
+    float4 v[kPer];
+    double yv = 0.0;
+    auto fetch = [&](long ch) {
+        const long base = ch * kGdRows;
+        const int rows = static_cast<int>(min(static_cast<long>(kGdRows), R - base));
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int i = t + 256 * u, r = i / (U / 4), c4 = (i % (U / 4)) * 4;
+            v[u] = r < rows ? __ldg(reinterpret_cast<const float4*>(H2 + (base + r) * U + c4))
+                            : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+        if (t < kGdRows) yv = t < rows ? y[base + t] - mu : 0.0;
+    };
+    if (static_cast<long>(blockIdx.x) < nch) fetch(blockIdx.x);
     for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
         const long base = ch * kGdRows;
         const int rows = static_cast<int>(min(static_cast<long>(kGdRows), R - base));
         __syncthreads();
-        for (int i = t; i < kGdRows * (U / 4); i += 256) {
-            const int r = i / (U / 4), c4 = (i % (U / 4)) * 4;
-            float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            if (r < rows) v = __ldg(reinterpret_cast<const float4*>(H2 + (base + r) * U + c4));
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int i = t + 256 * u, r = i / (U / 4), c4 = (i % (U / 4)) * 4;
             double* z = zs + r * kGdLD + c4;
-            z[0] = v.x;
-            z[1] = v.y;
-            z[2] = v.z;
-            z[3] = v.w;
+            z[0] = v[u].x;
+            z[1] = v[u].y;
+            z[2] = v[u].z;
+            z[3] = v[u].w;
         }
-        for (int r = t; r < kGdRows; r += 256) {
-            double* z = zs + r * kGdLD;
-            const bool in = r < rows;
-            z[U] = in ? 1.0 : 0.0;
-            z[U + 1] = in ? y[base + r] - mu : 0.0;
+        if (t < kGdRows) {
+            double* z = zs + t * kGdLD;
+            z[U] = t < rows ? 1.0 : 0.0;
+            z[U + 1] = yv;
             for (int c = U + 2; c < 72; ++c) z[c] = 0.0;
         }
         __syncthreads();
+        if (ch + gridDim.x < nch) fetch(ch + gridDim.x);
         for (int k0 = 0; k0 < kGdRows; k0 += 4) {
             const double* zr = zs + (k0 + fr) * kGdLD + fc;
 #pragma unroll
