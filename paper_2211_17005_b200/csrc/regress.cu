@@ -543,33 +543,55 @@ __global__ void k_refit(NetDims n, const double* gpart, int nct, double ridge, d
         for (int a = 0; a < m; ++a) G[a * m + a] += lam;
     }
     __syncthreads();
-    // LDL^T in place (lower part of G holds L), column by column.
+    // LDL^T in place (lower part of G holds L), column by column: d_j by warp 0 (lanes
+    // over k, fixed butterfly), the column below the diagonal by all threads (four
+    // interleaved partial sums over k), the substitutions by warp 0.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto wsum = [](double v) {
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
     for (int j = 0; j < m; ++j) {
-        if (threadIdx.x == 0) {
-            double dj = G[j * m + j];
-            for (int k = 0; k < j; ++k) dj -= G[j * m + k] * G[j * m + k] * D[k];
-            D[j] = dj;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int k = lane; k < j; k += 32) s += G[j * m + k] * G[j * m + k] * D[k];
+            s = wsum(s);
+            if (lane == 0) D[j] = G[j * m + j] - s;
         }
         __syncthreads();
         for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
-            double v = G[i * m + j];
-            for (int k = 0; k < j; ++k) v -= G[i * m + k] * G[j * m + k] * D[k];
-            G[i * m + j] = v / D[j];
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int k = 0;
+            for (; k + 3 < j; k += 4) {
+                a0 += G[i * m + k] * G[j * m + k] * D[k];
+                a1 += G[i * m + k + 1] * G[j * m + k + 1] * D[k + 1];
+                a2 += G[i * m + k + 2] * G[j * m + k + 2] * D[k + 2];
+                a3 += G[i * m + k + 3] * G[j * m + k + 3] * D[k + 3];
+            }
+            for (; k < j; ++k) a0 += G[i * m + k] * G[j * m + k] * D[k];
+            G[i * m + j] = (G[i * m + j] - ((a0 + a1) + (a2 + a3))) / D[j];
         }
         __syncthreads();
     }
+    if (warp == 0) {
+        for (int i = 0; i < m; ++i) {  // L z = rhs
+            double s = 0.0;
+            for (int k = lane; k < i; k += 32) s += G[i * m + k] * rhs[k];
+            s = wsum(s);
+            if (lane == 0) rhs[i] -= s;
+            __syncwarp();
+        }
+        for (int i = lane; i < m; i += 32) rhs[i] /= D[i];
+        __syncwarp();
+        for (int i = m - 1; i >= 0; --i) {  // L^T x = z
+            double s = 0.0;
+            for (int k = i + 1 + lane; k < m; k += 32) s += G[k * m + i] * rhs[k];
+            s = wsum(s);
+            if (lane == 0) rhs[i] -= s;
+            __syncwarp();
+        }
+    }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < m; ++i) {
-            double v = rhs[i];
-            for (int k = 0; k < i; ++k) v -= G[i * m + k] * rhs[k];
-            rhs[i] = v;
-        }
-        for (int i = 0; i < m; ++i) rhs[i] /= D[i];
-        for (int i = m - 1; i >= 0; --i) {
-            double v = rhs[i];
-            for (int k = i + 1; k < m; ++k) v -= G[k * m + i] * rhs[k];
-            rhs[i] = v;
-        }
         const int o = n.off[n.h];
         for (int c = 0; c < m; ++c) {
             p64[o + c] = rhs[c];
@@ -585,9 +607,11 @@ __global__ void k_switch(NetDims n, const double* mpart, int nct, double* p64, f
         m[i] = 0.0;
         v[i] = 0.0;
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the minimum is order-free: lanes take strided partials
         double mn = INFINITY;
-        for (int c = 0; c < nct; ++c) mn = fmin(mn, mpart[c]);
+        for (int c = threadIdx.x; c < nct; c += 32) mn = fmin(mn, mpart[c]);
+        for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (threadIdx.x != 0) return;
         const double mu_new = fmax(0.0, mn);
         const int bo = n.off[n.h] + n.u;
         p64[bo] += p64[n.P - 1] - mu_new;
@@ -599,24 +623,29 @@ __global__ void k_switch(NetDims n, const double* mpart, int nct, double* p64, f
 
 // Epoch bookkeeping (regressor.cpp:316-327): record the full-sample loss,
 // keep the best parameters on a strict improvement.
-__global__ void k_track(int P, const double* lpart, int nct, double R, int epoch, const double* p64, double* best,
-                        double* losses, double* best_loss, int* best_epoch, int* nonfinite) {
+__global__ void k_track(int P, const double* lpart, int nct, double R, int epoch, const double* __restrict__ p64,
+                        double* __restrict__ best, double* losses, double* best_loss, int* best_epoch, int* nonfinite) {
     __shared__ int improved;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // lanes sum strided partials (loads in flight together), then a fixed butterfly
         double s = 0.0;
-        for (int c = 0; c < nct; ++c) s += lpart[c];
+        for (int c = threadIdx.x; c < nct; c += 32) s += lpart[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         const double ev = s / R;
-        losses[epoch - 1] = ev;
-        if (!isfinite(ev)) *nonfinite = 1;
-        improved = ev < *best_loss;
-        if (improved) {
-            *best_loss = ev;
-            *best_epoch = epoch;
+        if (threadIdx.x == 0) {
+            losses[epoch - 1] = ev;
+            if (!isfinite(ev)) *nonfinite = 1;
+            improved = ev < *best_loss;
+            if (improved) {
+                *best_loss = ev;
+                *best_epoch = epoch;
+            }
         }
     }
     __syncthreads();
-    if (improved)
+    if (improved) {
+#pragma unroll 4
         for (int i = threadIdx.x; i < P; i += blockDim.x) best[i] = p64[i];
+    }
 }
 
 __global__ void k_to_f32(const double* a, float* b, int n) {
@@ -1056,7 +1085,7 @@ struct Trainer {
             }
             eval(X, y, R, 1, nullptr);
             const double* lp = rank_scalar(lpart.as<double>(), last_parts, 0);
-            k_track<<<1, 256, 0, ctx->stream>>>(n.P, lp, comm ? world : last_parts, static_cast<double>(R) * world, e,
+            k_track<<<1, 1024, 0, ctx->stream>>>(n.P, lp, comm ? world : last_parts, static_cast<double>(R) * world, e,
                                                  p64.as<double>(), best.as<double>(), losses_dev,
                                                  best_loss.as<double>(), best_epoch.as<int>(), flag.as<int>());
             check_launch(ctx);
