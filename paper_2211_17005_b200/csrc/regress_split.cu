@@ -62,13 +62,15 @@ constexpr uint32_t kGlo = 8 * 1024;          // row 64 + o of a 128-row SW128 ti
 constexpr int kBR = 32;                      // rows of the [indicators; path membership; 0] operand
 constexpr uint32_t kB = kBR * 128 * 4;       // its single (exact) plane (16 KB)
 constexpr int kSgdThreads = 512;             // 4 warpgroups x 16 columns
-constexpr int kSlots = 5;                    // per-tile indicator / path-sum blocks kept in TMEM
-// TMEM columns of the SGD kernel: D (layer-0 indicator part, layer 1, backward),
-// A hi | lo (H1, then G2), gW1 [hi rows; lo rows] x 64, the indicator A
-// operand, kSlots blocks of per-tile [128 x 32] indicator / path sums, and
-// act'(H1) (then G1) of the current tile.
-constexpr uint32_t kTD = 0, kTAh = 64, kTAl = 128, kTW1 = 192, kTInd = 256, kTSlot = 288, kTDh = 448;
-static_assert(kTSlot + 32 * kSlots <= kTDh, "TMEM columns");
+constexpr int kSlots = 5;                    // per-tile indicator / path-sum blocks kept in TMEM (N >= 128)
+constexpr int kSlotsWide = 3;                // ... for N < 128 (up to 9 paths per tile: 32-column blocks)
+// TMEM columns of the SGD kernel: D (layer-0 indicator part, then layer 1), A hi | lo
+// (H1, then G2), gW1 [hi rows; lo rows] x 64, the indicator A operand (8 used), DB
+// (the backward product G2 W1, then G1), the per-tile [128 x 16] (N >= 128) or
+// [128 x 32] indicator / path-sum blocks, and act'(H1) of the tile in flight.
+constexpr uint32_t kTD = 0, kTAh = 64, kTAl = 128, kTW1 = 192, kTInd = 256, kTB = 272, kTSlot = 336, kTDh = 448;
+static_assert(kTSlot + 16 * kSlots <= kTDh && kTSlot + 32 * kSlotsWide <= kTDh, "TMEM columns");
+__host__ __device__ constexpr int sgd_slots(int N) { return N >= 128 ? kSlots : kSlotsWide; }
 
 constexpr size_t sgd_split_smem() {
     return 2ull * kH + kG + kB + 4ull * kW1 + 2ull * kW0i + 4ull * (kPaths * kQ + 2 * kPaths * kU + 4 * 128 + 2 * kU) +
@@ -212,14 +214,16 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     float* vsh = fsh + 4 * 128;                            // b1 | w2
     // mbarriers: MMA completions 0 Z (D0), 1 F (F1), 2 X (B), 3 Y (gW1); 4 W (weights);
     // 5..8 operands ready for D0 / F1 / B + gW1 / slot + next D0 (one arrival per epilogue warp)
+    // 9 slot MMAs done
     uint64_t* bar = reinterpret_cast<uint64_t*>(vsh + 2 * kU);
-    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 9);
+    uint32_t* tbase = reinterpret_cast<uint32_t*>(bar + 10);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool issuer = warp == kSgdThreads / 32;  // warp 16 issues every MMA; warps 0-15 are rows x columns
     const int r = tid & 127, hf = (tid >> 7) & 3, cb = hf * 16;
     if (tid == 0) {
         for (int i = 0; i < 5; ++i) tc::mbar_init(&bar[i], 1);
         for (int i = 5; i < 9; ++i) tc::mbar_init(&bar[i], kSgdThreads / 32);
+        tc::mbar_init(&bar[9], 1);
         tc::fence_async_smem();
     }
     TRACE_FIX(0);
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
     pdl_wait();  // the optimizer's parameters and weight image
     const uint32_t id128 = tc::idesc_tf32(128, kU, 0, 0);
-    uint32_t ph[4] = {0, 0, 0, 0}, rph[4] = {0, 0, 0, 0};
+    uint32_t ph[4] = {0, 0, 0, 0}, rph[4] = {0, 0, 0, 0}, sph = 0;  // sph: slot-MMA completions (barrier 9)
     unsigned gsyncs = 0;
     for (int step = 0; step < nsteps; ++step) {
     const long sb0 = a.fuse ? a.b0 + step * a.bs : a.b0, sb1 = a.fuse ? sb0 + a.bs : a.b1;
@@ -281,7 +285,9 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
     int nt = 0;
 
     if (issuer) {
-        // ================= MMA issue (one lane), paced by the epilogue warps' ready barriers
+        // ================= MMA issue (one lane), paced by the epilogue warps' ready barriers.
+        // Per tile n: B(n), the next tile's D0, gW1(n), the next tile's F1, slot(n) -- so the
+        // next tile's layer 0 (epilogue) overlaps gW1(n) and its F1 follows gW1 directly.
         auto wait_ready = [&](int k) {
             tc::mbar_wait(&bar[5 + k], rph[k]);
             rph[k] ^= 1;
@@ -293,12 +299,19 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
             tc::mma_tf32_ts(tm + kTD, tm + kTInd, B.desc(1, 0), id128, 1);
             tc::commit(&bar[0]);
         };
+        auto issue_f1 = [&]() {  // F1: D = H1 W1^T, H1 from tensor memory; commit F
+            tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, id128, 0);
+            tc::commit(&bar[1]);
+        };
         tc::mbar_wait(&bar[4], step & 1);  // W1 / W1^T in shared memory
         long t = tf + blockIdx.x;
         if (t < t_end) {
             wait_ready(0);
             if (lane == 0) issue_d0();
+            wait_ready(1);
+            if (lane == 0) issue_f1();
         }
+        const uint32_t sw = static_cast<uint32_t>(pre ? 16 : 32);
         for (int n = 0; t < t_end; t += gridDim.x, ++n) {
             const bool more = t + gridDim.x < t_end;
             if (more) {  // the next tile's rows (default steps, labels) into L2 while this tile runs
@@ -310,16 +323,16 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 }
                 if (lane >= 16 && lane < 24) prefetch_l2(a.y + row0 + 16 * (lane - 16));  // 1 KB of labels
             }
-            wait_ready(1);
-            if (lane == 0) {  // ---- F1: D = H1 W1^T, H1 from tensor memory (also covers the last slot MMAs)
-                tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1, kW1, kU), kU, id128, 0);
-                tc::commit(&bar[1]);
-            }
             wait_ready(2);
-            if (lane == 0) {
-                // ---- B: D = G2 W1 (the W1^T tile), G2 from tensor memory; commit X
-                tc::gemm3_ts(tm + kTD, tm + kTAh, tm + kTAl, tc::kmajor(w1t, kW1, kU), kU, id128, 0);
+            if (lane == 0) {  // ---- B: DB = G2 W1 (the W1^T tile), G2 from tensor memory; commit X
+                tc::gemm3_ts(tm + kTB, tm + kTAh, tm + kTAl, tc::kmajor(w1t, kW1, kU), kU, id128, 0);
                 tc::commit(&bar[2]);
+            }
+            if (more) {
+                wait_ready(0);
+                if (lane == 0) issue_d0();  // the next tile's D0 (the epilogue's next layer 0 waits on it)
+            }
+            if (lane == 0) {
                 // ---- gW1 += [G2^T hi; G2^T lo] (H1^T hi + H1^T lo): M = 128, two MMAs per K step; commit Y
                 const tc::OperandSW A{tc::smem_u32(tG), 0, 128, 0};
                 const tc::OperandSW Bh{tc::smem_u32(tH), 0, kU, 0}, Bl{tc::smem_u32(tH) + kH, 0, kU, 0};
@@ -331,18 +344,21 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 }
                 tc::commit(&bar[3]);
             }
+            if (more) {
+                wait_ready(1);
+                if (lane == 0) issue_f1();  // the next tile's F1, queued behind gW1(n)
+            }
             wait_ready(3);
             if (lane == 0) {
-                if (more) issue_d0();  // the next tile's D0 first (the epilogue waits on it next)
-                // ---- slot = [G1^T hi; G1^T lo] [ind; member] (exact B, M = 128): read at the end
+                // ---- slot = [G1^T hi; G1^T lo] [ind; member] (exact B, M = 128): read at the end; commit S
                 const tc::OperandSW A{tc::smem_u32(tG), 0, 128, 0}, Bm{tc::smem_u32(tB), 0, kBR, 0};
-                const uint32_t id = tc::idesc_tf32(128, kBR, 0, 0), slot = tm + kTSlot + 32u * n;
+                const uint32_t id = tc::idesc_tf32(128, sw, 0, 0), slot = tm + kTSlot + sw * n;
 #pragma unroll 1
                 for (int ks = 0; ks < 16; ++ks) tc::mma_tf32(slot, A.desc(0, ks), Bm.desc(0, ks), id, ks > 0 ? 1 : 0);
+                tc::commit(&bar[9]);
             }
             nt = n + 1;
         }
-        if (lane == 0) tc::commit(&bar[1]);  // the last slot MMAs
         __syncwarp();
     } else {
         // ================= epilogue warps: 128 rows x 4 column groups of 16
@@ -405,56 +421,59 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 path_projection8(a, ysh, Psh + buf * kPaths * kU, st.np, tid, kSgdThreads);
             }
         };
+        // Layer 0 of a tile -> H1: hi | lo into tensor memory (the A operand of F1),
+        // act'(H1) into tensor memory; the transposed H1^T (the gW1 operand) is written
+        // separately (store_h1t), once the previous tile's gW1 has read its buffer.
+        auto layer0 = [&](const RowState& st, const float* Pt) {
+            float z[16], hi[16], lo[16], dh[16];
+            const float* P = Pt + st.p * kU + cb;
+            tc::tmem_ld16(tm + lb + kTD + cb, z);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const float h = act_f<ACT>(z[q] + P[q]);
+                hi[q] = tc::tf32_rna(h);
+                lo[q] = h - hi[q];
+                dh[q] = act_d<ACT>(h);
+            }
+            tc::tmem_st16(tm + lb + kTAh + cb, hi);
+            tc::tmem_st16(tm + lb + kTAl + cb, lo);
+            tc::tmem_st16(tm + lb + kTDh + cb, dh);
+        };
+        auto store_h1t = [&]() {  // H1^T hi | lo planes from the A operand in tensor memory
+            float hi[16], lo[16];
+            tc::tmem_ld16(tm + lb + kTAh + cb, hi);
+            tc::tmem_ld16(tm + lb + kTAl + cb, lo);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                sts(xH[q & 7] + (q >> 3) * 1024u, hi[q]);
+                sts(xH[q & 7] + (q >> 3) * 1024u + kH, lo[q]);
+            }
+        };
+        auto path_parts = [&](int k, int pbuf) {  // P of tile k of this step (pre) / the staged buffer
+            return pre ? Psh + 2 * k * kU : Psh + pbuf * kPaths * kU;
+        };
         int buf = 0;
         long tile = tf + blockIdx.x;
         RowState cur{};
-        if (tile < t_end) {
+        if (tile < t_end) {  // the step's first tile: stage, D0, layer 0, F1
             cur = row_state(a, tile, r, lfirst, sb0, sb1);
             stage_tile(cur, lfirst.yv, 0);
             ready(0);
+            epi_sync();  // Psh of the first tile complete
+            wait_done(0);
+            layer0(cur, path_parts(0, 0));
+            store_h1t();
+            ready(1);
         }
         TRACE_FIX(1);
         TRACE_FIX(2);
         for (; tile < t_end; tile += gridDim.x, ++nt, buf ^= 1) {
             const bool more = tile + gridDim.x < t_end;
             TRACE(0);
-            epi_sync();  // Psh of this tile complete
-            wait_done(0);  // D0 of this tile
+            wait_done(1);  // F1 of this tile
             TRACE(1);
-            // ---- layer 0 -> H1 (TMEM A, H1^T), act'(H1) -> TMEM
-            {
-                float dh[16];
-                float z[16], hi[16], lo[16];
-                const float* P = (pre ? Psh + (2 * nt + cur.p) * kU : Psh + buf * kPaths * kU + cur.p * kU) + cb;
-                tc::tmem_ld16(tm + lb + kTD + cb, z);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const float h = act_f<ACT>(z[q] + P[q]);
-                    hi[q] = tc::tf32_rna(h);
-                    lo[q] = h - hi[q];
-                    dh[q] = act_d<ACT>(h);
-                    sts(xH[q & 7] + (q >> 3) * 1024u, hi[q]);
-                    sts(xH[q & 7] + (q >> 3) * 1024u + kH, lo[q]);
-                }
-                tc::tmem_st16(tm + lb + kTAh + cb, hi);
-                tc::tmem_st16(tm + lb + kTAl + cb, lo);
-                tc::tmem_st16(tm + lb + kTDh + cb, dh);
-            }
-            ready(1);
-            TRACE(2);
-            TRACE(3);
-            TRACE(4);
-            wait_done(1);
-            TRACE(5);
-            // ---- epilogue 2: this row's column of [ind; member] (8 rows per warpgroup), H2, f, residual, G2
-#pragma unroll
-            for (int n = 0; n < kBR / 4; ++n) {
-                const int br = hf * (kBR / 4) + n;
-                float v = 0.0f;
-                if (br < kInd) v = ((cur.ind >> br) & 1u) ? 1.0f : 0.0f;
-                else if (br < kInd + kPaths) v = (cur.live && cur.p == br - kInd) ? 1.0f : 0.0f;
-                *reinterpret_cast<float*>(tB + tc::sw_off(br, r, kBR)) = v;
-            }
+            // ---- epilogue 2: H2, f, residual, G2 (TMEM A for B, G2^T for gW1), this tile's
+            // rows of the slot operand [ind; member]
             float h2[16];
             tc::tmem_ld16(tm + lb + kTD + cb, h2);
             float fp = 0.0f;
@@ -485,6 +504,20 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 for (int j = 0; j < 16; ++j) g[j] = dd * h2[j];
                 acc_w2 += bfly_sum<16>(g, lane);  // lane: column cb + lane % 16 over the warp's rows
             }
+            TRACE(2);
+            if (nt > 0) {  // the previous tile's slot MMAs have read G1^T and [ind; member]
+                tc::mbar_wait(&bar[9], sph);
+                sph ^= 1;
+                tc::fence_after_sync();
+            }
+#pragma unroll
+            for (int n = 0; n < kBR / 4; ++n) {
+                const int br = hf * (kBR / 4) + n;
+                float v = 0.0f;
+                if (br < kInd) v = ((cur.ind >> br) & 1u) ? 1.0f : 0.0f;
+                else if (br < kInd + kPaths) v = (cur.live && cur.p == br - kInd) ? 1.0f : 0.0f;
+                *reinterpret_cast<float*>(tB + tc::sw_off(br, r, kBR)) = v;
+            }
             {
                 float gv[16], hi[16], lo[16];
 #pragma unroll
@@ -500,29 +533,38 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                 acc_b1 += bfly_sum<16>(gv, lane);  // gb1: column sums of G2
             }
             ready(2);
+            TRACE(3);
             RowState nxt{};
-            if (more) {  // the next tile's layer-0 inputs, under the B GEMM and gW1
+            if (more) {  // the next tile's layer-0 inputs (indicator operand, P), under B; then its D0
                 const RowLoads ln = row_loads(a, tile + gridDim.x, r, tid, sb0, sb1);
                 nxt = row_state(a, tile + gridDim.x, r, ln, sb0, sb1);
                 stage_tile(nxt, ln.yv, buf ^ 1);
+                ready(0);
             }
-            TRACE(6);
-            wait_done(2);
-            TRACE(7);
-            {  // ---- G1 = D act'(H1) (tensor memory until gW1 has read G2^T)
+            TRACE(4);
+            wait_done(2);  // B: DB = G2 W1
+            TRACE(5);
+            {  // ---- G1 = DB act'(H1), kept in DB
                 float g1[16], dh[16];
-                tc::tmem_ld16(tm + lb + kTD + cb, g1);
+                tc::tmem_ld16(tm + lb + kTB + cb, g1);
                 tc::tmem_ld16(tm + lb + kTDh + cb, dh);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) g1[q] *= dh[q];
-                tc::tmem_st16(tm + lb + kTDh + cb, g1);
+                tc::tmem_st16(tm + lb + kTB + cb, g1);
             }
+            TRACE(6);
+            if (more) {  // ---- the next tile's layer 0, while gW1(n) runs
+                if (!pre) epi_sync();  // its staged P complete
+                wait_done(0);
+                layer0(nxt, path_parts(nt + 1, buf ^ 1));
+                ready(1);
+            }
+            TRACE(7);
+            wait_done(3);  // gW1(n): G2^T and H1^T read
             TRACE(8);
-            wait_done(3);
-            TRACE(9);
-            {
+            {  // ---- G1^T for the slot MMAs, then the next tile's H1^T
                 float g1[16];
-                tc::tmem_ld16(tm + lb + kTDh + cb, g1);
+                tc::tmem_ld16(tm + lb + kTB + cb, g1);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     const float hi = tc::tf32_rna(g1[q]);
@@ -530,11 +572,17 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
                     sts(xG[q & 7] + (q >> 3) * 1024u + kGlo, g1[q] - hi);
                 }
             }
+            if (more) store_h1t();
             ready(3);
+            TRACE(9);
             TRACE(10);
             cur = nxt;
         }
-        wait_done(1);  // the issuer's final commit: every MMA done
+        if (nt > 0) {  // the last slot MMAs (and with them every MMA of the step)
+            tc::mbar_wait(&bar[9], sph);
+            sph ^= 1;
+            tc::fence_after_sync();
+        }
     }
     __syncthreads();
     TRACE_FIX(3);
@@ -632,8 +680,14 @@ __global__ void __launch_bounds__(kSgdThreads + 32, 1) k_sgd_split(SplitArgs a, 
         for (int j = 0; j < kQg; ++j) acc_y[j] = 0.0f;
         for (int sl = 0; sl < nt; ++sl) {
             float v[32];
-            tc::tmem_ld16(tm + lb + kTSlot + 32u * sl, v);
-            tc::tmem_ld16(tm + lb + kTSlot + 32u * sl + 16, v + 16);
+            const uint32_t sw = pre ? 16u : 32u;
+            tc::tmem_ld16(tm + lb + kTSlot + sw * sl, v);
+            if (pre) {
+#pragma unroll
+                for (int c = 16; c < 32; ++c) v[c] = 0.0f;
+            } else {
+                tc::tmem_ld16(tm + lb + kTSlot + sw * sl + 16, v + 16);
+            }
 #pragma unroll
             for (int c = 0; c < kInd; ++c) acc_i[c] += v[c];
             const int np = snp[sl];
@@ -1099,8 +1153,8 @@ int split_max_ctas(int sm_count) { return 2 * sm_count; }
 int launch_sgd_split(const SplitArgs& a, int sm_count, cudaStream_t s) {
     if (a.b1 <= a.b0) throw contract_error("regression tile: empty row range");
     const long t_first = a.b0 / 128, n_tiles = (a.b1 - 1) / 128 - t_first + 1;
-    // one CTA per SM, at most kSlots tiles each (more CTAs run in later waves)
-    const long per = std::min<long>(kSlots, (n_tiles + sm_count - 1) / sm_count);
+    // one CTA per SM, at most sgd_slots tiles each (more CTAs run in later waves)
+    const long per = std::min<long>(sgd_slots(a.N), (n_tiles + sm_count - 1) / sm_count);
     const int ctas = static_cast<int>((n_tiles + per - 1) / per);
     switch (a.act) {
         case 0: launch_sgd_act<0>(a, t_first, n_tiles, ctas, s); break;
@@ -1115,7 +1169,7 @@ bool launch_sgd_split_fused(const SplitArgs& a, int sm_count, cudaStream_t s) {
     if (!a.fuse || a.nsteps < 1 || a.bs < 1 || a.bs % 128 || a.b0 % 128) return false;
     const long t_first = a.b0 / 128, n_tiles = a.bs / 128;  // tiles of each step's batch
     const long per = (n_tiles + sm_count - 1) / sm_count;
-    if (per > kSlots) return false;
+    if (per > sgd_slots(a.N)) return false;
     const int ctas = static_cast<int>((n_tiles + per - 1) / per);
     // the fused optimizer gives each thread of a CTA at most one parameter (slices of
     // a multiple of 4 for 16-byte gathers); the gathered rows fill the H1^T tile
