@@ -107,12 +107,13 @@ def test_split_predictions_validation_set():
         assert (err <= 1e-5 * np.abs(want) + 1e-6 * np.max(np.abs(want))).all(), (i, err.max())
 
 
-def test_split_backward_learn_matches_oracle():
-    """Alg. 2 on the split path: per step, from the engine's own warm start,
-    one train_base against the FP64 oracle's (best loss 1e-3), and the
-    engine's scaler equal to the oracle's (1e-12)."""
+@pytest.mark.parametrize("M,N", [(256, 128), (2048, 16)])
+def test_split_backward_learn_matches_oracle(M, N):
+    """Alg. 2 on the split path (persistent epochs): per step, from the
+    engine's own warm start, one train_base against the FP64 oracle's (best
+    loss 1e-3), and the engine's scaler equal to the oracle's (1e-12)."""
     R = oracle_api.restatement()
-    cfg, book, sim = c2_set(256, 128, steps=4)
+    cfg, book, sim = c2_set(M, N, steps=4)
     t = cfg.training
     t.epochs, t.n_batches = 4, 16
     models = rg.backward_learn(sim, t, "defaults")
@@ -141,11 +142,13 @@ def test_split_deterministic():
         assert np.array_equal(a.get(i)[0], b.get(i)[0])
 
 
-def test_persistent_epoch_matches_per_step_launches():
+@pytest.mark.parametrize("M,N", [(256, 128), (2048, 16)])
+def test_persistent_epoch_matches_per_step_launches(M, N):
     """The persistent epoch kernel (optimizer fused behind grid barriers) and
     per-step launches (k_sgd_split + k_adam, HCVA_FUSED_EPOCH=0) train the same
     network: the two reduce the same FP32 partial rows in different fixed
-    orders in FP64, so they agree to rounding (and in practice bit for bit)."""
+    orders in FP64, so they agree to rounding.  N = 128: per-step path parts
+    and 16-column slot blocks; N = 16: tiles of 8 paths, 32-column slots."""
     import os
     import subprocess
     import sys
@@ -156,7 +159,7 @@ def test_persistent_epoch_matches_per_step_launches():
         "from paper_2211_17005_b200 import regression as rg;"
         "j = cases.case('c2'); j['grid']['pricing_steps'] = 2; cfg = hcva.parse_config(json.dumps(j));"
         "t = cfg.training; t.epochs, t.n_batches = 4, 8;"
-        "sim = hcva.simulate_set(cfg, hcva.generate_book(cfg), 256, 128, hcva.RandomStream(cfg.seed).split(1));"
+        f"sim = hcva.simulate_set(cfg, hcva.generate_book(cfg), {M}, {N}, hcva.RandomStream(cfg.seed).split(1));"
         "m = rg.backward_learn(sim, t);"
         "print(json.dumps([list(m.get(i)[0]) for i in (1, 2)] + [rg.sgd_timing(sim, t, 2, steps=2)['fused_step_ms']]))"
     )
