@@ -600,6 +600,26 @@ __global__ void k_refit(NetDims n, const double* gpart, int nct, double ridge, d
     }
 }
 
+// The full-sample loss (head on) of the network whose output bias is b_out and mu
+// mu, from each row's kept output-layer sum s (k_eval_split mode 16): f = b_out + s in
+// FP32 as the evaluation kernel forms it, pred = max(f, 0) + mu, fixed-order partial
+// sums per CTA over contiguous row ranges.
+__global__ void __launch_bounds__(256) k_loss_fsum(const float* fsum, const double* y, long R, const float* b_out,
+                                                   const double* mu, double* lpart) {
+    __shared__ double red[32];
+    const long per = (R + gridDim.x - 1) / gridDim.x, r0 = blockIdx.x * per, r1 = min(R, r0 + per);
+    const float b = *b_out;
+    const double m = *mu;
+    double s = 0.0;
+    for (long r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const float f = b + fsum[r];
+        const double res = ((f < 0.0f) ? 0.0 : static_cast<double>(f)) + m - y[r];
+        s += res * res;
+    }
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) lpart[blockIdx.x] = t;
+}
+
 // Head switch (regressor.cpp:299-314): mu_new = max(0, min fit), output bias += mu - mu_new,
 // Adam state reset.
 __global__ void k_switch(NetDims n, const double* mpart, int nct, double* p64, float* p32, double* m, double* v) {
@@ -1072,9 +1092,16 @@ struct Trainer {
                 t += n_batches;
             else
                 for (int b = 0; b < n_batches; ++b) sgd_step(X, y, b * bs, (b + 1) * bs, head, ++t, lr, adam);
+            bool loss_done = false;
             if (e == sw) {
                 refit(X, y, R, ridge);
-                eval(X, y, R, 2, nullptr);
+                // split path: the minimum pass also keeps each row's output-layer sum, so the
+                // epoch loss after the switch (only mu and the output bias change) is one
+                // pass over those sums instead of a second full forward
+                const bool keep = split && !sa_over && h2.bytes >= static_cast<size_t>(R) * 4;
+                sa.fsum = keep ? h2.as<float>() : nullptr;
+                eval(X, y, R, keep ? 2 | 16 : 2, nullptr);
+                sa.fsum = nullptr;
                 wimg_valid = false;
                 const double* mp = rank_scalar(mpart.as<double>(), last_parts, 1);
                 k_switch<<<1, 256, 0, ctx->stream>>>(n, mp, comm ? world : last_parts, p64.as<double>(),
@@ -1082,8 +1109,16 @@ struct Trainer {
                 check_launch(ctx);
                 head = 1;
                 t = 0;
+                if (keep) {
+                    const int bo = n.off[n.h] + n.u;
+                    last_parts = ctx->sm_count;
+                    k_loss_fsum<<<last_parts, 256, 0, ctx->stream>>>(h2.as<float>(), y, R, p32.as<float>() + bo,
+                                                                       p64.as<double>() + n.P - 1, lpart.as<double>());
+                    check_launch(ctx);
+                    loss_done = true;
+                }
             }
-            eval(X, y, R, 1, nullptr);
+            if (!loss_done) eval(X, y, R, 1, nullptr);
             const double* lp = rank_scalar(lpart.as<double>(), last_parts, 0);
             k_track<<<1, 1024, 0, ctx->stream>>>(n.P, lp, comm ? world : last_parts, static_cast<double>(R) * world, e,
                                                  p64.as<double>(), best.as<double>(), losses_dev,
