@@ -600,6 +600,57 @@ __global__ void k_refit(NetDims n, const double* gpart, int nct, double ridge, d
     }
 }
 
+// The minimum of the fitted values f + mu (regressor.cpp:299-304) of a network whose
+// hidden layers produced the kept layer-2 activations H2 [R][64] and whose output layer
+// is (w2, b_out): the output sum in k_eval_split's order (four sequential 16-column
+// FMA chains, combined pairwise), kept per row in fsum for k_loss_fsum.
+__global__ void __launch_bounds__(512) k_min_from_h2(const float* H2, long R, const float* w2, const float* b_out,
+                                                     const double* mu, float* fsum, double* mpart) {
+    __shared__ float ws[64];
+    __shared__ double red[32];
+    if (threadIdx.x < 64) ws[threadIdx.x] = w2[threadIdx.x];
+    __syncthreads();
+    const float b = *b_out;
+    const double m = *mu;
+    double mn = INFINITY;
+    // four lanes per row (lane k: columns 16k..16k+15, 64 contiguous bytes): a warp reads
+    // 8 consecutive rows, 2 KB
+    const int k = threadIdx.x & 3;
+    const float* w = ws + 16 * k;
+    const long step = static_cast<long>(gridDim.x) * (blockDim.x / 4);
+    for (long r0 = blockIdx.x * static_cast<long>(blockDim.x / 4); r0 < R; r0 += step) {
+        const long r = r0 + (threadIdx.x >> 2);
+        float acc = 0.0f;
+        if (r < R) {
+            const float4* h = reinterpret_cast<const float4*>(H2 + r * 64 + 16 * k);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = __ldcs(h + q);
+                acc = fmaf(v.x, w[4 * q], acc);
+                acc = fmaf(v.y, w[4 * q + 1], acc);
+                acc = fmaf(v.z, w[4 * q + 2], acc);
+                acc = fmaf(v.w, w[4 * q + 3], acc);
+            }
+        }
+        const float a1 = __shfl_xor_sync(0xffffffffu, acc, 1);  // lane pair (g0, g1) / (g2, g3)
+        const float s01 = (k & 1) ? a1 + acc : acc + a1;        // g0 + g1 or g2 + g3, in that order
+        const float s23 = __shfl_xor_sync(0xffffffffu, s01, 2);
+        const float fs = (k & 2) ? s23 + s01 : s01 + s23;       // (g0 + g1) + (g2 + g3)
+        if (r < R && k == 0) {
+            fsum[r] = fs;
+            mn = fmin(mn, static_cast<double>(b + fs) + m);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmin(t, red[w]);
+        mpart[blockIdx.x] = t;
+    }
+}
+
 // The full-sample loss (head on) of the network whose output bias is b_out and mu
 // mu, from each row's kept output-layer sum s (k_eval_split mode 16): f = b_out + s in
 // FP32 as the evaluation kernel forms it, pred = max(f, 0) + mu, fixed-order partial
@@ -716,7 +767,7 @@ struct Trainer {
     int TR = 128, eval_ctas = 0;
     DeviceBuf p64, p32, m, v, best, gpart, lpart, mpart, gram, flag, losses, best_loss, best_epoch;
     // Tensor-core path: weight-gradient partials, transposed activations, packed operand images.
-    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2, gram_sum;
+    DeviceBuf gpartB, h1t, g2t, g1t, wimg, ximg, xt, h2, gram_sum, fsumb;
     int max_tiles = 0, last_parts = 0, dp = 0, gram_parts = 0;
     bool use_tc = false, xf32 = false;
     long ld_x = 0, ld_tmax = 0, x_rows = 0;
@@ -1095,13 +1146,22 @@ struct Trainer {
             bool loss_done = false;
             if (e == sw) {
                 refit(X, y, R, ridge);
-                // split path: the minimum pass also keeps each row's output-layer sum, so the
-                // epoch loss after the switch (only mu and the output bias change) is one
-                // pass over those sums instead of a second full forward
-                const bool keep = split && !sa_over && h2.bytes >= static_cast<size_t>(R) * 4;
-                sa.fsum = keep ? h2.as<float>() : nullptr;
-                eval(X, y, R, keep ? 2 | 16 : 2, nullptr);
-                sa.fsum = nullptr;
+                // split path: the refit changed only the output layer, so the minimum of the
+                // fitted values is one GEMV over the layer-2 activations the refit pass kept
+                // (the evaluation kernel's summation order: bit-identical output sums), and
+                // the epoch loss after the switch (mu and the output bias change) one pass
+                // over those sums -- instead of two full forward evaluations
+                const bool keep = split && !sa_over && h2.bytes >= static_cast<size_t>(R) * n.u * 4;
+                if (keep) {
+                    if (fsumb.bytes < static_cast<size_t>(R) * 4) fsumb.alloc(static_cast<size_t>(R) * 4);
+                    last_parts = split_max_ctas(ctx->sm_count);  // rows of mpart the trainer holds
+                    k_min_from_h2<<<last_parts, 512, 0, ctx->stream>>>(
+                        h2.as<float>(), R, p32.as<float>() + n.off[n.h], p32.as<float>() + n.off[n.h] + n.u,
+                        p64.as<double>() + n.P - 1, fsumb.as<float>(), mpart.as<double>());
+                    check_launch(ctx);
+                } else {
+                    eval(X, y, R, 2, nullptr);
+                }
                 wimg_valid = false;
                 const double* mp = rank_scalar(mpart.as<double>(), last_parts, 1);
                 k_switch<<<1, 256, 0, ctx->stream>>>(n, mp, comm ? world : last_parts, p64.as<double>(),
@@ -1112,7 +1172,7 @@ struct Trainer {
                 if (keep) {
                     const int bo = n.off[n.h] + n.u;
                     last_parts = ctx->sm_count;
-                    k_loss_fsum<<<last_parts, 256, 0, ctx->stream>>>(h2.as<float>(), y, R, p32.as<float>() + bo,
+                    k_loss_fsum<<<last_parts, 256, 0, ctx->stream>>>(fsumb.as<float>(), y, R, p32.as<float>() + bo,
                                                                        p64.as<double>() + n.P - 1, lpart.as<double>());
                     check_launch(ctx);
                     loss_done = true;

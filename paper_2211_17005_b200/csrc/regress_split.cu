@@ -1045,9 +1045,7 @@ __global__ void __launch_bounds__(kEvThreads + 32, 1) k_eval_split(SplitArgs a, 
             }
             fsh[hf * 128 + r] = fp;
             epi_sync();
-            const float fs = (fsh[r] + fsh[128 + r]) + (fsh[256 + r] + fsh[384 + r]);
-            const float f = b2 + fs;
-            if ((a.mode & 16) && live && hf == 0) a.fsum[rw] = fs;
+            const float f = b2 + ((fsh[r] + fsh[128 + r]) + (fsh[256 + r] + fsh[384 + r]));
             if ((a.mode & 8) && live)
 #pragma unroll
                 for (int j = 0; j < 16; j += 4)

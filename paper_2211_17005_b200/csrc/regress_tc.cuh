@@ -64,7 +64,6 @@ struct SplitArgs {
     double* mpart;             // [cta] min of f + mu
     double* pred;              // predictions, absolute row
     float* H2;                 // [R][U] layer-2 activations (mode 8)
-    float* fsum;               // [R] per-row output-layer sum w2 . h2 without the bias (mode 16), or null
     long long* trace;          // profiling: phase clocks of CTA 0 (HCVA_SPLIT_TRACE), or null
     const float* Pg;           // evaluation: layer-0 path parts [M][64] (k_path_proj)
     float* Pg_out;             // evaluation: where the launcher writes them
