@@ -115,6 +115,9 @@ __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, do
 }
 
 constexpr int kQueueCap = 128;  // per-warp queue of tail draws
+#ifndef HCVA_K1_KSCHED
+#define HCVA_K1_KSCHED 1
+#endif
 // Acklam's branch points 0.02425 and 0.97575 on the top 32 bits of a draw.
 constexpr uint32_t kTailLo32 = static_cast<uint32_t>(0.02425 * 4294967296.0);
 constexpr uint32_t kTailHi32 = static_cast<uint32_t>((1.0 - 0.02425) * 4294967296.0);
@@ -131,7 +134,14 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     double* chol_val = smem + 8 * D;
     int* chol_col = reinterpret_cast<int*>(chol_val + a.nnz);
     int* chol_row = chol_col + a.nnz;
+#if HCVA_K1_KSCHED
+    // Philox round keys of the CTA's paths, [10][P]: key + r W (rng.cpp:33-37), one shared
+    // load per round instead of a 64-bit add in every generator call
+    uint64_t* ksched = reinterpret_cast<uint64_t*>(smem + 8 * D + a.nnz + (a.nnz + D + 2) / 2);
+    double* qp_all = reinterpret_cast<double*>(ksched + 10 * P);    // [NW][cap] tail uniforms
+#else
     double* qp_all = smem + 8 * D + a.nnz + (a.nnz + D + 2) / 2;      // [NW][cap] tail uniforms
+#endif
     int* qs_all = reinterpret_cast<int*>(qp_all + NW * kQueueCap);    // [NW][cap] tail slots
     double* zs = qp_all + NW * kQueueCap + (NW * kQueueCap) / 2;      // [2][T*D][P]
 
@@ -196,6 +206,14 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         }
     };
     store(0);
+#if HCVA_K1_KSCHED
+    if (w == 0) {
+        uint64_t k = pkey;
+#pragma unroll
+        for (int rr = 0; rr < 10; ++rr, k += kPhiloxW) ksched[rr * P + p] = k;
+    }
+    const uint64_t* ks = ksched + p;
+#endif
     __syncthreads();
 
     const double h = a.h, sqh = a.sqh;
@@ -231,7 +249,22 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const int b = w + it * TPP;
         const bool vb = b < g.nb;
         uint64_t w0, w1;
+#if HCVA_K1_KSCHED
+        {  // past the chunk's last block the draws are discarded
+            uint64_t c0 = g.blk0 + b, c1 = 0;
+#pragma unroll
+            for (int rr = 0; rr < 10; ++rr) {
+                const uint64_t hi = __umul64hi(kPhiloxM, c0);
+                const uint64_t lo = kPhiloxM * c0;
+                c0 = hi ^ ks[rr * P] ^ c1;
+                c1 = lo;
+            }
+            w0 = c0;
+            w1 = c1;
+        }
+#else
         philox2x64(g.blk0 + b, pkey, w0, w1);  // past the chunk's last block the draws are discarded
+#endif
         const double uu[2] = {u64_to_uniform(w0), u64_to_uniform(w1)};
         const uint32_t hw[2] = {static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1 >> 32)};
         bool keep[2];
@@ -1125,10 +1158,11 @@ void choose_market_shape(hcva_sim* sim) {
         int T = std::max(2, ((2 * TPP * 7) / D) & ~1);
         T = std::min(T, 16);
         if (const char* e = std::getenv("HCVA_K1_T")) T = std::max(2, std::atoi(e) & ~1);  // profiling knob
-        size_t smem = sizeof(double) * (head + queue + 2 * static_cast<size_t>(T) * D * P);
+        const size_t hk = head + (HCVA_K1_KSCHED ? 10 * static_cast<size_t>(P) : 0);  // + the key schedule
+        size_t smem = sizeof(double) * (hk + queue + 2 * static_cast<size_t>(T) * D * P);
         while (smem > 100 * 1024 && T > 2) {
             T -= 2;
-            smem = sizeof(double) * (head + queue + 2 * static_cast<size_t>(T) * D * P);
+            smem = sizeof(double) * (hk + queue + 2 * static_cast<size_t>(T) * D * P);
         }
         if (smem > 227 * 1024) continue;
         HCVA_CUDA(cudaFuncSetAttribute(market_kernel(P), cudaFuncAttributeMaxDynamicSharedMemorySize,
