@@ -274,7 +274,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             const bool v = vb && j < nn;
             // Acklam's tail test on the draw's top 32 bits (p within 2^-32 of
             // 0.02425 may take either branch: both are refined to the same normal).
-            const bool tail = v && (hw[hf] < kTailLo32 || hw[hf] > kTailHi32);
+            const bool tail = v && (hw[hf] - kTailLo32 > kTailHi32 - kTailLo32);  // hw < lo or hw > hi
             const unsigned m = __ballot_sync(0xffffffffu, tail);
             const int pos = qn + __popc(m & lanemask_lt);
             asm volatile(
