@@ -150,7 +150,7 @@ struct hcva_sim {
     // --- execution plan (staged once, reused by every re-run) ---
     // market: per-factor coefficients, Cholesky CSR, initial states, group keys
     hcva::DeviceBuf m_coef, m_row, m_col, m_val, m_init, m_keys;
-    int m_nnz = 0, m_T = 0, m_ppg = 1, m_P = 8, m_NT = 128, m_We = 12;
+    int m_nnz = 0, m_T = 0, m_ppg = 1, m_P = 8, m_NT = 128, m_We = 12, m_qcap = 0;
     uint64_t m_local_offset = 0;
     size_t m_smem = 0;
     // MtM: coefficient tables (linear form) or the book (direct form)

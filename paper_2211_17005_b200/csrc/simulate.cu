@@ -59,6 +59,7 @@ struct MarketArgs {
     int E, Cn, D, substeps, n_store, M, T, nnz;
     int mode;    // profiling probe: bit 0 skips normal generation, bit 1 skips the recursion
     int W_econ;  // economy-thread slots per path (E rounded up to whole warps)
+    int qcap;    // per-warp tail-queue entries: 64 x the generator iterations of a chunk
     int paths_per_group;
     int shard_blk, shard_stride;  // interleaved shard map (0: identity), see shard_path
     uint64_t local_offset;
@@ -114,10 +115,7 @@ __device__ __forceinline__ double vasicek_step(double r, const FactorCoef& k, do
 #endif
 }
 
-constexpr int kQueueCap = 128;  // per-warp queue of tail draws
-#ifndef HCVA_K1_KSCHED
-#define HCVA_K1_KSCHED 1
-#endif
+constexpr int kMaxGenIters = 16;  // generator iterations per chunk: two tail bits each in a 32-bit mask
 // Acklam's branch points 0.02425 and 0.97575 on the top 32 bits of a draw.
 constexpr uint32_t kTailLo32 = static_cast<uint32_t>(0.02425 * 4294967296.0);
 constexpr uint32_t kTailHi32 = static_cast<uint32_t>((1.0 - 0.02425) * 4294967296.0);
@@ -134,16 +132,11 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     double* chol_val = smem + 8 * D;
     int* chol_col = reinterpret_cast<int*>(chol_val + a.nnz);
     int* chol_row = chol_col + a.nnz;
-#if HCVA_K1_KSCHED
     // Philox round keys of the CTA's paths, [10][P]: key + r W (rng.cpp:33-37), one shared
     // load per round instead of a 64-bit add in every generator call
     uint64_t* ksched = reinterpret_cast<uint64_t*>(smem + 8 * D + a.nnz + (a.nnz + D + 2) / 2);
-    double* qp_all = reinterpret_cast<double*>(ksched + 10 * P);    // [NW][cap] tail uniforms
-#else
-    double* qp_all = smem + 8 * D + a.nnz + (a.nnz + D + 2) / 2;      // [NW][cap] tail uniforms
-#endif
-    int* qs_all = reinterpret_cast<int*>(qp_all + NW * kQueueCap);    // [NW][cap] tail slots
-    double* zs = qp_all + NW * kQueueCap + (NW * kQueueCap) / 2;      // [2][T*D][P]
+    int* qs_all = reinterpret_cast<int*>(ksched + 10 * P);            // [NW][qcap] tail slots
+    double* zs = reinterpret_cast<double*>(ksched + 10 * P) + (NW * a.qcap + 1) / 2;  // [2][T*D][P]
 
     for (int t = threadIdx.x; t < D; t += NT) coef[t] = a.coef[t];
     for (int t = threadIdx.x; t < a.nnz; t += NT) {
@@ -154,11 +147,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
 
     const int p = threadIdx.x % P, w = threadIdx.x / P, TPP = NT / P;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lanemask_lt = (1u << lane) - 1u;
-    double* qp = qp_all + wid * kQueueCap;
-    int* qs = qs_all + wid * kQueueCap;
-    const uint32_t qp_s = static_cast<uint32_t>(__cvta_generic_to_shared(qp));
-    const uint32_t qs_s = static_cast<uint32_t>(__cvta_generic_to_shared(qs));
+    int* qs = qs_all + wid * a.qcap;
     const int M = a.M;
     const int kloc = static_cast<int>(blockIdx.x) * P + p;
     const bool valid = kloc < M;
@@ -206,14 +195,12 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         }
     };
     store(0);
-#if HCVA_K1_KSCHED
     if (w == 0) {
         uint64_t k = pkey;
 #pragma unroll
         for (int rr = 0; rr < 10; ++rr, k += kPhiloxW) ksched[rr * P + p] = k;
     }
     const uint64_t* ks = ksched + p;
-#endif
     __syncthreads();
 
     const double h = a.h, sqh = a.sqh;
@@ -226,7 +213,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     // thread).  Central draws are refined in place; the 4.85% in Acklam's tails
     // are queued per warp (ballot + popc) and refined by full warps at the end
     // of the chunk, so the log/sqrt branch does not serialise ~80% of warps.
-    // it, iters and qn are warp-uniform.
+    // it and iters are warp-uniform.
     // Per-chunk constants of the generator (hoisted out of the iterations).
     struct GenChunk {
         double* zb;         // the chunk's tile
@@ -243,14 +230,13 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         g.blk0 = (static_cast<uint64_t>(cc) * T * D) >> 1;
         return g;
     };
-    auto gen_iter = [&](const GenChunk& g, int it, int iters, int& qn) {
+    auto gen_iter = [&](const GenChunk& g, int it, int iters, uint32_t& tmask) {
         double* zb = g.zb;
         const int nn = g.nn;
         const int b = w + it * TPP;
         const bool vb = b < g.nb;
         uint64_t w0, w1;
-#if HCVA_K1_KSCHED
-        {  // past the chunk's last block the draws are discarded
+        {  // Philox-2x64-10 on the staged round keys; past the chunk's last block the draws are discarded
             uint64_t c0 = g.blk0 + b, c1 = 0;
 #pragma unroll
             for (int rr = 0; rr < 10; ++rr) {
@@ -262,35 +248,22 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             w0 = c0;
             w1 = c1;
         }
-#else
-        philox2x64(g.blk0 + b, pkey, w0, w1);  // past the chunk's last block the draws are discarded
-#endif
         const double uu[2] = {u64_to_uniform(w0), u64_to_uniform(w1)};
         const uint32_t hw[2] = {static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1 >> 32)};
-        bool keep[2];
+        bool v[2], tail[2];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-            const int j = 2 * b + hf;
-            const bool v = vb && j < nn;
-            // Acklam's tail test on the draw's top 32 bits (p within 2^-32 of
-            // 0.02425 may take either branch: both are refined to the same normal).
-            const bool tail = v && (hw[hf] - kTailLo32 > kTailHi32 - kTailLo32);  // hw < lo or hw > hi
-            const unsigned m = __ballot_sync(0xffffffffu, tail);
-            const int pos = qn + __popc(m & lanemask_lt);
-            asm volatile(
-                "{\n\t.reg .pred q;\n\t"
-                "setp.ne.b32 q, %0, 0;\n\t"
-                "@q st.shared.u32 [%1], %2;\n\t"
-                "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(static_cast<int>(tail)),
-                "r"(qs_s + 4u * pos), "r"(j * P + p), "r"(qp_s + 8u * pos), "d"(uu[hf])
-                : "memory");
-            qn += __popc(m);
-            keep[hf] = v && !tail;
+            v[hf] = vb && 2 * b + hf < nn;
+            // Acklam's tail test on the draw's top 32 bits (p within 2^-32 of 0.02425 may
+            // take either branch: both are refined to the same normal): hw < lo or hw > hi
+            tail[hf] = v[hf] && (hw[hf] - kTailLo32 > kTailHi32 - kTailLo32);
         }
-        // Both draws through the central transform, branch-free (a tail or
-        // invalid lane's value is simply not stored).
+        tmask |= (static_cast<uint32_t>(tail[0]) | (static_cast<uint32_t>(tail[1]) << 1)) << (2 * it);
+        // Both draws through the central transform, branch-free; a tail draw's slot keeps
+        // its uniform until the chunk's tail pass below refines it in place.
         double xx[2];
         normal_central_x2(uu, xx);
+        const double s0 = tail[0] ? uu[0] : xx[0], s1 = tail[1] ? uu[1] : xx[1];
         const uint32_t sa = g.zb_s + static_cast<uint32_t>((2 * b * P + p) * 8);
         asm volatile(
             "{\n\t.reg .pred q0, q1;\n\t"
@@ -298,19 +271,35 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             "setp.ne.b32 q1, %4, 0;\n\t"
             "@q0 st.shared.f64 [%0], %1;\n\t"
             "@q1 st.shared.f64 [%0+%5], %3;\n\t}" ::"r"(sa),
-            "d"(xx[0]), "r"(static_cast<int>(keep[0])), "d"(xx[1]), "r"(static_cast<int>(keep[1])), "n"(P * 8)
+            "d"(s0), "r"(static_cast<int>(v[0])), "d"(s1), "r"(static_cast<int>(v[1])), "n"(P * 8)
             : "memory");
-        if (qn > kQueueCap - 64 || it == iters - 1) {
+        if (it == iters - 1) {
+            // The chunk's tail draws (4.85%): each lane's bits compacted into the warp's slot
+            // list (exclusive scan of the counts), then refined by full warps.
+            const int cnt = __popc(tmask);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            int k = incl - cnt;
+            for (uint32_t m = tmask; m; m &= m - 1) {
+                const int bit = __ffs(m) - 1;
+                qs[k++] = (2 * (w + (bit >> 1) * TPP) + (bit & 1)) * P + p;
+            }
             __syncwarp();
-            for (int base = 0; base < qn; base += 32) {
+            for (int base = 0; base < total; base += 32) {
                 const int i = base + lane;
-                if (i < qn) {
-                    const double u = qp[i];
-                    zb[qs[i]] = halley_refine(acklam_tail_seed(u), u);
+                if (i < total) {
+                    const int slot = qs[i];
+                    const double u = zb[slot];
+                    zb[slot] = halley_refine(acklam_tail_seed(u), u);
                 }
             }
-            qn = 0;
             __syncwarp();
+            tmask = 0;
         }
     };
     auto gen_iters = [&](int cc) {
@@ -376,20 +365,20 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     // dependent chains hide under the generator's FP64 throughput.  One
     // __syncthreads per chunk publishes the next buffer.
     if (do_gen) {
-        int qn = 0;
+        uint32_t tmask = 0;
         const int iters = gen_iters(0);
         const GenChunk g0 = gen_chunk(0);
-        for (int it = 0; it < iters; ++it) gen_iter(g0, it, iters, qn);
+        for (int it = 0; it < iters; ++it) gen_iter(g0, it, iters, tmask);
     }
     __syncthreads();
     for (int c = 0; c < n_chunks; ++c) {
         const int iters = (do_gen && c + 1 < n_chunks) ? gen_iters(c + 1) : 0;
         const int tc = min(T, total_sub - c * T);
         const int steps = max(iters, tc);
-        int qn = 0;
+        uint32_t tmask = 0;
         const GenChunk gn = gen_chunk(c + 1);
         for (int s = 0; s < steps; ++s) {
-            if (s < iters) gen_iter(gn, s, iters, qn);
+            if (s < iters) gen_iter(gn, s, iters, tmask);
             if (s < tc && do_rec) rec_step(c, s);
         }
         __syncthreads();
@@ -1153,16 +1142,24 @@ void choose_market_shape(hcva_sim* sim) {
         const int NT = ((P * W + 31) / 32) * 32;
         if (NT > 512) continue;
         const int TPP = NT / P;
-        const size_t queue = static_cast<size_t>(NT / 32) * kQueueCap * 3 / 2;
+        auto qcap_of = [&](int T) {  // 64 tail slots per generator iteration of a chunk, per warp
+            return 64 * (((T * D + 1) / 2 + TPP - 1) / TPP);
+        };
         // T even, ~7 normal pairs per thread per chunk, bounded by shared memory.
         int T = std::max(2, ((2 * TPP * 7) / D) & ~1);
         T = std::min(T, 16);
         if (const char* e = std::getenv("HCVA_K1_T")) T = std::max(2, std::atoi(e) & ~1);  // profiling knob
-        const size_t hk = head + (HCVA_K1_KSCHED ? 10 * static_cast<size_t>(P) : 0);  // + the key schedule
-        size_t smem = sizeof(double) * (hk + queue + 2 * static_cast<size_t>(T) * D * P);
+        while (T > 2 && qcap_of(T) > 64 * kMaxGenIters) T -= 2;
+        if (qcap_of(T) > 64 * kMaxGenIters) continue;
+        const size_t hk = head + 10 * static_cast<size_t>(P);  // + the Philox key schedule
+        auto smem_of = [&](int T) {
+            return sizeof(double) * (hk + (static_cast<size_t>(NT / 32) * qcap_of(T) + 1) / 2 +
+                                     2 * static_cast<size_t>(T) * D * P);
+        };
+        size_t smem = smem_of(T);
         while (smem > 100 * 1024 && T > 2) {
             T -= 2;
-            smem = sizeof(double) * (hk + queue + 2 * static_cast<size_t>(T) * D * P);
+            smem = smem_of(T);
         }
         if (smem > 227 * 1024) continue;
         HCVA_CUDA(cudaFuncSetAttribute(market_kernel(P), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1179,6 +1176,7 @@ void choose_market_shape(hcva_sim* sim) {
             sim->m_NT = NT;
             sim->m_We = We;
             sim->m_T = T;
+            sim->m_qcap = qcap_of(T);
             sim->m_smem = smem;
         }
     }
@@ -1253,6 +1251,7 @@ void launch_market(hcva_sim* sim, uint64_t key0) {
     a.h = m.dt / m.substeps; a.sqh = std::sqrt(a.h);
     a.key0 = key0;
     a.W_econ = sim->m_We;
+    a.qcap = sim->m_qcap;
     if (const char* env = std::getenv("HCVA_K1_MODE")) a.mode = std::atoi(env);
     a.group_keys = sim->m_keys.p ? sim->m_keys.as<uint64_t>() : nullptr;
     a.init_state = sim->m_init.as<double>(); a.coef = sim->m_coef.as<FactorCoef>();
