@@ -302,10 +302,10 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
             tmask = 0;
         }
     };
-    auto gen_iters = [&](int cc) {
-        const int nb = (min(T, total_sub - cc * T) * D + 1) >> 1;
-        return (nb + TPP - 1) / TPP;
-    };
+    // generator iterations of a full chunk and of the last one (two divisions per launch)
+    const int iters_full = ((((T * D) + 1) >> 1) + TPP - 1) / TPP;
+    const int iters_last = ((((total_sub - (n_chunks - 1) * T) * D + 1) >> 1) + TPP - 1) / TPP;
+    auto gen_iters = [&](int cc) { return cc == n_chunks - 1 ? iters_last : iters_full; };
 
     // Recursion: substep t of chunk c for the factors this thread owns.  The
     // Cholesky rows of the owned factors live in registers (<= 2 nonzeros:
