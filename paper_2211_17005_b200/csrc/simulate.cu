@@ -219,7 +219,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         double* zb;         // the chunk's tile
         uint32_t zb_s;      // its shared-space address
         int nn, nb;         // draws and Philox blocks of the chunk
-        uint64_t blk0;      // first block
+        uint32_t blk0;      // first block (a path's blocks fit 32 bits: checked on the host)
     };
     auto gen_chunk = [&](int cc) {
         GenChunk g;
@@ -227,7 +227,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         g.zb_s = static_cast<uint32_t>(__cvta_generic_to_shared(g.zb));
         g.nn = min(T, total_sub - cc * T) * D;
         g.nb = (g.nn + 1) >> 1;
-        g.blk0 = (static_cast<uint64_t>(cc) * T * D) >> 1;
+        g.blk0 = static_cast<uint32_t>(cc * T * D) >> 1;
         return g;
     };
     auto gen_iter = [&](const GenChunk& g, int it, int iters, uint32_t& tmask) {
@@ -237,7 +237,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const bool vb = b < g.nb;
         uint64_t w0, w1;
         {  // Philox-2x64-10 on the staged round keys; past the chunk's last block the draws are discarded
-            uint64_t c0 = g.blk0 + b, c1 = 0;
+            uint64_t c0 = static_cast<uint32_t>(g.blk0 + b), c1 = 0;  // high word 0: a cheaper first round
 #pragma unroll
             for (int rr = 0; rr < 10; ++rr) {
                 const uint64_t hi = __umul64hi(kPhiloxM, c0);
@@ -1133,6 +1133,9 @@ const void* market_kernel(int P) {
 void choose_market_shape(hcva_sim* sim) {
     const Model& m = sim->model;
     const int D = m.D;
+    // K1 counts a path's Philox blocks (and its chunks' draws) in 32-bit integers
+    if (static_cast<long long>(sim->n) * m.substeps * D + 64LL * D >= (1LL << 31))
+        throw config_error("diffusion: normals per path exceed the engine's 32-bit draw counter");
     const size_t head = 8 * D + sim->m_nnz + (sim->m_nnz + D + 2) / 2;
     double best = -1.0;
     for (int P : {16, 8, 4, 2, 1}) {
