@@ -469,9 +469,9 @@ def sgd_roofline(hcva, cfg, sim):
 
 def k1_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of one K1 launch at C2, from
-    the committed ncu --set full capture (profiles/r1/ncu_K1_k_market.txt):
+    the committed ncu --set full capture (profiles/r2/ncu_K1_k_market.txt):
     the FP64-bound kernel's only DRAM traffic is its market stores."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "ncu_K1_k_market.txt")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2", "ncu_K1_k_market.txt")
     try:
         vals = {}
         for ln in open(path):
@@ -480,7 +480,7 @@ def k1_traffic():
                 num, unit = v.split()[0], v.split()[1]
                 vals[k.strip()] = float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
         return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
-                "source": "profiles/r1/ncu_K1_k_market.txt (ncu --set full, C2)"}
+                "source": "profiles/r2/ncu_K1_k_market.txt (ncu --set full, C2)"}
     except (OSError, KeyError, ValueError, IndexError):
         return None
 
