@@ -130,12 +130,13 @@ __constant__ double kAcklamB[5] = {-5.447609879822406e+01, 1.615858368580409e+02
                                    6.680131188771972e+01,  -1.328068155288572e+01};
 
 
-// exp(x^2/2) to ~3e-7 in single precision: enough for u, itself a ~1e-9
-// relative correction (its error enters x at < 1e-15 relative).
-__device__ __forceinline__ double exp_half_sq_approx(double x) {
+// sqrt(2 pi) exp(t) for t = y^2 = x^2/2 (the erf argument squared, already at hand)
+// to ~3e-7 in single precision: enough for u, itself a ~1e-9 relative correction
+// (its error enters x at < 1e-15 relative).
+__device__ __forceinline__ double sqrt2pi_exp_approx(double t) {
     float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(x * x) * 0.72134752044448170f));
-    return static_cast<double>(r);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(t) * 1.44269504088896341f));
+    return static_cast<double>(r * 2.50662827463100050f);
 }
 
 __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (&x)[2]) {
@@ -177,7 +178,7 @@ __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (
     for (int i = 0; i < 2; ++i) {
         const double y0 = -x[i] * kInvSqrt2;
         y[i] = fma(fma(-y0, kSqrt2, -x[i]), kInvSqrt2, y0);
-        t[i] = y[i] * y[i];
+        t[i] = y[i] * y[i];  // x^2 / 2
         P[i] = kErfE[14];
     }
 #pragma unroll
@@ -189,7 +190,7 @@ __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const double e = fma(-0.5, y[i] * P[i], 0.5 - p[i]);
-        const double u = e * kSqrt2Pi * exp_half_sq_approx(x[i]);
+        const double u = e * sqrt2pi_exp_approx(t[i]);
         const double v = x[i] * u * 0.5;
         x[i] = x[i] - u * (1.0 - v * (1.0 - v));
     }
@@ -204,12 +205,12 @@ __device__ __forceinline__ void normal_central_x2(const double (&p)[2], double (
 __device__ __forceinline__ double halley_central(double x, double p) {
     const double y0 = -x * kInvSqrt2;
     const double y = fma(fma(-y0, kSqrt2, -x), kInvSqrt2, y0);
-    const double t = y * y;
+    const double t = y * y;  // x^2 / 2
     double P = kErfE[14];
 #pragma unroll
     for (int j = 13; j >= 0; --j) P = fma(P, t, kErfE[j]);
     const double e = fma(-0.5, y * P, 0.5 - p);
-    const double u = e * kSqrt2Pi * exp_half_sq_approx(x);
+    const double u = e * sqrt2pi_exp_approx(t);
     const double v = x * u * 0.5;
     return x - u * (1.0 - v * (1.0 - v));
 }
