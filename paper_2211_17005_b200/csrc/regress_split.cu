@@ -53,7 +53,6 @@ constexpr int kU = 64;           // hidden width served here
 constexpr int kQ = 48;           // per-path columns (q <= 48), row stride of ysh
 constexpr int kInd = 8;          // indicator columns (Cc <= 8)
 constexpr int kPaths = 9;        // distinct paths per 128-row tile in the SGD kernel (N >= 16)
-constexpr int kEvPaths = 128;    // ... in the evaluation kernel (N >= 1)
 constexpr uint32_t kW1 = kU * kU * 4;        // one plane of W1 / W1^T (16 KB)
 constexpr uint32_t kW0i = kU * kInd * 4;     // one plane of the W0 indicator block (2 KB)
 constexpr uint32_t kH = kU * 128 * 4;        // one H1^T plane (32 KB)
@@ -76,8 +75,6 @@ constexpr size_t sgd_split_smem() {
     return 2ull * kH + kG + kB + 4ull * kW1 + 2ull * kW0i + 4ull * (kPaths * kQ + 2 * kPaths * kU + 4 * 128 + 2 * kU) +
            128 + 1024;
 }
-
-__device__ __forceinline__ long lmin(long x, long y) { return x < y ? x : y; }
 
 __device__ __forceinline__ void cta_sync() {
     tc::fence_before_sync();
