@@ -324,8 +324,7 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
     const FactorCoef kc_a = coef[econ ? fr : fg0], kc_b = coef[econ ? 0 : fg1];
     const double kx_c0 = coef[fx].c0, kx_c1 = coef[fx].c1;
     int sub_ctr = a.substeps, next_store = 1;  // countdown to the next pricing step
-    auto rec_step = [&](int cc, int t) {
-        const double* zt = zs + (cc & 1) * (T * D * P) + t * D * P + p;
+    auto rec_step = [&](const double* zt) {  // zt: this substep's row of the chunk tile, at path p
         auto zcorr = [&](const ZRow& k) {
             if (k.single) return dmul(k.v0, zt[k.o0]);
             if (!k.dense) return madd(k.v1, zt[k.o1], dmul(k.v0, zt[k.o0]));
@@ -377,9 +376,10 @@ __global__ void __maxnreg__(HCVA_K1_MAXNREG) k_market(MarketArgs a) {
         const int steps = max(iters, tc);
         uint32_t tmask = 0;
         const GenChunk gn = gen_chunk(c + 1);
-        for (int s = 0; s < steps; ++s) {
+        const double* zt = zs + (c & 1) * (T * D * P) + p;  // advanced by one substep row per step
+        for (int s = 0; s < steps; ++s, zt += D * P) {
             if (s < iters) gen_iter(gn, s, iters, tmask);
-            if (s < tc && do_rec) rec_step(c, s);
+            if (s < tc && do_rec) rec_step(zt);
         }
         __syncthreads();
     }
