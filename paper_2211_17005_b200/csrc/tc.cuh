@@ -27,10 +27,11 @@ __device__ __forceinline__ uint32_t core_off(int r, int c, int R) {
     return (static_cast<uint32_t>((c >> 2) * (R >> 3) + (r >> 3)) << 7) + ((r & 7) << 4) + ((c & 3) << 2);
 }
 
+// Round to the TF32 grid, ties away from zero (cvt.rna.tf32.f32 without its infinity
+// guard: two integer ops; every operand split here is finite -- a non-finite activation
+// or gradient is caught by the loss check).
 __device__ __forceinline__ float tf32_rna(float a) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(a) + 0x1000u) & 0xFFFFE000u);
 }
 
 // Store a into the hi / lo tiles (same layout, `lo_bytes` apart).
