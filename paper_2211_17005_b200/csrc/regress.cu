@@ -543,33 +543,33 @@ __global__ void k_refit(NetDims n, const double* gpart, int nct, double ridge, d
         for (int a = 0; a < m; ++a) G[a * m + a] += lam;
     }
     __syncthreads();
-    // LDL^T in place (lower part of G holds L), column by column: d_j by warp 0 (lanes
-    // over k, fixed butterfly), the column below the diagonal by all threads (four
-    // interleaved partial sums over k), the substitutions by warp 0.
+    // LDL^T in place (lower part of G holds L), right-looking: per column j, d_j and the
+    // column below it are saved, L[i][j] = c_i / d_j, and the trailing lower block takes
+    // the rank-1 update G[i][k] -= L[i][j] c_k (j < k <= i) in parallel.
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     auto wsum = [](double v) {
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         return v;
     };
+    double* cj = D + m;    // [m] column j below the diagonal, unscaled
+    double* lj = cj + m;   // [m] ... scaled: L[i][j]
     for (int j = 0; j < m; ++j) {
-        if (warp == 0) {
-            double s = 0.0;
-            for (int k = lane; k < j; k += 32) s += G[j * m + k] * G[j * m + k] * D[k];
-            s = wsum(s);
-            if (lane == 0) D[j] = G[j * m + j] - s;
-        }
-        __syncthreads();
+        const double dj = G[j * m + j];
         for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int k = 0;
-            for (; k + 3 < j; k += 4) {
-                a0 += G[i * m + k] * G[j * m + k] * D[k];
-                a1 += G[i * m + k + 1] * G[j * m + k + 1] * D[k + 1];
-                a2 += G[i * m + k + 2] * G[j * m + k + 2] * D[k + 2];
-                a3 += G[i * m + k + 3] * G[j * m + k + 3] * D[k + 3];
+            const double c = G[i * m + j];
+            cj[i] = c;
+            lj[i] = c / dj;
+            G[i * m + j] = c / dj;
+        }
+        if (threadIdx.x == 0) D[j] = dj;
+        __syncthreads();
+        const int nn = m - j - 1;
+        for (int t = threadIdx.x; t < nn * nn; t += blockDim.x) {
+            const int ii = t / nn, kk = t - ii * nn;
+            if (kk <= ii) {
+                const int i = j + 1 + ii, k = j + 1 + kk;
+                G[i * m + k] -= lj[i] * cj[k];
             }
-            for (; k < j; ++k) a0 += G[i * m + k] * G[j * m + k] * D[k];
-            G[i * m + j] = (G[i * m + j] - ((a0 + a1) + (a2 + a3))) / D[j];
         }
         __syncthreads();
     }
@@ -1070,7 +1070,7 @@ struct Trainer {
         }
         check_launch(ctx);
         const int mm = n.u + 1;
-        const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 2 * mm);
+        const size_t sm = sizeof(double) * (static_cast<size_t>(mm) * mm + 4 * mm);  // G, rhs, D, column j x2
         HCVA_CUDA(cudaFuncSetAttribute(k_refit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         const double* gsrc = gram.as<double>();
         if (nct > 8 || comm) {  // pre-reduce the partials across the GPU, k_refit then reads one
@@ -1086,7 +1086,7 @@ struct Trainer {
                 nct = world;
             }
         }
-        k_refit<<<1, 128, sm, ctx->stream>>>(n, gsrc, nct, ridge, p64.as<double>(), p32.as<float>());
+        k_refit<<<1, 256, sm, ctx->stream>>>(n, gsrc, nct, ridge, p64.as<double>(), p32.as<float>());
         wimg_valid = false;
         check_launch(ctx);
     }
