@@ -1394,33 +1394,56 @@ void launch_wgrad_u(const WgradArgs& a, int ctas, cudaStream_t s) {
 // accumulation): z = [h2, 1, y - mu, 0...] (72 columns, 9 blocks of 8); the
 // 45 upper block pairs (bi <= bj) of z^T z are split over 8 warps, each warp
 // walking the CTA's 64-row chunks in 4-row K steps (fixed order: chunk, then
-// K step), one partial per CTA in k_gram_h2's packed layout.
+// K step).
 constexpr int kGdRows = 64, kGdLD = 76;  // chunk rows, padded row (doubles)
+// The 45 upper-triangle 8x8 block pairs (bi <= bj) of the 72-column padded row, grouped
+// by block row so that each warp reads few distinct blocks per K step (6, 7, 7, 7, 6,
+// 5, 4 and 2 fragment loads for 6 x 7 + 3 MMAs): warp w owns pairs kGdPair[w][0..kGdCnt[w]).
+__device__ constexpr int kGdCnt[8] = {6, 6, 6, 6, 6, 6, 6, 3};
+__device__ constexpr int kGdPair[8][6][2] = {
+    {{0, 0}, {0, 1}, {0, 2}, {0, 3}, {0, 4}, {0, 5}}, {{0, 6}, {0, 7}, {0, 8}, {1, 1}, {1, 2}, {1, 3}},
+    {{1, 4}, {1, 5}, {1, 6}, {1, 7}, {1, 8}, {2, 2}}, {{2, 3}, {2, 4}, {2, 5}, {2, 6}, {2, 7}, {2, 8}},
+    {{3, 3}, {3, 4}, {3, 5}, {3, 6}, {3, 7}, {3, 8}}, {{4, 4}, {4, 5}, {4, 6}, {4, 7}, {4, 8}, {5, 5}},
+    {{5, 6}, {5, 7}, {5, 8}, {6, 6}, {6, 7}, {6, 8}}, {{7, 7}, {7, 8}, {8, 8}, {8, 8}, {8, 8}, {8, 8}}};
+
+// One 64-row chunk for warp W: the fragments of the blocks its pairs touch are loaded
+// once per K step (compile-time indices: they stay in registers), then its MMAs.
+template <int W>
+__device__ __forceinline__ void gram_chunk(const double* zs, int fr, int fc, double (&acc)[6][2]) {
+    constexpr int cnt = kGdCnt[W];
+    for (int k0 = 0; k0 < kGdRows; k0 += 4) {
+        const double* zr = zs + (k0 + fr) * kGdLD + fc;
+        double f[9];
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+            bool need = false;
+#pragma unroll
+            for (int q = 0; q < cnt; ++q) need = need || kGdPair[W][q][0] == b || kGdPair[W][q][1] == b;
+            f[b] = need ? zr[8 * b] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < cnt; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[q][0]), "+d"(acc[q][1])
+                         : "d"(f[kGdPair[W][q][0]]), "d"(f[kGdPair[W][q][1]]));
+    }
+}
+
+// The kernel: 64-row chunks staged as FP64 in shared memory (row pitch 76 doubles:
+// conflict-free fragment loads), the next chunk's rows prefetched into registers; one
+// partial per CTA in k_gram_h2's packed layout.
 __global__ void __launch_bounds__(256) k_gram_dmma(const float* __restrict__ H2, const double* __restrict__ y,
                                                     long R, const float* __restrict__ params, int P,
                                                     double* __restrict__ gpart) {
-    constexpr int U = 64, NBK = 9, pairs = 45, PW = 6;  // pairs per warp (8 warps x 6 >= 45)
+    constexpr int U = 64;
     __shared__ __align__(16) double zs[kGdRows * kGdLD];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    int pbi[PW], pbj[PW];
-#pragma unroll
-    for (int q = 0; q < PW; ++q) {  // pair index warp + 8 q -> (bi, bj), bi <= bj
-        int pt = warp + 8 * q, bi = 0;
-        if (pt >= pairs) pt = pairs - 1;  // duplicate, discarded at the end
-        while (pt >= NBK - bi) {
-            pt -= NBK - bi;
-            ++bi;
-        }
-        pbi[q] = bi;
-        pbj[q] = bi + pt;
-    }
     const double mu = static_cast<double>(params[P - 1]);
-    double acc[PW][2];
+    double acc[6][2];
 #pragma unroll
-    for (int q = 0; q < PW; ++q) acc[q][0] = acc[q][1] = 0.0;
+    for (int q = 0; q < 6; ++q) acc[q][0] = acc[q][1] = 0.0;
     const int fr = lane & 3, fc = lane >> 2;  // fragment: row (K) and column (M / N) of this lane
     const long nch = (R + kGdRows - 1) / kGdRows;
-    // register prefetch: the next chunk's rows are in flight while this chunk's MMAs run
     constexpr int kPer = kGdRows * (U / 4) / 256;  // float4 per thread per chunk
     float4 v[kPer];
     double yv = 0.0;
@@ -1437,8 +1460,7 @@ __global__ void __launch_bounds__(256) k_gram_dmma(const float* __restrict__ H2,
     };
     if (static_cast<long>(blockIdx.x) < nch) fetch(blockIdx.x);
     for (long ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-        const long base = ch * kGdRows;
-        const int rows = static_cast<int>(min(static_cast<long>(kGdRows), R - base));
+        const int rows = static_cast<int>(min(static_cast<long>(kGdRows), R - ch * kGdRows));
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
@@ -1457,26 +1479,27 @@ __global__ void __launch_bounds__(256) k_gram_dmma(const float* __restrict__ H2,
         }
         __syncthreads();
         if (ch + gridDim.x < nch) fetch(ch + gridDim.x);
-        for (int k0 = 0; k0 < kGdRows; k0 += 4) {
-            const double* zr = zs + (k0 + fr) * kGdLD + fc;
-#pragma unroll
-            for (int q = 0; q < PW; ++q) {
-                const double a = zr[8 * pbi[q]], b = zr[8 * pbj[q]];
-                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                             : "+d"(acc[q][0]), "+d"(acc[q][1])
-                             : "d"(a), "d"(b));
-            }
+        switch (warp) {
+            case 0: gram_chunk<0>(zs, fr, fc, acc); break;
+            case 1: gram_chunk<1>(zs, fr, fc, acc); break;
+            case 2: gram_chunk<2>(zs, fr, fc, acc); break;
+            case 3: gram_chunk<3>(zs, fr, fc, acc); break;
+            case 4: gram_chunk<4>(zs, fr, fc, acc); break;
+            case 5: gram_chunk<5>(zs, fr, fc, acc); break;
+            case 6: gram_chunk<6>(zs, fr, fc, acc); break;
+            default: gram_chunk<7>(zs, fr, fc, acc); break;
         }
     }
     // Packed output: (a, b) a <= b < m = U+1 -> upper-triangle index; rhs c = (c, U+1).
     constexpr int m = U + 1, tri = m * (m + 1) / 2;
     double* out = gpart + static_cast<size_t>(blockIdx.x) * (tri + m);
 #pragma unroll
-    for (int q = 0; q < PW; ++q) {
-        if (warp + 8 * q >= pairs) continue;
+    for (int q = 0; q < 6; ++q) {
+        if (q >= kGdCnt[warp]) continue;
+        const int bi = kGdPair[warp][q][0], bj = kGdPair[warp][q][1];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int ra = 8 * pbi[q] + fc, cb = 8 * pbj[q] + 2 * fr + e;  // D[row = lane/4][col = 2 (lane%4) + e]
+            const int ra = 8 * bi + fc, cb = 8 * bj + 2 * fr + e;  // D[row = lane/4][col = 2 (lane%4) + e]
             if (ra < m && cb < m && ra <= cb) out[ra * m - ra * (ra - 1) / 2 + (cb - ra)] = acc[q][e];
             else if (ra < m && cb == m) out[tri + ra] = acc[q][e];
         }
